@@ -1,0 +1,278 @@
+/*
+ * tierflow_b200.h — C ABI of the B200-native MLP-Offload update phase.
+ *
+ * The reference ("tierflow", /root/reference/proj) is a header-only C++20
+ * library with no FFI layer; its drop-in boundary is the C++ API the harness
+ * and tests call. Every entry point below replaces one of those calls and
+ * cites it as reference-file:line (paths relative to proj/include/tierflow/).
+ * Plain C types only: opaque handles, pointers and sizes; device pointers are
+ * `void*` / typed pointers into CUDA device memory; streams are
+ * `cudaStream_t` passed as `void*` (NULL = legacy default stream).
+ *
+ * Errors: every function returns a tfg_status. The C++ exception hierarchy of
+ * the reference (common.hpp:36-78) maps one to one onto the codes; the message
+ * of the last failure on the calling thread is returned by tfg_last_error().
+ * No exception crosses this boundary.
+ *
+ * Library: paper_2509_02480_b200/lib/libtierflow_b200.so (sm_100a).
+ */
+#ifndef TIERFLOW_B200_H
+#define TIERFLOW_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TFG_ABI_VERSION 1
+#define TFG_MAX_TIERS 8
+
+typedef enum tfg_status {
+    TFG_OK = 0,
+    TFG_ERROR = 1,                   /* tierflow::Error                       common.hpp:36  */
+    TFG_IO_ERROR = 2,                /* tierflow::IoError                     common.hpp:42  */
+    TFG_FORMAT_ERROR = 3,            /* tierflow::FormatError                 common.hpp:48  */
+    TFG_CONFIG_ERROR = 4,            /* tierflow::ConfigError                 common.hpp:54  */
+    TFG_PLACEMENT_INCONSISTENCY = 5, /* tierflow::PlacementInconsistencyError common.hpp:61  */
+    TFG_SCHEDULING_BUG = 6,          /* tierflow::SchedulingBugError          common.hpp:67  */
+    TFG_GRADIENT_OVERFLOW = 7,       /* tierflow::GradientOverflowError       common.hpp:73  */
+    TFG_CUDA_ERROR = 8               /* CUDA runtime failure (no reference counterpart)      */
+} tfg_status;
+
+/* 16-bit element kinds for gradients and working parameters. */
+typedef enum tfg_dtype { TFG_F16 = 0, TFG_BF16 = 1 } tfg_dtype;
+
+/* Tier kinds: tier.hpp:32 plus TFG_HOST_DRAM (pinned host blobs, zero-copy). */
+typedef enum tfg_tier_kind {
+    TFG_LOCAL_DIR = 0,
+    TFG_REMOTE_DIR = 1,
+    TFG_MEM_THROTTLED = 2,
+    TFG_HOST_DRAM = 3
+} tfg_tier_kind;
+
+/* AdamHyper, optimizer.hpp:17-31. */
+typedef struct tfg_adam_hyper {
+    double lr;
+    double beta1;
+    double beta2;
+    double eps;
+    double weight_decay;
+} tfg_adam_hyper;
+
+/* TierSpec, tier.hpp:43-51 (+ lock_width, direct_io). */
+typedef struct tfg_tier_spec {
+    int32_t tier_id;
+    int32_t kind;            /* tfg_tier_kind */
+    const char* root;        /* directory for *_DIR kinds, a label otherwise */
+    double read_bw;          /* bytes/s, configured (or 0 and probe) */
+    double write_bw;
+    int32_t io_parallelism;  /* >= 1 */
+    int32_t persistent;
+    int32_t lock_width;      /* tier semaphore width; 1 = exclusive flock (the reference) */
+    int32_t direct_io;       /* O_DIRECT on the engine path when the filesystem allows */
+} tfg_tier_spec;
+
+/* ScheduleOptions, scheduler.hpp:32-50. */
+typedef struct tfg_schedule_options {
+    int32_t pool_slots;
+    int32_t cache_slots;     /* -1 derives pool_slots - 3 */
+    int32_t enable_caching;
+    int32_t skip_gradients;  /* must be 1 on the GPU engine (fused widening) */
+    int32_t atomic_rw;
+    int32_t multi_path;
+    const char* lock_dir;    /* NULL/"" = <tmp>/tierflow-locks */
+    int32_t update_threads;  /* accepted for parity, unused (update runs on the GPU) */
+    double deadlock_timeout_s;
+    uint64_t update_pad_ns;
+} tfg_schedule_options;
+
+/* GPU placement of one engine (no reference counterpart). */
+typedef struct tfg_device_options {
+    int32_t device;          /* CUDA ordinal */
+    int32_t grad_dtype;      /* tfg_dtype of the device gradient buffers */
+    int32_t param_dtype;     /* tfg_dtype of the device working-parameter buffers */
+    int32_t device_buffers;  /* depth of the H2D -> kernel -> D2H ring (>= 1) */
+} tfg_device_options;
+
+typedef struct tfg_tier_observation { /* placement.hpp:138-145 */
+    uint64_t read_transfers;
+    double read_bytes;
+    double read_seconds;
+    uint64_t write_transfers;
+    double write_bytes;
+    double write_seconds;
+} tfg_tier_observation;
+
+typedef struct tfg_subgroup_io { /* scheduler.hpp:114-121 */
+    uint32_t id;
+    uint32_t fetched;
+    uint32_t flushed;
+    uint32_t pad;
+    uint64_t state_bytes;
+    double read_seconds;
+    double write_seconds;
+} tfg_subgroup_io;
+
+/* PhaseStats, scheduler.hpp:123-132, plus the device timeline. */
+typedef struct tfg_phase_stats {
+    double wall_seconds;
+    uint64_t params_updated;
+    uint64_t cache_hits;
+    uint64_t downscale_overflows;
+    int32_t retained;
+    int32_t n_tiers;
+    int32_t flush_allocation[TFG_MAX_TIERS];
+    tfg_tier_observation tier_obs[TFG_MAX_TIERS];
+    uint64_t n_subgroup_io;  /* entries available via tfg_engine_last_subgroup_io */
+    double device_seconds;   /* first H2D start -> last D2H end (CUDA events) */
+    double kernel_seconds;   /* sum of fused-kernel durations */
+    double h2d_seconds;
+    double d2h_seconds;
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+} tfg_phase_stats;
+
+/* Event, trace.hpp:65-72 (POD layout). */
+typedef struct tfg_event {
+    int64_t timestamp_ns;
+    int32_t worker_id;
+    int32_t kind;  /* EventKind order of trace.hpp:19-33 */
+    int64_t subgroup_id;
+    int32_t tier_id;
+    int32_t pad;
+    uint64_t bytes;
+} tfg_event;
+
+typedef struct tfg_subgroup_meta { /* Subgroup, optimizer.hpp:39-73 */
+    uint32_t id;
+    int32_t residency;  /* 0 host_cached, 1 in_flight, 2 on_tier */
+    int32_t tier;
+    int32_t slot;
+    uint64_t param_count;
+    uint64_t step_count;
+} tfg_subgroup_meta;
+
+typedef struct tfg_tier tfg_tier;
+typedef struct tfg_trace tfg_trace;
+typedef struct tfg_engine tfg_engine;
+
+/* ---- library ------------------------------------------------------------ */
+const char* tfg_last_error(void);
+int tfg_abi_version(void);
+int tfg_device_count(int* count);
+
+/* ---- kernels (device pointers, async on `stream`) ------------------------ */
+/* Fused upscale_f16_to_f32 -> adam_step -> downscale_f32_to_f16
+ * (precision.hpp:17, optimizer.hpp:116, precision.hpp:29; composed at
+ * scheduler.hpp:467-490). t >= 1 is the Adam timestep; bc1/bc2 are computed on
+ * the host with pow() as optimizer.hpp:129-130. counters (device, 2 x u64) are
+ * accumulated: [0] += non-finite gradients, [1] += +-Inf 16-bit outputs. */
+int tfg_adam_fused(float* p, float* m, float* v, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+                   int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                   unsigned long long* counters, void* stream);
+/* Same on one contiguous P||m||v state (StateView::from_contiguous, optimizer.hpp:82-86). */
+int tfg_adam_fused_contiguous(float* state, uint64_t n, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+                              int param_dtype, const tfg_adam_hyper* hyper, uint64_t t,
+                              unsigned long long* counters, void* stream);
+/* Reference-semantics synchronous step (adam_step, optimizer.hpp:116-157):
+ * validates, rejects non-finite gradients with TFG_GRADIENT_OVERFLOW before
+ * mutating state, then runs the fused kernel and synchronizes.
+ * overflows_out (host, may be NULL) receives the narrowing overflow count. */
+int tfg_adam_step(float* p, float* m, float* v, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+                  int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, uint64_t* overflows_out,
+                  void* stream);
+/* upscale_f16_to_f32, precision.hpp:17-25 (nonfinite: device u64, accumulated). */
+int tfg_upscale16(const uint16_t* src, float* dst, uint64_t n, int dtype, unsigned long long* nonfinite,
+                  void* stream);
+/* downscale_f32_to_f16, precision.hpp:29-37 (overflows: device u64, accumulated). */
+int tfg_downscale16(const float* src, uint16_t* dst, uint64_t n, int dtype, unsigned long long* overflows,
+                    void* stream);
+/* all_finite, precision.hpp:39-43 (count: device u64, accumulated). */
+int tfg_count_nonfinite16(const uint16_t* src, uint64_t n, int dtype, unsigned long long* count, void* stream);
+/* SyntheticGradSource::fill (+ GradBufferF16::accumulate when accumulate != 0),
+ * scheduler.hpp:85-102, precision.hpp:66-75. */
+int tfg_synthetic_grads(uint16_t* out, uint64_t n, int dtype, uint64_t seed, uint32_t subgroup, int iteration,
+                        int step, int accumulate, void* stream);
+/* synthetic_param_init into P, zeros into m and v (scheduler.hpp:104-110, 352). */
+int tfg_synthetic_state(float* p, float* m, float* v, uint64_t n, uint64_t seed, uint32_t subgroup, void* stream);
+
+/* ---- placement (host, pure) --------------------------------------------- */
+/* assign_subgroups, placement.hpp:30-100. counts_out[n_tiers]. */
+int tfg_assign_subgroups(int M, const double* bandwidths, int n_tiers, int* counts_out);
+/* DestinationPlan, placement.hpp:178-225: per order position, retain flag and tier. */
+int tfg_destination_plan(const uint32_t* order, int M, int capacity, const double* bandwidths, int n_tiers,
+                         int* retain_out, int* tier_out, int* flush_allocation_out);
+/* UpdatePlan::make, scheduler.hpp:60-67 (sorted_ids ascending). */
+int tfg_update_order(int iteration, const uint32_t* sorted_ids, int M, int alternate, uint32_t* order_out);
+/* ScheduleOptions::retention_capacity, scheduler.hpp:44-49. */
+int tfg_retention_capacity(int enable_caching, int pool_slots, int cache_slots, int subgroup_count, int* out);
+/* update_bandwidth_estimates, placement.hpp:149-162, on arrays of n_tiers. */
+int tfg_update_bandwidth_estimates(double* read_bw, double* write_bw, uint64_t* sample_count, int n_tiers,
+                                   double alpha, const tfg_tier_observation* observed, int n_observed);
+
+/* ---- trace --------------------------------------------------------------- */
+int tfg_trace_create(tfg_trace** out);                       /* EventTrace, trace.hpp:77 */
+int tfg_trace_destroy(tfg_trace* trace);
+int tfg_trace_size(tfg_trace* trace, uint64_t* size_out);
+int tfg_trace_copy(tfg_trace* trace, uint64_t begin, tfg_event* out, uint64_t max_n, uint64_t* n_out);
+int tfg_trace_record(tfg_trace* trace, int kind, int worker, int64_t subgroup, int tier, uint64_t bytes);
+int tfg_trace_write(tfg_trace* trace, const char* path);     /* .jsonl or CSV, trace.hpp:119-134 */
+int tfg_trace_clear(tfg_trace* trace);
+
+/* ---- tiers ---------------------------------------------------------------- */
+int tfg_tier_create(const tfg_tier_spec* spec, tfg_tier** out);            /* Tier(TierSpec), tier.hpp:159 */
+int tfg_tier_destroy(tfg_tier* tier);
+int tfg_tier_bandwidths(tfg_tier* tier, double* read_bw, double* write_bw);
+int tfg_tier_set_throttle_rates(tfg_tier* tier, double read_bps, double write_bps);   /* tier.hpp:181 */
+int tfg_tier_write_subgroup(tfg_tier* tier, uint32_t id, uint64_t params, const float* state,
+                            uint64_t* bytes_out, double* seconds_out);                 /* tier.hpp:192 */
+int tfg_tier_read_subgroup(tfg_tier* tier, uint32_t id, uint64_t params, float* state,
+                           uint64_t* bytes_out, double* seconds_out);                  /* tier.hpp:199 */
+int tfg_tier_write_grads(tfg_tier* tier, uint32_t id, uint64_t params, const float* grads);  /* tier.hpp:204 */
+int tfg_tier_read_grads(tfg_tier* tier, uint32_t id, uint64_t params, float* grads);         /* tier.hpp:209 */
+int tfg_tier_has_subgroup(tfg_tier* tier, uint32_t id, int* out);                            /* tier.hpp:214 */
+int tfg_tier_remove_subgroup(tfg_tier* tier, uint32_t id);                                   /* tier.hpp:216 */
+int tfg_tier_probe(tfg_tier* tier, uint64_t probe_bytes, int repetitions, double* read_bw, double* write_bw,
+                   int* low_confidence);                                                     /* tier.hpp:223 */
+int tfg_tier_available_bytes(tfg_tier* tier, uint64_t* out);                                 /* tier.hpp:244 */
+
+/* TierLockGuard, tier_lock.hpp:36-106: acquire returns an opaque token. */
+int tfg_tier_lock_acquire(const char* lock_dir, int tier, int worker, tfg_trace* trace, int width, void** token);
+int tfg_tier_lock_release(void* token);
+
+/* ---- engine (OffloadWorker, scheduler.hpp:286-864) ------------------------ */
+int tfg_engine_create(int worker_id, tfg_tier* const* tiers, int n_tiers, const tfg_schedule_options* options,
+                      const tfg_adam_hyper* hyper, tfg_trace* trace, const tfg_device_options* device,
+                      tfg_engine** out);                                                    /* :288-304 */
+int tfg_engine_destroy(tfg_engine* engine);
+int tfg_engine_set_alpha(tfg_engine* engine, double alpha);                                 /* :315 */
+int tfg_engine_set_fixed_ratio(tfg_engine* engine, const double* ratio, int n);             /* :322 */
+int tfg_engine_add_subgroup(tfg_engine* engine, uint32_t id, uint64_t param_count);         /* :324 */
+int tfg_engine_init_and_flush_all(tfg_engine* engine, uint64_t seed);                       /* :339 */
+int tfg_engine_run_backward_sim(tfg_engine* engine, int iteration, uint64_t seed, int accum_steps); /* :365 */
+int tfg_engine_gradients_finite(tfg_engine* engine, int* out);                              /* :395 */
+int tfg_engine_grad_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);             /* :401 */
+int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_ptr);
+int tfg_engine_params16_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);         /* shadow_, :861 */
+int tfg_engine_run_update(tfg_engine* engine, int iteration, tfg_phase_stats* stats);      /* :405 */
+int tfg_engine_last_subgroup_io(tfg_engine* engine, tfg_subgroup_io* out, uint64_t max_n, uint64_t* n_out);
+int tfg_engine_wait_host_resident(tfg_engine* engine, uint32_t id, int* slot_out);         /* :514 */
+/* enqueue_* return a ticket (0 = cache hit, nothing queued) to wait on. */
+int tfg_engine_enqueue_prefetch(tfg_engine* engine, uint32_t id, uint64_t* ticket_out);    /* :563 */
+int tfg_engine_enqueue_flush(tfg_engine* engine, uint32_t id, int dest, uint64_t* ticket_out); /* :553 */
+int tfg_engine_wait_ticket(tfg_engine* engine, uint64_t ticket, uint64_t* bytes_out, double* seconds_out);
+int tfg_engine_read_state(tfg_engine* engine, uint32_t id, float* out_3n);                  /* :611 */
+int tfg_engine_read_params16(tfg_engine* engine, uint32_t id, uint16_t* out_n);
+int tfg_engine_meta(tfg_engine* engine, uint32_t id, tfg_subgroup_meta* out);               /* :587 */
+int tfg_engine_residency_census(tfg_engine* engine, uint64_t* host_params, uint64_t* per_tier, int n_tiers); /* :597 */
+int tfg_engine_current_order(tfg_engine* engine, uint32_t* out, int max_n, int* n_out);     /* :582 */
+int tfg_engine_estimates(tfg_engine* engine, double* read_bw, double* write_bw, int n_tiers); /* :583 */
+int tfg_engine_pool_state(tfg_engine* engine, int slot, int* state_out, uint32_t* owner_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TIERFLOW_B200_H */

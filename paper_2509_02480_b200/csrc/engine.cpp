@@ -1,0 +1,963 @@
+// OffloadWorker: host scheduler + CUDA-stream update pipeline. See engine.hpp.
+#include "engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+
+#include "kernels.hpp"
+#include "tier_lock.hpp"
+
+namespace tfb {
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+struct DeviceGuard {
+    explicit DeviceGuard(int dev) { cuda_check(cudaSetDevice(dev), "cudaSetDevice"); }
+};
+
+constexpr std::uint64_t kSegAlign = 64;  // floats: 256-byte aligned P / m / v device segments
+
+std::uint64_t seg_stride(std::uint64_t pc) { return (pc + kSegAlign - 1) / kSegAlign * kSegAlign; }
+
+}  // namespace
+
+// --- hyperparameters ---------------------------------------------------------
+
+void AdamHyper::validate() const {
+    if (!(lr > 0.0)) throw ConfigError("optim.lr must be > 0");
+    if (beta1 < 0.0 || beta1 >= 1.0) throw ConfigError("optim.beta1 must be in [0, 1)");
+    if (beta2 < 0.0 || beta2 >= 1.0) throw ConfigError("optim.beta2 must be in [0, 1)");
+    if (!(eps > 0.0)) throw ConfigError("optim.eps must be > 0");
+    if (weight_decay < 0.0) throw ConfigError("optim.weight_decay must be >= 0");
+}
+
+AdamConsts AdamHyper::consts(std::uint64_t t) const {
+    if (t < 1) throw Error("adam_step: timestep must be >= 1");
+    validate();
+    AdamConsts c{};
+    c.lr = lr;
+    c.beta1 = beta1;
+    c.beta2 = beta2;
+    c.one_minus_beta1 = 1.0 - beta1;
+    c.one_minus_beta2 = 1.0 - beta2;
+    c.eps = eps;
+    c.lr_wd = weight_decay != 0.0 ? lr * weight_decay : 0.0;
+    c.bc1 = 1.0 - std::pow(beta1, static_cast<double>(t));
+    c.bc2 = 1.0 - std::pow(beta2, static_cast<double>(t));
+    return c;
+}
+
+// --- residency ---------------------------------------------------------------
+
+void Subgroup::begin_flush() {
+    if (residency != Residency::host_cached)
+        throw Error("subgroup " + std::to_string(id) + ": flush from non-host residency");
+    residency = Residency::in_flight;
+}
+void Subgroup::finish_flush(TierId dest) {
+    if (residency != Residency::in_flight)
+        throw Error("subgroup " + std::to_string(id) + ": finish_flush while not in flight");
+    residency = Residency::on_tier;
+    tier = dest;
+    slot = -1;
+}
+void Subgroup::begin_prefetch() {
+    if (residency != Residency::on_tier)
+        throw Error("subgroup " + std::to_string(id) + ": prefetch while not on a tier");
+    residency = Residency::in_flight;
+}
+void Subgroup::finish_prefetch(int pool_slot) {
+    if (residency != Residency::in_flight)
+        throw Error("subgroup " + std::to_string(id) + ": finish_prefetch while not in flight");
+    residency = Residency::host_cached;
+    slot = pool_slot;
+}
+
+// --- pool --------------------------------------------------------------------
+
+const char* slot_state_name(SlotState s) {
+    switch (s) {
+        case SlotState::free_slot: return "free";
+        case SlotState::prefetching: return "prefetching";
+        case SlotState::updating: return "updating";
+        case SlotState::flushing: return "flushing";
+        case SlotState::cached: return "cached";
+    }
+    return "unknown";
+}
+
+HostBufferPool::HostBufferPool(int slot_count, std::uint64_t max_params, bool require_pinned) {
+    if (slot_count < 3) throw ConfigError("host buffer pool needs >= 3 slots");
+    slots_.resize(static_cast<std::size_t>(slot_count));
+    for (auto& s : slots_) s.block = HostBlock::allocate(block_bytes_for(max_params), require_pinned);
+}
+
+std::size_t HostBufferPool::check(int slot) const {
+    if (slot < 0 || static_cast<std::size_t>(slot) >= slots_.size())
+        throw Error("bad pool slot index " + std::to_string(slot));
+    return static_cast<std::size_t>(slot);
+}
+
+void HostBufferPool::transition(int slot, SlotState expected, SlotState next) {
+    std::lock_guard<std::mutex> g(mu_);
+    Slot& s = slots_[check(slot)];
+    if (s.state != expected)
+        throw Error(std::string("pool slot ") + std::to_string(slot) + ": invalid transition " +
+                    slot_state_name(s.state) + " -> " + slot_state_name(next) + " (expected " +
+                    slot_state_name(expected) + ")");
+    s.state = next;
+}
+
+int HostBufferPool::try_reserve(SubgroupId owner) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (std::size_t i = 0; i < slots_.size(); ++i) {
+        if (slots_[i].state == SlotState::free_slot) {
+            slots_[i].state = SlotState::prefetching;
+            slots_[i].owner = owner;
+            return static_cast<int>(i);
+        }
+    }
+    return -1;
+}
+
+int HostBufferPool::find_cached(SubgroupId owner) const {
+    std::lock_guard<std::mutex> g(mu_);
+    for (std::size_t i = 0; i < slots_.size(); ++i)
+        if (slots_[i].state == SlotState::cached && slots_[i].owner == owner) return static_cast<int>(i);
+    return -1;
+}
+
+void HostBufferPool::flush_done(int slot) {
+    transition(slot, SlotState::flushing, SlotState::free_slot);
+    free_cv_.notify_all();
+}
+
+void HostBufferPool::evict(int slot) {
+    transition(slot, SlotState::cached, SlotState::free_slot);
+    free_cv_.notify_all();
+}
+
+void HostBufferPool::release_failed(int slot) {
+    std::lock_guard<std::mutex> g(mu_);
+    slots_[check(slot)].state = SlotState::free_slot;
+    free_cv_.notify_all();
+}
+
+SlotState HostBufferPool::state(int slot) const {
+    std::lock_guard<std::mutex> g(mu_);
+    return slots_[check(slot)].state;
+}
+
+SubgroupId HostBufferPool::owner(int slot) const {
+    std::lock_guard<std::mutex> g(mu_);
+    return slots_[check(slot)].owner;
+}
+
+int HostBufferPool::count(SlotState s) const {
+    std::lock_guard<std::mutex> g(mu_);
+    int n = 0;
+    for (const auto& slot : slots_) n += slot.state == s;
+    return n;
+}
+
+bool HostBufferPool::wait_for_free(std::chrono::milliseconds timeout) {
+    std::unique_lock<std::mutex> g(mu_);
+    return free_cv_.wait_for(g, timeout, [&] {
+        for (const auto& s : slots_)
+            if (s.state == SlotState::free_slot) return true;
+        return false;
+    });
+}
+
+// --- tier I/O workers ----------------------------------------------------------
+
+TierIoWorker::TierIoWorker(std::shared_ptr<Tier> tier, WorkerId worker, bool use_lock,
+                           std::filesystem::path lock_dir, EventTrace* trace)
+    : tier_(std::move(tier)), worker_(worker), use_lock_(use_lock), lock_dir_(std::move(lock_dir)), trace_(trace) {
+    thread_ = std::thread([this] { run(); });
+}
+
+TierIoWorker::~TierIoWorker() { shutdown(); }
+
+std::future<IoStats> TierIoWorker::submit(bool is_prefetch, std::int64_t sg, std::uint64_t bytes_hint,
+                                          std::function<IoStats()> transfer, Completion completion) {
+    Job job;
+    job.is_prefetch = is_prefetch;
+    job.sg = sg;
+    job.bytes_hint = bytes_hint;
+    job.transfer = std::move(transfer);
+    job.completion = std::move(completion);
+    auto fut = job.promise.get_future();
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        if (stop_) throw Error("tier I/O queue is shut down");
+        (is_prefetch ? prefetch_q_ : flush_q_).push_back(std::move(job));
+    }
+    cv_.notify_one();
+    return fut;
+}
+
+void TierIoWorker::shutdown() {
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        if (stop_) return;
+        stop_ = true;
+    }
+    cv_.notify_all();
+    if (thread_.joinable()) thread_.join();
+    std::deque<Job> left;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        left.swap(prefetch_q_);
+        for (auto& j : flush_q_) left.push_back(std::move(j));
+        flush_q_.clear();
+    }
+    for (auto& j : left) {
+        if (j.completion) j.completion(false, IoStats{});
+        j.promise.set_exception(std::make_exception_ptr(Error("tier I/O queue shut down, operation cancelled")));
+    }
+}
+
+void TierIoWorker::run() {
+    for (;;) {
+        Job job;
+        {
+            std::unique_lock<std::mutex> l(mu_);
+            cv_.wait(l, [&] { return stop_ || !prefetch_q_.empty() || !flush_q_.empty(); });
+            if (prefetch_q_.empty() && flush_q_.empty()) {
+                if (stop_) return;
+                continue;
+            }
+            auto& q = prefetch_q_.empty() ? flush_q_ : prefetch_q_;  // prefetches first
+            job = std::move(q.front());
+            q.pop_front();
+        }
+        execute(job);
+    }
+}
+
+void TierIoWorker::execute(Job& job) {
+    const EventKind start = job.is_prefetch ? EventKind::prefetch_start : EventKind::flush_start;
+    const EventKind end = job.is_prefetch ? EventKind::prefetch_end : EventKind::flush_end;
+    std::optional<TierLockGuard> guard;
+    try {
+        if (use_lock_) guard.emplace(lock_dir_, tier_->id(), worker_, trace_, tier_->spec().lock_width);
+        Event ev;
+        ev.timestamp_ns = now_ns();
+        ev.worker_id = worker_;
+        ev.kind = static_cast<int>(start);
+        ev.subgroup_id = job.sg;
+        ev.tier_id = tier_->id();
+        ev.bytes = job.bytes_hint;
+        const std::int64_t t_start = ev.timestamp_ns;
+        if (trace_) trace_->append(ev);
+        IoStats st = job.transfer();
+        ev.timestamp_ns = now_ns();
+        ev.kind = static_cast<int>(end);
+        ev.bytes = st.bytes;
+        if (trace_) trace_->append(ev);
+        // The traced interval is the duration the metrics use (reference scheduler.hpp:241-243).
+        st.seconds = static_cast<double>(ev.timestamp_ns - t_start) / 1e9;
+        guard.reset();
+        if (job.completion) job.completion(true, st);
+        job.promise.set_value(st);
+    } catch (...) {
+        if (trace_) trace_->record(end, worker_, job.sg, tier_->id(), 0);
+        guard.reset();
+        try {
+            if (job.completion) job.completion(false, IoStats{});
+        } catch (...) {
+        }
+        job.promise.set_exception(std::current_exception());
+    }
+}
+
+// --- OffloadWorker -------------------------------------------------------------
+
+OffloadWorker::OffloadWorker(WorkerId id, std::vector<std::shared_ptr<Tier>> tiers, ScheduleOptions opt,
+                             AdamHyper hyper, std::shared_ptr<EventTrace> trace, DeviceOptions dev)
+    : id_(id), tiers_(std::move(tiers)), opt_(std::move(opt)), hyper_(hyper), trace_(std::move(trace)), dev_(dev) {
+    if (tiers_.empty()) throw ConfigError("offload worker needs at least one tier");
+    if (!trace_) trace_ = std::make_shared<EventTrace>();
+    hyper_.validate();
+    if (opt_.pool_slots < 3) throw ConfigError("host buffer pool needs >= 3 slots");
+    if (dev_.device_buffers < 1) throw ConfigError("device_buffers must be >= 1");
+    if (dev_.grad_kind != kF16 && dev_.grad_kind != kBF16) throw ConfigError("unknown gradient dtype");
+    if (dev_.out_kind != kF16 && dev_.out_kind != kBF16) throw ConfigError("unknown working-param dtype");
+    if (opt_.lock_dir.empty()) opt_.lock_dir = (std::filesystem::temp_directory_path() / "tierflow-locks").string();
+    std::vector<double> rbw, wbw;
+    for (const auto& t : tiers_) {
+        rbw.push_back(t->spec().read_bw);
+        wbw.push_back(t->spec().write_bw);
+    }
+    est_ = BandwidthEstimate::init(rbw, wbw, 0.5);
+    for (const auto& t : tiers_)
+        io_.push_back(std::make_unique<TierIoWorker>(t, id_, opt_.atomic_rw, opt_.lock_dir, trace_.get()));
+}
+
+OffloadWorker::~OffloadWorker() {
+    // Let in-flight device work retire before tearing the pipeline down.
+    if (device_ready_) {
+        cudaSetDevice(dev_.device);
+        cudaStreamSynchronize(s_h2d_);
+        cudaStreamSynchronize(s_k_);
+        cudaStreamSynchronize(s_d2h_);
+    }
+    {
+        std::lock_guard<std::mutex> g(cq_mu_);
+        cq_stop_ = true;
+    }
+    cq_cv_.notify_all();
+    if (completer_.joinable()) completer_.join();
+    for (auto& w : io_) w->shutdown();
+    release_device();
+}
+
+void OffloadWorker::set_alpha(double alpha) {
+    if (!(alpha > 0.0) || alpha > 1.0) throw ConfigError("placement.alpha must be in (0, 1]");
+    est_.alpha = alpha;
+}
+
+void OffloadWorker::set_fixed_ratio(std::vector<double> ratio) { fixed_ratio_ = std::move(ratio); }
+
+void OffloadWorker::add_subgroup(SubgroupId id, std::uint64_t param_count) {
+    if (pool_) throw Error("add_subgroup after pipeline initialization");
+    if (param_count == 0) throw ConfigError("subgroup param_count must be > 0");
+    if (subgroups_.count(id)) throw ConfigError("duplicate subgroup id " + std::to_string(id));
+    Subgroup sg;
+    sg.id = id;
+    sg.param_count = param_count;
+    subgroups_.emplace(id, sg);
+    ids_.push_back(id);
+    max_params_ = std::max(max_params_, param_count);
+}
+
+std::vector<double> OffloadWorker::placement_bandwidths() const {
+    std::vector<double> b = fixed_ratio_.empty() ? est_.effective_all() : fixed_ratio_;
+    b.resize(tiers_.size(), 0.0);
+    if (!opt_.multi_path)
+        for (std::size_t i = 1; i < b.size(); ++i) b[i] = 0.0;
+    return b;
+}
+
+void OffloadWorker::setup_device() {
+    DeviceGuard dg(dev_.device);
+    cuda_check(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&s_k_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
+    ring_stride_ = seg_stride(max_params_);
+    ring_.assign(static_cast<std::size_t>(dev_.device_buffers), nullptr);
+    for (auto& r : ring_)
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&r), 3 * ring_stride_ * sizeof(float)), "cudaMalloc(ring)");
+    std::size_t arena = 0;
+    std::vector<std::size_t> offs;
+    for (const SubgroupId id : ids_) {
+        offs.push_back(arena);
+        arena += round_up(2 * subgroups_.at(id).param_count, 256);
+    }
+    cuda_check(cudaMalloc(&grad_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(grads)");
+    cuda_check(cudaMalloc(&p16_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(params16)");
+    cuda_check(cudaMemset(grad_arena_, 0, std::max<std::size_t>(arena, 256)), "cudaMemset(grads)");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&counters_), 2 * sizeof(unsigned long long)), "cudaMalloc");
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&sg_counts_), ids_.size() * sizeof(unsigned long long)),
+               "cudaMalloc");
+    grad_ptr_.clear();
+    p16_ptr_.clear();
+    events_.assign(ids_.size(), DeviceEvents{});
+    for (std::size_t k = 0; k < ids_.size(); ++k) {
+        index_of_[ids_[k]] = k;
+        grad_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(grad_arena_) + offs[k]));
+        p16_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(p16_arena_) + offs[k]));
+        DeviceEvents& e = events_[k];
+        for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_end})
+            cuda_check(cudaEventCreate(ev), "cudaEventCreate");
+    }
+    device_ready_ = true;
+    completer_ = std::thread([this] { completion_loop(); });
+}
+
+void OffloadWorker::release_device() {
+    if (!device_ready_) return;
+    cudaSetDevice(dev_.device);
+    for (auto& e : events_)
+        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_end})
+            if (ev) cudaEventDestroy(ev);
+    events_.clear();
+    for (float* r : ring_) cudaFree(r);
+    ring_.clear();
+    cudaFree(grad_arena_);
+    cudaFree(p16_arena_);
+    cudaFree(counters_);
+    cudaFree(sg_counts_);
+    cudaStreamDestroy(s_h2d_);
+    cudaStreamDestroy(s_k_);
+    cudaStreamDestroy(s_d2h_);
+    device_ready_ = false;
+}
+
+// Host P||m||v (contiguous, stride pc) <-> device P / m / v segments (stride
+// seg_stride(pc), 256-byte aligned). One copy when the strides coincide.
+void OffloadWorker::copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device,
+                               cudaStream_t s) {
+    const std::uint64_t ds = seg_stride(pc);
+    const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+    float* host = blk.payload();
+    if (ds == pc) {
+        const std::size_t bytes = 12 * pc;
+        cuda_check(to_device ? cudaMemcpyAsync(dev_base, host, bytes, kind, s)
+                             : cudaMemcpyAsync(host, dev_base, bytes, kind, s),
+                   "cudaMemcpyAsync(state)");
+        return;
+    }
+    for (int k = 0; k < 3; ++k) {
+        float* d = dev_base + k * ds;
+        float* h = host + k * pc;
+        cuda_check(to_device ? cudaMemcpyAsync(d, h, 4 * pc, kind, s) : cudaMemcpyAsync(h, d, 4 * pc, kind, s),
+                   "cudaMemcpyAsync(state segment)");
+    }
+}
+
+void OffloadWorker::init_and_flush_all(std::uint64_t seed) {
+    if (ids_.empty()) throw ConfigError("worker has no subgroups");
+    if (pool_) throw Error("init_and_flush_all called twice");
+    std::sort(ids_.begin(), ids_.end());
+    DeviceGuard dg(dev_.device);
+    pool_ = std::make_unique<HostBufferPool>(opt_.pool_slots, max_params_, /*require_pinned=*/true);
+    for (auto& t : tiers_) t->reserve_block_bytes(block_bytes_for(max_params_));
+    setup_device();
+
+    const std::vector<SubgroupId> order = update_order(0, ids_, false);
+    const DestinationPlan dests(order, 0, placement_bandwidths());
+    // Generate on the GPU into the ring, copy into a staging slot, persist.
+    HostBlock staging = HostBlock::allocate(block_bytes_for(max_params_), true);
+    for (const SubgroupId id : order) {
+        Subgroup& sg = subgroups_.at(id);
+        const std::uint64_t pc = sg.param_count;
+        const std::uint64_t ds = seg_stride(pc);
+        float* d = ring_[0];
+        cuda_check(launch_synthetic_state(d, d + ds, d + 2 * ds, pc, param_prefix(seed, id), s_k_),
+                   "synthetic_state");
+        cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+        copy_state(d, staging, pc, false, s_k_);
+        cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+        const TierAssignment a = dests.assign_storage_tier(id);
+        sg.begin_flush();
+        tiers_[static_cast<std::size_t>(a.tier)]->write_from(id, pc, staging);
+        sg.finish_flush(a.tier);
+    }
+}
+
+void OffloadWorker::run_backward_sim(int iteration, std::uint64_t seed, int accum_steps) {
+    if (accum_steps < 1) throw ConfigError("grad_accum_steps must be >= 1");
+    if (!device_ready_) throw Error("run_backward_sim before init_and_flush_all");
+    if (!opt_.skip_gradients)
+        throw ConfigError("skip_gradients=false (fp32 gradients through storage) is not supported by the B200 engine");
+    DeviceGuard dg(dev_.device);
+    for (std::size_t k = 0; k < ids_.size(); ++k) {
+        const SubgroupId id = ids_[k];
+        const std::uint64_t pc = subgroups_.at(id).param_count;
+        for (int step = 0; step < accum_steps; ++step)
+            cuda_check(launch_synthetic_grads(grad_ptr_[k], pc, dev_.grad_kind, grad_prefix(seed, id, iteration, step),
+                                              step > 0, s_k_),
+                       "synthetic_grads");
+    }
+    cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+}
+
+void* OffloadWorker::grad_buffer(SubgroupId id) {
+    if (!device_ready_) throw Error("grad_buffer before init_and_flush_all");
+    return grad_ptr_.at(index_of_.at(id));
+}
+
+void OffloadWorker::bind_grad_buffer(SubgroupId id, void* device_ptr) {
+    if (!device_ready_) throw Error("bind_grad_buffer before init_and_flush_all");
+    if (device_ptr == nullptr) throw ConfigError("bind_grad_buffer: null device pointer");
+    grad_ptr_.at(index_of_.at(id)) = static_cast<std::uint16_t*>(device_ptr);
+}
+
+void* OffloadWorker::params16_buffer(SubgroupId id) {
+    if (!device_ready_) throw Error("params16_buffer before init_and_flush_all");
+    return p16_ptr_.at(index_of_.at(id));
+}
+
+bool OffloadWorker::gradients_finite() {
+    if (!device_ready_) throw Error("gradients_finite before init_and_flush_all");
+    DeviceGuard dg(dev_.device);
+    cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+    for (std::size_t k = 0; k < ids_.size(); ++k)
+        cuda_check(launch_count_nonfinite16(grad_ptr_[k], subgroups_.at(ids_[k]).param_count, dev_.grad_kind,
+                                            sg_counts_ + k, s_k_),
+                   "count_nonfinite");
+    std::vector<unsigned long long> counts(ids_.size());
+    cuda_check(cudaMemcpyAsync(counts.data(), sg_counts_, counts.size() * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s_k_),
+               "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+    for (const auto c : counts)
+        if (c != 0) return false;
+    return true;
+}
+
+// The reference rejects non-finite gradients before mutating a subgroup
+// (precision.hpp:17-25 via scheduler.hpp:467-471). The fused kernel widens
+// and updates in one pass, so the whole phase is checked up front instead:
+// one 2-byte/param read, and no subgroup is mutated when any is bad.
+void OffloadWorker::check_grads_finite_or_throw() {
+    cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+    for (std::size_t k = 0; k < ids_.size(); ++k)
+        cuda_check(launch_count_nonfinite16(grad_ptr_[k], subgroups_.at(ids_[k]).param_count, dev_.grad_kind,
+                                            sg_counts_ + k, s_k_),
+                   "count_nonfinite");
+    std::vector<unsigned long long> counts(ids_.size());
+    cuda_check(cudaMemcpyAsync(counts.data(), sg_counts_, counts.size() * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s_k_),
+               "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+    for (const SubgroupId id : order_)
+        if (counts[index_of_.at(id)] != 0)
+            throw GradientOverflowError("subgroup " + std::to_string(id) +
+                                        ": non-finite gradients reached the update phase");
+}
+
+PhaseStats OffloadWorker::run_update(int iteration) {
+    if (!pool_) throw Error("run_update before init_and_flush_all");
+    DeviceGuard dg(dev_.device);
+    const auto t0 = Clock::now();
+    const AdamConsts c = hyper_.consts(static_cast<std::uint64_t>(iteration) + 1);
+
+    PhaseStats stats;
+    stats.tier_obs.assign(tiers_.size(), TierObservation{});
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        order_ = update_order(iteration, ids_, opt_.enable_caching);
+    }
+    check_grads_finite_or_throw();
+    cuda_check(cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+    std::vector<SubgroupId> order;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        const int cap = opt_.retention_capacity(static_cast<int>(ids_.size()));
+        dests_ = std::make_unique<DestinationPlan>(order_, cap, placement_bandwidths());
+        stats.retained = dests_->retained_count();
+        stats.flush_allocation = dests_->flush_allocation().counts;
+        frontier_ = 0;
+        prefetch_futures_.clear();
+        flush_futures_.clear();
+        cache_hits_this_phase_ = 0;
+        phase_stats_ = &stats;
+        completion_error_ = nullptr;
+        order = order_;
+        pump_locked();
+    }
+
+    try {
+        for (std::size_t j = 0; j < order.size(); ++j) {
+            const SubgroupId id = order[j];
+            const int slot = wait_host_resident(id);
+            issue_device_update(j, id, slot, c);
+            std::lock_guard<std::mutex> g(mu_);
+            Subgroup& sg = subgroups_.at(id);
+            sg.step_count = static_cast<std::uint64_t>(iteration) + 1;
+            stats.params_updated += sg.param_count;
+            stats.h2d_bytes += 12 * sg.param_count;
+            stats.d2h_bytes += 12 * sg.param_count;
+            if (completion_error_) std::rethrow_exception(completion_error_);
+        }
+        // All device updates retire, then the lazy flushes drain.
+        {
+            std::unique_lock<std::mutex> l(mu_);
+            std::uint64_t last = trace_->progress_count();
+            double stalled = 0.0;
+            while (in_flight_ > 0) {
+                if (inflight_cv_.wait_for(l, std::chrono::milliseconds(50)) == std::cv_status::timeout) {
+                    const std::uint64_t p = trace_->progress_count();
+                    if (p != last) {
+                        last = p;
+                        stalled = 0.0;
+                    } else if ((stalled += 0.05) >= opt_.deadlock_timeout_s) {
+                        throw SchedulingBugError("device pipeline made no progress for " +
+                                                 std::to_string(opt_.deadlock_timeout_s) + "s");
+                    }
+                }
+            }
+            if (completion_error_) std::rethrow_exception(completion_error_);
+        }
+        std::vector<std::pair<SubgroupId, std::shared_future<IoStats>>> pending;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            pending = flush_futures_;
+        }
+        for (auto& [fid, fut] : pending) watchdog_wait_value(fut);
+    } catch (...) {
+        std::lock_guard<std::mutex> g(mu_);
+        phase_stats_ = nullptr;
+        throw;
+    }
+
+    unsigned long long counters[2] = {0, 0};
+    cuda_check(cudaMemcpyAsync(counters, counters_, sizeof(counters), cudaMemcpyDeviceToHost, s_k_), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+    stats.downscale_overflows = counters[1];
+    if (counters[0] != 0)
+        throw SchedulingBugError("non-finite gradients reached the fused kernel after the pre-check");
+
+    // Device timeline of the phase.
+    for (const SubgroupId id : order) {
+        const DeviceEvents& e = events_[index_of_.at(id)];
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, e.h2d_start, e.h2d_done) == cudaSuccess) stats.h2d_seconds += ms / 1e3;
+        if (cudaEventElapsedTime(&ms, e.k_start, e.k_end) == cudaSuccess) stats.kernel_seconds += ms / 1e3;
+        if (cudaEventElapsedTime(&ms, e.k_end, e.d2h_end) == cudaSuccess) stats.d2h_seconds += ms / 1e3;
+    }
+    if (!order.empty()) {
+        float ms = 0.0f;
+        if (cudaEventElapsedTime(&ms, events_[index_of_.at(order.front())].h2d_start,
+                                 events_[index_of_.at(order.back())].d2h_end) == cudaSuccess)
+            stats.device_seconds = ms / 1e3;
+    }
+    (void)cudaGetLastError();
+
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        phase_stats_ = nullptr;
+        stats.cache_hits = cache_hits_this_phase_;
+        prefetch_futures_.clear();
+        flush_futures_.clear();
+    }
+    stats.wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
+    if (fixed_ratio_.empty()) est_.update(stats.tier_obs);
+    return stats;
+}
+
+// Enqueue subgroup j on the three pipeline streams. Ring buffer j % K is
+// reused once the D2H of subgroup j - K has drained it.
+void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, const AdamConsts& c) {
+    Subgroup& sg = subgroups_.at(id);
+    const std::uint64_t pc = sg.param_count;
+    const std::size_t k = index_of_.at(id);
+    const std::size_t K = ring_.size();
+    const DeviceEvents& e = events_[k];
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        pool_->begin_update(slot);
+        trace_->record(EventKind::update_start, id_, id, kNoTier, 12 * pc);
+        ++in_flight_;
+    }
+    float* d = ring_[j % K];
+    const std::uint64_t ds = seg_stride(pc);
+    const HostBlock& blk = pool_->block(slot);
+    if (j >= K) cuda_check(cudaStreamWaitEvent(s_h2d_, events_[index_of_.at(order_[j - K])].d2h_end, 0), "wait");
+    cuda_check(cudaEventRecord(e.h2d_start, s_h2d_), "cudaEventRecord");
+    copy_state(d, blk, pc, true, s_h2d_);
+    cuda_check(cudaEventRecord(e.h2d_done, s_h2d_), "cudaEventRecord");
+
+    cuda_check(cudaStreamWaitEvent(s_k_, e.h2d_done, 0), "wait");
+    cuda_check(cudaEventRecord(e.k_start, s_k_), "cudaEventRecord");
+    cuda_check(launch_spin_ns(opt_.update_pad_ns, s_k_), "spin");
+    AdamLaunch a;
+    a.p = d;
+    a.m = d + ds;
+    a.v = d + 2 * ds;
+    a.g = grad_ptr_[k];
+    a.p16 = p16_ptr_[k];
+    a.n = pc;
+    a.grad_kind = dev_.grad_kind;
+    a.out_kind = dev_.out_kind;
+    a.c = c;
+    a.counters = counters_;
+    cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
+    cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
+
+    cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
+    copy_state(d, blk, pc, false, s_d2h_);
+    cuda_check(cudaEventRecord(e.d2h_end, s_d2h_), "cudaEventRecord");
+    auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
+    cuda_check(cudaLaunchHostFunc(s_d2h_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
+}
+
+void CUDART_CB OffloadWorker::host_done(void* arg) {
+    auto* ctx = static_cast<std::pair<OffloadWorker*, Completion>*>(arg);
+    OffloadWorker* w = ctx->first;
+    {
+        std::lock_guard<std::mutex> g(w->cq_mu_);
+        w->cq_.push_back(ctx->second);
+    }
+    w->cq_cv_.notify_one();
+    delete ctx;
+}
+
+void OffloadWorker::completion_loop() {
+    cudaSetDevice(dev_.device);
+    for (;;) {
+        Completion c;
+        {
+            std::unique_lock<std::mutex> l(cq_mu_);
+            cq_cv_.wait(l, [&] { return cq_stop_ || !cq_.empty(); });
+            if (cq_.empty()) return;
+            c = cq_.front();
+            cq_.pop_front();
+        }
+        std::lock_guard<std::mutex> g(mu_);
+        try {
+            Subgroup& sg = subgroups_.at(c.id);
+            pool_->end_update(c.slot);
+            trace_->record(EventKind::update_end, id_, c.id, kNoTier, 12 * sg.param_count);
+            const TierAssignment a = dests_->assign_storage_tier(c.id);
+            if (!a.host_retain) start_flush_locked(c.id, a.tier, c.slot);
+            pump_locked();
+        } catch (...) {
+            if (!completion_error_) completion_error_ = std::current_exception();
+        }
+        --in_flight_;
+        inflight_cv_.notify_all();
+    }
+}
+
+int OffloadWorker::wait_host_resident(SubgroupId id) {
+    std::shared_future<IoStats> fut;
+    {
+        std::unique_lock<std::mutex> l(mu_);
+        for (;;) {
+            Subgroup& sg = subgroups_.at(id);
+            auto it = prefetch_futures_.find(id);
+            if (it != prefetch_futures_.end()) {
+                fut = it->second;
+                break;
+            }
+            if (sg.residency == Residency::host_cached) {
+                ++cache_hits_this_phase_;
+                trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
+                break;
+            }
+            const int slot = pool_->try_reserve(id);
+            if (slot >= 0) {
+                fut = start_prefetch_locked(id, slot);
+                break;
+            }
+            l.unlock();
+            wait_pool_free();
+            l.lock();
+        }
+    }
+    if (fut.valid()) watchdog_wait_value(fut);
+    std::lock_guard<std::mutex> g(mu_);
+    return subgroups_.at(id).slot;
+}
+
+std::shared_future<IoStats> OffloadWorker::enqueue_flush(SubgroupId id, TierId dest) {
+    std::lock_guard<std::mutex> g(mu_);
+    Subgroup& sg = subgroups_.at(id);
+    if (sg.residency != Residency::host_cached || sg.slot < 0) throw Error("enqueue_flush: subgroup not host-resident");
+    return start_flush_locked(id, dest, sg.slot);
+}
+
+std::optional<std::shared_future<IoStats>> OffloadWorker::enqueue_prefetch(SubgroupId id) {
+    std::unique_lock<std::mutex> l(mu_);
+    for (;;) {
+        Subgroup& sg = subgroups_.at(id);
+        auto it = prefetch_futures_.find(id);
+        if (it != prefetch_futures_.end()) return it->second;
+        if (sg.residency == Residency::host_cached) {
+            trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
+            ++cache_hits_this_phase_;
+            return std::nullopt;
+        }
+        const int slot = pool_->try_reserve(id);
+        if (slot >= 0) return start_prefetch_locked(id, slot);
+        l.unlock();
+        wait_pool_free();
+        l.lock();
+    }
+}
+
+void OffloadWorker::read_current_state(SubgroupId id, float* out) {
+    TierId tier;
+    std::uint64_t pc;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        const Subgroup& sg = subgroups_.at(id);
+        pc = sg.param_count;
+        if (sg.residency == Residency::host_cached) {
+            std::memcpy(out, pool_->block(sg.slot).payload(), 12 * pc);
+            return;
+        }
+        if (sg.residency != Residency::on_tier) throw Error("read_current_state: subgroup is in flight");
+        tier = sg.tier;
+    }
+    tiers_[static_cast<std::size_t>(tier)]->read_subgroup(id, pc, out);
+}
+
+Subgroup OffloadWorker::meta(SubgroupId id) {
+    std::lock_guard<std::mutex> g(mu_);
+    return subgroups_.at(id);
+}
+
+std::uint64_t OffloadWorker::total_params() const {
+    std::uint64_t n = 0;
+    for (const auto& [id, sg] : subgroups_) n += sg.param_count;
+    return n;
+}
+
+std::pair<std::uint64_t, std::vector<std::uint64_t>> OffloadWorker::residency_census() {
+    std::lock_guard<std::mutex> g(mu_);
+    std::uint64_t host = 0;
+    std::vector<std::uint64_t> per_tier(tiers_.size(), 0);
+    for (const auto& [id, sg] : subgroups_) {
+        if (sg.residency == Residency::host_cached)
+            host += sg.param_count;
+        else if (sg.residency == Residency::on_tier)
+            per_tier[static_cast<std::size_t>(sg.tier)] += sg.param_count;
+    }
+    return {host, per_tier};
+}
+
+std::vector<SubgroupId> OffloadWorker::current_order() {
+    std::lock_guard<std::mutex> g(mu_);
+    return order_;
+}
+
+// Keeps the prefetch frontier as deep as free slots allow (reference
+// scheduler.hpp:645-659). Called with mu_ held.
+void OffloadWorker::pump_locked() {
+    while (frontier_ < order_.size()) {
+        const SubgroupId id = order_[frontier_];
+        Subgroup& sg = subgroups_.at(id);
+        if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) {
+            ++frontier_;
+            continue;
+        }
+        const int slot = pool_->try_reserve(id);
+        if (slot < 0) break;
+        start_prefetch_locked(id, slot);
+        ++frontier_;
+    }
+}
+
+std::shared_future<IoStats> OffloadWorker::start_prefetch_locked(SubgroupId id, int slot) {
+    Subgroup& sg = subgroups_.at(id);
+    const TierId origin = sg.tier;
+    sg.begin_prefetch();
+    const std::uint64_t pc = sg.param_count;
+    auto tier = tiers_[static_cast<std::size_t>(origin)];
+    HostBufferPool* pool = pool_.get();
+    auto transfer = [tier, id, pc, pool, slot] { return tier->read_into(id, pc, pool->block(slot)); };
+    auto completion = [this, id, slot, origin](bool ok, const IoStats& st) {
+        std::lock_guard<std::mutex> g(mu_);
+        Subgroup& s = subgroups_.at(id);
+        if (ok) {
+            s.finish_prefetch(slot);
+            pool_->prefetch_done(slot);
+            record_read_locked(id, origin, st);
+        } else {
+            s.residency = Residency::on_tier;  // fetch failed: still on its tier
+            s.slot = -1;
+            pool_->release_failed(slot);
+        }
+    };
+    auto fut = io_[static_cast<std::size_t>(origin)]
+                   ->submit(true, id, 12 * pc, std::move(transfer), std::move(completion))
+                   .share();
+    prefetch_futures_[id] = fut;
+    return fut;
+}
+
+std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, TierId dest, int slot) {
+    if (dest < 0 || static_cast<std::size_t>(dest) >= tiers_.size()) throw Error("flush destination out of range");
+    Subgroup& sg = subgroups_.at(id);
+    const TierId origin = sg.tier;  // differs from dest when the allocation shifted
+    sg.begin_flush();
+    pool_->begin_flush(slot);
+    const std::uint64_t pc = sg.param_count;
+    auto tier = tiers_[static_cast<std::size_t>(dest)];
+    HostBufferPool* pool = pool_.get();
+    auto transfer = [tier, id, pc, pool, slot] { return tier->write_from(id, pc, pool->block(slot)); };
+    auto completion = [this, id, slot, dest, origin](bool ok, const IoStats& st) {
+        std::shared_ptr<Tier> stale;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            Subgroup& s = subgroups_.at(id);
+            if (ok) {
+                s.finish_flush(dest);
+                pool_->flush_done(slot);
+                record_write_locked(id, dest, st);
+                if (origin >= 0 && origin != dest) stale = tiers_[static_cast<std::size_t>(origin)];
+                pump_locked();
+            } else {
+                s.residency = Residency::host_cached;  // flush failed: the state stays in its slot
+                pool_->flush_failed(slot);
+            }
+        }
+        if (stale) stale->remove_subgroup(id);
+    };
+    auto fut = io_[static_cast<std::size_t>(dest)]
+                   ->submit(false, id, 12 * pc, std::move(transfer), std::move(completion))
+                   .share();
+    flush_futures_.emplace_back(id, fut);
+    return fut;
+}
+
+void OffloadWorker::record_read_locked(SubgroupId id, TierId tier, const IoStats& st) {
+    if (phase_stats_ == nullptr) return;
+    auto& obs = phase_stats_->tier_obs[static_cast<std::size_t>(tier)];
+    obs.read_transfers += 1;
+    obs.read_bytes += static_cast<double>(st.bytes);
+    obs.read_seconds += st.seconds;
+    auto& io = subgroup_io_entry_locked(id);
+    io.read_seconds += st.seconds;
+    io.fetched = true;
+}
+
+void OffloadWorker::record_write_locked(SubgroupId id, TierId tier, const IoStats& st) {
+    if (phase_stats_ == nullptr) return;
+    auto& obs = phase_stats_->tier_obs[static_cast<std::size_t>(tier)];
+    obs.write_transfers += 1;
+    obs.write_bytes += static_cast<double>(st.bytes);
+    obs.write_seconds += st.seconds;
+    auto& io = subgroup_io_entry_locked(id);
+    io.write_seconds += st.seconds;
+    io.flushed = true;
+}
+
+SubgroupIoTimes& OffloadWorker::subgroup_io_entry_locked(SubgroupId id) {
+    for (auto& e : phase_stats_->subgroup_io)
+        if (e.id == id) return e;
+    SubgroupIoTimes e;
+    e.id = id;
+    e.state_bytes = 12 * subgroups_.at(id).param_count;
+    phase_stats_->subgroup_io.push_back(e);
+    return phase_stats_->subgroup_io.back();
+}
+
+void OffloadWorker::wait_pool_free() {
+    const std::uint64_t start = trace_->progress_count();
+    double waited = 0.0;
+    while (!pool_->wait_for_free(std::chrono::milliseconds(50))) {
+        waited += 0.05;
+        if (trace_->progress_count() != start) return;  // progress elsewhere: re-examine
+        if (waited >= opt_.deadlock_timeout_s)
+            throw SchedulingBugError("host buffer pool made no progress (all slots busy) for " +
+                                     std::to_string(opt_.deadlock_timeout_s) + "s");
+    }
+}
+
+IoStats OffloadWorker::watchdog_wait_value(std::shared_future<IoStats>& fut) {
+    std::uint64_t last = trace_->progress_count();
+    double stalled = 0.0;
+    while (fut.wait_for(std::chrono::milliseconds(50)) != std::future_status::ready) {
+        const std::uint64_t p = trace_->progress_count();
+        if (p != last) {
+            last = p;
+            stalled = 0.0;
+        } else if ((stalled += 0.05) >= opt_.deadlock_timeout_s) {
+            throw SchedulingBugError("pipeline made no trace progress for " + std::to_string(opt_.deadlock_timeout_s) +
+                                     "s");
+        }
+    }
+    return fut.get();
+}
+
+}  // namespace tfb

@@ -1,0 +1,336 @@
+// The B200 update-phase engine: one OffloadWorker per GPU rank.
+//
+// Drop-in for the reference engine's per-iteration API (reference
+// proj/include/tierflow/scheduler.hpp:286-864): tier configuration,
+// add_subgroup partitioning, init_and_flush_all, run_update, the op-level
+// enqueue_prefetch / wait_host_resident / enqueue_flush / read_current_state.
+// Placement, ordering, retention, prefetch frontier and per-tier queue
+// discipline follow the reference rule for rule, so placement, fetch order
+// and cache-hit sequences are bit-identical (SURVEY.md §8a rules 1-5).
+//
+// What is different is where the update runs. A host-resident subgroup's
+// pinned slot is streamed through a ring of device buffers on three CUDA
+// streams: H2D (slot -> HBM) -> fused sm_100a Adam kernel (gradient from the
+// device-resident 16-bit gradient buffer, 16-bit working params written to
+// the device-resident parameter buffer) -> D2H (HBM -> slot). The coordinator
+// never blocks on the GPU: it issues subgroup j and moves on to j+1; a
+// completion thread retires finished subgroups (slot back to cached, lazy
+// flush or retention, frontier pump) exactly where the reference's
+// coordinator would after adam_step returns.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <condition_variable>
+#include <deque>
+#include <filesystem>
+#include <functional>
+#include <future>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+#include "host_block.hpp"
+#include "placement.hpp"
+#include "tier.hpp"
+#include "trace.hpp"
+#include "types.hpp"
+
+namespace tfb {
+
+struct ScheduleOptions {
+    int pool_slots = 4;
+    int cache_slots = -1;         // host retention capacity C; -1 derives pool_slots - 3
+    bool enable_caching = true;   // alternating order + host retention
+    bool skip_gradients = true;   // delayed 16-bit -> fp32 gradient conversion (fused in the kernel)
+    bool atomic_rw = true;        // tier semaphores around transfers
+    bool multi_path = true;       // place across all tiers vs tier 0 only
+    std::string lock_dir;
+    int update_threads = 1;       // accepted for API parity; the update runs on the GPU
+    double deadlock_timeout_s = 30.0;
+    std::uint64_t update_pad_ns = 0;  // synthetic extra device time per subgroup update
+
+    int retention_capacity(int subgroup_count) const {
+        return tfb::retention_capacity(enable_caching, pool_slots, cache_slots, subgroup_count);
+    }
+};
+
+struct AdamHyper {
+    double lr = 1e-3;
+    double beta1 = 0.9;
+    double beta2 = 0.999;
+    double eps = 1e-8;
+    double weight_decay = 0.0;
+
+    void validate() const;  // reference optimizer.hpp:24-30
+    AdamConsts consts(std::uint64_t t) const;
+};
+
+struct DeviceOptions {
+    int device = 0;
+    int grad_kind = kF16;    // 16-bit gradient element kind
+    int out_kind = kF16;     // 16-bit working-parameter element kind
+    int device_buffers = 3;  // depth of the H2D -> kernel -> D2H ring
+};
+
+enum class Residency : int { host_cached = 0, in_flight = 1, on_tier = 2 };
+
+struct Subgroup {
+    SubgroupId id = 0;
+    std::uint64_t param_count = 0;
+    Residency residency = Residency::host_cached;
+    TierId tier = kNoTier;
+    int slot = -1;
+    std::uint64_t step_count = 0;
+
+    // host_cached -> in_flight -> on_tier -> in_flight -> host_cached
+    // (reference optimizer.hpp:47-72).
+    void begin_flush();
+    void finish_flush(TierId dest);
+    void begin_prefetch();
+    void finish_prefetch(int pool_slot);
+};
+
+struct SubgroupIoTimes {
+    SubgroupId id = 0;
+    std::uint64_t state_bytes = 0;
+    double read_seconds = 0.0;
+    double write_seconds = 0.0;
+    bool fetched = false;
+    bool flushed = false;
+};
+
+struct PhaseStats {
+    double wall_seconds = 0.0;
+    std::uint64_t params_updated = 0;
+    std::uint64_t cache_hits = 0;
+    std::uint64_t downscale_overflows = 0;
+    int retained = 0;
+    std::vector<int> flush_allocation;
+    std::vector<TierObservation> tier_obs;
+    std::vector<SubgroupIoTimes> subgroup_io;
+    // Device side (CUDA events on the pipeline streams).
+    double device_seconds = 0.0;  // first H2D start -> last D2H end
+    double kernel_seconds = 0.0;  // sum of fused-kernel durations
+    double h2d_seconds = 0.0;     // sum of state H2D durations
+    double d2h_seconds = 0.0;     // sum of state D2H durations
+    std::uint64_t h2d_bytes = 0;
+    std::uint64_t d2h_bytes = 0;
+};
+
+// ---------------------------------------------------------------------------
+// Pinned staging slots with the reference slot state machine
+// (free -> prefetching -> cached -> updating -> cached -> flushing -> free;
+// reference pool.hpp:17-161). Each slot owns one HostBlock.
+enum class SlotState : int { free_slot = 0, prefetching, updating, flushing, cached };
+
+const char* slot_state_name(SlotState s);
+
+class HostBufferPool {
+public:
+    HostBufferPool(int slot_count, std::uint64_t max_params, bool require_pinned);
+
+    int slot_count() const { return static_cast<int>(slots_.size()); }
+    int try_reserve(SubgroupId owner);
+    int find_cached(SubgroupId owner) const;
+    void prefetch_done(int slot) { transition(slot, SlotState::prefetching, SlotState::cached); }
+    void begin_update(int slot) { transition(slot, SlotState::cached, SlotState::updating); }
+    void end_update(int slot) { transition(slot, SlotState::updating, SlotState::cached); }
+    void begin_flush(int slot) { transition(slot, SlotState::cached, SlotState::flushing); }
+    void flush_done(int slot);
+    void flush_failed(int slot) { transition(slot, SlotState::flushing, SlotState::cached); }
+    void evict(int slot);
+    void release_failed(int slot);
+    SlotState state(int slot) const;
+    SubgroupId owner(int slot) const;
+    int count(SlotState s) const;
+    bool wait_for_free(std::chrono::milliseconds timeout);
+    // The block is owned by whoever holds the slot in a non-free state.
+    HostBlock& block(int slot) { return slots_[check(slot)].block; }
+
+private:
+    struct Slot {
+        SlotState state = SlotState::free_slot;
+        SubgroupId owner = 0;
+        HostBlock block;
+    };
+    std::size_t check(int slot) const;
+    void transition(int slot, SlotState expected, SlotState next);
+
+    mutable std::mutex mu_;
+    std::condition_variable free_cv_;
+    std::vector<Slot> slots_;
+};
+
+// ---------------------------------------------------------------------------
+// One I/O thread per (worker, tier); pending prefetches drain before pending
+// flushes; each job runs under the tier semaphore when atomic_rw is on
+// (reference scheduler.hpp:142-266).
+class TierIoWorker {
+public:
+    using Completion = std::function<void(bool ok, const IoStats&)>;
+
+    TierIoWorker(std::shared_ptr<Tier> tier, WorkerId worker, bool use_lock, std::filesystem::path lock_dir,
+                 EventTrace* trace);
+    ~TierIoWorker();
+
+    std::future<IoStats> submit(bool is_prefetch, std::int64_t sg, std::uint64_t bytes_hint,
+                                std::function<IoStats()> transfer, Completion completion);
+    void shutdown();
+
+private:
+    struct Job {
+        bool is_prefetch = false;
+        std::int64_t sg = -1;
+        std::uint64_t bytes_hint = 0;
+        std::function<IoStats()> transfer;
+        Completion completion;
+        std::promise<IoStats> promise;
+    };
+    void run();
+    void execute(Job& job);
+
+    std::shared_ptr<Tier> tier_;
+    WorkerId worker_;
+    bool use_lock_;
+    std::filesystem::path lock_dir_;
+    EventTrace* trace_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Job> prefetch_q_;
+    std::deque<Job> flush_q_;
+    bool stop_ = false;
+    std::thread thread_;
+};
+
+// ---------------------------------------------------------------------------
+
+class OffloadWorker {
+public:
+    OffloadWorker(WorkerId id, std::vector<std::shared_ptr<Tier>> tiers, ScheduleOptions opt, AdamHyper hyper,
+                  std::shared_ptr<EventTrace> trace, DeviceOptions dev);
+    ~OffloadWorker();
+    OffloadWorker(const OffloadWorker&) = delete;
+    OffloadWorker& operator=(const OffloadWorker&) = delete;
+
+    WorkerId id() const { return id_; }
+    void set_alpha(double alpha);
+    void set_fixed_ratio(std::vector<double> ratio);
+    void add_subgroup(SubgroupId id, std::uint64_t param_count);
+
+    // Seeded fp32 states (synthetic_param_init, zero moments) generated on the
+    // GPU and flushed to the tiers Eq. 1 picks; every subgroup ends on_tier.
+    void init_and_flush_all(std::uint64_t seed);
+
+    // Backward stand-in: seeded 16-bit gradients generated on the GPU into the
+    // device gradient buffers (SyntheticGradSource + GradBufferF16 semantics).
+    void run_backward_sim(int iteration, std::uint64_t seed, int accum_steps);
+    bool gradients_finite();
+    // Device gradient buffer of a subgroup (param_count 16-bit elements); the
+    // caller may fill it (e.g. from a reduce-scatter) or rebind it.
+    void* grad_buffer(SubgroupId id);
+    void bind_grad_buffer(SubgroupId id, void* device_ptr);
+    void* params16_buffer(SubgroupId id);
+
+    PhaseStats run_update(int iteration);
+
+    int wait_host_resident(SubgroupId id);
+    std::shared_future<IoStats> enqueue_flush(SubgroupId id, TierId dest);
+    std::optional<std::shared_future<IoStats>> enqueue_prefetch(SubgroupId id);
+    void read_current_state(SubgroupId id, float* out);
+
+    const std::vector<SubgroupId>& subgroup_ids() const { return ids_; }
+    Subgroup meta(SubgroupId id);
+    std::uint64_t total_params() const;
+    std::pair<std::uint64_t, std::vector<std::uint64_t>> residency_census();
+    const BandwidthEstimate& estimates() const { return est_; }
+    std::vector<SubgroupId> current_order();
+    const ScheduleOptions& options() const { return opt_; }
+    HostBufferPool& pool() { return *pool_; }
+    const DeviceOptions& device_options() const { return dev_; }
+
+    // Watchdog-guarded wait on an I/O future (rethrows tier errors).
+    IoStats watchdog_wait_value(std::shared_future<IoStats>& fut);
+
+private:
+    struct DeviceEvents {
+        cudaEvent_t h2d_start = nullptr, h2d_done = nullptr, k_start = nullptr, k_end = nullptr, d2h_end = nullptr;
+    };
+    struct Completion {
+        SubgroupId id;
+        int slot;
+    };
+
+    std::vector<double> placement_bandwidths() const;
+    void pump_locked();
+    std::shared_future<IoStats> start_prefetch_locked(SubgroupId id, int slot);
+    std::shared_future<IoStats> start_flush_locked(SubgroupId id, TierId dest, int slot);
+    void record_read_locked(SubgroupId id, TierId tier, const IoStats& st);
+    void record_write_locked(SubgroupId id, TierId tier, const IoStats& st);
+    SubgroupIoTimes& subgroup_io_entry_locked(SubgroupId id);
+    void wait_pool_free();
+
+    void setup_device();
+    void release_device();
+    void issue_device_update(std::size_t j, SubgroupId id, int slot, const AdamConsts& c);
+    void copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device, cudaStream_t s);
+    void completion_loop();
+    static void CUDART_CB host_done(void* arg);
+    void check_grads_finite_or_throw();
+
+    WorkerId id_;
+    std::vector<std::shared_ptr<Tier>> tiers_;
+    ScheduleOptions opt_;
+    AdamHyper hyper_;
+    std::shared_ptr<EventTrace> trace_;
+    DeviceOptions dev_;
+
+    std::vector<std::unique_ptr<TierIoWorker>> io_;
+    std::unique_ptr<HostBufferPool> pool_;
+    std::unordered_map<SubgroupId, Subgroup> subgroups_;
+    std::vector<SubgroupId> ids_;
+    std::uint64_t max_params_ = 0;
+
+    BandwidthEstimate est_;
+    std::vector<double> fixed_ratio_;
+
+    std::mutex mu_;
+    std::vector<SubgroupId> order_;
+    std::unique_ptr<DestinationPlan> dests_;
+    std::size_t frontier_ = 0;
+    std::unordered_map<SubgroupId, std::shared_future<IoStats>> prefetch_futures_;
+    std::vector<std::pair<SubgroupId, std::shared_future<IoStats>>> flush_futures_;
+    PhaseStats* phase_stats_ = nullptr;
+    std::uint64_t cache_hits_this_phase_ = 0;
+
+    // Device resources.
+    bool device_ready_ = false;
+    cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr;
+    std::vector<float*> ring_;
+    std::uint64_t ring_stride_ = 0;  // floats per segment (P, m, v each) in a ring buffer
+    void* grad_arena_ = nullptr;
+    void* p16_arena_ = nullptr;
+    unsigned long long* counters_ = nullptr;  // [0] non-finite grads, [1] narrowing overflows
+    unsigned long long* sg_counts_ = nullptr; // per-subgroup non-finite counts (pre-check)
+    std::unordered_map<SubgroupId, std::size_t> index_of_;
+    std::vector<std::uint16_t*> grad_ptr_;
+    std::vector<std::uint16_t*> p16_ptr_;
+    std::vector<DeviceEvents> events_;
+
+    // Completion thread: retires subgroups whose D2H finished.
+    std::thread completer_;
+    std::mutex cq_mu_;
+    std::condition_variable cq_cv_;
+    std::deque<Completion> cq_;
+    bool cq_stop_ = false;
+    std::size_t in_flight_ = 0;  // guarded by mu_
+    std::condition_variable inflight_cv_;
+    std::exception_ptr completion_error_;
+};
+
+}  // namespace tfb

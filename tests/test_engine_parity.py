@@ -1,0 +1,295 @@
+"""The B200 update engine against the reference engine (golden fixtures from
+the unmodified reference, tests/golden/make_golden.py) and the oracle (-m gpu).
+
+Bit-exact: cache-hit counts and ids, per-tier prefetch order, per-tier flush
+sets, flush allocations, retained counts and the final P/m/v bits. The
+scenarios mirror the reference's test_scheduler.cpp."""
+import ast
+import hashlib
+import threading
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def make_engine(tf, tiers_cfg, params, *, pool_slots=4, cache_slots=-1, ratio=None, seed=42, lock_dir="",
+                wd=0.0, device_buffers=3, grad_dtype=0, param_dtype=0, deadlock=30.0, pad_ns=0, caching=True,
+                multi_path=True):
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(i, *cfg)) for i, cfg in enumerate(tiers_cfg)]
+    opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=lock_dir,
+                             deadlock_timeout_s=deadlock, update_pad_ns=pad_ns, enable_caching=caching,
+                             multi_path=multi_path)
+    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(weight_decay=wd), trace,
+                         tf.DeviceOptions(0, grad_dtype, param_dtype, device_buffers))
+    if ratio is not None:
+        w.set_fixed_ratio(ratio)
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    return w, trace, tiers
+
+
+def mem(rate_r, rate_w):
+    return (2, "mem", rate_r, rate_w)
+
+
+def run_golden(tf, golden, run, lock_dir, device_buffers=3):
+    cfg = golden[f"run_{run}_config"]
+    M, nt, pool, cache, seed, iters, accum, skip = (int(x) for x in cfg)
+    params = golden[f"run_{run}_params"].tolist()
+    rates = {"hits": [(500e6, 500e6), (250e6, 250e6)], "ragged": [(300e6, 300e6), (200e6, 200e6), (100e6, 100e6)],
+             "skip": [(400e6, 400e6), (200e6, 200e6)]}[run]
+    w, trace, tiers = make_engine(tf, [mem(*r) for r in rates], params, pool_slots=pool, cache_slots=cache,
+                                  ratio=golden[f"run_{run}_ratio"].tolist(), seed=seed, lock_dir=lock_dir,
+                                  wd=float(golden[f"run_{run}_wd"][0]), device_buffers=device_buffers)
+    stats, seqs = [], []
+    for it in range(iters):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed), accum)
+        if (skip >> it) & 1:
+            stats.append(None)
+            seqs.append({"hits": [], "prefetch": [[] for _ in range(nt)], "flush": [[] for _ in range(nt)]})
+            continue
+        mark = trace.size()
+        st = w.run_update(it)
+        ev = [(int(e.kind), e.subgroup_id, e.tier_id, e.bytes) for e in trace.snapshot(mark)]
+        seqs.append(oracle.phase_sequences(ev, 0, len(ev), nt))
+        stats.append(st)
+    return w, trace, stats, seqs, params, iters
+
+
+@pytest.mark.parametrize("run", ["hits", "ragged", "skip"])
+def test_sequences_and_state_match_reference_engine(tf, cuda, golden, lock_dir, run):
+    w, trace, stats, seqs, params, iters = run_golden(tf, golden, run, lock_dir)
+    want_seqs = [ast.literal_eval(s) for s in golden[f"run_{run}_seqs"]]
+    for it in range(iters):
+        assert seqs[it] == want_seqs[it], f"iteration {it}"
+        if stats[it] is None:
+            continue
+        assert stats[it].cache_hits == golden[f"run_{run}_hits"][it]
+        assert stats[it].retained == golden[f"run_{run}_retained"][it]
+        assert stats[it].flush_allocation == golden[f"run_{run}_alloc"][it].tolist()
+        assert stats[it].downscale_overflows == golden[f"run_{run}_overflows"][it]
+        assert stats[it].params_updated == sum(params)
+    if run == "hits":
+        assert [s.cache_hits for s in stats] == [0, 4, 4, 4]
+        for i in range(len(params)):
+            d = hashlib.sha256(w.read_current_state(i).tobytes()).hexdigest()
+            assert d == golden["run_hits_digest"][i], f"subgroup {i}"
+    else:
+        ref = golden[f"run_{run}_states"]
+        off = 0
+        for i, n in enumerate(params):
+            got = w.read_current_state(i)
+            assert np.array_equal(got.view(np.uint32), ref[off:off + 3 * n].view(np.uint32)), f"subgroup {i}"
+            # device working params = RNE(P) of the final state
+            assert np.array_equal(w.read_params16(i), oracle.f32_to_f16(got[:n]))
+            off += 3 * n
+    w.close()
+
+
+@pytest.mark.parametrize("ring", [1, 2, 5])
+def test_ring_depth_does_not_change_bits(tf, cuda, golden, lock_dir, ring):
+    w, _, _, _, params, _ = run_golden(tf, golden, "ragged", lock_dir, device_buffers=ring)
+    ref = golden["run_ragged_states"]
+    off = 0
+    for i, n in enumerate(params):
+        assert np.array_equal(w.read_current_state(i).view(np.uint32), ref[off:off + 3 * n].view(np.uint32))
+        off += 3 * n
+    w.close()
+
+
+def test_exactly_once_and_no_self_overlap(tf, cuda, lock_dir):
+    w, trace, _ = make_engine(tf, [mem(250e6, 250e6), mem(125e6, 125e6)], [350_000] * 8, pool_slots=4,
+                              lock_dir=lock_dir, pad_ns=8_000_000)
+    w.run_backward_sim(0, tf.SyntheticGradSource(3))
+    w.run_update(0)
+    ev = trace.snapshot()
+    iv = {}
+    for kind_s, kind_e in [("prefetch_start", "prefetch_end"), ("update_start", "update_end"),
+                           ("flush_start", "flush_end")]:
+        opened, out = {}, []
+        for e in ev:
+            if e.kind == tf.EventKind[kind_s]:
+                opened[e.subgroup_id] = e.timestamp_ns
+            elif e.kind == tf.EventKind[kind_e]:
+                out.append((opened.pop(e.subgroup_id), e.timestamp_ns, e.subgroup_id))
+        assert not opened
+        iv[kind_s] = out
+    ups = iv["update_start"]
+    assert sorted(u[2] for u in ups) == list(range(8))  # exactly once
+    ov = lambda a, b: max(a[0], b[0]) < min(a[1], b[1])
+    for u in ups:
+        for x in iv["prefetch_start"] + iv["flush_start"]:
+            if x[2] == u[2]:
+                assert not ov(u, x)
+    three = any(ov(u, p) and ov(u, f) and max(u[0], p[0], f[0]) < min(u[1], p[1], f[1])
+                for u in ups for p in iv["prefetch_start"] for f in iv["flush_start"])
+    assert three, "prefetch, update and flush never simultaneously in flight"
+    w.close()
+
+
+def test_nonfinite_gradient_rejects_phase_without_mutation(tf, cuda, lock_dir):
+    import torch
+    n = 10_000
+    w, trace, _ = make_engine(tf, [mem(800e6, 800e6)], [n] * 3, pool_slots=3, lock_dir=lock_dir)
+    w.run_backward_sim(0, tf.SyntheticGradSource(29))
+    before = [w.read_current_state(i) for i in range(3)]
+    g16 = oracle.synthetic_grads(n, 29, 1, 0)
+    g16[77] = 0x7C00
+    bad = torch.from_numpy(g16.view(np.int16)).cuda()
+    w.bind_grad_buffer(1, bad.data_ptr())
+    assert not w.gradients_finite()
+    with pytest.raises(tf.GradientOverflowError):
+        w.run_update(0)
+    for i in range(3):
+        assert np.array_equal(w.read_current_state(i), before[i])
+    # the harness skips the step; iteration 1 proceeds (Adam t = 2, parity key 1)
+    g16[77] = 0
+    good = torch.from_numpy(g16.view(np.int16)).cuda()
+    w.bind_grad_buffer(1, good.data_ptr())
+    assert w.gradients_finite()
+    st = w.run_update(1)
+    assert st.params_updated == 3 * n
+    p0 = oracle.synthetic_params(n, 42, 1)
+    want = oracle.adam_fused(p0, np.zeros(n, np.float32), np.zeros(n, np.float32), g16, 0, 0, 2)
+    assert np.array_equal(w.read_current_state(1).view(np.uint32), np.concatenate(want[:3]).view(np.uint32))
+    w.close()
+
+
+def test_prefetch_of_retained_subgroup_is_cache_hit(tf, cuda, lock_dir):
+    # test_scheduler.cpp:459-476
+    w, trace, _ = make_engine(tf, [mem(800e6, 800e6)], [10_000] * 2, pool_slots=4, lock_dir=lock_dir)
+    w.run_backward_sim(0, tf.SyntheticGradSource(23))
+    w.run_update(0)
+    assert w.meta(1).residency == tf.Residency.host_cached
+    mark = trace.size()
+    assert w.enqueue_prefetch(1) is None
+    assert any(e.kind == tf.EventKind.cache_hit and e.subgroup_id == 1 for e in trace.snapshot(mark))
+    w.close()
+
+
+def test_never_enqueued_subgroup_fetched_on_demand(tf, cuda, lock_dir):
+    # test_scheduler.cpp:522-535
+    w, trace, _ = make_engine(tf, [mem(400e6, 400e6)], [20_000] * 2, pool_slots=3, lock_dir=lock_dir)
+    assert w.meta(1).residency == tf.Residency.on_tier
+    assert w.wait_host_resident(1) >= 0
+    assert w.meta(1).residency == tf.Residency.host_cached
+    assert any(e.kind == tf.EventKind.prefetch_end and e.subgroup_id == 1 for e in trace.snapshot())
+    w.close()
+
+
+def test_queued_flush_defers_until_lock_release(tf, cuda, lock_dir):
+    # test_scheduler.cpp:409-435
+    w, trace, _ = make_engine(tf, [mem(800e6, 800e6)], [20_000], pool_slots=3, lock_dir=lock_dir)
+    w.enqueue_prefetch(0).get()
+    guard = tf.acquire_tier_lock(lock_dir, 0, 99, trace)
+    fl = w.enqueue_flush(0, 0)
+    time.sleep(0.08)
+    released = time.monotonic_ns()
+    guard.release()
+    fl.get()
+    start = [e.timestamp_ns for e in trace.snapshot() if e.kind == tf.EventKind.flush_start and e.subgroup_id == 0]
+    assert start and start[0] >= released
+    w.close()
+
+
+def test_flushes_to_distinct_tiers_overlap(tf, cuda, lock_dir):
+    # test_scheduler.cpp:437-457
+    w, trace, _ = make_engine(tf, [mem(150e6, 150e6), mem(150e6, 150e6)], [350_000] * 2, pool_slots=4,
+                              lock_dir=lock_dir)
+    for i in (0, 1):
+        t = w.enqueue_prefetch(i)
+        if t:
+            t.get()
+    mark = trace.size()
+    f0, f1 = w.enqueue_flush(0, 0), w.enqueue_flush(1, 1)
+    f0.get()
+    f1.get()
+    ev = trace.snapshot(mark)
+    iv = {}
+    for e in ev:
+        if e.kind == tf.EventKind.flush_start:
+            iv[e.subgroup_id] = [e.timestamp_ns, None, e.tier_id]
+        elif e.kind == tf.EventKind.flush_end:
+            iv[e.subgroup_id][1] = e.timestamp_ns
+    a, b = iv[0], iv[1]
+    assert a[2] != b[2] and max(a[0], b[0]) < min(a[1], b[1])
+    w.close()
+
+
+def test_wedged_pipeline_trips_watchdog(tf, cuda, lock_dir):
+    # test_scheduler.cpp:537-550
+    w, trace, _ = make_engine(tf, [mem(800e6, 800e6)], [10_000], pool_slots=3, lock_dir=lock_dir, deadlock=0.4)
+    w.run_backward_sim(0, tf.SyntheticGradSource(29))
+    guard = tf.TierLockGuard(lock_dir, 0, 98, trace)
+    with pytest.raises(tf.SchedulingBugError):
+        w.run_update(0)
+    guard.release()
+    time.sleep(0.2)
+    w.close()
+
+
+def test_dram_and_directory_tiers_zero_copy_path(tf, cuda, lock_dir, tmp_path):
+    """The B200 fast path: host_dram (block exchange) + local_dir (O_DIRECT
+    into pinned slots), ragged sizes; end state equals the oracle bitwise and
+    the on-disk files stay v1."""
+    params = [100_003, 100_000, 64_001, 100_000, 99_999]
+    tiers = [(3, "dram", 20e9, 20e9), (0, str(tmp_path / "nvme"), 3e9, 2e9)]
+    w, trace, tier_objs = make_engine(tf, tiers, params, pool_slots=5, ratio=[2.0, 1.0], seed=11, lock_dir=lock_dir,
+                                      wd=0.01)
+    iters = 4
+    for it in range(iters):
+        w.run_backward_sim(it, tf.SyntheticGradSource(11), 1)
+        st = w.run_update(it)
+        assert st.params_updated == sum(params)
+        assert st.h2d_bytes == 12 * sum(params) and st.kernel_seconds > 0
+    states, (order, hit, dest, origin) = oracle.run_engine_oracle(params, 11, iters, 5, -1, True, True, [2.0, 1.0],
+                                                                  weight_decay=0.01)
+    for i, n in enumerate(params):
+        got = w.read_current_state(i)
+        want = np.concatenate(states[i][:3])
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), f"subgroup {i}"
+        assert np.array_equal(w.read_params16(i), states[i][3])
+    on_disk = [i for i in range(len(params)) if w.meta(i).residency == tf.Residency.on_tier and w.meta(i).tier == 1]
+    for i in on_disk:
+        raw = (tmp_path / "nvme" / f"sg_{i:06d}.bin").read_bytes()
+        assert raw[:4] == b"OPLM" and len(raw) == 32 + 12 * params[i]
+    w.close()
+
+
+def test_bf16_engine_matches_oracle(tf, cuda, lock_dir):
+    params = [50_000, 33_333]
+    w, _, _ = make_engine(tf, [mem(2e9, 2e9)], params, pool_slots=4, seed=3, lock_dir=lock_dir, grad_dtype=1,
+                          param_dtype=1)
+    for it in range(3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(3), 2)
+        w.run_update(it)
+    states, _ = oracle.run_engine_oracle(params, 3, 3, 4, -1, True, True, [1.0], accum_steps=2, grad_kind=1,
+                                         out_kind=1)
+    for i in range(2):
+        assert np.array_equal(w.read_current_state(i).view(np.uint32),
+                              np.concatenate(states[i][:3]).view(np.uint32))
+        assert np.array_equal(w.read_params16(i), states[i][3])
+    w.close()
+
+
+def test_external_gradient_buffer_binding(tf, cuda, lock_dir):
+    """A caller-owned device gradient buffer (e.g. a reduce-scatter output)."""
+    import torch
+    n = 40_000
+    w, _, _ = make_engine(tf, [mem(2e9, 2e9)], [n], pool_slots=3, seed=8, lock_dir=lock_dir)
+    g16 = oracle.synthetic_grads(n, 123, 0, 0)
+    buf = torch.from_numpy(g16.view(np.int16)).cuda()
+    w.bind_grad_buffer(0, buf.data_ptr())
+    w.run_update(0)
+    p0 = oracle.synthetic_params(n, 8, 0)
+    want = oracle.adam_fused(p0, np.zeros(n, np.float32), np.zeros(n, np.float32), g16, 0, 0, 1)
+    got = w.read_current_state(0)
+    assert np.array_equal(got.view(np.uint32), np.concatenate(want[:3]).view(np.uint32))
+    w.close()

@@ -1,0 +1,193 @@
+"""sm_100a kernels against the CPU oracle, bit for bit (-m gpu).
+
+Tolerance: none. P, m, v and the 16-bit working params are compared as raw
+bits; overflow and non-finite counts exactly. (north_star allows 1e-6 relative
+on P/m/v and 1 ulp on 16-bit params; the kernel meets the stronger bar.)"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _dev(torch, a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _u16(torch, a, dev):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int16)).to(dev)
+
+
+def _np16(t):
+    return t.cpu().numpy().view(np.uint16)
+
+
+def run_fused(tf, torch, dev, p, m, v, g16, t, gk=0, ok=0, wd=0.0, contiguous=False):
+    n = p.size
+    counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    p16 = torch.zeros(n, dtype=torch.int16, device=dev)
+    hy = tf.AdamHyper(weight_decay=wd)
+    if contiguous:
+        st = _dev(torch, np.concatenate([p, m, v]), dev)
+        g = _u16(torch, g16, dev)
+        import ctypes as C
+        from paper_2509_02480_b200 import _lib
+        h = hy.c()
+        _lib.call("tfg_adam_fused_contiguous", st.data_ptr(), n, g.data_ptr(), gk, p16.data_ptr(), ok, C.byref(h), t,
+                  counters.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        s = st.cpu().numpy()
+        return s[:n], s[n:2 * n], s[2 * n:], _np16(p16), counters.cpu().numpy()
+    P, Mm, V, G = _dev(torch, p, dev), _dev(torch, m, dev), _dev(torch, v, dev), _u16(torch, g16, dev)
+    tf.adam_fused(P, Mm, V, G, p16, t, hy, gk, ok, counters=counters)
+    torch.cuda.synchronize()
+    return P.cpu().numpy(), Mm.cpu().numpy(), V.cpu().numpy(), _np16(p16), counters.cpu().numpy()
+
+
+def assert_bits(a, b, what):
+    a32, b32 = np.asarray(a).view(np.uint32), np.asarray(b).view(np.uint32)
+    bad = np.flatnonzero(a32 != b32)
+    assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[:5]}: {a[bad[:3]]} vs {b[bad[:3]]}"
+
+
+def test_golden_vectors(tf, cuda, golden):
+    import torch
+    for k in range(int(golden["adam_cases"][0])):
+        n, t, wd, over = golden[f"adam{k}_meta"]
+        for contiguous in (False, True):
+            p, m, v, p16, cnt = run_fused(tf, torch, cuda, golden[f"adam{k}_p"], golden[f"adam{k}_m"],
+                                          golden[f"adam{k}_v"], golden[f"adam{k}_g16"], int(t), wd=wd,
+                                          contiguous=contiguous)
+            assert_bits(p, golden[f"adam{k}_p_out"], f"case {k} P")
+            assert_bits(m, golden[f"adam{k}_m_out"], f"case {k} m")
+            assert_bits(v, golden[f"adam{k}_v_out"], f"case {k} v")
+            assert np.array_equal(p16, golden[f"adam{k}_p16"])
+            assert cnt[0] == 0 and cnt[1] == int(over)
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 1023, 4096, 65537, 1 << 20, 3_000_001])
+@pytest.mark.parametrize("gk,ok", [(0, 0), (0, 1), (1, 1), (1, 0)])
+def test_random_sizes_and_dtypes(tf, cuda, n, gk, ok):
+    import torch
+    rng = np.random.default_rng(n * 7 + gk * 3 + ok)
+    p = rng.uniform(-2, 2, n).astype(np.float32)
+    m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+    v = rng.uniform(0, 0.01, n).astype(np.float32)
+    g16 = oracle.synthetic_grads(n, 42, n % 97, 3, kind=gk)
+    for t, wd in [(1, 0.0), (5, 0.01)]:
+        want = oracle.adam_fused(p, m, v, g16, gk, ok, t, weight_decay=wd)
+        got = run_fused(tf, torch, cuda, p, m, v, g16, t, gk, ok, wd)
+        assert_bits(got[0], want[0], "P")
+        assert_bits(got[1], want[1], "m")
+        assert_bits(got[2], want[2], "v")
+        assert np.array_equal(got[3], want[3])
+        assert got[4][0] == 0 and got[4][1] == want[4]
+
+
+def test_extreme_values(tf, cuda):
+    """Subnormal moments, huge params overflowing 16-bit, zero grads, signed zeros."""
+    import torch
+    n = 8192
+    rng = np.random.default_rng(1)
+    p = np.concatenate([rng.uniform(-1e5, 1e5, n // 4), rng.uniform(-1e-30, 1e-30, n // 4),
+                        np.full(n // 4, 65519.9, np.float32), np.array([0.0, -0.0] * (n // 8))]).astype(np.float32)
+    m = np.concatenate([np.full(n // 2, 1e-40), rng.uniform(-1, 1, n // 2)]).astype(np.float32)
+    v = np.concatenate([np.full(n // 2, 1e-44), rng.uniform(0, 1e-3, n // 2)]).astype(np.float32)
+    g16 = np.concatenate([np.zeros(n // 4, np.uint16), np.full(n // 4, 0x8000, np.uint16),
+                          oracle.f32_to_f16(rng.uniform(-60000, 60000, n // 2).astype(np.float32))])
+    for t in (1, 2, 100, 10**6):
+        for ok in (0, 1):
+            want = oracle.adam_fused(p, m, v, g16, 0, ok, t, weight_decay=0.001)
+            got = run_fused(tf, torch, cuda, p, m, v, g16, t, 0, ok, 0.001)
+            for i in range(3):
+                assert_bits(got[i], want[i], f"t={t} slot {i}")
+            assert np.array_equal(got[3], want[3]) and got[4][1] == want[4]
+            assert want[4] > 0  # the fixture does exercise the overflow counter
+
+
+def test_nonfinite_gradients_are_counted_and_step_rejected(tf, cuda):
+    import torch
+    n = 1000
+    g16 = oracle.synthetic_grads(n, 1, 0, 0)
+    g16[17] = 0x7C00
+    g16[500] = 0x7E01
+    p = np.ones(n, np.float32)
+    _, _, _, _, cnt = run_fused(tf, torch, cuda, p, p * 0, p * 0, g16, 1)
+    assert cnt[0] == 2
+    # reference semantics (optimizer.hpp:123-127): reject before mutating
+    P = torch.ones(n, device=cuda)
+    Mm, V = torch.zeros(n, device=cuda), torch.zeros(n, device=cuda)
+    G = _u16(torch, g16, cuda)
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    with pytest.raises(tf.GradientOverflowError):
+        tf.adam_step(P, Mm, V, G, p16, 1)
+    assert bool((P == 1).all()) and bool((Mm == 0).all())
+    with pytest.raises(tf.Error):
+        tf.adam_step(P, Mm, V, G, p16, 0)  # t >= 1
+    with pytest.raises(tf.ConfigError):
+        tf.adam_step(P, Mm, V, G, p16, 1, tf.AdamHyper(beta1=1.0))
+
+
+def test_adam_step_returns_overflows(tf, cuda):
+    import torch
+    n = 100
+    P = torch.full((n,), 70000.0, device=cuda)
+    Mm, V = torch.zeros(n, device=cuda), torch.zeros(n, device=cuda)
+    G = torch.zeros(n, dtype=torch.int16, device=cuda)
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    assert tf.adam_step(P, Mm, V, G, p16, 1) == n
+
+
+def test_synthetic_generators_bitwise(tf, cuda, golden):
+    import torch
+    for sg, it, steps in [(0, 0, 1), (3, 5, 1), (11, 2, 3)]:
+        out = torch.zeros(4097, dtype=torch.int16, device=cuda)
+        for s in range(steps):
+            tf.synthetic_grads(out, 42, sg, it, s, accumulate=s > 0)
+        torch.cuda.synchronize()
+        assert np.array_equal(_np16(out), golden[f"grads_{sg}_{it}_{steps}"])
+    for kind in (0, 1):
+        out = torch.zeros(100003, dtype=torch.int16, device=cuda)
+        for s in range(2):
+            tf.synthetic_grads(out, 9, 4, 1, s, accumulate=s > 0, dtype=kind)
+        assert np.array_equal(_np16(out), oracle.synthetic_grads(100003, 9, 4, 1, 2, kind))
+    p = torch.empty(4097, device=cuda)
+    m, v = torch.ones(4097, device=cuda), torch.ones(4097, device=cuda)
+    tf.synthetic_state(p, m, v, 42, 9)
+    assert_bits(p.cpu().numpy(), golden["params_42_9"], "param init")
+    assert bool((m == 0).all()) and bool((v == 0).all())
+
+
+def test_narrow_widen_exhaustive_f32(tf, cuda):
+    """1/16 of all 2^32 float bit patterns (stride 16, every exponent and
+    sign, NaN payloads included) narrowed to f16 and bf16 on the GPU agree
+    with the oracle bit for bit, and the overflow counters agree."""
+    import torch
+    chunk = 1 << 26
+    out = torch.empty(chunk, dtype=torch.int16, device=cuda)
+    over = torch.zeros(1, dtype=torch.int64, device=cuda)
+    total_over = [0, 0]
+    for kind in (0, 1):
+        for q in range(4):  # stride-16 sample of each quarter of the 2^32 patterns (every exponent)
+            base = q * (1 << 30) + (q * 5 + 3) % 16
+            idx = torch.arange(chunk, dtype=torch.int64, device=cuda) * 16 + base
+            bits = idx.to(torch.int32).view(torch.float32)
+            tf.downscale16(bits, out, kind, over)
+            want, o = oracle.narrow16(bits.cpu().numpy(), kind)
+            assert np.array_equal(_np16(out), want), (kind, c)
+            total_over[kind] += o
+        assert int(over.item()) == total_over[kind]
+        over.zero_()
+    # widen: every 16-bit pattern
+    h = torch.arange(65536, dtype=torch.int32, device=cuda).to(torch.int16)
+    f = torch.empty(65536, device=cuda)
+    nf = torch.zeros(1, dtype=torch.int64, device=cuda)
+    for kind in (0, 1):
+        tf.upscale16(h, f, kind, nf)
+        want = oracle.widen16(np.arange(65536, dtype=np.uint16), kind)
+        got = f.cpu().numpy()
+        fin = ~np.isnan(want)
+        assert_bits(got[fin], want[fin], "widen")
+        assert np.isnan(got[~fin]).all()
+    assert int(nf.item()) == 2048 + 256  # non-finite f16 + bf16 patterns

@@ -1,0 +1,94 @@
+"""Product placement/ordering functions (C ABI, host) against the oracle and
+the reference known answers. CPU only."""
+import numpy as np
+
+import oracle
+
+
+def test_assign_subgroups_matches_oracle_and_golden(tf, golden):
+    for M, bw, counts in zip(golden["eq1_M"], golden["eq1_bw"], golden["eq1_counts"]):
+        n = int((bw >= 0).sum())
+        got = tf.assign_subgroups(int(M), bw[:n].tolist()).counts
+        assert got == counts[:n].tolist()
+    rng = np.random.default_rng(3)
+    for _ in range(500):
+        N = int(rng.integers(1, 5))
+        M = int(rng.integers(1, 200))
+        bw = [float(x) for x in np.where(rng.random(N) < 0.1, 0.0, 10 ** rng.uniform(-2, 2, N))]
+        if not any(bw):
+            bw[0] = 1.0
+        assert tf.assign_subgroups(M, bw).counts == oracle.assign_subgroups(M, bw)
+
+
+def test_assign_subgroups_properties(tf):
+    # test_placement.cpp:81-103: scale invariance and monotonicity.
+    rng = np.random.default_rng(5)
+    for _ in range(100):
+        M = int(rng.integers(1, 41))
+        B = rng.uniform(0.1, 50.0, 3).tolist()
+        a = tf.assign_subgroups(M, B).counts
+        for c in (0.5, 2.0, 1024.0, 3.7):
+            assert tf.assign_subgroups(M, [b * c for b in B]).counts == a
+        boosted = list(B)
+        boosted[1] *= 1.7
+        assert tf.assign_subgroups(M, boosted).counts[1] >= a[1]
+    assert tf.assign_subgroups(12, [2.0, 1.0]).counts == [8, 4]
+
+
+def test_destination_plan_matches_oracle(tf):
+    rng = np.random.default_rng(11)
+    for _ in range(300):
+        N = int(rng.integers(1, 5))
+        M = int(rng.integers(1, 40))
+        bw = [float(x) for x in 10 ** rng.uniform(-1, 1, N)]
+        cap = int(rng.integers(0, M + 3))
+        order = rng.permutation(M).tolist()
+        plan = tf.DestinationPlan(order, cap, bw)
+        r, t, a = oracle.destination_plan(M, cap, bw)
+        for k, sg in enumerate(order):
+            got = plan.assign_storage_tier(sg)
+            assert (int(got.host_retain), got.tier) == (r[k], t[k])
+        assert plan.flush_allocation().counts == a
+        assert plan.retained_count() == sum(r)
+
+
+def test_update_plan_alternates(tf):
+    # test_scheduler.cpp:127-142
+    even = tf.UpdatePlan.make(0, [0, 1, 2, 3], True)
+    odd = tf.UpdatePlan.make(1, [0, 1, 2, 3], True)
+    assert even.order == [0, 1, 2, 3] and even.ascending
+    assert odd.order == [3, 2, 1, 0] and not odd.ascending
+    assert tf.UpdatePlan.make(1, [0, 1, 2, 3], False).ascending
+    assert even.next_after(2) == 3 and even.next_after(3) is None
+    assert odd.next_after(3) == 2 and odd.next_after(0) is None
+
+
+def test_retention_capacity(tf):
+    for caching in (0, 1):
+        for pool in range(3, 12):
+            for cache in range(-1, 10):
+                for M in range(0, 12):
+                    assert tf.retention_capacity(bool(caching), pool, cache, M) == \
+                        oracle.lib().orc_retention_capacity(caching, pool, cache, M)
+
+
+def test_ema_arithmetic(tf):
+    # test_placement.cpp:122-167
+    est = tf.BandwidthEstimate([200e6], [200e6], 1.0)
+    tf.update_bandwidth_estimates(est, [tf.TierObservation(2, 300e6, 2.0, 2, 300e6, 2.0)])
+    assert abs(est.effective(0) - 150e6) < 1 and est.sample_count[0] == 4
+    est = tf.BandwidthEstimate([200e6, 64e6], [100e6, 64e6], 0.5)
+    tf.update_bandwidth_estimates(est, [tf.TierObservation(1, 50e6, 1.0, 0, 0, 0), tf.TierObservation()])
+    assert abs(est.read_bw[0] - 125e6) < 1 and est.write_bw[0] == 100e6 and est.effective(1) == 64e6
+
+
+def test_rebalance_after_bandwidth_drop(tf):
+    # test_placement.cpp:187-211 (acceptance criterion 11)
+    est = tf.BandwidthEstimate([200e6, 200e6], [200e6, 200e6], 0.5)
+    before = tf.assign_subgroups(16, est.effective_all()).counts[1]
+    obs = [tf.TierObservation(1, 200e6, 1.0, 1, 200e6, 1.0), tf.TierObservation(1, 100e6, 1.0, 1, 100e6, 1.0)]
+    tf.update_bandwidth_estimates(est, obs)
+    after1 = tf.assign_subgroups(16, est.effective_all()).counts[1]
+    tf.update_bandwidth_estimates(est, obs)
+    after2 = tf.assign_subgroups(16, est.effective_all()).counts[1]
+    assert after1 <= before and after2 < before
