@@ -118,6 +118,9 @@ _SIGS = {
     "tfg_adam_fused_contiguous": (_i, [_vp, _u64, _vp, _i, _vp, _i, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
     "tfg_adam_step": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
                            C.POINTER(_u64), _vp]),
+    "tfg_adam_variant_count": (_i, [C.POINTER(_i)]),
+    "tfg_adam_fused_variant": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
+    "tfg_selftest_div_const": (_i, [_d, _u64, _u64, _i, _i, C.POINTER(_u64), C.POINTER(_d)]),
     "tfg_upscale16": (_i, [_vp, _vp, _u64, _i, _vp, _vp]),
     "tfg_downscale16": (_i, [_vp, _vp, _u64, _i, _vp, _vp]),
     "tfg_count_nonfinite16": (_i, [_vp, _u64, _i, _vp, _vp]),

@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
-CU_SOURCES = ["kernels.cu"]
+CU_SOURCES = ["kernels.cu", "adam_kernel.cu"]
 CXX_SOURCES = ["tier.cpp", "engine.cpp", "capi.cpp"]
 
 
@@ -72,7 +72,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     with cf.ThreadPoolExecutor(max_workers=len(jobs)) as ex:
         logs = list(ex.map(lambda j: _run(j[1], verbose), jobs))
     ptxas = OBJ_DIR / "ptxas.log"
-    ptxas.write_text(logs[0])
+    ptxas.write_text("".join(logs[:len(CU_SOURCES)]))
     tmp = LIB.with_suffix(".so.tmp")
     _run([NVCC, GENCODE, "-shared", "-cudart", "static", "-o", str(tmp)] + [str(o) for o, _ in jobs]
          + ["-Xlinker", "--no-undefined", "-lpthread", "-ldl", "-lrt"], verbose)

@@ -172,6 +172,42 @@ int tfg_adam_step(float* p, float* m, float* v, const uint16_t* grad, int grad_d
     });
 }
 
+int tfg_adam_variant_count(int* count) {
+    return guarded([&] {
+        need(count, "count");
+        *count = tfb::adam_variant_count();
+    });
+}
+
+int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint16_t* grad, uint16_t* param16,
+                           uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters,
+                           void* stream) {
+    return guarded([&] {
+        if (variant < 0 || variant >= tfb::adam_variant_count()) throw tfb::ConfigError("unknown kernel variant");
+        const auto a = adam_launch(p, m, v, grad, TFG_F16, param16, TFG_F16, n, hyper, t, counters);
+        tfb::cuda_check(tfb::launch_adam_fused_variant(a, variant, as_stream(stream)), "adam_fused_variant");
+    });
+}
+
+int tfg_selftest_div_const(double divisor, uint64_t n, uint64_t seed, int exp_lo, int exp_span, uint64_t* mismatches,
+                           double* first_bad) {
+    return guarded([&] {
+        if (!(divisor > 0.0)) throw tfb::ConfigError("divisor must be > 0");
+        if (exp_span < 1) throw tfb::ConfigError("exp_span must be >= 1");
+        unsigned long long* d = nullptr;
+        tfb::cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), 16), "cudaMalloc");
+        tfb::cuda_check(cudaMemset(d, 0, 16), "cudaMemset");
+        const cudaError_t e = tfb::launch_divtest(divisor, 1.0 / divisor, n, seed, exp_lo, exp_span, d,
+                                                  reinterpret_cast<double*>(d + 1), nullptr);
+        unsigned long long h[2] = {0, 0};
+        const cudaError_t e2 = e == cudaSuccess ? cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost) : e;
+        cudaFree(d);
+        tfb::cuda_check(e2, "divtest");
+        if (mismatches) *mismatches = h[0];
+        if (first_bad) std::memcpy(first_bad, &h[1], sizeof(double));
+    });
+}
+
 int tfg_upscale16(const uint16_t* src, float* dst, uint64_t n, int dtype, unsigned long long* nonfinite,
                   void* stream) {
     return guarded([&] {

@@ -48,6 +48,8 @@ AdamConsts AdamHyper::consts(std::uint64_t t) const {
     c.lr_wd = weight_decay != 0.0 ? lr * weight_decay : 0.0;
     c.bc1 = 1.0 - std::pow(beta1, static_cast<double>(t));
     c.bc2 = 1.0 - std::pow(beta2, static_cast<double>(t));
+    c.inv_bc1 = 1.0 / c.bc1;
+    c.inv_bc2 = 1.0 / c.bc2;
     return c;
 }
 

@@ -22,128 +22,14 @@
 #include <cstdint>
 
 #include "kernels.hpp"
+#include "launch_util.cuh"
 #include "numerics.cuh"
 
 namespace tfb {
 
+using namespace detail;
+
 namespace {
-
-constexpr int kThreads = 256;
-
-__device__ __forceinline__ void warp_count_add(unsigned long long* dst, unsigned local) {
-    const unsigned total = __reduce_add_sync(0xFFFFFFFFu, local);
-    if (total != 0 && (threadIdx.x & 31) == 0) atomicAdd(dst, static_cast<unsigned long long>(total));
-}
-
-struct alignas(8) U16x4 {
-    uint16_t x, y, z, w;
-};
-
-__device__ __forceinline__ U16x4 load_u16x4(const uint16_t* p) {
-    const uint2 r = __ldcs(reinterpret_cast<const uint2*>(p));
-    U16x4 o;
-    o.x = static_cast<uint16_t>(r.x & 0xFFFFu);
-    o.y = static_cast<uint16_t>(r.x >> 16);
-    o.z = static_cast<uint16_t>(r.y & 0xFFFFu);
-    o.w = static_cast<uint16_t>(r.y >> 16);
-    return o;
-}
-
-__device__ __forceinline__ void store_u16x4(uint16_t* p, U16x4 v) {
-    uint2 r;
-    r.x = static_cast<uint32_t>(v.x) | (static_cast<uint32_t>(v.y) << 16);
-    r.y = static_cast<uint32_t>(v.z) | (static_cast<uint32_t>(v.w) << 16);
-    __stcs(reinterpret_cast<uint2*>(p), r);
-}
-
-// ---------------------------------------------------------------------------
-// Fused Adam. VEC = true: all five streams are 16-byte (P,m,v) / 8-byte (g,
-// p16) aligned and the body walks quads; the n % 4 tail is handled scalar by
-// the first threads. VEC = false: scalar everywhere (ragged contiguous P||m||v
-// views with P % 4 != 0).
-template <int GK, int OK, bool WD, bool VEC, int UNROLL>
-__global__ void __launch_bounds__(kThreads)
-    adam_fused_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                      const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t n,
-                      AdamConsts c, unsigned long long* __restrict__ counters) {
-    unsigned nonfinite = 0, overflow = 0;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-
-    if constexpr (VEC) {
-        const uint64_t nq = n / 4;
-        float4* p4 = reinterpret_cast<float4*>(p);
-        float4* m4 = reinterpret_cast<float4*>(m);
-        float4* v4 = reinterpret_cast<float4*>(v);
-        for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
-            float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
-            U16x4 rg[UNROLL];
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
-                if (q < nq) {
-                    rp[u] = __ldcs(p4 + q);
-                    rm[u] = __ldcs(m4 + q);
-                    rv[u] = __ldcs(v4 + q);
-                    rg[u] = load_u16x4(g + 4 * q);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
-                if (q < nq) {
-                    nonfinite += nonfinite16<GK>(rg[u].x) + nonfinite16<GK>(rg[u].y) +
-                                 nonfinite16<GK>(rg[u].z) + nonfinite16<GK>(rg[u].w);
-                    adam_element<WD>(rp[u].x, rm[u].x, rv[u].x, widen16<GK>(rg[u].x), c);
-                    adam_element<WD>(rp[u].y, rm[u].y, rv[u].y, widen16<GK>(rg[u].y), c);
-                    adam_element<WD>(rp[u].z, rm[u].z, rv[u].z, widen16<GK>(rg[u].z), c);
-                    adam_element<WD>(rp[u].w, rm[u].w, rv[u].w, widen16<GK>(rg[u].w), c);
-                    U16x4 h;
-                    h.x = narrow16<OK>(rp[u].x);
-                    h.y = narrow16<OK>(rp[u].y);
-                    h.z = narrow16<OK>(rp[u].z);
-                    h.w = narrow16<OK>(rp[u].w);
-                    overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) +
-                                is_inf16<OK>(h.w);
-                    __stcs(p4 + q, rp[u]);
-                    __stcs(m4 + q, rm[u]);
-                    __stcs(v4 + q, rv[u]);
-                    store_u16x4(p16 + 4 * q, h);
-                }
-            }
-        }
-        const uint64_t i = nq * 4 + tid;  // scalar tail: n % 4 elements
-        if (i < n) {
-            float pf = p[i], mf = m[i], vf = v[i];
-            const uint16_t gh = g[i];
-            nonfinite += nonfinite16<GK>(gh);
-            adam_element<WD>(pf, mf, vf, widen16<GK>(gh), c);
-            const uint16_t h = narrow16<OK>(pf);
-            overflow += is_inf16<OK>(h);
-            p[i] = pf;
-            m[i] = mf;
-            v[i] = vf;
-            p16[i] = h;
-        }
-    } else {
-        for (uint64_t i = tid; i < n; i += nthreads) {
-            float pf = __ldcs(p + i), mf = __ldcs(m + i), vf = __ldcs(v + i);
-            const uint16_t gh = __ldcs(g + i);
-            nonfinite += nonfinite16<GK>(gh);
-            adam_element<WD>(pf, mf, vf, widen16<GK>(gh), c);
-            const uint16_t h = narrow16<OK>(pf);
-            overflow += is_inf16<OK>(h);
-            __stcs(p + i, pf);
-            __stcs(m + i, mf);
-            __stcs(v + i, vf);
-            p16[i] = h;
-        }
-    }
-    if (counters != nullptr) {
-        warp_count_add(counters + 0, nonfinite);
-        warp_count_add(counters + 1, overflow);
-    }
-}
 
 // ---------------------------------------------------------------------------
 // Synthetic gradients. prefix = splitmix64 chain over (seed, sg, iteration,
@@ -245,65 +131,12 @@ __global__ void spin_kernel(uint64_t ns) {
     }
 }
 
-int g_num_sms = 0;
-
-int num_sms() {
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        int sms = 0;
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0)
-            sms = 148;
-        g_num_sms = sms;
-    }
-    return g_num_sms;
-}
-
-// Grid sized to whole waves of the SM count, capped by the work.
-unsigned grid_for(uint64_t work_items, int ctas_per_sm) {
-    const uint64_t need = (work_items + kThreads - 1) / kThreads;
-    const uint64_t cap = static_cast<uint64_t>(num_sms()) * static_cast<uint64_t>(ctas_per_sm);
-    return static_cast<unsigned>(std::max<uint64_t>(1, std::min(need, cap)));
-}
-
-template <int GK, int OK, bool WD>
-cudaError_t launch_adam_typed(const AdamLaunch& a, cudaStream_t stream) {
-    constexpr int kUnroll = 2;
-    const bool vec = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
-                       reinterpret_cast<uintptr_t>(a.v)) & 15u) == 0 &&
-                     ((reinterpret_cast<uintptr_t>(a.g) | reinterpret_cast<uintptr_t>(a.p16)) & 7u) == 0;
-    if (vec) {
-        const unsigned grid = grid_for((a.n / 4 + kUnroll - 1) / kUnroll, kAdamCtasPerSm);
-        adam_fused_kernel<GK, OK, WD, true, kUnroll><<<grid, kThreads, 0, stream>>>(
-            a.p, a.m, a.v, a.g, a.p16, a.n, a.c, a.counters);
-    } else {
-        const unsigned grid = grid_for(a.n, kAdamCtasPerSm);
-        adam_fused_kernel<GK, OK, WD, false, 1><<<grid, kThreads, 0, stream>>>(
-            a.p, a.m, a.v, a.g, a.p16, a.n, a.c, a.counters);
-    }
-    return cudaGetLastError();
-}
-
-template <int GK, int OK>
-cudaError_t launch_adam_wd(const AdamLaunch& a, cudaStream_t stream) {
-    return a.c.lr_wd != 0.0 ? launch_adam_typed<GK, OK, true>(a, stream)
-                            : launch_adam_typed<GK, OK, false>(a, stream);
-}
-
 }  // namespace
 
 cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t stream) {
     if (ns == 0) return cudaSuccess;
     spin_kernel<<<1, 1, 0, stream>>>(ns);
     return cudaGetLastError();
-}
-
-cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
-    if (a.n == 0) return cudaSuccess;
-    if (a.grad_kind == kF16 && a.out_kind == kF16) return launch_adam_wd<kF16, kF16>(a, stream);
-    if (a.grad_kind == kF16 && a.out_kind == kBF16) return launch_adam_wd<kF16, kBF16>(a, stream);
-    if (a.grad_kind == kBF16 && a.out_kind == kF16) return launch_adam_wd<kBF16, kF16>(a, stream);
-    return launch_adam_wd<kBF16, kBF16>(a, stream);
 }
 
 cudaError_t launch_synthetic_grads(uint16_t* out, uint64_t n, int kind, uint64_t prefix,

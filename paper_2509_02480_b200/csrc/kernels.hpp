@@ -11,8 +11,6 @@
 namespace tfb {
 
 
-// Resident CTAs per SM the fused kernel grid is sized for (grid = SMs x this).
-constexpr int kAdamCtasPerSm = 4;
 
 struct AdamLaunch {
     float* p = nullptr;  // fp32 master params, in place
@@ -30,6 +28,12 @@ struct AdamLaunch {
 };
 
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream);
+// Tuning variants of the fused kernel (0 = default; F16/F16 only otherwise).
+cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStream_t stream);
+int adam_variant_count();
+// Self-test: div_by_const(a, b, y) vs div.rn.f64 on generated numerators.
+cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
+                           unsigned long long* mismatches, double* first_bad, cudaStream_t stream);
 cudaError_t launch_synthetic_grads(uint16_t* out, uint64_t n, int kind, uint64_t prefix,
                                    bool accumulate, cudaStream_t stream);
 cudaError_t launch_synthetic_state(float* p, float* m, float* v, uint64_t n, uint64_t prefix,

@@ -20,6 +20,8 @@ struct AdamConsts {
     double lr_wd;  // lr * weight_decay; 0 disables decay (optimizer.hpp:94)
     double bc1;
     double bc2;
+    double inv_bc1;  // RN(1 / bc1): the constant-divisor path
+    double inv_bc2;  // RN(1 / bc2)
 };
 
 // splitmix64 (reference scheduler.hpp:76-81) for the host-folded prefixes of

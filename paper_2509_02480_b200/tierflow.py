@@ -696,6 +696,27 @@ def adam_step(p, m, v, grad16, param16, t: int, hyper: AdamHyper = AdamHyper(), 
     return over.value
 
 
+def adam_variant_count() -> int:
+    n = C.c_int()
+    _lib.call("tfg_adam_variant_count", C.byref(n))
+    return n.value
+
+
+def adam_fused_variant(variant: int, p, m, v, grad16, param16, t: int, hyper: AdamHyper = AdamHyper(), counters=None,
+                       stream=None) -> None:
+    """Tuning hook: the fused kernel in launch configuration `variant` (F16/F16)."""
+    hy = hyper.c()
+    _lib.call("tfg_adam_fused_variant", variant, _ptr(p), _ptr(m), _ptr(v), _ptr(grad16), _ptr(param16), p.numel(),
+              C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
+
+
+def selftest_div_const(divisor: float, n: int, seed: int = 1, exp_lo: int = -160, exp_span: int = 170):
+    """(mismatches, first_bad_numerator) of the constant-divisor quotient vs div.rn.f64."""
+    mm, fb = C.c_uint64(), C.c_double()
+    _lib.call("tfg_selftest_div_const", divisor, n, seed, exp_lo, exp_span, C.byref(mm), C.byref(fb))
+    return mm.value, fb.value
+
+
 def upscale16(src, dst, dtype: int = F16, nonfinite=None, stream=None) -> None:
     _lib.call("tfg_upscale16", _ptr(src), _ptr(dst), src.numel(), dtype,
               _ptr(nonfinite) if nonfinite is not None else None, _stream(stream))

@@ -1,0 +1,83 @@
+"""Times every launch-configuration variant of the fused Adam kernel on
+100M-param subgroups (CUDA events on the launching stream, inputs far larger
+than L2) and checks each variant bit-for-bit against variant 1.
+
+    python scripts/kernel_sweep.py [n_params] [subgroups] [reps]
+"""
+import json
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2509_02480_b200 import tierflow as tf  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+S = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+dev = torch.device("cuda:0")
+subs = []
+for k in range(S):
+    st = torch.empty(3 * n, device=dev)
+    g = torch.empty(n, dtype=torch.int16, device=dev)
+    tf.synthetic_state(st[:n], st[n:2 * n], st[2 * n:], 42, k)
+    tf.synthetic_grads(g, 42, k, 0)
+    subs.append((st, g, torch.empty(n, dtype=torch.int16, device=dev)))
+torch.cuda.synchronize()
+hy = tf.AdamHyper()
+results = {}
+# bitwise: every variant from the same input state
+base_in = subs[0][0].clone()
+ref_out = None
+for v in range(1, tf.adam_variant_count()):
+    for wd in (0.0, 0.01):
+        st = base_in.clone()
+        p16 = torch.empty(n, dtype=torch.int16, device=dev)
+        tf.adam_fused_variant(v, st[:n], st[n:2 * n], st[2 * n:], subs[0][1], p16, 3, tf.AdamHyper(weight_decay=wd))
+        torch.cuda.synchronize()
+        key = (wd,)
+        if v == 1:
+            results.setdefault("ref", {})[key] = (st.clone(), p16.clone())
+        else:
+            r_st, r_p16 = results["ref"][key]
+            same = bool(torch.equal(st.view(torch.int32), r_st.view(torch.int32))) and bool(torch.equal(p16, r_p16))
+            results.setdefault("bitwise", {})[f"v{v}_wd{wd}"] = same
+    del st
+results.pop("ref")
+torch.cuda.empty_cache()
+stream = torch.cuda.Stream()
+timing = {}
+for v in range(0, tf.adam_variant_count()):
+    t = 1
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            for st, g, p16 in subs:
+                tf.adam_fused_variant(v, st[:n], st[n:2 * n], st[2 * n:], g, p16, t, hy, stream=stream)
+                t += 1
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            for st, g, p16 in subs:
+                tf.adam_fused_variant(v, st[:n], st[n:2 * n], st[2 * n:], g, p16, t, hy, stream=stream)
+                t += 1
+        b.record(stream)
+    stream.synchronize()
+    us = a.elapsed_time(b) * 1e3 / (reps * S)
+    gbs = 28 * n / (us * 1e-6) / 1e9
+    timing[v] = {"us_per_launch": round(us, 1), "GBs": round(gbs, 1), "frac_of_6422.8": round(gbs / 6422.8, 4)}
+    print(f"variant {v}: {us:8.1f} us/launch  {gbs:7.1f} GB/s  {gbs/6422.8:.3f}", flush=True)
+# constant-division self-test: bias corrections of the default betas, t = 1..400
+bad = 0
+for t in range(1, 401):
+    for beta in (0.9, 0.999):
+        bc = 1.0 - beta ** t
+        mm, fb = tf.selftest_div_const(bc, 20_000_000, seed=t * 7 + int(beta * 1000))
+        bad += mm
+        if mm:
+            print("DIV MISMATCH", t, beta, mm, fb)
+results["div_selftest"] = {"divisors": 800, "numerators_each": 20_000_000, "mismatches": bad}
+results["timing"] = timing
+print(json.dumps(results, indent=1))
+Path("gpurun_out").mkdir(exist_ok=True)
+Path("gpurun_out/sweep.json").write_text(json.dumps(results, indent=1))

@@ -1,0 +1,28 @@
+"""Launches the fused Adam kernel on 100M-param subgroups for ncu captures.
+
+    ncu --set full -k regex:adam_fused -s 2 -c 1 -o gpurun_out/prof python scripts/profile_kernel.py
+"""
+import sys
+from pathlib import Path
+
+import torch
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_2509_02480_b200 import tierflow as tf  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 4
+gk = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+dev = torch.device("cuda:0")
+subs = []
+for k in range(reps):
+    st = torch.empty(3 * n, device=dev)
+    g = torch.empty(n, dtype=torch.int16, device=dev)
+    tf.synthetic_state(st[:n], st[n:2 * n], st[2 * n:], 42, k)
+    tf.synthetic_grads(g, 42, k, 0, dtype=gk)
+    subs.append((st, g, torch.empty(n, dtype=torch.int16, device=dev)))
+torch.cuda.synchronize()
+for t, (st, g, p16) in enumerate(subs, start=1):
+    tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], g, p16, t, tf.AdamHyper(), gk, 0)
+torch.cuda.synchronize()
+print("done")
