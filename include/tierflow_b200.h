@@ -145,6 +145,15 @@ typedef struct tfg_event {
     uint64_t bytes;
 } tfg_event;
 
+/* One subgroup's pass through the pipeline in the last phase (no reference
+ * counterpart): device times from CUDA events, ms from the first H2D start;
+ * host times ms from run_update entry. */
+typedef struct tfg_device_span {
+    uint32_t id;
+    float h2d_start, h2d_end, k_start, k_end, d2h_end;
+    float host_resident, host_retired;
+} tfg_device_span;
+
 typedef struct tfg_subgroup_meta { /* Subgroup, optimizer.hpp:39-73 */
     uint32_t id;
     int32_t residency;  /* 0 host_cached, 1 in_flight, 2 on_tier */
@@ -268,6 +277,7 @@ int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_pt
 int tfg_engine_params16_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);         /* shadow_, :861 */
 int tfg_engine_run_update(tfg_engine* engine, int iteration, tfg_phase_stats* stats);      /* :405 */
 int tfg_engine_last_subgroup_io(tfg_engine* engine, tfg_subgroup_io* out, uint64_t max_n, uint64_t* n_out);
+int tfg_engine_last_timeline(tfg_engine* engine, tfg_device_span* out, uint64_t max_n, uint64_t* n_out);
 int tfg_engine_wait_host_resident(tfg_engine* engine, uint32_t id, int* slot_out);         /* :514 */
 /* enqueue_* return a ticket (0 = cache hit, nothing queued) to wait on. */
 int tfg_engine_enqueue_prefetch(tfg_engine* engine, uint32_t id, uint64_t* ticket_out);    /* :563 */

@@ -101,6 +101,12 @@ class EventC(C.Structure):
                 ("subgroup_id", C.c_int64), ("tier_id", C.c_int32), ("pad", C.c_int32), ("bytes", C.c_uint64)]
 
 
+class DeviceSpanC(C.Structure):
+    _fields_ = [("id", C.c_uint32), ("h2d_start", C.c_float), ("h2d_end", C.c_float), ("k_start", C.c_float),
+                ("k_end", C.c_float), ("d2h_end", C.c_float), ("host_resident", C.c_float),
+                ("host_retired", C.c_float)]
+
+
 class SubgroupMetaC(C.Structure):
     _fields_ = [("id", C.c_uint32), ("residency", C.c_int32), ("tier", C.c_int32), ("slot", C.c_int32),
                 ("param_count", C.c_uint64), ("step_count", C.c_uint64)]
@@ -168,6 +174,7 @@ _SIGS = {
     "tfg_engine_params16_buffer": (_i, [_vp, C.c_uint32, C.POINTER(_vp)]),
     "tfg_engine_run_update": (_i, [_vp, _i, C.POINTER(PhaseStatsC)]),
     "tfg_engine_last_subgroup_io": (_i, [_vp, C.POINTER(SubgroupIoC), _u64, C.POINTER(_u64)]),
+    "tfg_engine_last_timeline": (_i, [_vp, C.POINTER(DeviceSpanC), _u64, C.POINTER(_u64)]),
     "tfg_engine_wait_host_resident": (_i, [_vp, C.c_uint32, C.POINTER(_i)]),
     "tfg_engine_enqueue_prefetch": (_i, [_vp, C.c_uint32, C.POINTER(_u64)]),
     "tfg_engine_enqueue_flush": (_i, [_vp, C.c_uint32, _i, C.POINTER(_u64)]),

@@ -28,6 +28,7 @@ struct tfg_trace {
 struct tfg_engine {
     std::unique_ptr<tfb::OffloadWorker> w;
     std::vector<tfb::SubgroupIoTimes> last_io;
+    std::vector<tfb::DeviceSpan> last_timeline;
     std::mutex mu;
     std::map<std::uint64_t, std::shared_future<tfb::IoStats>> tickets;
     std::uint64_t next_ticket = 1;
@@ -621,6 +622,7 @@ int tfg_engine_run_update(tfg_engine* engine, int iteration, tfg_phase_stats* st
         need(engine, "engine");
         const tfb::PhaseStats st = engine->w->run_update(iteration);
         engine->last_io = st.subgroup_io;
+        engine->last_timeline = st.timeline;
         if (stats == nullptr) return;
         std::memset(stats, 0, sizeof(*stats));
         stats->wall_seconds = st.wall_seconds;
@@ -655,6 +657,17 @@ int tfg_engine_last_subgroup_io(tfg_engine* engine, tfg_subgroup_io* out, uint64
             out[i] = tfg_subgroup_io{e.id, e.fetched ? 1u : 0u, e.flushed ? 1u : 0u, 0u, e.state_bytes, e.read_seconds,
                                      e.write_seconds};
         }
+        if (n_out) *n_out = n;
+    });
+}
+
+int tfg_engine_last_timeline(tfg_engine* engine, tfg_device_span* out, uint64_t max_n, uint64_t* n_out) {
+    static_assert(sizeof(tfg_device_span) == sizeof(tfb::DeviceSpan), "span layout");
+    return guarded([&] {
+        need(engine, "engine");
+        const std::size_t n = std::min<std::size_t>(max_n, engine->last_timeline.size());
+        if (n > 0) need(out, "out");
+        std::memcpy(out, engine->last_timeline.data(), n * sizeof(tfg_device_span));
         if (n_out) *n_out = n;
     });
 }

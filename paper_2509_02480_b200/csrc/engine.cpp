@@ -370,12 +370,14 @@ void OffloadWorker::setup_device() {
     grad_ptr_.clear();
     p16_ptr_.clear();
     events_.assign(ids_.size(), DeviceEvents{});
+    host_resident_ns_.assign(ids_.size(), 0);
+    host_retired_ns_.assign(ids_.size(), 0);
     for (std::size_t k = 0; k < ids_.size(); ++k) {
         index_of_[ids_[k]] = k;
         grad_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(grad_arena_) + offs[k]));
         p16_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(p16_arena_) + offs[k]));
         DeviceEvents& e = events_[k];
-        for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_end})
+        for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_start, &e.d2h_end})
             cuda_check(cudaEventCreate(ev), "cudaEventCreate");
     }
     device_ready_ = true;
@@ -386,7 +388,7 @@ void OffloadWorker::release_device() {
     if (!device_ready_) return;
     cudaSetDevice(dev_.device);
     for (auto& e : events_)
-        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_end})
+        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_start, e.d2h_end})
             if (ev) cudaEventDestroy(ev);
     events_.clear();
     for (float* r : ring_) cudaFree(r);
@@ -529,6 +531,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
     if (!pool_) throw Error("run_update before init_and_flush_all");
     DeviceGuard dg(dev_.device);
     const auto t0 = Clock::now();
+    phase_t0_ns_ = now_ns();
     const AdamConsts c = hyper_.consts(static_cast<std::uint64_t>(iteration) + 1);
 
     PhaseStats stats;
@@ -560,6 +563,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         for (std::size_t j = 0; j < order.size(); ++j) {
             const SubgroupId id = order[j];
             const int slot = wait_host_resident(id);
+            host_resident_ns_[index_of_.at(id)] = now_ns();
             issue_device_update(j, id, slot, c);
             std::lock_guard<std::mutex> g(mu_);
             Subgroup& sg = subgroups_.at(id);
@@ -607,19 +611,32 @@ PhaseStats OffloadWorker::run_update(int iteration) {
     if (counters[0] != 0)
         throw SchedulingBugError("non-finite gradients reached the fused kernel after the pre-check");
 
-    // Device timeline of the phase.
-    for (const SubgroupId id : order) {
-        const DeviceEvents& e = events_[index_of_.at(id)];
-        float ms = 0.0f;
-        if (cudaEventElapsedTime(&ms, e.h2d_start, e.h2d_done) == cudaSuccess) stats.h2d_seconds += ms / 1e3;
-        if (cudaEventElapsedTime(&ms, e.k_start, e.k_end) == cudaSuccess) stats.kernel_seconds += ms / 1e3;
-        if (cudaEventElapsedTime(&ms, e.k_end, e.d2h_end) == cudaSuccess) stats.d2h_seconds += ms / 1e3;
-    }
+    // Device timeline of the phase (CUDA events) + host retire times.
     if (!order.empty()) {
-        float ms = 0.0f;
-        if (cudaEventElapsedTime(&ms, events_[index_of_.at(order.front())].h2d_start,
-                                 events_[index_of_.at(order.back())].d2h_end) == cudaSuccess)
-            stats.device_seconds = ms / 1e3;
+        const cudaEvent_t origin = events_[index_of_.at(order.front())].h2d_start;
+        auto at = [&](cudaEvent_t ev) {
+            float ms = 0.0f;
+            return cudaEventElapsedTime(&ms, origin, ev) == cudaSuccess ? ms : -1.0f;
+        };
+        for (const SubgroupId id : order) {
+            const std::size_t k = index_of_.at(id);
+            const DeviceEvents& e = events_[k];
+            DeviceSpan sp;
+            sp.id = id;
+            sp.h2d_start = at(e.h2d_start);
+            sp.h2d_end = at(e.h2d_done);
+            sp.k_start = at(e.k_start);
+            sp.k_end = at(e.k_end);
+            sp.d2h_end = at(e.d2h_end);
+            const float d2h_start = at(e.d2h_start);
+            sp.host_resident = static_cast<float>((host_resident_ns_[k] - phase_t0_ns_) / 1e6);
+            sp.host_retired = static_cast<float>((host_retired_ns_[k] - phase_t0_ns_) / 1e6);
+            stats.h2d_seconds += (sp.h2d_end - sp.h2d_start) / 1e3;
+            stats.kernel_seconds += (sp.k_end - sp.k_start) / 1e3;
+            stats.d2h_seconds += (sp.d2h_end - d2h_start) / 1e3;
+            stats.timeline.push_back(sp);
+        }
+        stats.device_seconds = at(events_[index_of_.at(order.back())].d2h_end) / 1e3;
     }
     (void)cudaGetLastError();
 
@@ -675,6 +692,7 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
 
     cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
+    cuda_check(cudaEventRecord(e.d2h_start, s_d2h_), "cudaEventRecord");
     copy_state(d, blk, pc, false, s_d2h_);
     cuda_check(cudaEventRecord(e.d2h_end, s_d2h_), "cudaEventRecord");
     auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
@@ -706,6 +724,7 @@ void OffloadWorker::completion_loop() {
         std::lock_guard<std::mutex> g(mu_);
         try {
             Subgroup& sg = subgroups_.at(c.id);
+            host_retired_ns_[index_of_.at(c.id)] = now_ns();
             pool_->end_update(c.slot);
             trace_->record(EventKind::update_end, id_, c.id, kNoTier, 12 * sg.param_count);
             const TierAssignment a = dests_->assign_storage_tier(c.id);

@@ -105,6 +105,16 @@ struct SubgroupIoTimes {
     bool flushed = false;
 };
 
+// Per-subgroup timeline of one phase, milliseconds from the phase start.
+// Device times come from CUDA events on the pipeline streams (zero = the
+// first H2D start); host times from CLOCK_MONOTONIC (zero = run_update entry).
+struct DeviceSpan {
+    SubgroupId id = 0;
+    float h2d_start = 0, h2d_end = 0, k_start = 0, k_end = 0, d2h_end = 0;
+    float host_resident = 0;  // wait_host_resident returned
+    float host_retired = 0;   // completion thread retired the subgroup
+};
+
 struct PhaseStats {
     double wall_seconds = 0.0;
     std::uint64_t params_updated = 0;
@@ -121,6 +131,7 @@ struct PhaseStats {
     double d2h_seconds = 0.0;     // sum of state D2H durations
     std::uint64_t h2d_bytes = 0;
     std::uint64_t d2h_bytes = 0;
+    std::vector<DeviceSpan> timeline;  // plan order
 };
 
 // ---------------------------------------------------------------------------
@@ -259,7 +270,8 @@ public:
 
 private:
     struct DeviceEvents {
-        cudaEvent_t h2d_start = nullptr, h2d_done = nullptr, k_start = nullptr, k_end = nullptr, d2h_end = nullptr;
+        cudaEvent_t h2d_start = nullptr, h2d_done = nullptr, k_start = nullptr, k_end = nullptr,
+                    d2h_start = nullptr, d2h_end = nullptr;
     };
     struct Completion {
         SubgroupId id;
@@ -321,6 +333,9 @@ private:
     std::vector<std::uint16_t*> grad_ptr_;
     std::vector<std::uint16_t*> p16_ptr_;
     std::vector<DeviceEvents> events_;
+    std::int64_t phase_t0_ns_ = 0;
+    std::vector<std::int64_t> host_resident_ns_;  // per subgroup index
+    std::vector<std::int64_t> host_retired_ns_;
 
     // Completion thread: retires subgroups whose D2H finished.
     std::thread completer_;

@@ -597,6 +597,16 @@ class OffloadWorker:
             device_seconds=st.device_seconds, kernel_seconds=st.kernel_seconds, h2d_seconds=st.h2d_seconds,
             d2h_seconds=st.d2h_seconds, h2d_bytes=st.h2d_bytes, d2h_bytes=st.d2h_bytes)
 
+    def last_timeline(self) -> list:
+        """Per-subgroup pipeline timeline of the last run_update, plan order:
+        dicts of h2d_start/h2d_end/k_start/k_end/d2h_end (device ms) and
+        host_resident/host_retired (host ms)."""
+        n = len(self._params)
+        buf = (_lib.DeviceSpanC * max(n, 1))()
+        got = C.c_uint64()
+        _lib.call("tfg_engine_last_timeline", self._h, buf, n, C.byref(got))
+        return [{f: getattr(s, f) for f, _ in _lib.DeviceSpanC._fields_} for s in buf[:got.value]]
+
     def wait_host_resident(self, sg: int) -> int:
         slot = C.c_int()
         _lib.call("tfg_engine_wait_host_resident", self._h, sg, C.byref(slot))
