@@ -308,6 +308,7 @@ OffloadWorker::~OffloadWorker() {
         cudaStreamSynchronize(s_h2d_);
         cudaStreamSynchronize(s_k_);
         cudaStreamSynchronize(s_d2h_);
+        cudaStreamSynchronize(s_d2h2_);
     }
     {
         std::lock_guard<std::mutex> g(cq_mu_);
@@ -351,6 +352,7 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&s_k_, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&s_d2h2_, cudaStreamNonBlocking), "cudaStreamCreate");
     ring_stride_ = seg_stride(max_params_);
     ring_.assign(static_cast<std::size_t>(dev_.device_buffers), nullptr);
     for (auto& r : ring_)
@@ -379,6 +381,7 @@ void OffloadWorker::setup_device() {
         DeviceEvents& e = events_[k];
         for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_start, &e.d2h_end})
             cuda_check(cudaEventCreate(ev), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&e.d2h_half, cudaEventDisableTiming), "cudaEventCreate");
     }
     device_ready_ = true;
     completer_ = std::thread([this] { completion_loop(); });
@@ -388,7 +391,7 @@ void OffloadWorker::release_device() {
     if (!device_ready_) return;
     cudaSetDevice(dev_.device);
     for (auto& e : events_)
-        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_start, e.d2h_end})
+        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_start, e.d2h_end, e.d2h_half})
             if (ev) cudaEventDestroy(ev);
     events_.clear();
     for (float* r : ring_) cudaFree(r);
@@ -400,6 +403,7 @@ void OffloadWorker::release_device() {
     cudaStreamDestroy(s_h2d_);
     cudaStreamDestroy(s_k_);
     cudaStreamDestroy(s_d2h_);
+    cudaStreamDestroy(s_d2h2_);
     device_ready_ = false;
 }
 
@@ -666,9 +670,37 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
         trace_->record(EventKind::update_start, id_, id, kNoTier, 12 * pc);
         ++in_flight_;
     }
+    const HostBlock& blk = pool_->block(slot);
+    AdamLaunch a;
+    a.g = grad_ptr_[k];
+    a.p16 = p16_ptr_[k];
+    a.n = pc;
+    a.grad_kind = dev_.grad_kind;
+    a.out_kind = dev_.out_kind;
+    a.c = c;
+    a.counters = counters_;
+    if (dev_.zero_copy) {
+        // The kernel streams P||m||v straight from and back to the pinned
+        // slot over PCIe: reads and writes interleave at cache-line grain,
+        // loading both link directions evenly; no device ring, no DMA.
+        float* hp = nullptr;
+        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hp), blk.payload(), 0),
+                   "cudaHostGetDevicePointer");
+        a.p = hp;
+        a.m = hp + pc;
+        a.v = hp + 2 * pc;
+        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start})
+            cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
+        cuda_check(launch_spin_ns(opt_.update_pad_ns, s_k_), "spin");
+        cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
+        for (cudaEvent_t ev : {e.k_end, e.d2h_start, e.d2h_end})
+            cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
+        auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
+        cuda_check(cudaLaunchHostFunc(s_k_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
+        return;
+    }
     float* d = ring_[j % K];
     const std::uint64_t ds = seg_stride(pc);
-    const HostBlock& blk = pool_->block(slot);
     if (j >= K) cuda_check(cudaStreamWaitEvent(s_h2d_, events_[index_of_.at(order_[j - K])].d2h_end, 0), "wait");
     cuda_check(cudaEventRecord(e.h2d_start, s_h2d_), "cudaEventRecord");
     copy_state(d, blk, pc, true, s_h2d_);
@@ -677,23 +709,30 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     cuda_check(cudaStreamWaitEvent(s_k_, e.h2d_done, 0), "wait");
     cuda_check(cudaEventRecord(e.k_start, s_k_), "cudaEventRecord");
     cuda_check(launch_spin_ns(opt_.update_pad_ns, s_k_), "spin");
-    AdamLaunch a;
     a.p = d;
     a.m = d + ds;
     a.v = d + 2 * ds;
-    a.g = grad_ptr_[k];
-    a.p16 = p16_ptr_[k];
-    a.n = pc;
-    a.grad_kind = dev_.grad_kind;
-    a.out_kind = dev_.out_kind;
-    a.c = c;
-    a.counters = counters_;
     cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
     cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
 
     cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
     cuda_check(cudaEventRecord(e.d2h_start, s_d2h_), "cudaEventRecord");
-    copy_state(d, blk, pc, false, s_d2h_);
+    if (dev_.d2h_split > 1 && ds == pc) {
+        // Two concurrent D2H halves on two copy engines: the write-back gets
+        // a larger share of the duplex link against the H2D stream.
+        const std::size_t bytes = 12 * pc;
+        const std::size_t half = (bytes / 2) & ~static_cast<std::size_t>(4095);
+        auto* host = reinterpret_cast<char*>(blk.payload());
+        auto* dev = reinterpret_cast<char*>(d);
+        cuda_check(cudaStreamWaitEvent(s_d2h2_, e.d2h_start, 0), "wait");
+        cuda_check(cudaMemcpyAsync(host, dev, half, cudaMemcpyDeviceToHost, s_d2h_), "cudaMemcpyAsync");
+        cuda_check(cudaMemcpyAsync(host + half, dev + half, bytes - half, cudaMemcpyDeviceToHost, s_d2h2_),
+                   "cudaMemcpyAsync");
+        cuda_check(cudaEventRecord(e.d2h_half, s_d2h2_), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(s_d2h_, e.d2h_half, 0), "wait");
+    } else {
+        copy_state(d, blk, pc, false, s_d2h_);
+    }
     cuda_check(cudaEventRecord(e.d2h_end, s_d2h_), "cudaEventRecord");
     auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
     cuda_check(cudaLaunchHostFunc(s_d2h_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");

@@ -76,6 +76,8 @@ struct DeviceOptions {
     int grad_kind = kF16;    // 16-bit gradient element kind
     int out_kind = kF16;     // 16-bit working-parameter element kind
     int device_buffers = 3;  // depth of the H2D -> kernel -> D2H ring
+    int zero_copy = 0;       // 1: the kernel reads/writes the pinned slot over PCIe (no ring, no DMA)
+    int d2h_split = 1;       // concurrent D2H copy streams per subgroup (1 or 2)
 };
 
 enum class Residency : int { host_cached = 0, in_flight = 1, on_tier = 2 };
@@ -271,7 +273,7 @@ public:
 private:
     struct DeviceEvents {
         cudaEvent_t h2d_start = nullptr, h2d_done = nullptr, k_start = nullptr, k_end = nullptr,
-                    d2h_start = nullptr, d2h_end = nullptr;
+                    d2h_start = nullptr, d2h_end = nullptr, d2h_half = nullptr;
     };
     struct Completion {
         SubgroupId id;
@@ -322,7 +324,7 @@ private:
 
     // Device resources.
     bool device_ready_ = false;
-    cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr;
+    cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr, s_d2h2_ = nullptr;
     std::vector<float*> ring_;
     std::uint64_t ring_stride_ = 0;  // floats per segment (P, m, v each) in a ring buffer
     void* grad_arena_ = nullptr;

@@ -49,7 +49,7 @@ public:
         HostBlock b;
         bytes = round_up(bytes, kPageBytes);
         void* p = nullptr;
-        const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable);
+        const cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocPortable | cudaHostAllocMapped);
         if (e == cudaSuccess) {
             b.pinned_ = true;
         } else {

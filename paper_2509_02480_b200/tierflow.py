@@ -133,6 +133,8 @@ class DeviceOptions:
     grad_dtype: int = F16
     param_dtype: int = F16
     device_buffers: int = 3
+    zero_copy: bool = False
+    d2h_split: int = 1
 
 
 @dataclass
@@ -507,7 +509,8 @@ class OffloadWorker:
         arr = (C.c_void_p * len(self._tiers))(*[t.handle.value for t in self._tiers])
         h = C.c_void_p()
         o, hy = opt.c(), hyper.c()
-        d = _lib.DeviceOptionsC(device.device, device.grad_dtype, device.param_dtype, device.device_buffers)
+        d = _lib.DeviceOptionsC(device.device, device.grad_dtype, device.param_dtype, device.device_buffers,
+                                int(device.zero_copy), device.d2h_split)
         _lib.call("tfg_engine_create", worker_id, arr, len(self._tiers), C.byref(o), C.byref(hy),
                   trace.handle if trace else None, C.byref(d), C.byref(h))
         self._h = h

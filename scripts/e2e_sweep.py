@@ -19,7 +19,7 @@ sys.path.insert(0, str(ROOT))
 from paper_2509_02480_b200 import tierflow as tf  # noqa: E402
 
 total = int(sys.argv[1]) if len(sys.argv) > 1 else 6_738_415_616
-configs = [tuple(int(x) for x in c.split(":")) for c in sys.argv[2:]] or [(8, -1, 3), (12, 5, 3), (12, 5, 4), (16, 5, 6)]
+configs = [tuple(int(x) for x in c.split(":")) for c in sys.argv[2:]] or [(12, 5, 3, 0, 1), (12, 5, 3, 0, 2), (12, 5, 3, 1, 1)]
 sub = 100_000_000
 sizes = [min(sub, total - k * sub) for k in range((total + sub - 1) // sub)]
 root = ROOT / "gpurun_out" / "e2e_sweep_tiers"
@@ -29,11 +29,11 @@ nvme = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, i
 pr = nvme.probe_bandwidth(256 << 20, 3)
 print(f"nvme probe r={pr.read_bw/1e9:.2f} w={pr.write_bw/1e9:.2f} GB/s", flush=True)
 out = []
-for pool, cache, ring in configs:
+for pool, cache, ring, zc, split in configs:
     trace = tf.EventTrace()
     w = tf.OffloadWorker(0, [dram, nvme], tf.ScheduleOptions(pool_slots=pool, cache_slots=cache,
                                                             lock_dir=str(root / "locks")),
-                         tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, ring))
+                         tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, ring, bool(zc), split))
     for k, n in enumerate(sizes):
         w.add_subgroup(k, n)
     t0 = time.time()
@@ -53,14 +53,14 @@ for pool, cache, ring in configs:
         span = tl[-1]["d2h_end"]
         phases.append(dict(ms=ms, span=span, h2d_busy=h2d_busy, d2h_busy=d2h_busy, h2d_gaps=h2d_gaps,
                            hits=st.cache_hits, alloc=st.flush_allocation, kernel_ms=st.kernel_seconds * 1e3))
-        print(f"pool={pool} cache={cache} ring={ring} phase {it}: {ms:7.1f} ms (device span {span:7.1f}) "
+        print(f"pool={pool} cache={cache} ring={ring} zc={zc} split={split} phase {it}: {ms:7.1f} ms (device span {span:7.1f}) "
               f"h2d busy {h2d_busy:7.1f} gaps {h2d_gaps:6.1f} d2h busy {d2h_busy:7.1f} hits {st.cache_hits} "
               f"alloc {st.flush_allocation}", flush=True)
         if it == 6:
             Path("gpurun_out").mkdir(exist_ok=True)
-            Path(f"gpurun_out/timeline_p{pool}_c{cache}_r{ring}.json").write_text(json.dumps(tl))
+            Path(f"gpurun_out/timeline_p{pool}_c{cache}_r{ring}_z{zc}_s{split}.json").write_text(json.dumps(tl))
     steady = phases[3:]
-    out.append(dict(pool=pool, cache=cache, ring=ring, init_s=init_s,
+    out.append(dict(pool=pool, cache=cache, ring=ring, zero_copy=zc, d2h_split=split, init_s=init_s,
                     ms=statistics.mean(p["ms"] for p in steady), phases=phases))
     w.close()
     del w

@@ -293,3 +293,29 @@ def test_external_gradient_buffer_binding(tf, cuda, lock_dir):
     got = w.read_current_state(0)
     assert np.array_equal(got.view(np.uint32), np.concatenate(want[:3]).view(np.uint32))
     w.close()
+
+
+@pytest.mark.parametrize("zero_copy,split", [(True, 1), (False, 2)])
+def test_transfer_modes_bitwise(tf, cuda, lock_dir, tmp_path, zero_copy, split):
+    """Zero-copy (kernel streams the pinned slot over PCIe) and split-D2H
+    copy mode give the same bits as the oracle."""
+    params = [100_000, 64_000, 99_996]
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=5, lock_dir=lock_dir), tf.AdamHyper(), trace,
+                         tf.DeviceOptions(0, 0, 0, 2, zero_copy, split))
+    w.set_fixed_ratio([1.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(17)
+    for it in range(3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(17))
+        w.run_update(it)
+    states, _ = oracle.run_engine_oracle(params, 17, 3, 5, -1, True, True, [1.0, 1.0])
+    for i in range(len(params)):
+        assert np.array_equal(w.read_current_state(i).view(np.uint32), np.concatenate(states[i][:3]).view(np.uint32))
+        assert np.array_equal(w.read_params16(i), states[i][3])
+    tl = w.last_timeline()
+    assert len(tl) == len(params) and all(s["k_end"] >= s["k_start"] for s in tl)
+    w.close()
