@@ -1,0 +1,106 @@
+"""Turns the ncu outputs brought back in gpurun_out/ into committed
+summaries under profiles/:
+  launches.csv (gpu__time_duration per launch) -> profiles/<tag>_launches.md
+  prof_adam.ncu-rep (--set full, fused kernel) -> profiles/ncu_adam_fused.json
+                                                 + profiles/<tag>_ncu_adam_fused.txt
+
+    python scripts/summarize_ncu.py <tag>
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+from collections import defaultdict
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "gpurun_out"
+PROF = ROOT / "profiles"
+tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
+PROF.mkdir(exist_ok=True)
+
+UNIT = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}
+
+launches = OUT / "launches.csv"
+if launches.exists():
+    rows = list(csv.reader(open(launches)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = defaultdict(lambda: [0, 0.0])
+    for r in rows[start + 1:]:
+        name = r[ki].split("(")[0]
+        agg[name][0] += 1
+        agg[name][1] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
+    total = sum(v[1] for v in agg.values())
+    lines = [f"# ncu launch list ({tag}): `ncu --metrics gpu__time_duration.sum --clock-control none "
+             f"python bench.py --steps 2 --warmup 1 --skip-e2e --skip-cpu`",
+             "", "Cold-cache, serialised per-launch times: compare shares, not absolutes.", "",
+             "| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
+    for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| `{name}` | {c} | {t:.1f} | {t / c:.1f} | {100 * t / total:.2f}% |")
+    (PROF / f"{tag}_launches.md").write_text("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+rep = OUT / "prof_adam.ncu-rep"
+if rep.exists():
+    raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units, vals = rows[0], rows[1], rows[2]
+    get = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
+
+    def num(key, scale=1.0):
+        v, u = get.get(key, ("nan", ""))
+        try:
+            x = float(v.replace(",", ""))
+        except ValueError:
+            return None
+        if u in ("Gbyte",):
+            x *= 1e9
+        elif u in ("Mbyte",):
+            x *= 1e6
+        elif u in ("Kbyte",):
+            x *= 1e3
+        elif u in ("usecond", "us"):
+            x *= 1e-6
+        elif u in ("nsecond", "ns"):
+            x *= 1e-9
+        elif u in ("msecond", "ms"):
+            x *= 1e-3
+        return x * scale
+
+    keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+            "launch__occupancy_limit_registers", "launch__grid_size", "launch__block_size",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second",
+            "launch__func_cache_config", "smsp__inst_executed.sum"]
+    text = [f"# ncu --set full, fused Adam kernel ({tag}); scripts/profile_kernel.py (100M params, f16 grads)"]
+    for k in keys:
+        if k in get:
+            text.append(f"{k} = {get[k][0]} {get[k][1]}")
+    stalls = sorted(((h, v) for h, v in get.items() if "smsp__average_warp_latency_issue_stalled" in h
+                     or ("warp_issue_stalled" in h and "pct" in h)), key=lambda x: x[0])
+    for h, (v, u) in stalls[:40]:
+        text.append(f"{h} = {v} {u}")
+    name = get.get("Kernel Name", ("?", ""))[0]
+    dur = num("gpu__time_duration.sum")
+    rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
+    n = 100_000_000
+    summary = {"kernel": name, "params_per_launch": n, "duration_s": dur, "dram_bytes_read": rd,
+               "dram_bytes_write": wr, "dram_bytes_per_launch": (rd or 0) + (wr or 0),
+               "algorithmic_bytes_per_launch": 28 * n,
+               "traffic_over_algorithmic": ((rd or 0) + (wr or 0)) / (28 * n),
+               "registers": num("launch__registers_per_thread"),
+               "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
+               "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+               "xu_pipe_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
+               "dram_throughput_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+               "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+               "tag": tag, "source": "gpurun_out/prof_adam.ncu-rep (ncu --set full --clock-control none)"}
+    (PROF / "ncu_adam_fused.json").write_text(json.dumps(summary, indent=1) + "\n")
+    (PROF / f"{tag}_ncu_adam_fused.txt").write_text("\n".join(text) + "\n")
+    print(json.dumps(summary, indent=1))
