@@ -71,3 +71,36 @@ def test_engine_refuses_without_gpu_or_reports_device(tf):
     t = tf.Tier(tf.TierSpec(0, tf.TierKind.mem_throttled, "m", 1e9, 1e9))
     with pytest.raises(tf.CudaError):
         tf.OffloadWorker(0, [t], tf.ScheduleOptions(), tf.AdamHyper(), tf.EventTrace())
+
+
+def test_cxx_adapter_compiles_links_and_runs(tf, tmp_path):
+    """include/tierflow_b200.hpp: a reference-style C++ caller against the
+    shared library (host-only calls; no GPU needed)."""
+    lib = ROOT / "paper_2509_02480_b200" / "lib"
+    src = tmp_path / "adapter.cpp"
+    src.write_text(r'''
+#include "tierflow_b200.hpp"
+#include <cstdio>
+using namespace tierflow_b200;
+int main() {
+    auto a = assign_subgroups(12, {2.0, 1.0});
+    if (a.counts != std::vector<int>{8, 4}) return 1;
+    try { assign_subgroups(0, {1.0}); return 2; } catch (const ConfigError&) {}
+    TierSpec s; s.kind = TierKind::mem_throttled; s.root = "m"; s.read_bw = 1e9; s.write_bw = 1e9;
+    Tier t(s);
+    std::vector<float> st(300), back;
+    for (int i = 0; i < 300; ++i) st[i] = 0.5f * i;
+    t.write_subgroup(7, 100, st);
+    t.read_subgroup(7, 100, back);
+    if (back != st) return 3;
+    try { t.read_subgroup(8, 100, back); return 4; } catch (const PlacementInconsistencyError&) {}
+    EventTrace trace;
+    std::puts("adapter ok");
+    return 0;
+}
+''')
+    exe = tmp_path / "adapter"
+    subprocess.run(["g++", "-std=c++20", "-Wall", "-Werror", "-I", str(ROOT / "include"), str(src), "-o", str(exe),
+                    "-L", str(lib), "-ltierflow_b200", f"-Wl,-rpath,{lib}"], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and "adapter ok" in out.stdout, (out.returncode, out.stdout, out.stderr)
