@@ -272,6 +272,20 @@ def pcie_probe():
     return out
 
 
+def e2e_shard(sizes, world, pool_slots):
+    """Subgroups each rank streams in the e2e leg. The host-DRAM tier pins
+    12 B/param per rank (plus the pool slots); with N ranks on one host the
+    shard is capped to 60% of MemAvailable so N concurrent ranks fit."""
+    try:
+        avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable:"))
+    except (OSError, StopIteration):
+        return sizes
+    per_rank = 0.6 * avail / world
+    block = 12 * max(sizes) + 4096
+    fit = int(per_rank // block) - pool_slots
+    return sizes[:max(1, min(len(sizes), fit))]
+
+
 def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring):
     # The bandwidth EMA re-places subgroups off the slow directory tier over the
     # first phases (paper §3.3); time the converged pipeline.
@@ -448,7 +462,10 @@ def main(argv=None):
     e2e = None
     if not a.skip_e2e:
         try:
-            r = e2e_leg(tf, sizes, base_id, a.steps, a.warmup, a.seed, rank, world, a.tier_root, a.pool_slots,
+            e_sizes = e2e_shard(sizes, world, a.pool_slots)
+            if len(e_sizes) < len(sizes):
+                log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank")
+            r = e2e_leg(tf, e_sizes, base_id, a.steps, a.warmup, a.seed, rank, world, a.tier_root, a.pool_slots,
                         a.cache_slots, a.ring)
             e_ms = allmax(world, r["ms"])
             e2e = {"value": world * r["params"] / (e_ms / 1e3), "unit": "params/s",
