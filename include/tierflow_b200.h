@@ -41,8 +41,9 @@ typedef enum tfg_status {
     TFG_CUDA_ERROR = 8               /* CUDA runtime failure (no reference counterpart)      */
 } tfg_status;
 
-/* 16-bit element kinds for gradients and working parameters. */
-typedef enum tfg_dtype { TFG_F16 = 0, TFG_BF16 = 1 } tfg_dtype;
+/* Element kinds: gradients F16 / BF16 / F32 (F32 = the ZeRO-3 baseline flow's
+ * stored fp32 gradients); working parameters F16 / BF16. */
+typedef enum tfg_dtype { TFG_F16 = 0, TFG_BF16 = 1, TFG_F32 = 2 } tfg_dtype;
 
 /* Tier kinds: tier.hpp:32 plus TFG_HOST_DRAM (pinned host blobs, zero-copy). */
 typedef enum tfg_tier_kind {
@@ -180,11 +181,19 @@ int tfg_device_count(int* count);
  * scheduler.hpp:467-490). t >= 1 is the Adam timestep; bc1/bc2 are computed on
  * the host with pow() as optimizer.hpp:129-130. counters (device, 2 x u64) are
  * accumulated: [0] += non-finite gradients, [1] += +-Inf 16-bit outputs. */
-int tfg_adam_fused(float* p, float* m, float* v, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+int tfg_adam_fused(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
                    int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
                    unsigned long long* counters, void* stream);
+/* Reduce + update in one pass: the gradient is the fp32 sum, in source order,
+ * of n_sources (<= 8) 16-bit buffers — e.g. every data-parallel peer's
+ * contribution to this rank's subgroup, read over NVLink through mapped peer
+ * pointers — rounded once to grad_dtype, then the fused Adam step. Replaces a
+ * reduce-scatter followed by tfg_adam_fused. */
+int tfg_adam_fused_multi(float* p, float* m, float* v, const void* const* grads, int n_sources, int grad_dtype,
+                         uint16_t* param16, int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                         unsigned long long* counters, void* stream);
 /* Same on one contiguous P||m||v state (StateView::from_contiguous, optimizer.hpp:82-86). */
-int tfg_adam_fused_contiguous(float* state, uint64_t n, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+int tfg_adam_fused_contiguous(float* state, uint64_t n, const void* grad, int grad_dtype, uint16_t* param16,
                               int param_dtype, const tfg_adam_hyper* hyper, uint64_t t,
                               unsigned long long* counters, void* stream);
 /* Reference-semantics synchronous step (adam_step, optimizer.hpp:116-157):

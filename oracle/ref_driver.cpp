@@ -175,6 +175,7 @@ struct RefRunCfg {
     int accum_steps;
     double lr, beta1, beta2, eps, weight_decay;
     uint32_t skip_mask;  // bit i: skip iteration i's update (non-finite step)
+    int skip_gradients;  // 0: the ZeRO-3 baseline flow (fp32 gradients through storage)
 };
 
 struct RefIterOut {
@@ -219,7 +220,7 @@ int ref_run_engine(const RefRunCfg* c, RefIterOut* iters_out, float* states_out,
         o.pool_slots = c->pool_slots;
         o.cache_slots = c->cache_slots;
         o.enable_caching = c->enable_caching != 0;
-        o.skip_gradients = true;
+        o.skip_gradients = c->skip_gradients != 0;
         o.atomic_rw = c->atomic_rw != 0;
         o.multi_path = c->multi_path != 0;
         o.update_threads = c->update_threads;

@@ -122,6 +122,8 @@ _SIGS = {
     "tfg_device_count": (_i, [C.POINTER(_i)]),
     "tfg_adam_fused": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
     "tfg_adam_fused_contiguous": (_i, [_vp, _u64, _vp, _i, _vp, _i, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
+    "tfg_adam_fused_multi": (_i, [_vp, _vp, _vp, C.POINTER(_vp), _i, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
+                                  _vp, _vp]),
     "tfg_adam_step": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
                            C.POINTER(_u64), _vp]),
     "tfg_adam_variant_count": (_i, [C.POINTER(_i)]),

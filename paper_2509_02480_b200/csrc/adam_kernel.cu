@@ -23,14 +23,102 @@ using namespace detail;
 
 namespace {
 
-// VEC = true: P, m, v 16-byte aligned and g, p16 8-byte aligned; the body
-// walks quads (float4 / 4 x 16-bit) and the n % 4 tail is scalar.
-// VEC = false: scalar everywhere (e.g. a contiguous P||m||v with P % 4 != 0).
-template <int GK, int OK, bool WD, bool VEC, int UNROLL, bool DIVC, int MINB>
+// Gradient sources of one launch. GMODE 0: one 16-bit buffer (GK = F16 or
+// BF16). GMODE 1: one fp32 buffer (GK = F32; the ZeRO-3 baseline flow that
+// fetches fp32 gradients from storage). GMODE 2: the sum of n 16-bit buffers,
+// e.g. the same subgroup's gradient contributions in every data-parallel
+// peer's memory over NVLink: summed in fp32 in source order, rounded once to
+// GK — the reduce-scatter fused into the update.
+struct GradSources {
+    const void* src[kMaxGradSources];
+    int n;
+};
+
+template <int GK, int GMODE>
+__device__ __forceinline__ float4 load_grad4(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
+    if constexpr (GMODE == 1) {
+        const float4 f = __ldcs(reinterpret_cast<const float4*>(gs.src[0]) + q);
+        nonfinite += !isfinite(f.x) + !isfinite(f.y) + !isfinite(f.z) + !isfinite(f.w);
+        return f;
+    } else {
+        U16x4 h;
+        if constexpr (GMODE == 0) {
+            h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
+        } else {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int s = 0; s < kMaxGradSources; ++s) {
+                if (s < gs.n) {
+                    const U16x4 x = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q);
+                    acc.x = __fadd_rn(acc.x, widen16<GK>(x.x));
+                    acc.y = __fadd_rn(acc.y, widen16<GK>(x.y));
+                    acc.z = __fadd_rn(acc.z, widen16<GK>(x.z));
+                    acc.w = __fadd_rn(acc.w, widen16<GK>(x.w));
+                }
+            }
+            h.x = narrow16<GK>(acc.x);
+            h.y = narrow16<GK>(acc.y);
+            h.z = narrow16<GK>(acc.z);
+            h.w = narrow16<GK>(acc.w);
+        }
+        nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
+        return make_float4(widen16<GK>(h.x), widen16<GK>(h.y), widen16<GK>(h.z), widen16<GK>(h.w));
+    }
+}
+
+// Register form of one gradient quad: a single 16-bit source stays packed
+// (2 registers) and is widened at use; fp32 and summed sources hold floats.
+template <int GK, int GMODE>
+struct GradReg {
+    float4 f;
+    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
+        f = load_grad4<GK, GMODE>(gs, q, nonfinite);
+    }
+    __device__ __forceinline__ float get(int k) const { return k == 0 ? f.x : k == 1 ? f.y : k == 2 ? f.z : f.w; }
+};
+
+template <int GK>
+struct GradReg<GK, 0> {
+    U16x4 h;
+    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
+        h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
+        nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
+    }
+    __device__ __forceinline__ float get(int k) const {
+        return widen16<GK>(k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w);
+    }
+};
+
+template <int GK, int GMODE>
+__device__ __forceinline__ float load_grad1(const GradSources& gs, uint64_t i, unsigned& nonfinite) {
+    if constexpr (GMODE == 1) {
+        const float f = __ldcs(reinterpret_cast<const float*>(gs.src[0]) + i);
+        nonfinite += !isfinite(f);
+        return f;
+    } else {
+        uint16_t h;
+        if constexpr (GMODE == 0) {
+            h = __ldcs(reinterpret_cast<const uint16_t*>(gs.src[0]) + i);
+        } else {
+            float acc = 0.f;
+#pragma unroll
+            for (int s = 0; s < kMaxGradSources; ++s)
+                if (s < gs.n) acc = __fadd_rn(acc, widen16<GK>(__ldcs(reinterpret_cast<const uint16_t*>(gs.src[s]) + i)));
+            h = narrow16<GK>(acc);
+        }
+        nonfinite += nonfinite16<GK>(h);
+        return widen16<GK>(h);
+    }
+}
+
+// VEC = true: P, m, v 16-byte aligned and the gradient / p16 streams 8-byte
+// (16-bit) or 16-byte (fp32) aligned; the body walks quads (float4 / 4 x
+// 16-bit) and the n % 4 tail is scalar. VEC = false: scalar everywhere (e.g.
+// a contiguous P||m||v with P % 4 != 0).
+template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, bool DIVC, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-    adam_fused_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                      const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t n,
-                      AdamConsts c, unsigned long long* __restrict__ counters) {
+    adam_fused_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const GradSources gs,
+                      uint16_t* __restrict__ p16, uint64_t n, AdamConsts c, unsigned long long* __restrict__ counters) {
     unsigned nonfinite = 0, overflow = 0;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -42,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         float4* v4 = reinterpret_cast<float4*>(v);
         for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
             float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
-            U16x4 rg[UNROLL];
+            GradReg<GK, GMODE> rg[UNROLL];
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {  // all loads first: UNROLL quads in flight
                 const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
@@ -50,19 +138,17 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     rp[u] = __ldcs(p4 + q);
                     rm[u] = __ldcs(m4 + q);
                     rv[u] = __ldcs(v4 + q);
-                    rg[u] = load_u16x4(g + 4 * q);
+                    rg[u].load(gs, q, nonfinite);
                 }
             }
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {
                 const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
                 if (q < nq) {
-                    nonfinite += nonfinite16<GK>(rg[u].x) + nonfinite16<GK>(rg[u].y) +
-                                 nonfinite16<GK>(rg[u].z) + nonfinite16<GK>(rg[u].w);
-                    adam_element<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, widen16<GK>(rg[u].x), c);
-                    adam_element<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, widen16<GK>(rg[u].y), c);
-                    adam_element<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, widen16<GK>(rg[u].z), c);
-                    adam_element<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, widen16<GK>(rg[u].w), c);
+                    adam_element<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
+                    adam_element<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
+                    adam_element<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
+                    adam_element<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
                     U16x4 h;
                     h.x = narrow16<OK>(rp[u].x);
                     h.y = narrow16<OK>(rp[u].y);
@@ -79,9 +165,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const uint64_t i = nq * 4 + tid;  // scalar tail: n % 4 elements
         if (i < n) {
             float pf = p[i], mf = m[i], vf = v[i];
-            const uint16_t gh = g[i];
-            nonfinite += nonfinite16<GK>(gh);
-            adam_element<WD, DIVC>(pf, mf, vf, widen16<GK>(gh), c);
+            const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
+            adam_element<WD, DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
             p[i] = pf;
@@ -92,9 +177,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     } else {
         for (uint64_t i = tid; i < n; i += nthreads) {
             float pf = __ldcs(p + i), mf = __ldcs(m + i), vf = __ldcs(v + i);
-            const uint16_t gh = __ldcs(g + i);
-            nonfinite += nonfinite16<GK>(gh);
-            adam_element<WD, DIVC>(pf, mf, vf, widen16<GK>(gh), c);
+            const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
+            adam_element<WD, DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
             __stcs(p + i, pf);
@@ -116,39 +200,66 @@ struct Cfg {
     static constexpr int kMinBlocks = MINB;
 };
 
-bool is_vec(const AdamLaunch& a) {
-    return ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) | reinterpret_cast<uintptr_t>(a.v)) &
-            15u) == 0 &&
-           ((reinterpret_cast<uintptr_t>(a.g) | reinterpret_cast<uintptr_t>(a.p16)) & 7u) == 0;
+GradSources sources_of(const AdamLaunch& a) {
+    GradSources gs{};
+    if (a.n_peers > 0) {
+        for (int s = 0; s < a.n_peers; ++s) gs.src[s] = a.peers[s];
+        gs.n = a.n_peers;
+    } else {
+        gs.src[0] = a.g;
+        gs.n = 1;
+    }
+    return gs;
 }
 
-template <int GK, int OK, bool WD, class C>
+bool is_vec(const AdamLaunch& a) {
+    const uintptr_t state = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                            reinterpret_cast<uintptr_t>(a.v);
+    uintptr_t grads = 0;
+    const GradSources gs = sources_of(a);
+    for (int s = 0; s < gs.n; ++s) grads |= reinterpret_cast<uintptr_t>(gs.src[s]);
+    const uintptr_t galign = a.grad_kind == kF32 ? 15u : 7u;
+    return (state & 15u) == 0 && (grads & galign) == 0 && (reinterpret_cast<uintptr_t>(a.p16) & 7u) == 0;
+}
+
+template <int GK, int GMODE, int OK, bool WD, class C>
 cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     constexpr int U = C::kUnroll;
     constexpr int B = C::kMinBlocks;
+    const GradSources gs = sources_of(a);
     if (is_vec(a)) {
         const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
-        adam_fused_kernel<GK, OK, WD, true, U, C::kDivc, B>
-            <<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p16, a.n, a.c, a.counters);
+        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B>
+            <<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters);
     } else {
         const unsigned grid = grid_for(a.n, B);
-        adam_fused_kernel<GK, OK, WD, false, 1, C::kDivc, B>
-            <<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p16, a.n, a.c, a.counters);
+        adam_fused_kernel<GK, GMODE, OK, WD, false, 1, C::kDivc, B>
+            <<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters);
     }
     return cudaGetLastError();
 }
 
-template <int GK, int OK, class C>
+template <int GK, int GMODE, int OK, class C>
 cudaError_t launch_wd(const AdamLaunch& a, cudaStream_t stream) {
-    return a.c.lr_wd != 0.0 ? launch_cfg<GK, OK, true, C>(a, stream) : launch_cfg<GK, OK, false, C>(a, stream);
+    return a.c.lr_wd != 0.0 ? launch_cfg<GK, GMODE, OK, true, C>(a, stream)
+                            : launch_cfg<GK, GMODE, OK, false, C>(a, stream);
 }
 
 template <class C>
 cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
-    if (a.grad_kind == kF16 && a.out_kind == kF16) return launch_wd<kF16, kF16, C>(a, stream);
-    if (a.grad_kind == kF16 && a.out_kind == kBF16) return launch_wd<kF16, kBF16, C>(a, stream);
-    if (a.grad_kind == kBF16 && a.out_kind == kF16) return launch_wd<kBF16, kF16, C>(a, stream);
-    return launch_wd<kBF16, kBF16, C>(a, stream);
+    if (a.out_kind != kF16 && a.out_kind != kBF16) return cudaErrorInvalidValue;
+    if (a.n_peers > 0) {  // fused multi-source reduction: 16-bit sources, same kind in and out
+        if (a.n_peers > kMaxGradSources || a.grad_kind == kF32) return cudaErrorInvalidValue;
+        if (a.grad_kind == kF16)
+            return a.out_kind == kF16 ? launch_wd<kF16, 2, kF16, C>(a, stream) : launch_wd<kF16, 2, kBF16, C>(a, stream);
+        return a.out_kind == kF16 ? launch_wd<kBF16, 2, kF16, C>(a, stream) : launch_wd<kBF16, 2, kBF16, C>(a, stream);
+    }
+    if (a.grad_kind == kF32)
+        return a.out_kind == kF16 ? launch_wd<kF32, 1, kF16, C>(a, stream) : launch_wd<kF32, 1, kBF16, C>(a, stream);
+    if (a.grad_kind == kF16 && a.out_kind == kF16) return launch_wd<kF16, 0, kF16, C>(a, stream);
+    if (a.grad_kind == kF16 && a.out_kind == kBF16) return launch_wd<kF16, 0, kBF16, C>(a, stream);
+    if (a.grad_kind == kBF16 && a.out_kind == kF16) return launch_wd<kBF16, 0, kF16, C>(a, stream);
+    return launch_wd<kBF16, 0, kBF16, C>(a, stream);
 }
 
 // Shipped configuration: one quad per thread per iteration, constant-divisor
@@ -160,17 +271,17 @@ using VariantDefault = Cfg<1, true, 4>;
 // Tuning variants (F16 gradients and params only), for the kernel sweep.
 template <int V>
 cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
-    if constexpr (V == 1) return launch_wd<kF16, kF16, Cfg<2, false, 1>>(a, stream);
-    if constexpr (V == 2) return launch_wd<kF16, kF16, Cfg<1, false, 4>>(a, stream);
-    if constexpr (V == 3) return launch_wd<kF16, kF16, Cfg<2, false, 3>>(a, stream);
-    if constexpr (V == 4) return launch_wd<kF16, kF16, Cfg<1, true, 4>>(a, stream);
-    if constexpr (V == 5) return launch_wd<kF16, kF16, Cfg<2, true, 3>>(a, stream);
-    if constexpr (V == 6) return launch_wd<kF16, kF16, Cfg<2, true, 2>>(a, stream);
-    if constexpr (V == 7) return launch_wd<kF16, kF16, Cfg<1, true, 3>>(a, stream);
-    if constexpr (V == 8) return launch_wd<kF16, kF16, Cfg<4, true, 2>>(a, stream);
-    if constexpr (V == 9) return launch_wd<kF16, kF16, Cfg<1, true, 5>>(a, stream);
-    if constexpr (V == 10) return launch_wd<kF16, kF16, Cfg<2, true, 4>>(a, stream);
-    if constexpr (V == 11) return launch_wd<kF16, kF16, Cfg<1, true, 6>>(a, stream);
+    if constexpr (V == 1) return launch_wd<kF16, 0, kF16, Cfg<2, false, 1>>(a, stream);
+    if constexpr (V == 2) return launch_wd<kF16, 0, kF16, Cfg<1, false, 4>>(a, stream);
+    if constexpr (V == 3) return launch_wd<kF16, 0, kF16, Cfg<2, false, 3>>(a, stream);
+    if constexpr (V == 4) return launch_wd<kF16, 0, kF16, Cfg<1, true, 4>>(a, stream);
+    if constexpr (V == 5) return launch_wd<kF16, 0, kF16, Cfg<2, true, 3>>(a, stream);
+    if constexpr (V == 6) return launch_wd<kF16, 0, kF16, Cfg<2, true, 2>>(a, stream);
+    if constexpr (V == 7) return launch_wd<kF16, 0, kF16, Cfg<1, true, 3>>(a, stream);
+    if constexpr (V == 8) return launch_wd<kF16, 0, kF16, Cfg<4, true, 2>>(a, stream);
+    if constexpr (V == 9) return launch_wd<kF16, 0, kF16, Cfg<1, true, 5>>(a, stream);
+    if constexpr (V == 10) return launch_wd<kF16, 0, kF16, Cfg<2, true, 4>>(a, stream);
+    if constexpr (V == 11) return launch_wd<kF16, 0, kF16, Cfg<1, true, 6>>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -212,7 +323,7 @@ cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
 cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
     if (variant == 0) return launch_adam_fused(a, stream);
-    if (a.grad_kind != kF16 || a.out_kind != kF16) return cudaErrorInvalidValue;
+    if (a.grad_kind != kF16 || a.out_kind != kF16 || a.n_peers > 0) return cudaErrorInvalidValue;
     switch (variant) {
         case 1: return launch_variant<1>(a, stream);
         case 2: return launch_variant<2>(a, stream);

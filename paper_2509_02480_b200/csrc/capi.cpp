@@ -64,6 +64,10 @@ void check_dtype(int d) {
     if (d != TFG_F16 && d != TFG_BF16) throw tfb::ConfigError("unknown 16-bit dtype " + std::to_string(d));
 }
 
+void check_grad_dtype(int d) {
+    if (d != TFG_F16 && d != TFG_BF16 && d != TFG_F32) throw tfb::ConfigError("unknown gradient dtype " + std::to_string(d));
+}
+
 tfb::AdamHyper to_hyper(const tfg_adam_hyper* h) {
     need(h, "hyper");
     tfb::AdamHyper a;
@@ -77,9 +81,9 @@ tfb::AdamHyper to_hyper(const tfg_adam_hyper* h) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-tfb::AdamLaunch adam_launch(float* p, float* m, float* v, const uint16_t* g, int gk, uint16_t* p16, int ok,
+tfb::AdamLaunch adam_launch(float* p, float* m, float* v, const void* g, int gk, uint16_t* p16, int ok,
                             uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters) {
-    check_dtype(gk);
+    check_grad_dtype(gk);
     check_dtype(ok);
     if (n > 0) {
         need(p, "p");
@@ -125,7 +129,7 @@ int tfg_device_count(int* count) {
 
 // ---- kernels -------------------------------------------------------------------
 
-int tfg_adam_fused(float* p, float* m, float* v, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+int tfg_adam_fused(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
                    int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
                    unsigned long long* counters, void* stream) {
     return guarded([&] {
@@ -134,7 +138,23 @@ int tfg_adam_fused(float* p, float* m, float* v, const uint16_t* grad, int grad_
     });
 }
 
-int tfg_adam_fused_contiguous(float* state, uint64_t n, const uint16_t* grad, int grad_dtype, uint16_t* param16,
+int tfg_adam_fused_multi(float* p, float* m, float* v, const void* const* grads, int n_sources, int grad_dtype,
+                         uint16_t* param16, int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                         unsigned long long* counters, void* stream) {
+    return guarded([&] {
+        check_dtype(grad_dtype);
+        if (n_sources < 1 || n_sources > tfb::kMaxGradSources)
+            throw tfb::ConfigError("n_sources must be in [1, " + std::to_string(tfb::kMaxGradSources) + "]");
+        need(grads, "grads");
+        for (int s = 0; s < n_sources; ++s) need(grads[s], "grads[s]");
+        auto a = adam_launch(p, m, v, grads[0], grad_dtype, param16, param_dtype, n, hyper, t, counters);
+        for (int s = 0; s < n_sources; ++s) a.peers[s] = grads[s];
+        a.n_peers = n_sources;
+        tfb::cuda_check(tfb::launch_adam_fused(a, as_stream(stream)), "adam_fused_multi");
+    });
+}
+
+int tfg_adam_fused_contiguous(float* state, uint64_t n, const void* grad, int grad_dtype, uint16_t* param16,
                               int param_dtype, const tfg_adam_hyper* hyper, uint64_t t,
                               unsigned long long* counters, void* stream) {
     return guarded([&] {
@@ -149,6 +169,7 @@ int tfg_adam_step(float* p, float* m, float* v, const uint16_t* grad, int grad_d
                   int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, uint64_t* overflows_out,
                   void* stream) {
     return guarded([&] {
+        check_dtype(grad_dtype);  // the pre-check counts 16-bit patterns
         auto a = adam_launch(p, m, v, grad, grad_dtype, param16, param_dtype, n, hyper, t, nullptr);
         cudaStream_t s = as_stream(stream);
         unsigned long long* dc = nullptr;

@@ -92,10 +92,10 @@ const char* slot_state_name(SlotState s) {
     return "unknown";
 }
 
-HostBufferPool::HostBufferPool(int slot_count, std::uint64_t max_params, bool require_pinned) {
+HostBufferPool::HostBufferPool(int slot_count, std::size_t block_bytes, bool require_pinned) {
     if (slot_count < 3) throw ConfigError("host buffer pool needs >= 3 slots");
     slots_.resize(static_cast<std::size_t>(slot_count));
-    for (auto& s : slots_) s.block = HostBlock::allocate(block_bytes_for(max_params), require_pinned);
+    for (auto& s : slots_) s.block = HostBlock::allocate(block_bytes, require_pinned);
 }
 
 std::size_t HostBufferPool::check(int slot) const {
@@ -357,6 +357,13 @@ void OffloadWorker::setup_device() {
     ring_.assign(static_cast<std::size_t>(dev_.device_buffers), nullptr);
     for (auto& r : ring_)
         cuda_check(cudaMalloc(reinterpret_cast<void**>(&r), 3 * ring_stride_ * sizeof(float)), "cudaMalloc(ring)");
+    if (!opt_.skip_gradients) {
+        ring_grad_.assign(ring_.size(), nullptr);
+        for (auto& r : ring_grad_)
+            cuda_check(cudaMalloc(reinterpret_cast<void**>(&r), ring_stride_ * sizeof(float)), "cudaMalloc(ring grads)");
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&grad32_dev_), ring_stride_ * sizeof(float)), "cudaMalloc");
+        grad_stage_ = HostBlock::allocate(4 * static_cast<std::size_t>(max_params_), true);
+    }
     std::size_t arena = 0;
     std::vector<std::size_t> offs;
     for (const SubgroupId id : ids_) {
@@ -396,6 +403,10 @@ void OffloadWorker::release_device() {
     events_.clear();
     for (float* r : ring_) cudaFree(r);
     ring_.clear();
+    for (float* r : ring_grad_) cudaFree(r);
+    ring_grad_.clear();
+    if (grad32_dev_) cudaFree(grad32_dev_);
+    grad32_dev_ = nullptr;
     cudaFree(grad_arena_);
     cudaFree(p16_arena_);
     cudaFree(counters_);
@@ -434,14 +445,16 @@ void OffloadWorker::init_and_flush_all(std::uint64_t seed) {
     if (pool_) throw Error("init_and_flush_all called twice");
     std::sort(ids_.begin(), ids_.end());
     DeviceGuard dg(dev_.device);
-    pool_ = std::make_unique<HostBufferPool>(opt_.pool_slots, max_params_, /*require_pinned=*/true);
-    for (auto& t : tiers_) t->reserve_block_bytes(block_bytes_for(max_params_));
+    state_block_bytes_ = block_bytes_for(max_params_);
+    annex_bytes_ = opt_.skip_gradients ? 0 : round_up(4 * static_cast<std::size_t>(max_params_), kPageBytes);
+    pool_ = std::make_unique<HostBufferPool>(opt_.pool_slots, state_block_bytes_ + annex_bytes_, /*require_pinned=*/true);
+    for (auto& t : tiers_) t->reserve_block_bytes(state_block_bytes_ + annex_bytes_);
     setup_device();
 
     const std::vector<SubgroupId> order = update_order(0, ids_, false);
     const DestinationPlan dests(order, 0, placement_bandwidths());
     // Generate on the GPU into the ring, copy into a staging slot, persist.
-    HostBlock staging = HostBlock::allocate(block_bytes_for(max_params_), true);
+    HostBlock staging = HostBlock::allocate(state_block_bytes_ + annex_bytes_, true);
     for (const SubgroupId id : order) {
         Subgroup& sg = subgroups_.at(id);
         const std::uint64_t pc = sg.param_count;
@@ -462,8 +475,6 @@ void OffloadWorker::init_and_flush_all(std::uint64_t seed) {
 void OffloadWorker::run_backward_sim(int iteration, std::uint64_t seed, int accum_steps) {
     if (accum_steps < 1) throw ConfigError("grad_accum_steps must be >= 1");
     if (!device_ready_) throw Error("run_backward_sim before init_and_flush_all");
-    if (!opt_.skip_gradients)
-        throw ConfigError("skip_gradients=false (fp32 gradients through storage) is not supported by the B200 engine");
     DeviceGuard dg(dev_.device);
     for (std::size_t k = 0; k < ids_.size(); ++k) {
         const SubgroupId id = ids_[k];
@@ -474,6 +485,65 @@ void OffloadWorker::run_backward_sim(int iteration, std::uint64_t seed, int accu
                        "synthetic_grads");
     }
     cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+    if (!opt_.skip_gradients) flush_grads_to_storage();
+}
+
+// ZeRO-3 data flow (reference scheduler.hpp:377-391): widen every subgroup's
+// accumulated gradient to fp32 (on the GPU here, traced as the upscale), copy
+// it to the host and flush it to the subgroup's current tier (tier 0 when the
+// subgroup is host-resident) through the tier's I/O queue; 4 bytes/param of
+// storage writes that the engine flow avoids.
+void OffloadWorker::flush_grads_to_storage() {
+    std::vector<std::future<IoStats>> pending;
+    for (std::size_t k = 0; k < ids_.size(); ++k) {
+        const SubgroupId id = ids_[k];
+        const std::uint64_t pc = subgroups_.at(id).param_count;
+        trace_->record(EventKind::grad_upscale_start, id_, id, kNoTier, 4 * pc);
+        cuda_check(launch_widen16(grad_ptr_[k], grad32_dev_, pc, dev_.grad_kind, nullptr, s_k_), "widen16");
+        cuda_check(cudaMemcpyAsync(grad_stage_.base(), grad32_dev_, 4 * pc, cudaMemcpyDeviceToHost, s_k_),
+                   "cudaMemcpyAsync(grads)");
+        cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+        auto grads32 = std::make_shared<std::vector<float>>(reinterpret_cast<const float*>(grad_stage_.base()),
+                                                             reinterpret_cast<const float*>(grad_stage_.base()) + pc);
+        trace_->record(EventKind::grad_upscale_end, id_, id, kNoTier, 4 * pc);
+        TierId dest;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            const Subgroup& sg = subgroups_.at(id);
+            dest = sg.residency == Residency::on_tier ? sg.tier : 0;
+            grad_tier_[id] = dest;
+        }
+        auto tier = tiers_[static_cast<std::size_t>(dest)];
+        pending.push_back(io_[static_cast<std::size_t>(dest)]->submit(
+            false, id, 4 * pc, [tier, id, pc, grads32] { return tier->write_grads(id, pc, grads32->data()); },
+            nullptr));
+    }
+    for (auto& f : pending) {
+        std::shared_future<IoStats> s = f.share();
+        watchdog_wait_value(s);
+    }
+}
+
+// Grad-only fetch for a host-retained subgroup (reference scheduler.hpp:746-765).
+void OffloadWorker::fetch_grads_for_cached(SubgroupId id) {
+    TierId gt;
+    std::uint64_t pc;
+    int slot;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        gt = grad_tier_.at(id);
+        pc = subgroups_.at(id).param_count;
+        slot = subgroups_.at(id).slot;
+    }
+    auto tier = tiers_[static_cast<std::size_t>(gt)];
+    float* dst = grad_annex(pool_->block(slot));
+    std::shared_future<IoStats> fut =
+        io_[static_cast<std::size_t>(gt)]
+            ->submit(true, id, 4 * pc, [tier, id, pc, dst] { return tier->read_grads(id, pc, dst); }, nullptr)
+            .share();
+    const IoStats st = watchdog_wait_value(fut);
+    std::lock_guard<std::mutex> g(mu_);
+    record_read_locked(id, gt, st, /*state_fetch=*/false);
 }
 
 void* OffloadWorker::grad_buffer(SubgroupId id) {
@@ -573,7 +643,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             Subgroup& sg = subgroups_.at(id);
             sg.step_count = static_cast<std::uint64_t>(iteration) + 1;
             stats.params_updated += sg.param_count;
-            stats.h2d_bytes += 12 * sg.param_count;
+            stats.h2d_bytes += (opt_.skip_gradients ? 12 : 16) * sg.param_count;
             stats.d2h_bytes += 12 * sg.param_count;
             if (completion_error_) std::rethrow_exception(completion_error_);
         }
@@ -689,6 +759,12 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
         a.p = hp;
         a.m = hp + pc;
         a.v = hp + 2 * pc;
+        if (!opt_.skip_gradients) {  // baseline flow: fp32 gradients from the slot's annex
+            void* hg = nullptr;
+            cuda_check(cudaHostGetDevicePointer(&hg, grad_annex(blk), 0), "cudaHostGetDevicePointer");
+            a.g = hg;
+            a.grad_kind = kF32;
+        }
         for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start})
             cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
         cuda_check(launch_spin_ns(opt_.update_pad_ns, s_k_), "spin");
@@ -704,6 +780,13 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     if (j >= K) cuda_check(cudaStreamWaitEvent(s_h2d_, events_[index_of_.at(order_[j - K])].d2h_end, 0), "wait");
     cuda_check(cudaEventRecord(e.h2d_start, s_h2d_), "cudaEventRecord");
     copy_state(d, blk, pc, true, s_h2d_);
+    if (!opt_.skip_gradients) {  // baseline flow: fp32 gradients fetched with the state
+        float* dg = ring_grad_[j % K];
+        cuda_check(cudaMemcpyAsync(dg, grad_annex(blk), 4 * pc, cudaMemcpyHostToDevice, s_h2d_),
+                   "cudaMemcpyAsync(grads)");
+        a.g = dg;
+        a.grad_kind = kF32;
+    }
     cuda_check(cudaEventRecord(e.h2d_done, s_h2d_), "cudaEventRecord");
 
     cuda_check(cudaStreamWaitEvent(s_k_, e.h2d_done, 0), "wait");
@@ -779,6 +862,7 @@ void OffloadWorker::completion_loop() {
 
 int OffloadWorker::wait_host_resident(SubgroupId id) {
     std::shared_future<IoStats> fut;
+    bool need_grad_fetch = false;
     {
         std::unique_lock<std::mutex> l(mu_);
         for (;;) {
@@ -791,6 +875,7 @@ int OffloadWorker::wait_host_resident(SubgroupId id) {
             if (sg.residency == Residency::host_cached) {
                 ++cache_hits_this_phase_;
                 trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
+                need_grad_fetch = !opt_.skip_gradients && grad_tier_.count(id) != 0;
                 break;
             }
             const int slot = pool_->try_reserve(id);
@@ -804,6 +889,7 @@ int OffloadWorker::wait_host_resident(SubgroupId id) {
         }
     }
     if (fut.valid()) watchdog_wait_value(fut);
+    if (need_grad_fetch) fetch_grads_for_cached(id);
     std::lock_guard<std::mutex> g(mu_);
     return subgroups_.at(id).slot;
 }
@@ -904,14 +990,27 @@ std::shared_future<IoStats> OffloadWorker::start_prefetch_locked(SubgroupId id, 
     const std::uint64_t pc = sg.param_count;
     auto tier = tiers_[static_cast<std::size_t>(origin)];
     HostBufferPool* pool = pool_.get();
-    auto transfer = [tier, id, pc, pool, slot] { return tier->read_into(id, pc, pool->block(slot)); };
+    // Baseline flow: the fp32 gradients stored with the state come along
+    // (16 bytes/param; reference scheduler.hpp:667-680).
+    const bool fetch_grads = !opt_.skip_gradients && grad_tier_.count(id) != 0 && grad_tier_.at(id) == origin;
+    const std::size_t annex_off = state_block_bytes_;
+    auto transfer = [tier, id, pc, pool, slot, fetch_grads, annex_off] {
+        IoStats st = tier->read_into(id, pc, pool->block(slot));
+        if (fetch_grads) {
+            float* dst = reinterpret_cast<float*>(pool->block(slot).base() + annex_off);
+            const IoStats gs = tier->read_grads(id, pc, dst);
+            st.bytes += gs.bytes;
+            st.seconds += gs.seconds;
+        }
+        return st;
+    };
     auto completion = [this, id, slot, origin](bool ok, const IoStats& st) {
         std::lock_guard<std::mutex> g(mu_);
         Subgroup& s = subgroups_.at(id);
         if (ok) {
             s.finish_prefetch(slot);
             pool_->prefetch_done(slot);
-            record_read_locked(id, origin, st);
+            record_read_locked(id, origin, st, /*state_fetch=*/true);
         } else {
             s.residency = Residency::on_tier;  // fetch failed: still on its tier
             s.slot = -1;
@@ -919,7 +1018,7 @@ std::shared_future<IoStats> OffloadWorker::start_prefetch_locked(SubgroupId id, 
         }
     };
     auto fut = io_[static_cast<std::size_t>(origin)]
-                   ->submit(true, id, 12 * pc, std::move(transfer), std::move(completion))
+                   ->submit(true, id, 12 * pc + (fetch_grads ? 4 * pc : 0), std::move(transfer), std::move(completion))
                    .share();
     prefetch_futures_[id] = fut;
     return fut;
@@ -960,7 +1059,7 @@ std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, Tie
     return fut;
 }
 
-void OffloadWorker::record_read_locked(SubgroupId id, TierId tier, const IoStats& st) {
+void OffloadWorker::record_read_locked(SubgroupId id, TierId tier, const IoStats& st, bool state_fetch) {
     if (phase_stats_ == nullptr) return;
     auto& obs = phase_stats_->tier_obs[static_cast<std::size_t>(tier)];
     obs.read_transfers += 1;
@@ -968,7 +1067,7 @@ void OffloadWorker::record_read_locked(SubgroupId id, TierId tier, const IoStats
     obs.read_seconds += st.seconds;
     auto& io = subgroup_io_entry_locked(id);
     io.read_seconds += st.seconds;
-    io.fetched = true;
+    if (state_fetch) io.fetched = true;
 }
 
 void OffloadWorker::record_write_locked(SubgroupId id, TierId tier, const IoStats& st) {

@@ -146,7 +146,7 @@ const char* slot_state_name(SlotState s);
 
 class HostBufferPool {
 public:
-    HostBufferPool(int slot_count, std::uint64_t max_params, bool require_pinned);
+    HostBufferPool(int slot_count, std::size_t block_bytes, bool require_pinned);
 
     int slot_count() const { return static_cast<int>(slots_.size()); }
     int try_reserve(SubgroupId owner);
@@ -284,8 +284,14 @@ private:
     void pump_locked();
     std::shared_future<IoStats> start_prefetch_locked(SubgroupId id, int slot);
     std::shared_future<IoStats> start_flush_locked(SubgroupId id, TierId dest, int slot);
-    void record_read_locked(SubgroupId id, TierId tier, const IoStats& st);
+    void record_read_locked(SubgroupId id, TierId tier, const IoStats& st, bool state_fetch);
     void record_write_locked(SubgroupId id, TierId tier, const IoStats& st);
+    // ZeRO-3 baseline flow (skip_gradients = false): fp32 gradients through storage.
+    void flush_grads_to_storage();
+    void fetch_grads_for_cached(SubgroupId id);
+    float* grad_annex(const HostBlock& blk) const {
+        return reinterpret_cast<float*>(blk.base() + state_block_bytes_);
+    }
     SubgroupIoTimes& subgroup_io_entry_locked(SubgroupId id);
     void wait_pool_free();
 
@@ -326,6 +332,12 @@ private:
     bool device_ready_ = false;
     cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr, s_d2h2_ = nullptr;
     std::vector<float*> ring_;
+    std::vector<float*> ring_grad_;  // baseline flow: fp32 gradient segment per ring buffer
+    float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H
+    HostBlock grad_stage_;           // baseline flow: pinned D2H staging of fp32 gradients
+    std::size_t state_block_bytes_ = 0;  // header + P||m||v of the largest subgroup, 4 KiB multiple
+    std::size_t annex_bytes_ = 0;        // baseline flow: fp32 gradient annex after the state
+    std::unordered_map<SubgroupId, TierId> grad_tier_;  // tier holding each subgroup's fp32 gradients
     std::uint64_t ring_stride_ = 0;  // floats per segment (P, m, v each) in a ring buffer
     void* grad_arena_ = nullptr;
     void* p16_arena_ = nullptr;

@@ -10,14 +10,20 @@
 
 namespace tfb {
 
-
+// Maximum gradient sources of one fused launch (the data-parallel peers whose
+// contributions the fused reduce + update sums).
+constexpr int kMaxGradSources = 8;
 
 struct AdamLaunch {
     float* p = nullptr;  // fp32 master params, in place
     float* m = nullptr;  // fp32 first moment, in place
     float* v = nullptr;  // fp32 second moment, in place
-    const uint16_t* g = nullptr;  // 16-bit gradient (grad_kind)
-    uint16_t* p16 = nullptr;      // 16-bit working params out (out_kind)
+    const void* g = nullptr;  // gradient: 16-bit (grad_kind F16/BF16) or fp32 (grad_kind F32)
+    // n_peers > 0: the gradient is the fp32 sum over these 16-bit sources (in
+    // order), rounded once to grad_kind; g is ignored.
+    const void* peers[kMaxGradSources] = {};
+    int n_peers = 0;
+    uint16_t* p16 = nullptr;  // 16-bit working params out (out_kind)
     uint64_t n = 0;
     int grad_kind = 0;
     int out_kind = 0;

@@ -6,7 +6,9 @@
 namespace tfb {
 
 // Gradient / working-parameter element kinds (16-bit storage).
-enum Half16Kind : int { kF16 = 0, kBF16 = 1 };
+// kF32 is a gradient kind only: the ZeRO-3 baseline flow fetches fp32
+// gradients from storage (reference scheduler.hpp:377-391, 667-680).
+enum Half16Kind : int { kF16 = 0, kBF16 = 1, kF32 = 2 };
 
 // Per-launch Adam constants, all computed on the host in double exactly as the
 // reference does (bc_k = 1 - pow(beta_k, t), reference optimizer.hpp:129-130).

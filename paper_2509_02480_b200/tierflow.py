@@ -693,6 +693,22 @@ def adam_fused(p, m, v, grad16, param16, t: int, hyper: AdamHyper = AdamHyper(),
               C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
 
 
+def adam_fused_multi(p, m, v, grads: Sequence, param16, t: int, hyper: AdamHyper = AdamHyper(),
+                     grad_dtype: int = F16, param_dtype: int = F16, counters=None, stream=None) -> None:
+    """Reduce + update in one pass: the gradient is the fp32 sum (in order) of
+    the 16-bit `grads` buffers — tensors, or raw device pointers such as mapped
+    NVLink peer buffers — rounded once to grad_dtype."""
+    n = p.numel()
+    ptrs = [g if isinstance(g, int) else _ptr(g) for g in grads]
+    arr = (C.c_void_p * len(ptrs))(*ptrs)
+    hy = hyper.c()
+    _lib.call("tfg_adam_fused_multi", _ptr(p), _ptr(m), _ptr(v), arr, len(ptrs), grad_dtype, _ptr(param16),
+              param_dtype, n, C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
+
+
+F32 = 2  # gradient kind of the ZeRO-3 baseline flow (fp32 gradients from storage)
+
+
 def adam_step(p, m, v, grad16, param16, t: int, hyper: AdamHyper = AdamHyper(), grad_dtype: int = F16,
               param_dtype: int = F16, stream=None) -> int:
     """Reference-semantics step (optimizer.hpp:116-157): raises

@@ -107,18 +107,34 @@ def main() -> None:
             # a skipped iteration keeps the parity key (SURVEY.md §8a rule 2)
             "skip": dict(params=[5000] * 8, tiers=[(400e6, 400e6), (200e6, 200e6)], ratio=[1.0, 1.0],
                          pool_slots=6, cache_slots=2, seed=5, iterations=4, accum=1, wd=0.0, skip=0b10),
+            # the ZeRO-3 baseline flow: caching, skip-gradients, atomic R/W and multi-path all off
+            "baseline": dict(params=[20000] * 6, tiers=[(300e6, 300e6), (150e6, 150e6)], ratio=None,
+                             pool_slots=6, cache_slots=-1, seed=1234, iterations=3, accum=2, wd=0.0, skip=0,
+                             mode="baseline"),
         }
         for name, c in runs.items():
             tiers = [dict(kind=2, read_bps=r, write_bps=w) for r, w in c["tiers"]]
+            base = c.get("mode") == "baseline"
             res = oracle.run_ref_engine(c["params"], tiers, fixed_ratio=c["ratio"], pool_slots=c["pool_slots"],
                                         cache_slots=c["cache_slots"], seed=c["seed"], iterations=c["iterations"],
                                         accum_steps=c["accum"], weight_decay=c["wd"], skip_mask=c["skip"],
-                                        lock_dir=locks)
+                                        lock_dir=locks, enable_caching=not base, multi_path=not base,
+                                        atomic_rw=not base, skip_gradients=not base)
+            # storage bytes per iteration: backward flushes, update-phase fetches
+            bw_bytes, up_bytes, prev = [], [], 0
+            for it in res["iters"]:
+                ev = res["events"]
+                bw_bytes.append(sum(b for k, _s, _t, b in ev[prev:it["trace_begin"]] if k == oracle.EV_FLUSH_END))
+                up_bytes.append(sum(b for k, _s, _t, b in ev[it["trace_begin"]:it["trace_end"]]
+                                    if k == oracle.EV_PREFETCH_END))
+                prev = it["trace_end"]
+            g[f"run_{name}_backward_bytes"] = np.array(bw_bytes, np.int64)
+            g[f"run_{name}_fetch_bytes"] = np.array(up_bytes, np.int64)
             g[f"run_{name}_config"] = np.array(
                 [len(c["params"]), len(c["tiers"]), c["pool_slots"], c["cache_slots"], c["seed"], c["iterations"],
                  c["accum"], c["skip"]], np.int64)
             g[f"run_{name}_params"] = np.array(c["params"], np.int64)
-            g[f"run_{name}_ratio"] = np.array(c["ratio"], np.float64)
+            g[f"run_{name}_ratio"] = np.array(c["ratio"] if c["ratio"] else [], np.float64)
             g[f"run_{name}_wd"] = np.array([c["wd"]])
             g[f"run_{name}_hits"] = np.array([it["cache_hits"] for it in res["iters"]], np.int64)
             g[f"run_{name}_retained"] = np.array([it["retained"] for it in res["iters"]], np.int64)
@@ -130,7 +146,7 @@ def main() -> None:
                 s = oracle.phase_sequences(res["events"], it["trace_begin"], it["trace_end"], nt)
                 seqs.append(repr(s))
             g[f"run_{name}_seqs"] = np.array(seqs)
-            if name == "hits":  # large: keep a digest per subgroup
+            if name in ("hits", "baseline"):  # large: keep a digest per subgroup
                 g[f"run_{name}_digest"] = np.array([hashlib.sha256(x.tobytes()).hexdigest() for x in res["states"]])
             else:
                 g[f"run_{name}_states"] = np.concatenate(res["states"])

@@ -135,3 +135,40 @@ def test_c5_cache_hits_engine_harness(tf, cuda, lock_dir):
     iters, trace = run_bench(tf, [(300, 300), (150, 150)], 20_000, 12, 4, pool_slots=7, lock_dir=lock_dir)
     assert [r["hits"] for r in iters] == [0, 4, 4, 4]
     assert sum(1 for e in trace.snapshot() if e.kind == tf.EventKind.cache_hit) == 12
+
+
+def test_c10_ablation_monotonicity(tf, cuda, lock_dir):
+    # acceptance.cpp:445-490: the four §4.6 flags enabled progressively; mean
+    # update time non-increasing within a 5% band, all-on the fastest.
+    def ladder(step):
+        trace = tf.EventTrace()
+        tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.mem_throttled, "m0", 200e6, 200e6)),
+                 tf.Tier(tf.TierSpec(1, tf.TierKind.mem_throttled, "m1", 100e6, 100e6))]
+        opt = tf.ScheduleOptions(pool_slots=5, lock_dir=lock_dir, enable_caching=step >= 1, skip_gradients=step >= 2,
+                                 atomic_rw=step >= 3, multi_path=step >= 4)
+        engines = []
+        for w in range(2):
+            e = tf.OffloadWorker(w, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0))
+            for k in range(8):
+                e.add_subgroup(w * 8 + k, 1_000_000)
+            e.init_and_flush_all(424242)
+            engines.append(e)
+        import time
+        times = []
+        for it in range(4):
+            for e in engines:
+                e.run_backward_sim(it, tf.SyntheticGradSource(424242), 1)
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=e.run_update, args=(it,)) for e in engines]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            times.append(time.perf_counter() - t0)
+        for e in engines:
+            e.close()
+        return sum(times[1:]) / 3
+    t = [ladder(s) for s in range(5)]
+    for i in range(4):
+        assert t[i + 1] <= t[i] * 1.05, t
+    assert t[4] <= min(t) * 1.0 + 1e-12, t

@@ -319,3 +319,69 @@ def test_transfer_modes_bitwise(tf, cuda, lock_dir, tmp_path, zero_copy, split):
     tl = w.last_timeline()
     assert len(tl) == len(params) and all(s["k_end"] >= s["k_start"] for s in tl)
     w.close()
+
+
+def _baseline_engine(tf, params, lock_dir, *, baseline, seed=1234, pool_slots=6):
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.mem_throttled, "m0", 300e6, 300e6)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.mem_throttled, "m1", 150e6, 150e6))]
+    opt = tf.ScheduleOptions(pool_slots=pool_slots, lock_dir=lock_dir, enable_caching=not baseline,
+                             skip_gradients=not baseline, atomic_rw=not baseline, multi_path=not baseline)
+    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0))
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    return w, trace, tiers
+
+
+def test_zero3_baseline_flow_matches_reference(tf, cuda, golden, lock_dir):
+    """skip_gradients=false: fp32 gradients flushed in backward (4 B/param) and
+    fetched with the state (16 B/param) — reference scheduler.hpp:377-391,
+    667-680; test_scheduler.cpp:357-390."""
+    params = golden["run_baseline_params"].tolist()
+    cfg = golden["run_baseline_config"]
+    iters, accum, seed = int(cfg[5]), int(cfg[6]), int(cfg[4])
+    w, trace, _ = _baseline_engine(tf, params, lock_dir, baseline=True, seed=seed)
+    want_seqs = [ast.literal_eval(s) for s in golden["run_baseline_seqs"]]
+    for it in range(iters):
+        m0 = trace.size()
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed), accum)
+        bw = sum(e.bytes for e in trace.snapshot(m0) if e.kind == tf.EventKind.flush_end)
+        assert bw == golden["run_baseline_backward_bytes"][it] == 4 * sum(params)
+        m1 = trace.size()
+        st = w.run_update(it)
+        ev = trace.snapshot(m1)
+        fetched = sum(e.bytes for e in ev if e.kind == tf.EventKind.prefetch_end)
+        assert fetched == golden["run_baseline_fetch_bytes"][it] == 16 * sum(params)
+        seq = oracle.phase_sequences([(int(e.kind), e.subgroup_id, e.tier_id, e.bytes) for e in ev], 0, len(ev), 2)
+        assert seq == want_seqs[it]
+        assert st.cache_hits == 0 and st.flush_allocation == golden["run_baseline_alloc"][it].tolist()
+    for i in range(len(params)):
+        assert hashlib.sha256(w.read_current_state(i).tobytes()).hexdigest() == golden["run_baseline_digest"][i]
+    w.close()
+
+
+def test_engine_and_baseline_modes_bitwise_identical(tf, cuda, lock_dir):
+    # acceptance criterion 4 / test_scheduler.cpp:329-355
+    params = [30_000] * 6
+    out = []
+    for baseline in (False, True):
+        w, _, _ = _baseline_engine(tf, params, lock_dir, baseline=baseline)
+        for it in range(4):
+            w.run_backward_sim(it, tf.SyntheticGradSource(1234), 2)
+            w.run_update(it)
+        out.append([w.read_current_state(i) for i in range(6)])
+        w.close()
+    for a, b in zip(*out):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_engine_mode_backward_writes_nothing(tf, cuda, lock_dir):
+    # acceptance criterion 6: backward-phase tier writes: engine 0, baseline 4*P*M
+    P, M = 25_000, 5
+    for baseline, want in ((False, 0), (True, 4 * P * M)):
+        w, trace, _ = _baseline_engine(tf, [P] * M, lock_dir, baseline=baseline, pool_slots=4)
+        m0 = trace.size()
+        w.run_backward_sim(0, tf.SyntheticGradSource(5), 1)
+        assert sum(e.bytes for e in trace.snapshot(m0) if e.kind == tf.EventKind.flush_end) == want
+        w.close()
