@@ -222,3 +222,57 @@ def test_kernel_variants_bitwise(tf, cuda, variant):
     assert_bits(Mm.cpu().numpy(), want[1], "m")
     assert_bits(V.cpu().numpy(), want[2], "v")
     assert np.array_equal(_np16(p16), want[3])
+
+
+@pytest.mark.parametrize("nsrc", [1, 2, 3, 8])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_fused_reduce_update_matches_oracle(tf, cuda, nsrc, kind):
+    """tfg_adam_fused_multi: gradient = fp32 sum of n 16-bit sources in order,
+    rounded once, then Adam — the reduce-scatter fused into the update."""
+    import torch
+    n = 300_001
+    rng = np.random.default_rng(nsrc * 10 + kind)
+    srcs = [oracle.synthetic_grads(n, 77, s, 2, kind=kind) for s in range(nsrc)]
+    acc = np.zeros(n, np.float32)
+    for s in srcs:
+        acc = (acc + oracle.widen16(s, kind)).astype(np.float32)
+    g16, _ = oracle.narrow16(acc, kind)
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+    v = rng.uniform(0, 0.01, n).astype(np.float32)
+    want = oracle.adam_fused(p, m, v, g16, kind, kind, 3, weight_decay=0.01)
+    P, Mm, V = _dev(torch, p, cuda), _dev(torch, m, cuda), _dev(torch, v, cuda)
+    G = [_u16(torch, s, cuda) for s in srcs]
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    counters = torch.zeros(2, dtype=torch.int64, device=cuda)
+    tf.adam_fused_multi(P, Mm, V, G, p16, 3, tf.AdamHyper(weight_decay=0.01), kind, kind, counters)
+    torch.cuda.synchronize()
+    assert_bits(P.cpu().numpy(), want[0], "P")
+    assert_bits(Mm.cpu().numpy(), want[1], "m")
+    assert_bits(V.cpu().numpy(), want[2], "v")
+    assert np.array_equal(_np16(p16), want[3])
+    assert counters.cpu().tolist() == [0, want[4]]
+
+
+def test_fp32_gradient_kind(tf, cuda):
+    """grad_dtype F32: the baseline flow's stored fp32 gradients."""
+    import torch
+    import ctypes as C
+    from paper_2509_02480_b200 import _lib
+    n = 100_003
+    rng = np.random.default_rng(4)
+    g = oracle.widen16(oracle.synthetic_grads(n, 5, 1, 1), 0).copy()
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    m, v = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    wp, wm, wv = p.copy(), m.copy(), v.copy()
+    assert oracle.lib().orc_adam_step(wp, wm, wv, g, n, 1e-3, 0.9, 0.999, 1e-8, 0.0, 2) == 0
+    P, Mm, V, Gd = (_dev(torch, x, cuda) for x in (p, m, v, g))
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    h = tf.AdamHyper().c()
+    _lib.call("tfg_adam_fused", P.data_ptr(), Mm.data_ptr(), V.data_ptr(), Gd.data_ptr(), tf.F32, p16.data_ptr(),
+              0, n, C.byref(h), 2, None, None)
+    torch.cuda.synchronize()
+    assert_bits(P.cpu().numpy(), wp, "P")
+    assert_bits(Mm.cpu().numpy(), wm, "m")
+    assert_bits(V.cpu().numpy(), wv, "v")
+    assert np.array_equal(_np16(p16), oracle.f32_to_f16(wp))
