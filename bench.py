@@ -50,6 +50,7 @@ WORKLOADS = {
                       desc="Llama-2-7B-shaped optimizer state: 68 subgroups x 100M params (last 38,415,616)"),
     "20b": dict(total=20_000_000_000, sub=100_000_000, desc="20B-param state, 200 subgroups x 100M"),
     "ref-1b": dict(total=1_000_000_000, sub=125_000_000, desc="reference CPU config: 1B params, 8 x 125M"),
+    "tiny": dict(total=8 * 10_000_000, sub=10_000_000, desc="smoke-sized: 8 subgroups x 10M params"),
 }
 
 
@@ -122,15 +123,22 @@ class ClockSampler:
 
 
 def dist_init():
+    """One process per GPU. TFB_BENCH_BACKEND=gloo (with local ranks folded
+    onto the visible devices) exercises the multi-rank path on a 1-GPU box."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    import torch
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
-        import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("TFB_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -145,7 +153,8 @@ def allmax(world, x: float) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
