@@ -508,7 +508,10 @@ def main(argv=None):
                 "data": "synthetic (seeded reference generators: synthetic_param_init, SyntheticGradSource)",
                 "config": {"workload": wl["desc"], "params_per_rank": params_rank, "subgroups_per_rank": len(sizes),
                            "grad_dtype": "f16", "param_dtype": "f16", "state": "fp32 P/m/v resident in HBM",
-                           "l2": "inputs larger than L2 (1.2 GB per subgroup launch, no flush needed)",
+                           "l2": (f"inputs larger than L2 ({ALG_BYTES_PER_PARAM * max(sizes) / 1e9:.2f} GB per "
+                                  "subgroup launch vs 126 MB L2; no flush needed)"
+                                  if ALG_BYTES_PER_PARAM * max(sizes) > 2 * 126e6 else
+                                  "WARNING: launch working set fits in L2; not a roofline-valid size"),
                            "parallelism": f"zero3-shard x{world} (weak)"},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": dl["launches"] + e2e_launches,

@@ -95,7 +95,9 @@ typedef struct tfg_device_options {
     int32_t grad_dtype;      /* tfg_dtype of the device gradient buffers */
     int32_t param_dtype;     /* tfg_dtype of the device working-parameter buffers */
     int32_t device_buffers;  /* depth of the H2D -> kernel -> D2H ring (>= 1) */
-    int32_t zero_copy;       /* 1: the fused kernel streams the pinned slot over PCIe itself */
+    int32_t zero_copy;       /* 0: copy engines via the device ring; 1: the fused kernel streams the
+                                pinned slot over PCIe both ways; 2: DMA in, the kernel's epilogue
+                                writes the updated state back into the pinned slot */
     int32_t d2h_split;       /* copy mode: concurrent D2H streams per subgroup (1 or 2) */
 } tfg_device_options;
 

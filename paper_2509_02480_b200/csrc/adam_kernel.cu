@@ -111,23 +111,40 @@ __device__ __forceinline__ float load_grad1(const GradSources& gs, uint64_t i, u
     }
 }
 
+// Where one launch reads and writes the fp32 state. In place (in == out) for
+// the device ring and the HBM-resident path; out may instead be mapped pinned
+// host memory, which fuses the D2H write-back into the kernel's epilogue.
+struct StateIO {
+    const float* p;
+    const float* m;
+    const float* v;
+    float* po;
+    float* mo;
+    float* vo;
+};
+
 // VEC = true: P, m, v 16-byte aligned and the gradient / p16 streams 8-byte
 // (16-bit) or 16-byte (fp32) aligned; the body walks quads (float4 / 4 x
 // 16-bit) and the n % 4 tail is scalar. VEC = false: scalar everywhere (e.g.
-// a contiguous P||m||v with P % 4 != 0).
+// a contiguous P||m||v with P % 4 != 0). Loads and stores are explicit
+// evict-first intrinsics, issued in program order per element, so in-place
+// aliasing of in and out is well defined.
 template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, bool DIVC, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-    adam_fused_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const GradSources gs,
-                      uint16_t* __restrict__ p16, uint64_t n, AdamConsts c, unsigned long long* __restrict__ counters) {
+    adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
+                      unsigned long long* __restrict__ counters) {
     unsigned nonfinite = 0, overflow = 0;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
 
     if constexpr (VEC) {
         const uint64_t nq = n / 4;
-        float4* p4 = reinterpret_cast<float4*>(p);
-        float4* m4 = reinterpret_cast<float4*>(m);
-        float4* v4 = reinterpret_cast<float4*>(v);
+        const float4* p4 = reinterpret_cast<const float4*>(io.p);
+        const float4* m4 = reinterpret_cast<const float4*>(io.m);
+        const float4* v4 = reinterpret_cast<const float4*>(io.v);
+        float4* po4 = reinterpret_cast<float4*>(io.po);
+        float4* mo4 = reinterpret_cast<float4*>(io.mo);
+        float4* vo4 = reinterpret_cast<float4*>(io.vo);
         for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
             float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
             GradReg<GK, GMODE> rg[UNROLL];
@@ -155,35 +172,35 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     h.z = narrow16<OK>(rp[u].z);
                     h.w = narrow16<OK>(rp[u].w);
                     overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
-                    __stcs(p4 + q, rp[u]);
-                    __stcs(m4 + q, rm[u]);
-                    __stcs(v4 + q, rv[u]);
+                    __stcs(po4 + q, rp[u]);
+                    __stcs(mo4 + q, rm[u]);
+                    __stcs(vo4 + q, rv[u]);
                     store_u16x4(p16 + 4 * q, h);
                 }
             }
         }
         const uint64_t i = nq * 4 + tid;  // scalar tail: n % 4 elements
         if (i < n) {
-            float pf = p[i], mf = m[i], vf = v[i];
+            float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
             const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
             adam_element<WD, DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
-            p[i] = pf;
-            m[i] = mf;
-            v[i] = vf;
+            __stcs(io.po + i, pf);
+            __stcs(io.mo + i, mf);
+            __stcs(io.vo + i, vf);
             p16[i] = h;
         }
     } else {
         for (uint64_t i = tid; i < n; i += nthreads) {
-            float pf = __ldcs(p + i), mf = __ldcs(m + i), vf = __ldcs(v + i);
+            float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
             const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
             adam_element<WD, DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
-            __stcs(p + i, pf);
-            __stcs(m + i, mf);
-            __stcs(v + i, vf);
+            __stcs(io.po + i, pf);
+            __stcs(io.mo + i, mf);
+            __stcs(io.vo + i, vf);
             p16[i] = h;
         }
     }
@@ -212,9 +229,15 @@ GradSources sources_of(const AdamLaunch& a) {
     return gs;
 }
 
+StateIO state_io(const AdamLaunch& a) {
+    return StateIO{a.p, a.m, a.v, a.p_out ? a.p_out : a.p, a.m_out ? a.m_out : a.m, a.v_out ? a.v_out : a.v};
+}
+
 bool is_vec(const AdamLaunch& a) {
-    const uintptr_t state = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
-                            reinterpret_cast<uintptr_t>(a.v);
+    const StateIO io = state_io(a);
+    const uintptr_t state = reinterpret_cast<uintptr_t>(io.p) | reinterpret_cast<uintptr_t>(io.m) |
+                            reinterpret_cast<uintptr_t>(io.v) | reinterpret_cast<uintptr_t>(io.po) |
+                            reinterpret_cast<uintptr_t>(io.mo) | reinterpret_cast<uintptr_t>(io.vo);
     uintptr_t grads = 0;
     const GradSources gs = sources_of(a);
     for (int s = 0; s < gs.n; ++s) grads |= reinterpret_cast<uintptr_t>(gs.src[s]);
@@ -230,11 +253,11 @@ cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     if (is_vec(a)) {
         const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
         adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B>
-            <<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters);
+            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
     } else {
         const unsigned grid = grid_for(a.n, B);
         adam_fused_kernel<GK, GMODE, OK, WD, false, 1, C::kDivc, B>
-            <<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters);
+            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
     }
     return cudaGetLastError();
 }

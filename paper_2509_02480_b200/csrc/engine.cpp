@@ -795,6 +795,23 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     a.p = d;
     a.m = d + ds;
     a.v = d + 2 * ds;
+    if (dev_.zero_copy == 2) {
+        // DMA brings the state in; the kernel's epilogue stores the updated
+        // P, m, v straight into the mapped pinned slot (the D2H fused into
+        // the kernel), so no copy engine serves the write-back.
+        float* hp = nullptr;
+        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hp), blk.payload(), 0),
+                   "cudaHostGetDevicePointer");
+        a.p_out = hp;
+        a.m_out = hp + pc;
+        a.v_out = hp + 2 * pc;
+        cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
+        for (cudaEvent_t ev : {e.k_end, e.d2h_start, e.d2h_end})
+            cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
+        auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
+        cuda_check(cudaLaunchHostFunc(s_k_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
+        return;
+    }
     cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
     cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
 

@@ -24,6 +24,11 @@ struct AdamLaunch {
     const void* peers[kMaxGradSources] = {};
     int n_peers = 0;
     uint16_t* p16 = nullptr;  // 16-bit working params out (out_kind)
+    // Optional separate destinations of the updated state (null = in place),
+    // e.g. mapped pinned host memory: the D2H write-back fused into the kernel.
+    float* p_out = nullptr;
+    float* m_out = nullptr;
+    float* v_out = nullptr;
     uint64_t n = 0;
     int grad_kind = 0;
     int out_kind = 0;

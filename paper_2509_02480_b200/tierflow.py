@@ -133,7 +133,9 @@ class DeviceOptions:
     grad_dtype: int = F16
     param_dtype: int = F16
     device_buffers: int = 3
-    zero_copy: bool = False
+    # 0: copy engines both ways through the device ring; 1: the kernel streams
+    # the pinned slot over PCIe both ways; 2: DMA in, kernel epilogue writes back.
+    zero_copy: int = 0
     d2h_split: int = 1
 
 

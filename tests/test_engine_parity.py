@@ -295,7 +295,7 @@ def test_external_gradient_buffer_binding(tf, cuda, lock_dir):
     w.close()
 
 
-@pytest.mark.parametrize("zero_copy,split", [(True, 1), (False, 2)])
+@pytest.mark.parametrize("zero_copy,split", [(1, 1), (0, 2), (2, 1)])
 def test_transfer_modes_bitwise(tf, cuda, lock_dir, tmp_path, zero_copy, split):
     """Zero-copy (kernel streams the pinned slot over PCIe) and split-D2H
     copy mode give the same bits as the oracle."""
