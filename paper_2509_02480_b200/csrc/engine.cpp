@@ -749,7 +749,7 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     a.out_kind = dev_.out_kind;
     a.c = c;
     a.counters = counters_;
-    if (dev_.zero_copy) {
+    if (dev_.zero_copy == 1) {
         // The kernel streams P||m||v straight from and back to the pinned
         // slot over PCIe: reads and writes interleave at cache-line grain,
         // loading both link directions evenly; no device ring, no DMA.
