@@ -285,6 +285,162 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
     return launch_wd<kBF16, 0, kBF16, C>(a, stream);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged variant: one producer warp streams tiles of P, m, v and g into a
+// ring of shared-memory stages with 1D bulk copies (cp.async.bulk, completion
+// counted on an mbarrier), the consumer warps compute from shared memory and
+// store straight to global. Memory parallelism comes from the stage ring
+// (S x 14 KiB per CTA in flight) instead of registers.
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(smem_addr(bar)), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
+
+constexpr int kTmaConsumerWarps = 8;
+
+template <int T, int S, bool WD, int MINB>
+__global__ void __launch_bounds__((kTmaConsumerWarps + 1) * 32, MINB)
+    adam_tma_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                    const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t ntiles, AdamConsts c,
+                    unsigned long long* __restrict__ counters) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* sp = reinterpret_cast<float*>(smem);
+    float* sm = sp + S * T;
+    float* sv = sm + S * T;
+    uint16_t* sg = reinterpret_cast<uint16_t*>(sv + S * T);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
+    uint64_t* empty = full + S;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kTmaConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kTmaConsumerWarps) {  // producer warp: one lane issues the bulk copies
+        if (lane == 0) {
+            uint64_t k = 0;
+            for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+                const int s = static_cast<int>(k % S);
+                const uint32_t round = static_cast<uint32_t>(k / S);
+                if (k >= static_cast<uint64_t>(S)) mbar_wait(&empty[s], (round - 1) & 1u);
+                mbar_arrive_expect_tx(&full[s], 14u * T);
+                const uint64_t off = tile * T;
+                bulk_load(sp + s * T, p + off, 4u * T, &full[s]);
+                bulk_load(sm + s * T, m + off, 4u * T, &full[s]);
+                bulk_load(sv + s * T, v + off, 4u * T, &full[s]);
+                bulk_load(sg + s * T, g + off, 2u * T, &full[s]);
+            }
+        }
+        return;
+    }
+    unsigned nonfinite = 0, overflow = 0;
+    uint64_t k = 0;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
+        const uint64_t off = tile * T;
+        const float4* tp = reinterpret_cast<const float4*>(sp + s * T);
+        const float4* tm = reinterpret_cast<const float4*>(sm + s * T);
+        const float4* tv = reinterpret_cast<const float4*>(sv + s * T);
+        const uint2* tg = reinterpret_cast<const uint2*>(sg + s * T);
+#pragma unroll 1
+        for (int qi = threadIdx.x; qi < T / 4; qi += kTmaConsumerWarps * 32) {
+            float4 rp = tp[qi], rm = tm[qi], rv = tv[qi];
+            const uint2 graw = tg[qi];
+            U16x4 gh;
+            gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
+            gh.y = static_cast<uint16_t>(graw.x >> 16);
+            gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
+            gh.w = static_cast<uint16_t>(graw.y >> 16);
+            nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
+                         nonfinite16<kF16>(gh.w);
+            adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
+            adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
+            adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
+            adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
+            U16x4 h;
+            h.x = narrow16<kF16>(rp.x);
+            h.y = narrow16<kF16>(rp.y);
+            h.z = narrow16<kF16>(rp.z);
+            h.w = narrow16<kF16>(rp.w);
+            overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
+            __stcs(reinterpret_cast<float4*>(p + off) + qi, rp);
+            __stcs(reinterpret_cast<float4*>(m + off) + qi, rm);
+            __stcs(reinterpret_cast<float4*>(v + off) + qi, rv);
+            store_u16x4(p16 + off + 4 * qi, h);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (counters != nullptr) {
+        warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+template <int T, int S, int MINB>
+cudaError_t launch_tma(const AdamLaunch& a, cudaStream_t stream) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
+                           reinterpret_cast<uintptr_t>(a.p16)) & 15u) == 0;
+    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
+        return cudaErrorInvalidValue;
+    const uint64_t ntiles = a.n / T;
+    constexpr size_t smem = static_cast<size_t>(S) * T * 14 + 2 * S * sizeof(uint64_t);
+    if (ntiles > 0) {
+        auto kern = a.c.lr_wd != 0.0 ? adam_tma_kernel<T, S, true, MINB> : adam_tma_kernel<T, S, false, MINB>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
+        kern<<<grid, (kTmaConsumerWarps + 1) * 32, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g),
+                                                                   a.p16, ntiles, a.c, a.counters);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t done = ntiles * T;
+    if (done == a.n) return cudaSuccess;
+    AdamLaunch tail = a;  // the n % T remainder through the register-streaming kernel
+    tail.p += done;
+    tail.m += done;
+    tail.v += done;
+    tail.g = static_cast<const uint16_t*>(a.g) + done;
+    tail.p16 += done;
+    tail.n = a.n - done;
+    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
+}
+
 // Shipped configuration: one quad per thread per iteration, constant-divisor
 // quotients, <= 64 registers for 4 resident CTAs (32 warps) per SM. The
 // 2026-10-17 sweep (profiles/kernel_sweep_r1.json) measured it at 474 us per
@@ -305,6 +461,10 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 9) return launch_wd<kF16, 0, kF16, Cfg<1, true, 5>>(a, stream);
     if constexpr (V == 10) return launch_wd<kF16, 0, kF16, Cfg<2, true, 4>>(a, stream);
     if constexpr (V == 11) return launch_wd<kF16, 0, kF16, Cfg<1, true, 6>>(a, stream);
+    if constexpr (V == 12) return launch_tma<1024, 4, 2>(a, stream);
+    if constexpr (V == 13) return launch_tma<1024, 3, 3>(a, stream);
+    if constexpr (V == 14) return launch_tma<2048, 3, 2>(a, stream);
+    if constexpr (V == 15) return launch_tma<512, 4, 4>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -359,11 +519,15 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 9: return launch_variant<9>(a, stream);
         case 10: return launch_variant<10>(a, stream);
         case 11: return launch_variant<11>(a, stream);
+        case 12: return launch_variant<12>(a, stream);
+        case 13: return launch_variant<13>(a, stream);
+        case 14: return launch_variant<14>(a, stream);
+        case 15: return launch_variant<15>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 12; }
+int adam_variant_count() { return 16; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {
