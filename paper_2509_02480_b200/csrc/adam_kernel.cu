@@ -441,6 +441,116 @@ cudaError_t launch_tma(const AdamLaunch& a, cudaStream_t stream) {
     return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
 }
 
+// ---------------------------------------------------------------------------
+// cp.async double-buffered variant: each thread copies its NEXT quad of P, m,
+// v, g into its own shared-memory slots with cp.async (LDGSTS, no registers
+// held) before computing the current one, so memory latency overlaps the FP64
+// chain without giving up occupancy. Same element math and stores as the
+// register kernel; F16 in and out.
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <bool WD, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    adam_cpasync_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                        const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t nq, AdamConsts c,
+                        unsigned long long* __restrict__ counters) {
+    __shared__ float4 sbuf[2][3][kThreads];
+    __shared__ uint2 sgrad[2][kThreads];
+    unsigned nonfinite = 0, overflow = 0;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int t = threadIdx.x;
+    float4* p4 = reinterpret_cast<float4*>(p);
+    float4* m4 = reinterpret_cast<float4*>(m);
+    float4* v4 = reinterpret_cast<float4*>(v);
+    const uint2* g2 = reinterpret_cast<const uint2*>(g);
+    auto issue = [&](uint64_t qq, int s) {
+        cp_async16(&sbuf[s][0][t], p4 + qq);
+        cp_async16(&sbuf[s][1][t], m4 + qq);
+        cp_async16(&sbuf[s][2][t], v4 + qq);
+        cp_async8(&sgrad[s][t], g2 + qq);
+    };
+    int s = 0;
+    if (q < nq) issue(q, 0);
+    cp_async_commit();
+    for (; q < nq; q += nthreads, s ^= 1) {
+        const uint64_t nxt = q + nthreads;
+        if (nxt < nq) issue(nxt, s ^ 1);
+        cp_async_commit();
+        cp_async_wait<1>();  // the current quad has landed; the next stays in flight
+        float4 rp = sbuf[s][0][t], rm = sbuf[s][1][t], rv = sbuf[s][2][t];
+        const uint2 graw = sgrad[s][t];
+        U16x4 gh;
+        gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
+        gh.y = static_cast<uint16_t>(graw.x >> 16);
+        gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
+        gh.w = static_cast<uint16_t>(graw.y >> 16);
+        nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
+                     nonfinite16<kF16>(gh.w);
+        adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
+        adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
+        adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
+        adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
+        U16x4 h;
+        h.x = narrow16<kF16>(rp.x);
+        h.y = narrow16<kF16>(rp.y);
+        h.z = narrow16<kF16>(rp.z);
+        h.w = narrow16<kF16>(rp.w);
+        overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
+        __stcs(p4 + q, rp);
+        __stcs(m4 + q, rm);
+        __stcs(v4 + q, rv);
+        store_u16x4(p16 + 4 * q, h);
+    }
+    cp_async_wait<0>();
+    if (counters != nullptr) {
+        warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+template <int MINB>
+cudaError_t launch_cpasync(const AdamLaunch& a, cudaStream_t stream) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                           reinterpret_cast<uintptr_t>(a.v)) & 15u) == 0 &&
+                         ((reinterpret_cast<uintptr_t>(a.g) | reinterpret_cast<uintptr_t>(a.p16)) & 7u) == 0;
+    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
+        return cudaErrorInvalidValue;
+    const uint64_t nq = a.n / 4;
+    if (nq > 0) {
+        const unsigned grid = grid_for(nq, MINB);
+        if (a.c.lr_wd != 0.0)
+            adam_cpasync_kernel<true, MINB><<<grid, kThreads, 0, stream>>>(
+                a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, nq, a.c, a.counters);
+        else
+            adam_cpasync_kernel<false, MINB><<<grid, kThreads, 0, stream>>>(
+                a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, nq, a.c, a.counters);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (nq * 4 == a.n) return cudaSuccess;
+    AdamLaunch tail = a;  // the n % 4 remainder through the register-streaming kernel
+    const uint64_t done = nq * 4;
+    tail.p += done;
+    tail.m += done;
+    tail.v += done;
+    tail.g = static_cast<const uint16_t*>(a.g) + done;
+    tail.p16 += done;
+    tail.n = a.n - done;
+    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
+}
+
 // Shipped configuration: one quad per thread per iteration, constant-divisor
 // quotients, <= 64 registers for 4 resident CTAs (32 warps) per SM. The
 // 2026-10-17 sweep (profiles/kernel_sweep_r1.json) measured it at 474 us per
@@ -465,6 +575,8 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 13) return launch_tma<1024, 3, 3>(a, stream);
     if constexpr (V == 14) return launch_tma<2048, 3, 2>(a, stream);
     if constexpr (V == 15) return launch_tma<512, 4, 4>(a, stream);
+    if constexpr (V == 16) return launch_cpasync<4>(a, stream);
+    if constexpr (V == 17) return launch_cpasync<3>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -523,11 +635,13 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 13: return launch_variant<13>(a, stream);
         case 14: return launch_variant<14>(a, stream);
         case 15: return launch_variant<15>(a, stream);
+        case 16: return launch_variant<16>(a, stream);
+        case 17: return launch_variant<17>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 16; }
+int adam_variant_count() { return 18; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {
