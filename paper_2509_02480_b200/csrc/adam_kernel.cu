@@ -129,7 +129,9 @@ struct StateIO {
 // a contiguous P||m||v with P % 4 != 0). Loads and stores are explicit
 // evict-first intrinsics, issued in program order per element, so in-place
 // aliasing of in and out is well defined.
-template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, bool DIVC, int MINB>
+// DIVC selects the element math: 0 = div.rn quotients, 1 = constant-divisor
+// quotients, 2 = verified fast path (numerics.cuh adam_element_fast).
+template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                       unsigned long long* __restrict__ counters) {
@@ -162,10 +164,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
             for (int u = 0; u < UNROLL; ++u) {
                 const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
                 if (q < nq) {
-                    adam_element<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
-                    adam_element<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
-                    adam_element<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
-                    adam_element<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
+                    adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
+                    adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
+                    adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
+                    adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
                     U16x4 h;
                     h.x = narrow16<OK>(rp[u].x);
                     h.y = narrow16<OK>(rp[u].y);
@@ -183,7 +185,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (i < n) {
             float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
             const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
-            adam_element<WD, DIVC>(pf, mf, vf, gf, c);
+            adam_math<WD, DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
             __stcs(io.po + i, pf);
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (uint64_t i = tid; i < n; i += nthreads) {
             float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
             const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
-            adam_element<WD, DIVC>(pf, mf, vf, gf, c);
+            adam_math<WD, DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
             __stcs(io.po + i, pf);
@@ -210,10 +212,10 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
-template <int UNROLL, bool DIVC, int MINB>
+template <int UNROLL, int DIVC, int MINB>
 struct Cfg {
     static constexpr int kUnroll = UNROLL;
-    static constexpr bool kDivc = DIVC;
+    static constexpr int kDivc = DIVC;
     static constexpr int kMinBlocks = MINB;
 };
 
@@ -577,6 +579,9 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 15) return launch_tma<512, 4, 4>(a, stream);
     if constexpr (V == 16) return launch_cpasync<4>(a, stream);
     if constexpr (V == 17) return launch_cpasync<3>(a, stream);
+    if constexpr (V == 18) return launch_wd<kF16, 0, kF16, Cfg<1, 2, 4>>(a, stream);
+    if constexpr (V == 19) return launch_wd<kF16, 0, kF16, Cfg<2, 2, 3>>(a, stream);
+    if constexpr (V == 20) return launch_wd<kF16, 0, kF16, Cfg<1, 2, 5>>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -637,11 +642,14 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 15: return launch_variant<15>(a, stream);
         case 16: return launch_variant<16>(a, stream);
         case 17: return launch_variant<17>(a, stream);
+        case 18: return launch_variant<18>(a, stream);
+        case 19: return launch_variant<19>(a, stream);
+        case 20: return launch_variant<20>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 18; }
+int adam_variant_count() { return 21; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {

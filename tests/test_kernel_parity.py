@@ -204,7 +204,7 @@ def test_constant_division_matches_div_rn(tf, cuda):
             assert mism == 0, (beta, t, first)
 
 
-@pytest.mark.parametrize("variant", range(1, 18))
+@pytest.mark.parametrize("variant", range(1, 21))
 def test_kernel_variants_bitwise(tf, cuda, variant):
     import torch
     n = 1_000_003
@@ -276,3 +276,50 @@ def test_fp32_gradient_kind(tf, cuda):
     assert_bits(Mm.cpu().numpy(), wm, "m")
     assert_bits(V.cpu().numpy(), wv, "v")
     assert np.array_equal(_np16(p16), oracle.f32_to_f16(wp))
+
+
+def _near_midpoint_inputs(count=40, seed=11, t=3, tol_bits=96):
+    """Elements whose exact p_new = RN64(p - D) lies within `tol_bits` double
+    ulps of a binary32 rounding midpoint: the cases the verified fast path
+    must hand to the exact chain. Found by a vectorised search in float64
+    (numpy rounds every op, no contraction: the reference chain)."""
+    rng = np.random.default_rng(seed)
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    bc1, bc2 = 1 - b1 ** t, 1 - b2 ** t
+    found = [np.empty(0, np.float32)] * 4
+    while found[0].size < count:
+        n = 4_000_000
+        p = rng.uniform(-2, 2, n).astype(np.float32)
+        m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+        v = rng.uniform(0, 0.01, n).astype(np.float32)
+        g16 = oracle.f32_to_f16(rng.uniform(-0.25, 0.25, n).astype(np.float32))
+        g = oracle.widen16(g16, 0).astype(np.float64)
+        m64 = b1 * m.astype(np.float64) + (1 - b1) * g
+        v64 = b2 * v.astype(np.float64) + ((1 - b2) * g) * g
+        pn = p.astype(np.float64) - (lr * (m64 / bc1)) / (np.sqrt(v64 / bc2) + eps)
+        low = pn.view(np.uint64) & np.uint64((1 << 29) - 1)
+        dist = np.abs(low.astype(np.int64) - (1 << 28))
+        sel = dist <= tol_bits
+        found = [np.concatenate([f, x[sel]]) for f, x in zip(found, (p, m, v, g16.astype(np.float32)))]
+    return found[0], found[1], found[2], found[3].astype(np.uint16), t
+
+
+@pytest.mark.parametrize("variant", [0, 18, 19])
+def test_fast_path_fallback_on_midpoint_cases(tf, cuda, variant):
+    import torch
+    p, m, v, g16, t = _near_midpoint_inputs()
+    rng = np.random.default_rng(5)
+    n_fill = 100_000
+    p = np.concatenate([p, rng.uniform(-2, 2, n_fill).astype(np.float32)])
+    m = np.concatenate([m, (rng.uniform(-0.5, 0.5, n_fill) * 0.1).astype(np.float32)])
+    v = np.concatenate([v, rng.uniform(0, 0.01, n_fill).astype(np.float32)])
+    g16 = np.concatenate([g16, oracle.synthetic_grads(n_fill, 3, 3, 3)])
+    want = oracle.adam_fused(p, m, v, g16, 0, 0, t)
+    P, Mm, V, G = _dev(torch, p, cuda), _dev(torch, m, cuda), _dev(torch, v, cuda), _u16(torch, g16, cuda)
+    p16 = torch.zeros(p.size, dtype=torch.int16, device=cuda)
+    tf.adam_fused_variant(variant, P, Mm, V, G, p16, t, tf.AdamHyper())
+    torch.cuda.synchronize()
+    assert_bits(P.cpu().numpy(), want[0], "P")
+    assert_bits(Mm.cpu().numpy(), want[1], "m")
+    assert_bits(V.cpu().numpy(), want[2], "v")
+    assert np.array_equal(_np16(p16), want[3])
