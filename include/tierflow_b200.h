@@ -177,6 +177,19 @@ const char* tfg_last_error(void);
 int tfg_abi_version(void);
 int tfg_device_count(int* count);
 
+/* ---- peer memory (fused data-parallel gradient exchange) ----------------- */
+/* Device buffers that other ranks map over NVLink: cudaMalloc'd (whole
+ * allocations, so an IPC handle maps exactly this buffer), shared as the
+ * 64-byte cudaIpcMemHandle_t. Opening maps the peer's buffer with lazy peer
+ * access; a rank never opens its own handle. No reference counterpart: they
+ * replace the NCCL reduce in front of the update. */
+#define TFG_IPC_HANDLE_BYTES 64
+int tfg_device_alloc(int device, uint64_t bytes, void** out);
+int tfg_device_free(int device, void* ptr);
+int tfg_ipc_get_handle(int device, void* ptr, unsigned char* handle_out);
+int tfg_ipc_open_handle(int device, const unsigned char* handle, void** out);
+int tfg_ipc_close_handle(int device, void* ptr);
+
 /* ---- kernels (device pointers, async on `stream`) ------------------------ */
 /* Fused upscale_f16_to_f32 -> adam_step -> downscale_f32_to_f16
  * (precision.hpp:17, optimizer.hpp:116, precision.hpp:29; composed at
@@ -287,6 +300,12 @@ int tfg_engine_run_backward_sim(tfg_engine* engine, int iteration, uint64_t seed
 int tfg_engine_gradients_finite(tfg_engine* engine, int* out);                              /* :395 */
 int tfg_engine_grad_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);             /* :401 */
 int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_ptr);
+/* Fused data-parallel reduction: the update of `id` consumes the fp32 sum (in
+ * order, rounded once to grad_kind) of n (1..8) 16-bit device buffers, e.g.
+ * every peer's contribution mapped over NVLink (CUDA IPC). Replaces the
+ * reduce_grads_to_owners step in front of run_update.
+ * TFG_ERR_CONFIG in the baseline gradient flow (skip_gradients = 0). */
+int tfg_engine_bind_grad_sources(tfg_engine* engine, uint32_t id, const void* const* device_ptrs, int n);
 int tfg_engine_params16_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);         /* shadow_, :861 */
 int tfg_engine_run_update(tfg_engine* engine, int iteration, tfg_phase_stats* stats);      /* :405 */
 int tfg_engine_last_subgroup_io(tfg_engine* engine, tfg_subgroup_io* out, uint64_t max_n, uint64_t* n_out);

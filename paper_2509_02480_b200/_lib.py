@@ -120,6 +120,11 @@ _SIGS = {
     "tfg_last_error": (C.c_char_p, []),
     "tfg_abi_version": (_i, []),
     "tfg_device_count": (_i, [C.POINTER(_i)]),
+    "tfg_device_alloc": (_i, [_i, _u64, C.POINTER(_vp)]),
+    "tfg_device_free": (_i, [_i, _vp]),
+    "tfg_ipc_get_handle": (_i, [_i, _vp, C.c_char_p]),
+    "tfg_ipc_open_handle": (_i, [_i, C.c_char_p, C.POINTER(_vp)]),
+    "tfg_ipc_close_handle": (_i, [_i, _vp]),
     "tfg_adam_fused": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
     "tfg_adam_fused_contiguous": (_i, [_vp, _u64, _vp, _i, _vp, _i, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
     "tfg_adam_fused_multi": (_i, [_vp, _vp, _vp, C.POINTER(_vp), _i, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
@@ -173,6 +178,7 @@ _SIGS = {
     "tfg_engine_gradients_finite": (_i, [_vp, C.POINTER(_i)]),
     "tfg_engine_grad_buffer": (_i, [_vp, C.c_uint32, C.POINTER(_vp)]),
     "tfg_engine_bind_grad_buffer": (_i, [_vp, C.c_uint32, _vp]),
+    "tfg_engine_bind_grad_sources": (_i, [_vp, C.c_uint32, C.POINTER(_vp), C.c_int]),
     "tfg_engine_params16_buffer": (_i, [_vp, C.c_uint32, C.POINTER(_vp)]),
     "tfg_engine_run_update": (_i, [_vp, _i, C.POINTER(PhaseStatsC)]),
     "tfg_engine_last_subgroup_io": (_i, [_vp, C.POINTER(SubgroupIoC), _u64, C.POINTER(_u64)]),

@@ -127,6 +127,66 @@ int tfg_device_count(int* count) {
     });
 }
 
+// ---- peer memory ---------------------------------------------------------------
+
+namespace {
+struct DeviceScope {
+    int prev = 0;
+    explicit DeviceScope(int d) {
+        tfb::cuda_check(cudaGetDevice(&prev), "cudaGetDevice");
+        tfb::cuda_check(cudaSetDevice(d), "cudaSetDevice");
+    }
+    ~DeviceScope() { cudaSetDevice(prev); }
+};
+static_assert(sizeof(cudaIpcMemHandle_t) == TFG_IPC_HANDLE_BYTES, "IPC handle size");
+}  // namespace
+
+int tfg_device_alloc(int device, uint64_t bytes, void** out) {
+    return guarded([&] {
+        need(out, "out");
+        if (bytes == 0) throw tfb::ConfigError("device_alloc: zero bytes");
+        DeviceScope ds(device);
+        tfb::cuda_check(cudaMalloc(out, bytes), "cudaMalloc");
+    });
+}
+
+int tfg_device_free(int device, void* ptr) {
+    return guarded([&] {
+        DeviceScope ds(device);
+        tfb::cuda_check(cudaFree(ptr), "cudaFree");
+    });
+}
+
+int tfg_ipc_get_handle(int device, void* ptr, unsigned char* handle_out) {
+    return guarded([&] {
+        need(ptr, "ptr");
+        need(handle_out, "handle_out");
+        DeviceScope ds(device);
+        cudaIpcMemHandle_t h;
+        tfb::cuda_check(cudaIpcGetMemHandle(&h, ptr), "cudaIpcGetMemHandle");
+        std::memcpy(handle_out, &h, sizeof(h));
+    });
+}
+
+int tfg_ipc_open_handle(int device, const unsigned char* handle, void** out) {
+    return guarded([&] {
+        need(handle, "handle");
+        need(out, "out");
+        DeviceScope ds(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        tfb::cuda_check(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int tfg_ipc_close_handle(int device, void* ptr) {
+    return guarded([&] {
+        need(ptr, "ptr");
+        DeviceScope ds(device);
+        tfb::cuda_check(cudaIpcCloseMemHandle(ptr), "cudaIpcCloseMemHandle");
+    });
+}
+
 // ---- kernels -------------------------------------------------------------------
 
 int tfg_adam_fused(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
@@ -630,6 +690,14 @@ int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_pt
     return guarded([&] {
         need(engine, "engine");
         engine->w->bind_grad_buffer(id, device_ptr);
+    });
+}
+
+int tfg_engine_bind_grad_sources(tfg_engine* engine, uint32_t id, const void* const* device_ptrs, int n) {
+    return guarded([&] {
+        need(engine, "engine");
+        if (n < 0 || (n > 0 && device_ptrs == nullptr)) throw tfb::ConfigError("bind_grad_sources: bad source list");
+        engine->w->bind_grad_sources(id, std::vector<const void*>(device_ptrs, device_ptrs + n));
     });
 }
 

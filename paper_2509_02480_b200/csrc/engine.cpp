@@ -379,6 +379,7 @@ void OffloadWorker::setup_device() {
     grad_ptr_.clear();
     p16_ptr_.clear();
     events_.assign(ids_.size(), DeviceEvents{});
+    grad_sources_.assign(ids_.size(), {});
     host_resident_ns_.assign(ids_.size(), 0);
     host_retired_ns_.assign(ids_.size(), 0);
     for (std::size_t k = 0; k < ids_.size(); ++k) {
@@ -554,7 +555,19 @@ void* OffloadWorker::grad_buffer(SubgroupId id) {
 void OffloadWorker::bind_grad_buffer(SubgroupId id, void* device_ptr) {
     if (!device_ready_) throw Error("bind_grad_buffer before init_and_flush_all");
     if (device_ptr == nullptr) throw ConfigError("bind_grad_buffer: null device pointer");
-    grad_ptr_.at(index_of_.at(id)) = static_cast<std::uint16_t*>(device_ptr);
+    const std::size_t k = index_of_.at(id);
+    grad_ptr_.at(k) = static_cast<std::uint16_t*>(device_ptr);
+    grad_sources_.at(k).clear();
+}
+
+void OffloadWorker::bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources) {
+    if (!device_ready_) throw Error("bind_grad_sources before init_and_flush_all");
+    if (sources.empty() || sources.size() > static_cast<std::size_t>(kMaxGradSources))
+        throw ConfigError("bind_grad_sources: 1.." + std::to_string(kMaxGradSources) + " sources");
+    if (!opt_.skip_gradients) throw ConfigError("bind_grad_sources: not available in the baseline gradient flow");
+    for (const void* s : sources)
+        if (s == nullptr) throw ConfigError("bind_grad_sources: null device pointer");
+    grad_sources_.at(index_of_.at(id)) = sources;
 }
 
 void* OffloadWorker::params16_buffer(SubgroupId id) {
@@ -562,20 +575,32 @@ void* OffloadWorker::params16_buffer(SubgroupId id) {
     return p16_ptr_.at(index_of_.at(id));
 }
 
-bool OffloadWorker::gradients_finite() {
-    if (!device_ready_) throw Error("gradients_finite before init_and_flush_all");
-    DeviceGuard dg(dev_.device);
+// Non-finite gradient count per subgroup (index order): of the bound buffer,
+// or of the rounded fp32 sum for a subgroup fed by several sources.
+std::vector<unsigned long long> OffloadWorker::nonfinite_counts() {
     cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
-    for (std::size_t k = 0; k < ids_.size(); ++k)
-        cuda_check(launch_count_nonfinite16(grad_ptr_[k], subgroups_.at(ids_[k]).param_count, dev_.grad_kind,
-                                            sg_counts_ + k, s_k_),
-                   "count_nonfinite");
+    for (std::size_t k = 0; k < ids_.size(); ++k) {
+        const std::uint64_t pc = subgroups_.at(ids_[k]).param_count;
+        if (grad_sources_[k].empty())
+            cuda_check(launch_count_nonfinite16(grad_ptr_[k], pc, dev_.grad_kind, sg_counts_ + k, s_k_),
+                       "count_nonfinite");
+        else
+            cuda_check(launch_count_nonfinite_sum16(grad_sources_[k].data(), static_cast<int>(grad_sources_[k].size()),
+                                                    pc, dev_.grad_kind, sg_counts_ + k, s_k_),
+                       "count_nonfinite_sum");
+    }
     std::vector<unsigned long long> counts(ids_.size());
     cuda_check(cudaMemcpyAsync(counts.data(), sg_counts_, counts.size() * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s_k_),
                "cudaMemcpyAsync");
     cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
-    for (const auto c : counts)
+    return counts;
+}
+
+bool OffloadWorker::gradients_finite() {
+    if (!device_ready_) throw Error("gradients_finite before init_and_flush_all");
+    DeviceGuard dg(dev_.device);
+    for (const auto c : nonfinite_counts())
         if (c != 0) return false;
     return true;
 }
@@ -583,18 +608,10 @@ bool OffloadWorker::gradients_finite() {
 // The reference rejects non-finite gradients before mutating a subgroup
 // (precision.hpp:17-25 via scheduler.hpp:467-471). The fused kernel widens
 // and updates in one pass, so the whole phase is checked up front instead:
-// one 2-byte/param read, and no subgroup is mutated when any is bad.
+// one 2-byte/param read (2n for n summed sources), and no subgroup is
+// mutated when any is bad.
 void OffloadWorker::check_grads_finite_or_throw() {
-    cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
-    for (std::size_t k = 0; k < ids_.size(); ++k)
-        cuda_check(launch_count_nonfinite16(grad_ptr_[k], subgroups_.at(ids_[k]).param_count, dev_.grad_kind,
-                                            sg_counts_ + k, s_k_),
-                   "count_nonfinite");
-    std::vector<unsigned long long> counts(ids_.size());
-    cuda_check(cudaMemcpyAsync(counts.data(), sg_counts_, counts.size() * sizeof(unsigned long long),
-                               cudaMemcpyDeviceToHost, s_k_),
-               "cudaMemcpyAsync");
-    cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+    const auto counts = nonfinite_counts();
     for (const SubgroupId id : order_)
         if (counts[index_of_.at(id)] != 0)
             throw GradientOverflowError("subgroup " + std::to_string(id) +
@@ -743,6 +760,10 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     const HostBlock& blk = pool_->block(slot);
     AdamLaunch a;
     a.g = grad_ptr_[k];
+    if (!grad_sources_[k].empty()) {  // reduce + update in one pass over the peers' contributions
+        for (std::size_t i = 0; i < grad_sources_[k].size(); ++i) a.peers[i] = grad_sources_[k][i];
+        a.n_peers = static_cast<int>(grad_sources_[k].size());
+    }
     a.p16 = p16_ptr_[k];
     a.n = pc;
     a.grad_kind = dev_.grad_kind;

@@ -248,6 +248,10 @@ public:
     // caller may fill it (e.g. from a reduce-scatter) or rebind it.
     void* grad_buffer(SubgroupId id);
     void bind_grad_buffer(SubgroupId id, void* device_ptr);
+    // Several gradient sources (e.g. every data-parallel peer's contribution,
+    // mapped over NVLink): the update sums them in fp32 in order, rounds once
+    // to the gradient kind, and applies Adam in the same kernel pass.
+    void bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources);
     void* params16_buffer(SubgroupId id);
 
     PhaseStats run_update(int iteration);
@@ -302,6 +306,7 @@ private:
     void completion_loop();
     static void CUDART_CB host_done(void* arg);
     void check_grads_finite_or_throw();
+    std::vector<unsigned long long> nonfinite_counts();
 
     WorkerId id_;
     std::vector<std::shared_ptr<Tier>> tiers_;
@@ -345,6 +350,7 @@ private:
     unsigned long long* sg_counts_ = nullptr; // per-subgroup non-finite counts (pre-check)
     std::unordered_map<SubgroupId, std::size_t> index_of_;
     std::vector<std::uint16_t*> grad_ptr_;
+    std::vector<std::vector<const void*>> grad_sources_;  // non-empty: fused multi-source reduction
     std::vector<std::uint16_t*> p16_ptr_;
     std::vector<DeviceEvents> events_;
     std::int64_t phase_t0_ns_ = 0;

@@ -188,4 +188,46 @@ cudaError_t launch_count_nonfinite16(const uint16_t* src, uint64_t n, int kind,
     return cudaGetLastError();
 }
 
+namespace {
+
+struct SumSources {
+    const uint16_t* src[kMaxGradSources];
+    int n;
+};
+
+// Non-finite count of the reduced gradient the fused multi-source update
+// will see: the fp32 sum of the sources in order, rounded once to K. An
+// overflow created by the sum itself is caught here, before any state moves.
+template <int K>
+__global__ void __launch_bounds__(kThreads)
+    count_nonfinite_sum_kernel(SumSources s, uint64_t n, unsigned long long* __restrict__ out) {
+    unsigned bad = 0;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t i = tid; i < n; i += nthreads) {
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < kMaxGradSources; ++k)
+            if (k < s.n) acc = __fadd_rn(acc, widen16<K>(__ldcs(s.src[k] + i)));
+        bad += nonfinite16<K>(narrow16<K>(acc));
+    }
+    warp_count_add(out, bad);
+}
+
+}  // namespace
+
+cudaError_t launch_count_nonfinite_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind,
+                                         unsigned long long* out, cudaStream_t stream) {
+    if (n == 0) return cudaSuccess;
+    if (nsrc < 1 || nsrc > kMaxGradSources) return cudaErrorInvalidValue;
+    SumSources s{};
+    for (int k = 0; k < nsrc; ++k) s.src[k] = static_cast<const uint16_t*>(srcs[k]);
+    s.n = nsrc;
+    if (kind == kF16)
+        count_nonfinite_sum_kernel<kF16><<<grid_for(n, 8), kThreads, 0, stream>>>(s, n, out);
+    else
+        count_nonfinite_sum_kernel<kBF16><<<grid_for(n, 8), kThreads, 0, stream>>>(s, n, out);
+    return cudaGetLastError();
+}
+
 }  // namespace tfb

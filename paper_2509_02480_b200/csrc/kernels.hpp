@@ -56,5 +56,9 @@ cudaError_t launch_narrow16(const float* src, uint16_t* dst, uint64_t n, int kin
 cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t stream);
 cudaError_t launch_count_nonfinite16(const uint16_t* src, uint64_t n, int kind,
                                      unsigned long long* out, cudaStream_t stream);
+// Non-finite count of the fp32 sum (in order, rounded once to kind) of nsrc
+// 16-bit sources: the pre-check of the fused multi-source update.
+cudaError_t launch_count_nonfinite_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind,
+                                         unsigned long long* out, cudaStream_t stream);
 
 }  // namespace tfb

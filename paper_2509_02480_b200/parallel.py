@@ -10,6 +10,12 @@ gradient exchange that feeds each rank's engine.
   (SURVEY §8e). Backend: NCCL over NVLink on GPUs, gloo on CPU (tests).
   The output buffers are what a rank binds into its engine with
   OffloadWorker.bind_grad_buffer (no copy).
+* PeerGradients: the fused alternative — no collective on the data path.
+  Every rank writes its contribution into one flat device buffer shared with
+  the other ranks over CUDA IPC (NVLink peer mappings); the owner of a
+  subgroup binds the world's slices of it with
+  OffloadWorker.bind_grad_sources, and the update kernel sums them (fp32, in
+  rank order, rounded once) while it streams the optimizer state.
 """
 from __future__ import annotations
 
@@ -77,3 +83,90 @@ def parity_contribution(full_grad16, world: int, rank: int):
 def owned_ids(M: int, world: int, rank: int) -> List[int]:
     b, c = shard(M, world, rank)
     return list(range(b, b + c))
+
+
+class _DeviceArray:
+    """__cuda_array_interface__ view of a raw device range (torch.as_tensor)."""
+
+    def __init__(self, ptr: int, n: int, typestr: str):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class PeerGradients:
+    """One flat 16-bit gradient buffer per rank covering every subgroup,
+    mapped by every other rank over CUDA IPC.
+
+    local(sg) is this rank's contribution to subgroup sg (a torch view to fill
+    in backward); sources(sg) are the device pointers of all ranks'
+    contributions in rank order, for OffloadWorker.bind_grad_sources on the
+    owner. Subgroup slices start on 16-byte boundaries so the update kernel
+    keeps its 128-bit loads. Synchronisation is the caller's: every rank's
+    writes must be complete (stream synchronised + barrier) before an owner's
+    run_update reads them, and every owner's update must be done (barrier)
+    before a rank overwrites its buffer."""
+
+    def __init__(self, sizes: Sequence[int], world: int, rank: int, device: int = 0, dtype: str = "f16",
+                 group=None):
+        import torch.distributed as dist
+
+        from . import tierflow as tf
+        if dtype not in ("f16", "bf16"):
+            raise ValueError("dtype must be f16 or bf16")
+        self._tf, self.device, self.world, self.rank = tf, device, world, rank
+        self.sizes = list(sizes)
+        self.dtype = dtype
+        self.offsets: List[int] = []
+        off = 0
+        for n in self.sizes:
+            self.offsets.append(off)
+            off += (n + 7) // 8 * 8
+        self.total = max(off, 8)
+        self._local = tf.device_alloc(device, 2 * self.total)
+        self._opened: List[int] = []
+        self.bases: List[int] = []
+        try:
+            handle = tf.ipc_get_handle(device, self._local)
+            handles: List[object] = [None] * world
+            if world > 1:
+                dist.all_gather_object(handles, handle, group=group)
+            else:
+                handles = [handle]
+            for r, h in enumerate(handles):
+                if r == rank:
+                    self.bases.append(self._local)
+                else:
+                    ptr = tf.ipc_open_handle(device, h)
+                    self._opened.append(ptr)
+                    self.bases.append(ptr)
+        except BaseException:
+            self.close()
+            raise
+
+    def local(self, sg: int):
+        import torch
+        dt = torch.float16 if self.dtype == "f16" else torch.bfloat16
+        arr = _DeviceArray(self._local + 2 * self.offsets[sg], self.sizes[sg], "<i2")
+        return torch.as_tensor(arr, device=f"cuda:{self.device}").view(dt)
+
+    def sources(self, sg: int) -> List[int]:
+        return [b + 2 * self.offsets[sg] for b in self.bases]
+
+    def bind(self, worker, owned: Sequence[int]) -> None:
+        """Bind every owned subgroup of `worker` to the world's contributions."""
+        for sg in owned:
+            worker.bind_grad_sources(sg, self.sources(sg))
+
+    def close(self) -> None:
+        for ptr in self._opened:
+            self._tf.ipc_close_handle(self.device, ptr)
+        self._opened = []
+        if self._local:
+            self._tf.device_free(self.device, self._local)
+            self._local = 0
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

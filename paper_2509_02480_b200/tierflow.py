@@ -579,6 +579,12 @@ class OffloadWorker:
     def bind_grad_buffer(self, sg: int, device_ptr: int) -> None:
         _lib.call("tfg_engine_bind_grad_buffer", self._h, sg, C.c_void_p(device_ptr))
 
+    def bind_grad_sources(self, sg: int, device_ptrs) -> None:
+        """Feed subgroup `sg` from the fp32 sum of several 16-bit device
+        buffers (in order, rounded once): the fused reduce + update."""
+        arr = (C.c_void_p * len(device_ptrs))(*device_ptrs)
+        _lib.call("tfg_engine_bind_grad_sources", self._h, sg, arr, len(device_ptrs))
+
     def params16_buffer(self, sg: int) -> int:
         p = C.c_void_p()
         _lib.call("tfg_engine_params16_buffer", self._h, sg, C.byref(p))
@@ -770,6 +776,37 @@ def synthetic_grads(out, seed: int, subgroup: int, iteration: int, step: int = 0
 
 def synthetic_state(p, m, v, seed: int, subgroup: int, stream=None) -> None:
     _lib.call("tfg_synthetic_state", _ptr(p), _ptr(m), _ptr(v), p.numel(), seed, subgroup, _stream(stream))
+
+
+IPC_HANDLE_BYTES = 64
+
+
+def device_alloc(device: int, nbytes: int) -> int:
+    p = C.c_void_p()
+    _lib.call("tfg_device_alloc", device, nbytes, C.byref(p))
+    return p.value
+
+
+def device_free(device: int, ptr: int) -> None:
+    _lib.call("tfg_device_free", device, C.c_void_p(ptr))
+
+
+def ipc_get_handle(device: int, ptr: int) -> bytes:
+    buf = C.create_string_buffer(IPC_HANDLE_BYTES)
+    _lib.call("tfg_ipc_get_handle", device, C.c_void_p(ptr), buf)
+    return buf.raw
+
+
+def ipc_open_handle(device: int, handle: bytes) -> int:
+    if len(handle) != IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be 64 bytes")
+    p = C.c_void_p()
+    _lib.call("tfg_ipc_open_handle", device, handle, C.byref(p))
+    return p.value
+
+
+def ipc_close_handle(device: int, ptr: int) -> None:
+    _lib.call("tfg_ipc_close_handle", device, C.c_void_p(ptr))
 
 
 def device_count() -> int:
