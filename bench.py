@@ -295,7 +295,8 @@ def e2e_shard(sizes, world, pool_slots):
     return sizes[:max(1, min(len(sizes), fit))]
 
 
-def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring):
+def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring,
+            hbm_retain=1):
     # The bandwidth EMA re-places subgroups off the slow directory tier over the
     # first phases (paper §3.3); time the converged pipeline.
     warmup = max(warmup, 5)
@@ -314,7 +315,7 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=str(root / "locks"))
     w = tf.OffloadWorker(rank, [dram, nvme], opt, tf.AdamHyper(), trace,
-                         tf.DeviceOptions(dev, tf.F16, tf.F16, ring))
+                         tf.DeviceOptions(dev, tf.F16, tf.F16, ring, 0, 1, hbm_retain))
     for k, n in enumerate(sizes):
         w.add_subgroup(base_id + k, n)
     t0 = time.time()
@@ -346,16 +347,18 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     hits = statistics.mean(p[1].cache_hits for p in phases)
     retained = last.retained
     alloc = last.flush_allocation
-    # Pipeline roofline per phase. PCIe: 12 B/param each way, against each
-    # direction alone and against the measured duplex ceiling. Tiers: bytes
-    # actually moved (PhaseStats.tier_obs) over the tier's probed rates; the
-    # host_dram tier moves blocks by exchange, so it costs no tier time.
-    bytes_dir = 12 * params
-    pcie_s = max(bytes_dir / pcie["h2d"], bytes_dir / pcie["d2h"], 2 * bytes_dir / pcie["bidir"])
+    # Pipeline roofline per phase. PCIe: the bytes each direction moved
+    # (12 B/param, minus the HBM-retained subgroups), against each direction
+    # alone and against the measured duplex ceiling. Tiers: bytes actually
+    # moved (PhaseStats.tier_obs) over the tier's probed rates; the host_dram
+    # tier moves blocks by exchange, so it costs no tier time.
+    h2d_b = statistics.mean(p[1].h2d_bytes for p in phases)
+    d2h_b = statistics.mean(p[1].d2h_bytes for p in phases)
+    pcie_s = max(h2d_b / pcie["h2d"], d2h_b / pcie["d2h"], (h2d_b + d2h_b) / pcie["bidir"])
     obs = last.tier_obs
     nvme_s = obs[1].read_bytes / probe.read_bw + obs[1].write_bytes / probe.write_bw
     bound_s = max(pcie_s, nvme_s)
-    res = dict(ms=ms, params=params, h2d=bytes_dir, d2h=bytes_dir, init_s=init_s, hits=hits,
+    res = dict(ms=ms, params=params, h2d=int(h2d_b), d2h=int(d2h_b), init_s=init_s, hits=hits,
                alloc=alloc, retained=retained, pcie=pcie, nvme=dict(read=probe.read_bw, write=probe.write_bw),
                bound_ms=bound_s * 1e3, pcie_bound_ms=pcie_s * 1e3, tier_bound_ms=nvme_s * 1e3,
                kernel_ms=statistics.mean(p[1].kernel_seconds for p in phases) * 1e3,
@@ -417,6 +420,7 @@ def main(argv=None):
     ap.add_argument("--pool-slots", type=int, default=12)
     ap.add_argument("--cache-slots", type=int, default=5)
     ap.add_argument("--ring", type=int, default=3)
+    ap.add_argument("--hbm-retain", type=int, default=1, help="retained subgroups stay in HBM between phases")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
@@ -475,7 +479,7 @@ def main(argv=None):
             if len(e_sizes) < len(sizes):
                 log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank")
             r = e2e_leg(tf, e_sizes, base_id, a.steps, a.warmup, a.seed, rank, world, a.tier_root, a.pool_slots,
-                        a.cache_slots, a.ring)
+                        a.cache_slots, a.ring, a.hbm_retain)
             e_ms = allmax(world, r["ms"])
             e2e = {"value": world * r["params"] / (e_ms / 1e3), "unit": "params/s",
                    "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": e_ms,
@@ -486,6 +490,7 @@ def main(argv=None):
                    "pcie_gbs": {k: round(v / 1e9, 1) for k, v in r["pcie"].items()},
                    "nvme_gbs": {k: round(v / 1e9, 2) for k, v in r["nvme"].items()},
                    "kernel_ms_per_phase": r["kernel_ms"], "init_s": r["init_s"], "gpu_launches": r["launches"],
+                   "hbm_retain": a.hbm_retain,
                    "path": "C ABI tfg_engine_run_update, tiers [host_dram pinned, local_dir O_DIRECT]"}
         except Exception as exc:  # keep the device-timed line; report the failure
             e2e = {"error": f"{type(exc).__name__}: {exc}"}

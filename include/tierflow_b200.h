@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define TFG_ABI_VERSION 1
+#define TFG_ABI_VERSION 2
 #define TFG_MAX_TIERS 8
 
 typedef enum tfg_status {
@@ -99,6 +99,8 @@ typedef struct tfg_device_options {
                                 pinned slot over PCIe both ways; 2: DMA in, the kernel's epilogue
                                 writes the updated state back into the pinned slot */
     int32_t d2h_split;       /* copy mode: concurrent D2H streams per subgroup (1 or 2) */
+    int32_t hbm_retain;      /* copy mode, 16-bit gradients: retained subgroups keep their state in
+                                HBM between phases (no D2H now, no H2D at the next update) */
 } tfg_device_options;
 
 typedef struct tfg_tier_observation { /* placement.hpp:138-145 */

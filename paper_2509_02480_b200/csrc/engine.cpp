@@ -376,6 +376,18 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&counters_), 2 * sizeof(unsigned long long)), "cudaMalloc");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&sg_counts_), ids_.size() * sizeof(unsigned long long)),
                "cudaMalloc");
+    hbm_slot_.assign(ids_.size(), -1);
+    if (dev_.hbm_retain != 0 && dev_.zero_copy == 0 && opt_.skip_gradients) {
+        const int cap = opt_.retention_capacity(static_cast<int>(ids_.size()));
+        hbm_cache_.assign(static_cast<std::size_t>(cap), nullptr);
+        hbm_ready_.assign(hbm_cache_.size(), nullptr);
+        for (std::size_t b = 0; b < hbm_cache_.size(); ++b) {
+            cuda_check(cudaMalloc(reinterpret_cast<void**>(&hbm_cache_[b]), 3 * ring_stride_ * sizeof(float)),
+                       "cudaMalloc(hbm retention)");
+            cuda_check(cudaEventCreateWithFlags(&hbm_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
+            hbm_free_.push_back(static_cast<int>(hbm_cache_.size() - 1 - b));
+        }
+    }
     grad_ptr_.clear();
     p16_ptr_.clear();
     events_.assign(ids_.size(), DeviceEvents{});
@@ -404,6 +416,13 @@ void OffloadWorker::release_device() {
     events_.clear();
     for (float* r : ring_) cudaFree(r);
     ring_.clear();
+    for (float* r : hbm_cache_) cudaFree(r);
+    for (cudaEvent_t ev : hbm_ready_)
+        if (ev) cudaEventDestroy(ev);
+    hbm_cache_.clear();
+    hbm_ready_.clear();
+    hbm_free_.clear();
+    hbm_slot_.clear();
     for (float* r : ring_grad_) cudaFree(r);
     ring_grad_.clear();
     if (grad32_dev_) cudaFree(grad32_dev_);
@@ -655,13 +674,13 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             const SubgroupId id = order[j];
             const int slot = wait_host_resident(id);
             host_resident_ns_[index_of_.at(id)] = now_ns();
-            issue_device_update(j, id, slot, c);
+            const auto moved = issue_device_update(j, id, slot, c);
             std::lock_guard<std::mutex> g(mu_);
             Subgroup& sg = subgroups_.at(id);
             sg.step_count = static_cast<std::uint64_t>(iteration) + 1;
             stats.params_updated += sg.param_count;
-            stats.h2d_bytes += (opt_.skip_gradients ? 12 : 16) * sg.param_count;
-            stats.d2h_bytes += 12 * sg.param_count;
+            stats.h2d_bytes += moved.first;
+            stats.d2h_bytes += moved.second;
             if (completion_error_) std::rethrow_exception(completion_error_);
         }
         // All device updates retire, then the lazy flushes drain.
@@ -745,7 +764,8 @@ PhaseStats OffloadWorker::run_update(int iteration) {
 
 // Enqueue subgroup j on the three pipeline streams. Ring buffer j % K is
 // reused once the D2H of subgroup j - K has drained it.
-void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, const AdamConsts& c) {
+std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot,
+                                                                         const AdamConsts& c) {
     Subgroup& sg = subgroups_.at(id);
     const std::uint64_t pc = sg.param_count;
     const std::size_t k = index_of_.at(id);
@@ -794,17 +814,42 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
             cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
         auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
         cuda_check(cudaLaunchHostFunc(s_k_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
-        return;
+        return {(opt_.skip_gradients ? 12 : 16) * pc, 12 * pc};
     }
-    float* d = ring_[j % K];
+    // HBM retention: a subgroup whose state stayed in HBM since the last phase
+    // skips the H2D; one the plan retains now skips the D2H and keeps (or
+    // takes) a retention buffer. Without a free buffer it takes the host path.
+    const int held = hbm_slot_[k];
+    int hslot = held;
+    bool keep_in_hbm = false;
+    if (!hbm_cache_.empty()) {
+        std::lock_guard<std::mutex> g(mu_);
+        const bool retain = dests_->assign_storage_tier(id).host_retain;
+        if (retain && hslot < 0 && !hbm_free_.empty()) {
+            hslot = hbm_free_.back();
+            hbm_free_.pop_back();
+        }
+        keep_in_hbm = retain && hslot >= 0;
+    }
+    float* d = hslot >= 0 ? hbm_cache_[static_cast<std::size_t>(hslot)] : ring_[j % K];
     const std::uint64_t ds = seg_stride(pc);
-    if (j >= K) cuda_check(cudaStreamWaitEvent(s_h2d_, events_[index_of_.at(order_[j - K])].d2h_end, 0), "wait");
+    // Ring buffer j % K was last drained by the D2H of j - K (the D2H stream
+    // is FIFO, so j - K's d2h_end also covers an earlier HBM-resident user).
+    if (hslot < 0 && j >= K)
+        cuda_check(cudaStreamWaitEvent(s_h2d_, events_[index_of_.at(order_[j - K])].d2h_end, 0), "wait");
     cuda_check(cudaEventRecord(e.h2d_start, s_h2d_), "cudaEventRecord");
-    copy_state(d, blk, pc, true, s_h2d_);
+    std::uint64_t h2d_bytes = 0, d2h_bytes = 0;
+    if (held < 0) {
+        if (hslot >= 0)  // the buffer's previous occupant has been written back
+            cuda_check(cudaStreamWaitEvent(s_h2d_, hbm_ready_[static_cast<std::size_t>(hslot)], 0), "wait");
+        copy_state(d, blk, pc, true, s_h2d_);
+        h2d_bytes += 12 * pc;
+    }
     if (!opt_.skip_gradients) {  // baseline flow: fp32 gradients fetched with the state
         float* dg = ring_grad_[j % K];
         cuda_check(cudaMemcpyAsync(dg, grad_annex(blk), 4 * pc, cudaMemcpyHostToDevice, s_h2d_),
                    "cudaMemcpyAsync(grads)");
+        h2d_bytes += 4 * pc;
         a.g = dg;
         a.grad_kind = kF32;
     }
@@ -831,14 +876,16 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
             cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
         auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
         cuda_check(cudaLaunchHostFunc(s_k_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
-        return;
+        return {h2d_bytes, 12 * pc};
     }
     cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
     cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
 
     cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
     cuda_check(cudaEventRecord(e.d2h_start, s_d2h_), "cudaEventRecord");
-    if (dev_.d2h_split > 1 && ds == pc) {
+    if (keep_in_hbm) {
+        // no write-back: the host slot copy is stale until the next update
+    } else if (dev_.d2h_split > 1 && ds == pc) {
         // Two concurrent D2H halves on two copy engines: the write-back gets
         // a larger share of the duplex link against the H2D stream.
         const std::size_t bytes = 12 * pc;
@@ -854,9 +901,41 @@ void OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot, 
     } else {
         copy_state(d, blk, pc, false, s_d2h_);
     }
+    if (!keep_in_hbm) d2h_bytes += 12 * pc;
     cuda_check(cudaEventRecord(e.d2h_end, s_d2h_), "cudaEventRecord");
+    if (hslot >= 0) {
+        std::lock_guard<std::mutex> g(mu_);
+        if (keep_in_hbm) {
+            hbm_slot_[k] = hslot;
+        } else {  // written back: the buffer is free once this D2H drains
+            cuda_check(cudaEventRecord(hbm_ready_[static_cast<std::size_t>(hslot)], s_d2h_), "cudaEventRecord");
+            hbm_free_.push_back(hslot);
+            hbm_slot_[k] = -1;
+        }
+    }
     auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
     cuda_check(cudaLaunchHostFunc(s_d2h_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
+    return {h2d_bytes, d2h_bytes};
+}
+
+// Synchronous D2H of a P/m/v buffer (segment stride seg_stride(pc)) into a
+// contiguous host P||m||v. Only called with the pipeline drained.
+void OffloadWorker::device_state_to_host(const float* dev, float* host, std::uint64_t pc) {
+    DeviceGuard dg(dev_.device);
+    const std::uint64_t ds = seg_stride(pc);
+    for (int s = 0; s < 3; ++s)
+        cuda_check(cudaMemcpy(host + s * pc, dev + s * ds, 4 * pc, cudaMemcpyDeviceToHost), "cudaMemcpy(state)");
+}
+
+// Refreshes the host slot of an HBM-retained subgroup and frees its buffer
+// (op-level flush outside a phase). Called with mu_ held.
+void OffloadWorker::writeback_hbm_copy_locked(std::size_t k, int slot) {
+    const int b = hbm_slot_[k];
+    if (b < 0) return;
+    device_state_to_host(hbm_cache_[static_cast<std::size_t>(b)], pool_->block(slot).payload(),
+                         subgroups_.at(ids_[k]).param_count);
+    hbm_slot_[k] = -1;
+    hbm_free_.push_back(b);
 }
 
 void CUDART_CB OffloadWorker::host_done(void* arg) {
@@ -936,6 +1015,7 @@ std::shared_future<IoStats> OffloadWorker::enqueue_flush(SubgroupId id, TierId d
     std::lock_guard<std::mutex> g(mu_);
     Subgroup& sg = subgroups_.at(id);
     if (sg.residency != Residency::host_cached || sg.slot < 0) throw Error("enqueue_flush: subgroup not host-resident");
+    if (!hbm_slot_.empty()) writeback_hbm_copy_locked(index_of_.at(id), sg.slot);
     return start_flush_locked(id, dest, sg.slot);
 }
 
@@ -966,7 +1046,11 @@ void OffloadWorker::read_current_state(SubgroupId id, float* out) {
         const Subgroup& sg = subgroups_.at(id);
         pc = sg.param_count;
         if (sg.residency == Residency::host_cached) {
-            std::memcpy(out, pool_->block(sg.slot).payload(), 12 * pc);
+            const int b = hbm_slot_.empty() ? -1 : hbm_slot_[index_of_.at(id)];
+            if (b >= 0)
+                device_state_to_host(hbm_cache_[static_cast<std::size_t>(b)], out, pc);
+            else
+                std::memcpy(out, pool_->block(sg.slot).payload(), 12 * pc);
             return;
         }
         if (sg.residency != Residency::on_tier) throw Error("read_current_state: subgroup is in flight");

@@ -78,6 +78,10 @@ struct DeviceOptions {
     int device_buffers = 3;  // depth of the H2D -> kernel -> D2H ring
     int zero_copy = 0;       // 1: the kernel reads/writes the pinned slot over PCIe (no ring, no DMA)
     int d2h_split = 1;       // concurrent D2H copy streams per subgroup (1 or 2)
+    // Copy mode, 16-bit gradient flow: a subgroup the destination plan retains
+    // keeps its updated state in HBM until its next update (no D2H now, no H2D
+    // then); the host slot stays reserved and is refreshed on demand.
+    int hbm_retain = 1;
 };
 
 enum class Residency : int { host_cached = 0, in_flight = 1, on_tier = 2 };
@@ -301,7 +305,11 @@ private:
 
     void setup_device();
     void release_device();
-    void issue_device_update(std::size_t j, SubgroupId id, int slot, const AdamConsts& c);
+    // Returns the PCIe bytes moved {H2D, D2H}.
+    std::pair<std::uint64_t, std::uint64_t> issue_device_update(std::size_t j, SubgroupId id, int slot,
+                                                                const AdamConsts& c);
+    void device_state_to_host(const float* dev, float* host, std::uint64_t pc);
+    void writeback_hbm_copy_locked(std::size_t k, int slot);
     void copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device, cudaStream_t s);
     void completion_loop();
     static void CUDART_CB host_done(void* arg);
@@ -338,6 +346,14 @@ private:
     cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr, s_d2h2_ = nullptr;
     std::vector<float*> ring_;
     std::vector<float*> ring_grad_;  // baseline flow: fp32 gradient segment per ring buffer
+    // HBM retention (DeviceOptions::hbm_retain): one device buffer per
+    // retention slot. hbm_slot_[k] >= 0 while subgroup k's authoritative state
+    // lives there (its host slot copy is stale); hbm_ready_[b] is the last D2H
+    // out of buffer b, which a new occupant's H2D waits for.
+    std::vector<float*> hbm_cache_;
+    std::vector<cudaEvent_t> hbm_ready_;
+    std::vector<int> hbm_free_;
+    std::vector<int> hbm_slot_;
     float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H
     HostBlock grad_stage_;           // baseline flow: pinned D2H staging of fp32 gradients
     std::size_t state_block_bytes_ = 0;  // header + P||m||v of the largest subgroup, 4 KiB multiple

@@ -137,6 +137,8 @@ class DeviceOptions:
     # the pinned slot over PCIe both ways; 2: DMA in, kernel epilogue writes back.
     zero_copy: int = 0
     d2h_split: int = 1
+    # Retained subgroups keep their updated state in HBM between phases.
+    hbm_retain: int = 1
 
 
 @dataclass
@@ -512,7 +514,7 @@ class OffloadWorker:
         h = C.c_void_p()
         o, hy = opt.c(), hyper.c()
         d = _lib.DeviceOptionsC(device.device, device.grad_dtype, device.param_dtype, device.device_buffers,
-                                int(device.zero_copy), device.d2h_split)
+                                int(device.zero_copy), device.d2h_split, int(device.hbm_retain))
         _lib.call("tfg_engine_create", worker_id, arr, len(self._tiers), C.byref(o), C.byref(hy),
                   trace.handle if trace else None, C.byref(d), C.byref(h))
         self._h = h

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol(tf):
 
 def test_abi_version_and_errors(tf):
     from paper_2509_02480_b200 import _lib
-    assert _lib.load().tfg_abi_version() == 1
+    assert _lib.load().tfg_abi_version() == 2
     with pytest.raises(tf.ConfigError):
         tf.assign_subgroups(0, [1.0])
     with pytest.raises(tf.ConfigError):

@@ -385,3 +385,54 @@ def test_engine_mode_backward_writes_nothing(tf, cuda, lock_dir):
         w.run_backward_sim(0, tf.SyntheticGradSource(5), 1)
         assert sum(e.bytes for e in trace.snapshot(m0) if e.kind == tf.EventKind.flush_end) == want
         w.close()
+
+
+@pytest.mark.parametrize("hbm", [0, 1])
+def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
+    """Retained subgroups keep their state in HBM between phases: no D2H when
+    retained, no H2D at the next update. Same bits and cache hits as the
+    host-retention path and the oracle, including re-retention (C > M/2), a
+    skipped iteration (same direction twice) and an op-level flush of an
+    HBM-resident subgroup."""
+    params = [100_000, 64_000, 99_996, 50_000, 77_777]
+    seed, C = 23, 3
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=C + 3, lock_dir=lock_dir), tf.AdamHyper(), trace,
+                         tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    w.set_fixed_ratio([1.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    S = sum(params)
+    applied = [0, 1, 2, 4]
+    prev_retained = set()
+    for it in applied:
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        st = w.run_update(it)
+        order = list(range(len(params))) if it % 2 == 0 else list(reversed(range(len(params))))
+        retained = set(order[-C:])
+        assert st.cache_hits == len(prev_retained)
+        if hbm:
+            assert st.h2d_bytes == 12 * (S - sum(params[i] for i in prev_retained))
+            assert st.d2h_bytes == 12 * (S - sum(params[i] for i in retained))
+        else:
+            assert st.h2d_bytes == st.d2h_bytes == 12 * S
+        prev_retained = retained
+    want = {}
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in applied:
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        want[sg] = (np.concatenate([p, m, v]).view(np.uint32), p16)
+    for sg in range(len(params)):
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), want[sg][0]), sg
+        assert np.array_equal(w.read_params16(sg), want[sg][1])
+    # op-level flush of a retained (HBM-resident) subgroup writes the current bits
+    w.enqueue_flush(3, 1).get()
+    got = np.empty(3 * params[3], np.float32)
+    tiers[1].read_subgroup(3, params[3], got)
+    assert np.array_equal(got.view(np.uint32), want[3][0])
+    assert np.array_equal(w.read_current_state(3).view(np.uint32), want[3][0])
+    w.close()
