@@ -417,8 +417,8 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama2-7b")
     ap.add_argument("--tier-root", default=os.environ.get("TFB_TIER_ROOT", str(ROOT / "gpurun_out" / "bench_tiers")))
-    ap.add_argument("--pool-slots", type=int, default=12)
-    ap.add_argument("--cache-slots", type=int, default=5)
+    ap.add_argument("--pool-slots", type=int, default=16)
+    ap.add_argument("--cache-slots", type=int, default=-1, help="-1: C = pool_slots - 3 (reference default)")
     ap.add_argument("--ring", type=int, default=3)
     ap.add_argument("--hbm-retain", type=int, default=1, help="retained subgroups stay in HBM between phases")
     ap.add_argument("--seed", type=int, default=42)

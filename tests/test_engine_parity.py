@@ -244,11 +244,14 @@ def test_dram_and_directory_tiers_zero_copy_path(tf, cuda, lock_dir, tmp_path):
     w, trace, tier_objs = make_engine(tf, tiers, params, pool_slots=5, ratio=[2.0, 1.0], seed=11, lock_dir=lock_dir,
                                       wd=0.01)
     iters = 4
+    held = []  # HBM-retained by the previous phase (C = 5 - 3): no H2D this phase
     for it in range(iters):
         w.run_backward_sim(it, tf.SyntheticGradSource(11), 1)
         st = w.run_update(it)
         assert st.params_updated == sum(params)
-        assert st.h2d_bytes == 12 * sum(params) and st.kernel_seconds > 0
+        assert st.h2d_bytes == 12 * (sum(params) - sum(params[i] for i in held)) and st.kernel_seconds > 0
+        order = list(range(5)) if it % 2 == 0 else list(range(4, -1, -1))
+        held = order[-2:]
     states, (order, hit, dest, origin) = oracle.run_engine_oracle(params, 11, iters, 5, -1, True, True, [2.0, 1.0],
                                                                   weight_decay=0.01)
     for i, n in enumerate(params):
