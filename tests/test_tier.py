@@ -84,6 +84,10 @@ def test_throttle_rate_is_enforced(tf):
     t = tf.Tier(tf.TierSpec(0, tf.TierKind.mem_throttled, "m", 200e6, 100e6))
     P = 700_000  # 8.4 MB
     s = _state(P, 3)
+    # The first write also allocates and page-faults the blob (host time, not
+    # device time); measure the rewrite, as the reference's fidelity check is
+    # otherwise flaky on slow hosts (proj/test_output.txt:15-25).
+    t.write_subgroup(1, P, s)
     w = t.write_subgroup(1, P, s)
     r = t.read_subgroup(1, P, np.empty_like(s))
     assert 0.85 < (12 * P / w.seconds) / 100e6 < 1.1
