@@ -24,16 +24,32 @@ configs = [tuple(int(x) for x in c.split(":")) for c in sys.argv[2:]] or [(12, 5
 configs = [c if len(c) == 6 else c + (1,) for c in configs]
 sub = 100_000_000
 sizes = [min(sub, total - k * sub) for k in range((total + sub - 1) // sub)]
+import os
 root = ROOT / "gpurun_out" / "e2e_sweep_tiers"
 shutil.rmtree(root, ignore_errors=True)
-dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9))
-nvme = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4))
-pr = nvme.probe_bandwidth(256 << 20, 3)
-print(f"nvme probe r={pr.read_bw/1e9:.2f} w={pr.write_bw/1e9:.2f} GB/s", flush=True)
+# TFB_TIERS: "dram,nvme" (default) or "nvme,remote" (host DRAM only as pool
+# slots: the state spills to the directory tiers)
+tier_set = os.environ.get("TFB_TIERS", "dram,nvme").split(",")
+remote_root = Path(os.environ.get("TFB_REMOTE_ROOT", "/tmp/tfb_remote"))
+shutil.rmtree(remote_root, ignore_errors=True)
+tiers = []
+for name in tier_set:
+    tid = len(tiers)
+    if name == "dram":
+        tiers.append(tf.Tier(tf.TierSpec(tid, tf.TierKind.host_dram, "dram", 50e9, 50e9)))
+    elif name == "nvme":
+        tiers.append(tf.Tier(tf.TierSpec(tid, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4)))
+    elif name == "remote":
+        tiers.append(tf.Tier(tf.TierSpec(tid, tf.TierKind.remote_dir, str(remote_root), 0, 0, io_parallelism=4)))
+    else:
+        raise SystemExit(f"unknown tier {name}")
+    if name != "dram":
+        pr = tiers[-1].probe_bandwidth(256 << 20, 3)
+        print(f"{name} probe r={pr.read_bw/1e9:.2f} w={pr.write_bw/1e9:.2f} GB/s", flush=True)
 out = []
 for pool, cache, ring, zc, split, hbm in configs:
     trace = tf.EventTrace()
-    w = tf.OffloadWorker(0, [dram, nvme], tf.ScheduleOptions(pool_slots=pool, cache_slots=cache,
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=pool, cache_slots=cache,
                                                             lock_dir=str(root / "locks")),
                          tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, ring, zc, split, hbm))
     for k, n in enumerate(sizes):
@@ -61,12 +77,13 @@ for pool, cache, ring, zc, split, hbm in configs:
               f"alloc {st.flush_allocation} h2d {st.h2d_bytes/1e9:.1f} GB d2h {st.d2h_bytes/1e9:.1f} GB", flush=True)
         if it == 6:
             Path("gpurun_out").mkdir(exist_ok=True)
-            Path(f"gpurun_out/timeline_p{pool}_c{cache}_r{ring}_z{zc}_s{split}_h{hbm}.json").write_text(json.dumps(tl))
+            Path(f"gpurun_out/timeline_{'_'.join(tier_set)}_p{pool}_c{cache}_r{ring}_z{zc}_s{split}_h{hbm}.json").write_text(json.dumps(tl))
     steady = phases[3:]
     out.append(dict(pool=pool, cache=cache, ring=ring, zero_copy=zc, d2h_split=split, hbm_retain=hbm, init_s=init_s,
                     ms=statistics.mean(p["ms"] for p in steady), phases=phases))
     w.close()
     del w
 print(json.dumps([{k: v for k, v in o.items() if k != "phases"} for o in out], indent=1))
-Path("gpurun_out/e2e_sweep.json").write_text(json.dumps(out, indent=1))
+Path(os.environ.get("TFB_SWEEP_OUT", "gpurun_out/e2e_sweep.json")).write_text(json.dumps(out, indent=1))
 shutil.rmtree(root, ignore_errors=True)
+shutil.rmtree(remote_root, ignore_errors=True)
