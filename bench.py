@@ -240,6 +240,104 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
 
 
 # ---------------------------------------------------------------------------
+# leg 1b (--exchange): the gradient reduce-scatter inside the update phase.
+# Strong scaling over ONE model: every rank holds its 16-bit
+# gradient contribution to every subgroup (the backward's output), owns the
+# contiguous block parallel.shard() gives it, and per step either
+#   fused  reads all ranks' contributions of its subgroups over CUDA IPC
+#          (NVLink peer loads) inside the Adam kernel (tfg_adam_fused_multi), or
+#   nccl   runs one NCCL reduce_scatter of the padded flat gradient, then the
+#          single-source kernel (the collective-then-kernel baseline).
+
+
+def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2509_02480_b200 import parallel
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.Stream(dev)
+    M = len(sizes)
+    begin, count = parallel.shard(M, world, rank)
+    owned = list(range(begin, begin + count))
+    states, p16s = {}, {}
+    counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    hyper = tf.AdamHyper()
+    pg = None
+    flat = mine = None
+    with torch.cuda.stream(stream):
+        for sg in owned:
+            n = sizes[sg]
+            st = torch.empty(3 * n, dtype=torch.float32, device=dev)
+            tf.synthetic_state(st[:n], st[n:2 * n], st[2 * n:], seed, sg, stream=stream)
+            states[sg] = st
+            p16s[sg] = torch.empty(n, dtype=torch.int16, device=dev)
+        if mode == "fused":
+            pg = parallel.PeerGradients(sizes, world, rank, device=dev.index)
+            for sg, n in enumerate(sizes):  # this rank's contribution to every subgroup
+                tf.synthetic_grads(pg.local(sg).view(torch.int16), seed + 100 * rank, sg, 0, stream=stream)
+        else:
+            # padded layout: rank r's block = shard(r) subgroups x max subgroup size
+            cmax = max(parallel.shard(M, world, r)[1] for r in range(world))
+            sub = max(sizes)
+            flat = torch.zeros(world * cmax * sub, dtype=torch.int16, device=dev)
+            for r in range(world):
+                b, c = parallel.shard(M, world, r)
+                for k in range(c):
+                    off = (r * cmax + k) * sub
+                    tf.synthetic_grads(flat[off:off + sizes[b + k]], seed + 100 * rank, b + k, 0, stream=stream)
+            mine = torch.empty(cmax * sub, dtype=torch.int16, device=dev) if world > 1 else flat
+    stream.synchronize()
+    barrier(world)  # every contribution written before any owner reads it
+
+    def step(t, events=None):
+        if mode == "nccl" and world > 1:
+            with torch.cuda.stream(stream):
+                dist.reduce_scatter_tensor(mine.view(torch.float16), flat.view(torch.float16), op=dist.ReduceOp.SUM)
+        for k, sg in enumerate(owned):
+            n = sizes[sg]
+            st = states[sg]
+            if events is not None:
+                events[k][0].record(stream)
+            if mode == "fused":
+                tf.adam_fused_multi(st[:n], st[n:2 * n], st[2 * n:], pg.sources(sg), p16s[sg], t, hyper,
+                                    counters=counters, stream=stream)
+            else:
+                off = k * max(sizes)
+                tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], mine[off:off + n], p16s[sg], t, hyper,
+                              counters=counters, stream=stream)
+            if events is not None:
+                events[k][1].record(stream)
+
+    for w in range(warmup):
+        step(w + 1)
+    stream.synchronize()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in owned]
+          for _ in range(steps)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        start.record(stream)
+        for s in range(steps):
+            step(warmup + s + 1, ev[s])
+        end.record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)  # no rank frees its contribution while a peer still reads it
+    total_ms = start.elapsed_time(end)
+    kernel_ms = sum(a.elapsed_time(b) for row in ev for a, b in row)
+    if counters[0].item() != 0:
+        raise RuntimeError("non-finite gradients in the exchange leg")
+    if pg is not None:
+        pg.close()
+    del states, p16s, flat, mine
+    torch.cuda.empty_cache()
+    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(owned), clocks=clk.summary(),
+                owned_params=sum(sizes[sg] for sg in owned), owned=len(owned))
+
+
+# ---------------------------------------------------------------------------
 # leg 2: end to end through the engine C ABI with host tiers (e2e)
 
 
@@ -281,18 +379,23 @@ def pcie_probe():
     return out
 
 
-def e2e_shard(sizes, world, pool_slots):
-    """Subgroups each rank streams in the e2e leg. The host-DRAM tier pins
-    12 B/param per rank (plus the pool slots); with N ranks on one host the
-    shard is capped to 60% of MemAvailable so N concurrent ranks fit."""
+def e2e_shard(sizes, world, pool_slots, cache_slots):
+    """(subgroups, pool_slots, cache_slots) each rank streams in the e2e leg.
+    Every subgroup pins one 12 B/param host block (a pool slot or a host-DRAM
+    tier blob); N ranks on one host share 60% of MemAvailable. When the
+    requested pool plus the shard does not fit, the pool shrinks first (to a
+    third of the rank's blocks, at least 4 slots) and then the shard."""
     try:
         avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable:"))
     except (OSError, StopIteration):
-        return sizes
-    per_rank = 0.6 * avail / world
-    block = 12 * max(sizes) + 4096
-    fit = int(per_rank // block) - pool_slots
-    return sizes[:max(1, min(len(sizes), fit))]
+        return sizes, pool_slots, cache_slots
+    blocks = int(0.6 * avail / world // (12 * max(sizes) + 4096))
+    pool = pool_slots
+    if pool + len(sizes) > blocks:
+        pool = max(4, min(pool_slots, blocks // 3))
+    n = max(1, min(len(sizes), blocks - pool))
+    cache = cache_slots if cache_slots < 0 else min(cache_slots, max(0, pool - 3))
+    return sizes[:n], pool, cache
 
 
 def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring,
@@ -417,11 +520,17 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama2-7b")
     ap.add_argument("--tier-root", default=os.environ.get("TFB_TIER_ROOT", str(ROOT / "gpurun_out" / "bench_tiers")))
-    ap.add_argument("--pool-slots", type=int, default=16)
-    ap.add_argument("--cache-slots", type=int, default=-1, help="-1: C = pool_slots - 3 (reference default)")
-    ap.add_argument("--ring", type=int, default=3)
+    # Pool 42 / C 29 / ring 12: 29 retained subgroups (35 GB) + 12 ring
+    # buffers (14 GB) of HBM beside the 27 GB of 16-bit gradients and working
+    # params, 76 GB of the 180 GB; 97 GB of pinned host memory.
+    ap.add_argument("--pool-slots", type=int, default=42)
+    ap.add_argument("--cache-slots", type=int, default=29, help="-1: C = pool_slots - 3 (reference default)")
+    ap.add_argument("--ring", type=int, default=12)
     ap.add_argument("--hbm-retain", type=int, default=1, help="retained subgroups stay in HBM between phases")
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--exchange", choices=["none", "fused", "nccl"], default="none",
+                    help="strong scaling over one model with the gradient reduce-scatter in the update "
+                         "(fused: peer loads in the Adam kernel; nccl: reduce_scatter then the kernel)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     a = ap.parse_args(argv)
@@ -457,29 +566,45 @@ def main(argv=None):
     torch.cuda.set_device(local)
     base_id = rank * len(sizes)
 
-    dl = device_leg(tf, sizes, base_id, a.steps, a.warmup, a.seed, rank, world)
-    step_ms = allmax(world, dl["total_ms"] / a.steps)
-    params_rank = sum(sizes)
-    value = world * params_rank / (step_ms / 1e3)
     pk = peaks()
-    kernel_s_per_launch = dl["kernel_ms"] / 1e3 / dl["launches"]
-    bytes_per_launch = ALG_BYTES_PER_PARAM * params_rank / len(sizes)
+    alg_bytes = ALG_BYTES_PER_PARAM
+    if a.exchange != "none":
+        dl = exchange_leg(tf, sizes, a.steps, a.warmup, a.seed, rank, world, a.exchange)
+        step_ms = allmax(world, dl["total_ms"] / a.steps)
+        value = sum(sizes) / (step_ms / 1e3)
+        params_rank = dl["owned_params"]
+        launches_rank = max(1, dl["owned"])
+        if a.exchange == "fused":  # own contribution local, world-1 over NVLink
+            alg_bytes = 26 + 2 * world
+    else:
+        dl = device_leg(tf, sizes, base_id, a.steps, a.warmup, a.seed, rank, world)
+        step_ms = allmax(world, dl["total_ms"] / a.steps)
+        params_rank = sum(sizes)
+        value = world * params_rank / (step_ms / 1e3)
+        launches_rank = len(sizes)
+    kernel_s_per_launch = dl["kernel_ms"] / 1e3 / max(1, dl["launches"])
+    bytes_per_launch = alg_bytes * params_rank / launches_rank
     achieved = bytes_per_launch / kernel_s_per_launch / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": ncu_traffic(params_rank / len(sizes)),
-                "peak_source": pk["source"], "alg_bytes_per_param": ALG_BYTES_PER_PARAM,
+                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": ncu_traffic(params_rank / launches_rank),
+                "peak_source": pk["source"], "alg_bytes_per_param": alg_bytes,
                 "kernel": "adam_fused_kernel (float4 quads, binary64 element math, constant-divisor "
-                          "quotients, 4 CTAs x 256 threads per SM)",
+                          "quotients, 4 CTAs x 256 threads per SM)"
+                          + (f"; {world} gradient sources summed in-kernel, {world - 1} over NVLink peer loads"
+                             if a.exchange == "fused" else ""),
                 "traffic_source": "profiles/ncu_adam_fused.json (ncu --set full, dram bytes per 100M-param launch)"}
 
     e2e = None
-    if not a.skip_e2e:
+    if a.exchange != "none":
+        e2e = {"skipped": "the --exchange mode times the device-resident update with the in-phase reduce-scatter"}
+    elif not a.skip_e2e:
         try:
-            e_sizes = e2e_shard(sizes, world, a.pool_slots)
-            if len(e_sizes) < len(sizes):
-                log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank")
-            r = e2e_leg(tf, e_sizes, base_id, a.steps, a.warmup, a.seed, rank, world, a.tier_root, a.pool_slots,
-                        a.cache_slots, a.ring, a.hbm_retain)
+            e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots)
+            if len(e_sizes) < len(sizes) or pool != a.pool_slots:
+                log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank, "
+                    f"pool {pool}, cache {cache}")
+            r = e2e_leg(tf, e_sizes, base_id, a.steps, a.warmup, a.seed, rank, world, a.tier_root, pool, cache,
+                        a.ring, a.hbm_retain)
             e_ms = allmax(world, r["ms"])
             e2e = {"value": world * r["params"] / (e_ms / 1e3), "unit": "params/s",
                    "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": e_ms,
@@ -490,13 +615,17 @@ def main(argv=None):
                    "pcie_gbs": {k: round(v / 1e9, 1) for k, v in r["pcie"].items()},
                    "nvme_gbs": {k: round(v / 1e9, 2) for k, v in r["nvme"].items()},
                    "kernel_ms_per_phase": r["kernel_ms"], "init_s": r["init_s"], "gpu_launches": r["launches"],
-                   "hbm_retain": a.hbm_retain,
+                   "hbm_retain": a.hbm_retain, "pool_slots": pool, "cache_slots": cache, "ring": a.ring,
+                   "subgroups_per_rank": len(e_sizes),
                    "path": "C ABI tfg_engine_run_update, tiers [host_dram pinned, local_dir O_DIRECT]"}
         except Exception as exc:  # keep the device-timed line; report the failure
             e2e = {"error": f"{type(exc).__name__}: {exc}"}
             log(f"e2e leg failed: {exc}")
 
     e2e_launches = (e2e or {}).get("gpu_launches", 0)
+    scaling = "strong" if a.exchange != "none" else "weak"
+    parallelism = (f"zero3-shard x{world}, gradient reduce-scatter {a.exchange} (strong)" if a.exchange != "none"
+                   else f"zero3-shard x{world} (weak)")
     cpu = None
     if rank == 0 and not a.skip_cpu:
         try:
@@ -508,16 +637,16 @@ def main(argv=None):
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "params/s", "n_gpus": world, "steps": a.steps,
-                "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": "weak",
+                "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded reference generators: synthetic_param_init, SyntheticGradSource)",
-                "config": {"workload": wl["desc"], "params_per_rank": params_rank, "subgroups_per_rank": len(sizes),
+                "config": {"workload": wl["desc"], "params_per_rank": params_rank, "subgroups_per_rank": launches_rank,
                            "grad_dtype": "f16", "param_dtype": "f16", "state": "fp32 P/m/v resident in HBM",
                            "l2": (f"inputs larger than L2 ({ALG_BYTES_PER_PARAM * max(sizes) / 1e9:.2f} GB per "
                                   "subgroup launch vs 126 MB L2; no flush needed)"
                                   if ALG_BYTES_PER_PARAM * max(sizes) > 2 * 126e6 else
                                   "WARNING: launch working set fits in L2; not a roofline-valid size"),
-                           "parallelism": f"zero3-shard x{world} (weak)"},
+                           "parallelism": parallelism},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": dl["launches"] + e2e_launches,
                 "clocks": dl["clocks"]}

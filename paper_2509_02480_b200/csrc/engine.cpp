@@ -355,8 +355,12 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaStreamCreateWithFlags(&s_d2h2_, cudaStreamNonBlocking), "cudaStreamCreate");
     ring_stride_ = seg_stride(max_params_);
     ring_.assign(static_cast<std::size_t>(dev_.device_buffers), nullptr);
-    for (auto& r : ring_)
-        cuda_check(cudaMalloc(reinterpret_cast<void**>(&r), 3 * ring_stride_ * sizeof(float)), "cudaMalloc(ring)");
+    ring_ready_.assign(ring_.size(), nullptr);
+    for (std::size_t b = 0; b < ring_.size(); ++b) {
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&ring_[b]), 3 * ring_stride_ * sizeof(float)), "cudaMalloc(ring)");
+        cuda_check(cudaEventCreateWithFlags(&ring_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
+    }
+    ring_next_ = 0;
     if (!opt_.skip_gradients) {
         ring_grad_.assign(ring_.size(), nullptr);
         for (auto& r : ring_grad_)
@@ -385,7 +389,7 @@ void OffloadWorker::setup_device() {
             cuda_check(cudaMalloc(reinterpret_cast<void**>(&hbm_cache_[b]), 3 * ring_stride_ * sizeof(float)),
                        "cudaMalloc(hbm retention)");
             cuda_check(cudaEventCreateWithFlags(&hbm_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
-            hbm_free_.push_back(static_cast<int>(hbm_cache_.size() - 1 - b));
+            hbm_free_.push_back(static_cast<int>(b));
         }
     }
     grad_ptr_.clear();
@@ -416,6 +420,9 @@ void OffloadWorker::release_device() {
     events_.clear();
     for (float* r : ring_) cudaFree(r);
     ring_.clear();
+    for (cudaEvent_t ev : ring_ready_)
+        if (ev) cudaEventDestroy(ev);
+    ring_ready_.clear();
     for (float* r : hbm_cache_) cudaFree(r);
     for (cudaEvent_t ev : hbm_ready_)
         if (ev) cudaEventDestroy(ev);
@@ -674,7 +681,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             const SubgroupId id = order[j];
             const int slot = wait_host_resident(id);
             host_resident_ns_[index_of_.at(id)] = now_ns();
-            const auto moved = issue_device_update(j, id, slot, c);
+            const auto moved = issue_device_update(id, slot, c);
             std::lock_guard<std::mutex> g(mu_);
             Subgroup& sg = subgroups_.at(id);
             sg.step_count = static_cast<std::uint64_t>(iteration) + 1;
@@ -762,9 +769,8 @@ PhaseStats OffloadWorker::run_update(int iteration) {
     return stats;
 }
 
-// Enqueue subgroup j on the three pipeline streams. Ring buffer j % K is
-// reused once the D2H of subgroup j - K has drained it.
-std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(std::size_t j, SubgroupId id, int slot,
+// Enqueue one subgroup on the three pipeline streams (H2D -> kernel -> D2H).
+std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(SubgroupId id, int slot,
                                                                          const AdamConsts& c) {
     Subgroup& sg = subgroups_.at(id);
     const std::uint64_t pc = sg.param_count;
@@ -826,17 +832,22 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(std::
         std::lock_guard<std::mutex> g(mu_);
         const bool retain = dests_->assign_storage_tier(id).host_retain;
         if (retain && hslot < 0 && !hbm_free_.empty()) {
-            hslot = hbm_free_.back();
-            hbm_free_.pop_back();
+            // FIFO: the buffer whose write-back was queued first drains first
+            hslot = hbm_free_.front();
+            hbm_free_.pop_front();
         }
         keep_in_hbm = retain && hslot >= 0;
     }
-    float* d = hslot >= 0 ? hbm_cache_[static_cast<std::size_t>(hslot)] : ring_[j % K];
+    // Ring buffers go round-robin to the subgroups that stream through the
+    // ring (HBM-resident ones do not), each reused once the D2H of its last
+    // user has drained it (ring_ready_; a never-recorded event does not wait).
+    std::size_t rb = 0;
+    if (hslot < 0) {
+        rb = ring_next_++ % K;
+        cuda_check(cudaStreamWaitEvent(s_h2d_, ring_ready_[rb], 0), "wait");
+    }
+    float* d = hslot >= 0 ? hbm_cache_[static_cast<std::size_t>(hslot)] : ring_[rb];
     const std::uint64_t ds = seg_stride(pc);
-    // Ring buffer j % K was last drained by the D2H of j - K (the D2H stream
-    // is FIFO, so j - K's d2h_end also covers an earlier HBM-resident user).
-    if (hslot < 0 && j >= K)
-        cuda_check(cudaStreamWaitEvent(s_h2d_, events_[index_of_.at(order_[j - K])].d2h_end, 0), "wait");
     cuda_check(cudaEventRecord(e.h2d_start, s_h2d_), "cudaEventRecord");
     std::uint64_t h2d_bytes = 0, d2h_bytes = 0;
     if (held < 0) {
@@ -846,7 +857,7 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(std::
         h2d_bytes += 12 * pc;
     }
     if (!opt_.skip_gradients) {  // baseline flow: fp32 gradients fetched with the state
-        float* dg = ring_grad_[j % K];
+        float* dg = ring_grad_[rb];
         cuda_check(cudaMemcpyAsync(dg, grad_annex(blk), 4 * pc, cudaMemcpyHostToDevice, s_h2d_),
                    "cudaMemcpyAsync(grads)");
         h2d_bytes += 4 * pc;
@@ -903,6 +914,7 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(std::
     }
     if (!keep_in_hbm) d2h_bytes += 12 * pc;
     cuda_check(cudaEventRecord(e.d2h_end, s_d2h_), "cudaEventRecord");
+    if (hslot < 0) cuda_check(cudaEventRecord(ring_ready_[rb], s_d2h_), "cudaEventRecord");
     if (hslot >= 0) {
         std::lock_guard<std::mutex> g(mu_);
         if (keep_in_hbm) {

@@ -306,8 +306,7 @@ private:
     void setup_device();
     void release_device();
     // Returns the PCIe bytes moved {H2D, D2H}.
-    std::pair<std::uint64_t, std::uint64_t> issue_device_update(std::size_t j, SubgroupId id, int slot,
-                                                                const AdamConsts& c);
+    std::pair<std::uint64_t, std::uint64_t> issue_device_update(SubgroupId id, int slot, const AdamConsts& c);
     void device_state_to_host(const float* dev, float* host, std::uint64_t pc);
     void writeback_hbm_copy_locked(std::size_t k, int slot);
     void copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device, cudaStream_t s);
@@ -345,6 +344,8 @@ private:
     bool device_ready_ = false;
     cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr, s_d2h2_ = nullptr;
     std::vector<float*> ring_;
+    std::vector<cudaEvent_t> ring_ready_;  // last D2H out of each ring buffer
+    std::size_t ring_next_ = 0;           // round-robin ring cursor
     std::vector<float*> ring_grad_;  // baseline flow: fp32 gradient segment per ring buffer
     // HBM retention (DeviceOptions::hbm_retain): one device buffer per
     // retention slot. hbm_slot_[k] >= 0 while subgroup k's authoritative state
@@ -352,7 +353,7 @@ private:
     // out of buffer b, which a new occupant's H2D waits for.
     std::vector<float*> hbm_cache_;
     std::vector<cudaEvent_t> hbm_ready_;
-    std::vector<int> hbm_free_;
+    std::deque<int> hbm_free_;
     std::vector<int> hbm_slot_;
     float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H
     HostBlock grad_stage_;           // baseline flow: pinned D2H staging of fp32 gradients
