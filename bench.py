@@ -382,14 +382,14 @@ def pcie_probe():
 def e2e_shard(sizes, world, pool_slots, cache_slots):
     """(subgroups, pool_slots, cache_slots) each rank streams in the e2e leg.
     Every subgroup pins one 12 B/param host block (a pool slot or a host-DRAM
-    tier blob); N ranks on one host share 60% of MemAvailable. When the
+    tier blob); N ranks on one host share 70% of MemAvailable. When the
     requested pool plus the shard does not fit, the pool shrinks first (to a
     third of the rank's blocks, at least 4 slots) and then the shard."""
     try:
         avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable:"))
     except (OSError, StopIteration):
         return sizes, pool_slots, cache_slots
-    blocks = int(0.6 * avail / world // (12 * max(sizes) + 4096))
+    blocks = int(0.7 * avail / world // (12 * max(sizes) + 4096))
     pool = pool_slots
     if pool + len(sizes) > blocks:
         pool = max(4, min(pool_slots, blocks // 3))

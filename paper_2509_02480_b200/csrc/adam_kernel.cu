@@ -28,65 +28,70 @@ namespace {
 // fetches fp32 gradients from storage). GMODE 2: the sum of n 16-bit buffers,
 // e.g. the same subgroup's gradient contributions in every data-parallel
 // peer's memory over NVLink: summed in fp32 in source order, rounded once to
-// GK — the reduce-scatter fused into the update.
+// GK — the reduce-scatter fused into the update. NS > 0 fixes n at compile
+// time (the 2/4/8-rank cases: unrolled loads, no per-source predicates);
+// NS = 0 reads gs.n at run time.
 struct GradSources {
     const void* src[kMaxGradSources];
     int n;
 };
 
-template <int GK, int GMODE>
-__device__ __forceinline__ float4 load_grad4(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
-    if constexpr (GMODE == 1) {
-        const float4 f = __ldcs(reinterpret_cast<const float4*>(gs.src[0]) + q);
-        nonfinite += !isfinite(f.x) + !isfinite(f.y) + !isfinite(f.z) + !isfinite(f.w);
-        return f;
-    } else {
-        U16x4 h;
-        if constexpr (GMODE == 0) {
-            h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
-        } else {
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+// In-order fp32 sum of one quad over the sources, rounded once to GK.
+template <int GK, int NS>
+__device__ __forceinline__ U16x4 sum_quad16(const GradSources& gs, uint64_t q) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto add = [&](const U16x4& x) {
+        acc.x = __fadd_rn(acc.x, widen16<GK>(x.x));
+        acc.y = __fadd_rn(acc.y, widen16<GK>(x.y));
+        acc.z = __fadd_rn(acc.z, widen16<GK>(x.z));
+        acc.w = __fadd_rn(acc.w, widen16<GK>(x.w));
+    };
+    if constexpr (NS > 0) {
+        U16x4 x[NS];
 #pragma unroll
-            for (int s = 0; s < kMaxGradSources; ++s) {
-                if (s < gs.n) {
-                    const U16x4 x = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q);
-                    acc.x = __fadd_rn(acc.x, widen16<GK>(x.x));
-                    acc.y = __fadd_rn(acc.y, widen16<GK>(x.y));
-                    acc.z = __fadd_rn(acc.z, widen16<GK>(x.z));
-                    acc.w = __fadd_rn(acc.w, widen16<GK>(x.w));
-                }
-            }
-            h.x = narrow16<GK>(acc.x);
-            h.y = narrow16<GK>(acc.y);
-            h.z = narrow16<GK>(acc.z);
-            h.w = narrow16<GK>(acc.w);
-        }
-        nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
-        return make_float4(widen16<GK>(h.x), widen16<GK>(h.y), widen16<GK>(h.z), widen16<GK>(h.w));
+        for (int s = 0; s < NS; ++s)  // all loads first: NS independent streams in flight
+            x[s] = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) add(x[s]);
+    } else {
+#pragma unroll
+        for (int s = 0; s < kMaxGradSources; ++s)
+            if (s < gs.n) add(load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q));
     }
+    U16x4 h;
+    h.x = narrow16<GK>(acc.x);
+    h.y = narrow16<GK>(acc.y);
+    h.z = narrow16<GK>(acc.z);
+    h.w = narrow16<GK>(acc.w);
+    return h;
 }
 
-// Register form of one gradient quad: a single 16-bit source stays packed
-// (2 registers) and is widened at use; fp32 and summed sources hold floats.
-template <int GK, int GMODE>
+// Register form of one gradient quad: 16-bit sources stay packed (2
+// registers; a summed quad is held already rounded) and are widened at use;
+// fp32 sources (GMODE 1) hold floats.
+template <int GK, int GMODE, int NS>
 struct GradReg {
-    float4 f;
-    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
-        f = load_grad4<GK, GMODE>(gs, q, nonfinite);
-    }
-    __device__ __forceinline__ float get(int k) const { return k == 0 ? f.x : k == 1 ? f.y : k == 2 ? f.z : f.w; }
-};
-
-template <int GK>
-struct GradReg<GK, 0> {
     U16x4 h;
     __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
-        h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
+        if constexpr (GMODE == 0)
+            h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
+        else
+            h = sum_quad16<GK, NS>(gs, q);
         nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
     }
     __device__ __forceinline__ float get(int k) const {
         return widen16<GK>(k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w);
     }
+};
+
+template <int GK, int NS>
+struct GradReg<GK, 1, NS> {
+    float4 f;
+    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
+        f = __ldcs(reinterpret_cast<const float4*>(gs.src[0]) + q);
+        nonfinite += !isfinite(f.x) + !isfinite(f.y) + !isfinite(f.z) + !isfinite(f.w);
+    }
+    __device__ __forceinline__ float get(int k) const { return k == 0 ? f.x : k == 1 ? f.y : k == 2 ? f.z : f.w; }
 };
 
 template <int GK, int GMODE>
@@ -130,8 +135,9 @@ struct StateIO {
 // evict-first intrinsics, issued in program order per element, so in-place
 // aliasing of in and out is well defined.
 // DIVC selects the element math: 0 = div.rn quotients, 1 = constant-divisor
-// quotients, 2 = verified fast path (numerics.cuh adam_element_fast).
-template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB>
+// quotients, 2 = verified fast path (numerics.cuh adam_element_fast), 3 =
+// constant-divisor quotients with the quad's elements walked one at a time.
+template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                       unsigned long long* __restrict__ counters) {
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         float4* vo4 = reinterpret_cast<float4*>(io.vo);
         for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
             float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
-            GradReg<GK, GMODE> rg[UNROLL];
+            GradReg<GK, GMODE, NS> rg[UNROLL];
 #pragma unroll
             for (int u = 0; u < UNROLL; ++u) {  // all loads first: UNROLL quads in flight
                 const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
@@ -164,10 +170,26 @@ __global__ void __launch_bounds__(kThreads, MINB)
             for (int u = 0; u < UNROLL; ++u) {
                 const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
                 if (q < nq) {
-                    adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
-                    adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
-                    adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
-                    adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
+                    if constexpr (DIVC == 3) {
+                        // one element at a time (no cross-element ILP, fewer
+                        // live registers): rotate the quad through .x
+                        float g4[4] = {rg[u].get(0), rg[u].get(1), rg[u].get(2), rg[u].get(3)};
+                        float gx = g4[0], gy = g4[1], gz = g4[2], gw = g4[3];
+#pragma unroll 1
+                        for (int k = 0; k < 4; ++k) {
+                            adam_math<WD, 1>(rp[u].x, rm[u].x, rv[u].x, gx, c);
+                            const float tp = rp[u].x, tm = rm[u].x, tv = rv[u].x, tg = gx;
+                            rp[u].x = rp[u].y; rp[u].y = rp[u].z; rp[u].z = rp[u].w; rp[u].w = tp;
+                            rm[u].x = rm[u].y; rm[u].y = rm[u].z; rm[u].z = rm[u].w; rm[u].w = tm;
+                            rv[u].x = rv[u].y; rv[u].y = rv[u].z; rv[u].z = rv[u].w; rv[u].w = tv;
+                            gx = gy; gy = gz; gz = gw; gw = tg;
+                        }
+                    } else {
+                        adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
+                        adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
+                        adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
+                        adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
+                    }
                     U16x4 h;
                     h.x = narrow16<OK>(rp[u].x);
                     h.y = narrow16<OK>(rp[u].y);
@@ -185,7 +207,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         if (i < n) {
             float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
             const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
-            adam_math<WD, DIVC>(pf, mf, vf, gf, c);
+            adam_math<WD, DIVC == 3 ? 1 : DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
             __stcs(io.po + i, pf);
@@ -197,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         for (uint64_t i = tid; i < n; i += nthreads) {
             float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
             const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
-            adam_math<WD, DIVC>(pf, mf, vf, gf, c);
+            adam_math<WD, DIVC == 3 ? 1 : DIVC>(pf, mf, vf, gf, c);
             const uint16_t h = narrow16<OK>(pf);
             overflow += is_inf16<OK>(h);
             __stcs(io.po + i, pf);
@@ -247,14 +269,14 @@ bool is_vec(const AdamLaunch& a) {
     return (state & 15u) == 0 && (grads & galign) == 0 && (reinterpret_cast<uintptr_t>(a.p16) & 7u) == 0;
 }
 
-template <int GK, int GMODE, int OK, bool WD, class C>
+template <int GK, int GMODE, int OK, bool WD, class C, int NS = 0>
 cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     constexpr int U = C::kUnroll;
     constexpr int B = C::kMinBlocks;
     const GradSources gs = sources_of(a);
     if (is_vec(a)) {
         const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
-        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B>
+        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS>
             <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
     } else {
         const unsigned grid = grid_for(a.n, B);
@@ -264,10 +286,22 @@ cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     return cudaGetLastError();
 }
 
-template <int GK, int GMODE, int OK, class C>
+template <int GK, int GMODE, int OK, class C, int NS = 0>
 cudaError_t launch_wd(const AdamLaunch& a, cudaStream_t stream) {
-    return a.c.lr_wd != 0.0 ? launch_cfg<GK, GMODE, OK, true, C>(a, stream)
-                            : launch_cfg<GK, GMODE, OK, false, C>(a, stream);
+    return a.c.lr_wd != 0.0 ? launch_cfg<GK, GMODE, OK, true, C, NS>(a, stream)
+                            : launch_cfg<GK, GMODE, OK, false, C, NS>(a, stream);
+}
+
+// Summed sources: the 2-, 4- and 8-way sums (the 2/4/8-GPU data-parallel
+// worlds) get a compile-time source count, other counts the run-time loop.
+template <int GK, int OK, class C>
+cudaError_t launch_sum(const AdamLaunch& a, cudaStream_t stream) {
+    switch (a.n_peers) {
+        case 2: return launch_wd<GK, 2, OK, C, 2>(a, stream);
+        case 4: return launch_wd<GK, 2, OK, C, 4>(a, stream);
+        case 8: return launch_wd<GK, 2, OK, C, 8>(a, stream);
+        default: return launch_wd<GK, 2, OK, C, 0>(a, stream);
+    }
 }
 
 template <class C>
@@ -276,8 +310,8 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
     if (a.n_peers > 0) {  // fused multi-source reduction: 16-bit sources, same kind in and out
         if (a.n_peers > kMaxGradSources || a.grad_kind == kF32) return cudaErrorInvalidValue;
         if (a.grad_kind == kF16)
-            return a.out_kind == kF16 ? launch_wd<kF16, 2, kF16, C>(a, stream) : launch_wd<kF16, 2, kBF16, C>(a, stream);
-        return a.out_kind == kF16 ? launch_wd<kBF16, 2, kF16, C>(a, stream) : launch_wd<kBF16, 2, kBF16, C>(a, stream);
+            return a.out_kind == kF16 ? launch_sum<kF16, kF16, C>(a, stream) : launch_sum<kF16, kBF16, C>(a, stream);
+        return a.out_kind == kF16 ? launch_sum<kBF16, kF16, C>(a, stream) : launch_sum<kBF16, kBF16, C>(a, stream);
     }
     if (a.grad_kind == kF32)
         return a.out_kind == kF16 ? launch_wd<kF32, 1, kF16, C>(a, stream) : launch_wd<kF32, 1, kBF16, C>(a, stream);
@@ -553,6 +587,20 @@ cudaError_t launch_cpasync(const AdamLaunch& a, cudaStream_t stream) {
     return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
 }
 
+// Scalar-element form at a given occupancy (tuning variants): 4-byte
+// coalesced streams, one element per thread per iteration.
+template <bool WD, int MINB>
+cudaError_t launch_scalar(const AdamLaunch& a, cudaStream_t stream) {
+    const unsigned grid = grid_for(a.n, MINB);
+    adam_fused_kernel<kF16, 0, kF16, WD, false, 1, 1, MINB>
+        <<<grid, kThreads, 0, stream>>>(state_io(a), sources_of(a), a.p16, a.n, a.c, a.counters);
+    return cudaGetLastError();
+}
+template <int MINB>
+cudaError_t launch_scalar_wd(const AdamLaunch& a, cudaStream_t stream) {
+    return a.c.lr_wd != 0.0 ? launch_scalar<true, MINB>(a, stream) : launch_scalar<false, MINB>(a, stream);
+}
+
 // Shipped configuration: one quad per thread per iteration, constant-divisor
 // quotients, <= 64 registers for 4 resident CTAs (32 warps) per SM. The
 // 2026-10-17 sweep (profiles/kernel_sweep_r1.json) measured it at 474 us per
@@ -582,6 +630,11 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 18) return launch_wd<kF16, 0, kF16, Cfg<1, 2, 4>>(a, stream);
     if constexpr (V == 19) return launch_wd<kF16, 0, kF16, Cfg<2, 2, 3>>(a, stream);
     if constexpr (V == 20) return launch_wd<kF16, 0, kF16, Cfg<1, 2, 5>>(a, stream);
+    if constexpr (V == 21) return launch_scalar_wd<4>(a, stream);
+    if constexpr (V == 22) return launch_scalar_wd<5>(a, stream);
+    if constexpr (V == 23) return launch_scalar_wd<6>(a, stream);
+    if constexpr (V == 24) return launch_wd<kF16, 0, kF16, Cfg<1, 3, 5>>(a, stream);
+    if constexpr (V == 25) return launch_wd<kF16, 0, kF16, Cfg<1, 3, 6>>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -645,11 +698,16 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 18: return launch_variant<18>(a, stream);
         case 19: return launch_variant<19>(a, stream);
         case 20: return launch_variant<20>(a, stream);
+        case 21: return launch_variant<21>(a, stream);
+        case 22: return launch_variant<22>(a, stream);
+        case 23: return launch_variant<23>(a, stream);
+        case 24: return launch_variant<24>(a, stream);
+        case 25: return launch_variant<25>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 21; }
+int adam_variant_count() { return 26; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {

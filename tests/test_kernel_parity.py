@@ -224,7 +224,7 @@ def test_kernel_variants_bitwise(tf, cuda, variant):
     assert np.array_equal(_np16(p16), want[3])
 
 
-@pytest.mark.parametrize("nsrc", [1, 2, 3, 8])
+@pytest.mark.parametrize("nsrc", [1, 2, 3, 4, 8])
 @pytest.mark.parametrize("kind", [0, 1])
 def test_fused_reduce_update_matches_oracle(tf, cuda, nsrc, kind):
     """tfg_adam_fused_multi: gradient = fp32 sum of n 16-bit sources in order,
