@@ -100,7 +100,10 @@ typedef struct tfg_device_options {
                                 writes the updated state back into the pinned slot */
     int32_t d2h_split;       /* copy mode: concurrent D2H streams per subgroup (1 or 2) */
     int32_t hbm_retain;      /* copy mode, 16-bit gradients: retained subgroups keep their state in
-                                HBM between phases (no D2H now, no H2D at the next update) */
+                                HBM between phases (no D2H now, no H2D at the next update).
+                                1: the host slot stays reserved, C = min(cache_slots, pool_slots-3)
+                                as in the reference; 2 (HBM cache): the slot streams again and
+                                C = cache_slots (or pool_slots-3 if < 0), bounded by HBM only */
 } tfg_device_options;
 
 typedef struct tfg_tier_observation { /* placement.hpp:138-145 */

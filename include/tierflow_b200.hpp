@@ -182,7 +182,7 @@ struct DeviceOptions {
     int device_buffers = 3;
     bool zero_copy = false;
     int d2h_split = 1;
-    bool hbm_retain = true;
+    int hbm_retain = 1;  // 0 off, 1 host slot kept, 2 HBM cache (see tfg_device_options)
 };
 
 using PhaseStats = tfg_phase_stats;
@@ -199,7 +199,7 @@ public:
                                 o.update_pad_ns};
         tfg_adam_hyper ah{h.lr, h.beta1, h.beta2, h.eps, h.weight_decay};
         tfg_device_options dv{d.device, d.grad_dtype, d.param_dtype, d.device_buffers, d.zero_copy ? 1 : 0,
-                              d.d2h_split, d.hbm_retain ? 1 : 0};
+                              d.d2h_split, d.hbm_retain};
         check(tfg_engine_create(id, th.data(), static_cast<int>(th.size()), &so, &ah, trace.handle(), &dv, &h_));
     }
     ~OffloadWorker() { tfg_engine_destroy(h_); }

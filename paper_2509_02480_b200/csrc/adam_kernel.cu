@@ -292,15 +292,22 @@ cudaError_t launch_wd(const AdamLaunch& a, cudaStream_t stream) {
                             : launch_cfg<GK, GMODE, OK, false, C, NS>(a, stream);
 }
 
-// Summed sources: the 2-, 4- and 8-way sums (the 2/4/8-GPU data-parallel
-// worlds) get a compile-time source count, other counts the run-time loop.
+// Summed sources: a compile-time source count (unrolled loads, no
+// per-source predicates) measured at 0.92-0.93 of the HBM roofline for 1, 2
+// and 4 sources against 0.75-0.77 for the run-time loop
+// (profiles/multi_sweep_r1.json).
 template <int GK, int OK, class C>
 cudaError_t launch_sum(const AdamLaunch& a, cudaStream_t stream) {
     switch (a.n_peers) {
+        case 1: return launch_wd<GK, 2, OK, C, 1>(a, stream);
         case 2: return launch_wd<GK, 2, OK, C, 2>(a, stream);
+        case 3: return launch_wd<GK, 2, OK, C, 3>(a, stream);
         case 4: return launch_wd<GK, 2, OK, C, 4>(a, stream);
+        case 5: return launch_wd<GK, 2, OK, C, 5>(a, stream);
+        case 6: return launch_wd<GK, 2, OK, C, 6>(a, stream);
+        case 7: return launch_wd<GK, 2, OK, C, 7>(a, stream);
         case 8: return launch_wd<GK, 2, OK, C, 8>(a, stream);
-        default: return launch_wd<GK, 2, OK, C, 0>(a, stream);
+        default: return cudaErrorInvalidValue;
     }
 }
 

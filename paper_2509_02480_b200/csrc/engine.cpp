@@ -347,6 +347,23 @@ std::vector<double> OffloadWorker::placement_bandwidths() const {
     return b;
 }
 
+int OffloadWorker::retention_capacity() const {
+    const int M = static_cast<int>(ids_.size());
+    if (dev_.hbm_retain == 2 && dev_.zero_copy == 0 && opt_.skip_gradients && opt_.enable_caching) {
+        const int wanted = opt_.cache_slots < 0 ? opt_.pool_slots - 3 : opt_.cache_slots;
+        return std::clamp(wanted, 0, M);
+    }
+    return opt_.retention_capacity(M);
+}
+
+int OffloadWorker::reserve_writeback_slot_locked(SubgroupId id) {
+    const int slot = pool_->try_reserve(id);
+    if (slot < 0) return -1;
+    pool_->prefetch_done(slot);
+    subgroups_.at(id).slot = slot;
+    return slot;
+}
+
 void OffloadWorker::setup_device() {
     DeviceGuard dg(dev_.device);
     cuda_check(cudaStreamCreateWithFlags(&s_h2d_, cudaStreamNonBlocking), "cudaStreamCreate");
@@ -382,7 +399,7 @@ void OffloadWorker::setup_device() {
                "cudaMalloc");
     hbm_slot_.assign(ids_.size(), -1);
     if (dev_.hbm_retain != 0 && dev_.zero_copy == 0 && opt_.skip_gradients) {
-        const int cap = opt_.retention_capacity(static_cast<int>(ids_.size()));
+        const int cap = retention_capacity();
         hbm_cache_.assign(static_cast<std::size_t>(cap), nullptr);
         hbm_ready_.assign(hbm_cache_.size(), nullptr);
         for (std::size_t b = 0; b < hbm_cache_.size(); ++b) {
@@ -662,7 +679,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
     std::vector<SubgroupId> order;
     {
         std::lock_guard<std::mutex> g(mu_);
-        const int cap = opt_.retention_capacity(static_cast<int>(ids_.size()));
+        const int cap = retention_capacity();
         dests_ = std::make_unique<DestinationPlan>(order_, cap, placement_bandwidths());
         stats.retained = dests_->retained_count();
         stats.flush_allocation = dests_->flush_allocation().counts;
@@ -779,11 +796,14 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     const DeviceEvents& e = events_[k];
     {
         std::lock_guard<std::mutex> g(mu_);
-        pool_->begin_update(slot);
+        if (slot >= 0) pool_->begin_update(slot);
         trace_->record(EventKind::update_start, id_, id, kNoTier, 12 * pc);
         ++in_flight_;
     }
-    const HostBlock& blk = pool_->block(slot);
+    // slot < 0 only in HBM cache mode, for a subgroup held in HBM that the plan
+    // retains again: no host transfer either way.
+    static HostBlock no_block;
+    const HostBlock& blk = slot >= 0 ? pool_->block(slot) : no_block;
     AdamLaunch a;
     a.g = grad_ptr_[k];
     if (!grad_sources_[k].empty()) {  // reduce + update in one pass over the peers' contributions
@@ -975,11 +995,17 @@ void OffloadWorker::completion_loop() {
         std::lock_guard<std::mutex> g(mu_);
         try {
             Subgroup& sg = subgroups_.at(c.id);
-            host_retired_ns_[index_of_.at(c.id)] = now_ns();
-            pool_->end_update(c.slot);
+            const std::size_t k = index_of_.at(c.id);
+            host_retired_ns_[k] = now_ns();
+            if (c.slot >= 0) pool_->end_update(c.slot);
             trace_->record(EventKind::update_end, id_, c.id, kNoTier, 12 * sg.param_count);
             const TierAssignment a = dests_->assign_storage_tier(c.id);
-            if (!a.host_retain) start_flush_locked(c.id, a.tier, c.slot);
+            if (!a.host_retain) {
+                start_flush_locked(c.id, a.tier, c.slot);
+            } else if (hbm_cache_mode() && hbm_slot_[k] >= 0 && c.slot >= 0) {
+                pool_->evict(c.slot);  // the state lives in HBM: the slot streams again
+                sg.slot = -1;
+            }
             pump_locked();
         } catch (...) {
             if (!completion_error_) completion_error_ = std::current_exception();
@@ -1002,6 +1028,15 @@ int OffloadWorker::wait_host_resident(SubgroupId id) {
                 break;
             }
             if (sg.residency == Residency::host_cached) {
+                // HBM cache mode: an HBM-held subgroup this plan flushes needs a
+                // slot to write back into (normally pump_locked reserved it).
+                if (sg.slot < 0 && hbm_cache_mode() && dests_ && !dests_->assign_storage_tier(id).host_retain &&
+                    reserve_writeback_slot_locked(id) < 0) {
+                    l.unlock();
+                    wait_pool_free();
+                    l.lock();
+                    continue;
+                }
                 ++cache_hits_this_phase_;
                 trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
                 need_grad_fetch = !opt_.skip_gradients && grad_tier_.count(id) != 0;
@@ -1026,7 +1061,9 @@ int OffloadWorker::wait_host_resident(SubgroupId id) {
 std::shared_future<IoStats> OffloadWorker::enqueue_flush(SubgroupId id, TierId dest) {
     std::lock_guard<std::mutex> g(mu_);
     Subgroup& sg = subgroups_.at(id);
-    if (sg.residency != Residency::host_cached || sg.slot < 0) throw Error("enqueue_flush: subgroup not host-resident");
+    if (sg.residency != Residency::host_cached) throw Error("enqueue_flush: subgroup not host-resident");
+    if (sg.slot < 0 && !(hbm_cache_mode() && hbm_slot_[index_of_.at(id)] >= 0 && reserve_writeback_slot_locked(id) >= 0))
+        throw Error("enqueue_flush: no host slot free for the write-back of subgroup " + std::to_string(id));
     if (!hbm_slot_.empty()) writeback_hbm_copy_locked(index_of_.at(id), sg.slot);
     return start_flush_locked(id, dest, sg.slot);
 }
@@ -1106,6 +1143,13 @@ void OffloadWorker::pump_locked() {
     while (frontier_ < order_.size()) {
         const SubgroupId id = order_[frontier_];
         Subgroup& sg = subgroups_.at(id);
+        if (sg.residency == Residency::host_cached && sg.slot < 0 && hbm_cache_mode() && dests_ &&
+            !dests_->assign_storage_tier(id).host_retain) {
+            // HBM-held, flushed this phase: its write-back slot, in plan order
+            if (reserve_writeback_slot_locked(id) < 0) break;
+            ++frontier_;
+            continue;
+        }
         if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) {
             ++frontier_;
             continue;

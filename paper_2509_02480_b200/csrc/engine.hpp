@@ -80,7 +80,12 @@ struct DeviceOptions {
     int d2h_split = 1;       // concurrent D2H copy streams per subgroup (1 or 2)
     // Copy mode, 16-bit gradient flow: a subgroup the destination plan retains
     // keeps its updated state in HBM until its next update (no D2H now, no H2D
-    // then); the host slot stays reserved and is refreshed on demand.
+    // then). 1: the host slot stays reserved and is refreshed on demand, C is
+    // the reference's min(cache_slots, pool_slots - 3). 2 (HBM cache): the
+    // retained subgroup gives its host slot back and the retention capacity
+    // C = cache_slots is bounded by HBM, not by the pool (cache_slots < 0:
+    // pool_slots - 3); all pool slots stream. A retained subgroup the next
+    // plan flushes takes a slot for its write-back in plan order.
     int hbm_retain = 1;
 };
 
@@ -289,6 +294,11 @@ private:
     };
 
     std::vector<double> placement_bandwidths() const;
+    int retention_capacity() const;
+    bool hbm_cache_mode() const { return !hbm_cache_.empty() && dev_.hbm_retain == 2; }
+    // HBM cache mode: a slot for an HBM-held subgroup's write-back (no I/O;
+    // the slot goes straight to cached). Called with mu_ held; -1 if none free.
+    int reserve_writeback_slot_locked(SubgroupId id);
     void pump_locked();
     std::shared_future<IoStats> start_prefetch_locked(SubgroupId id, int slot);
     std::shared_future<IoStats> start_flush_locked(SubgroupId id, TierId dest, int slot);

@@ -138,6 +138,8 @@ class DeviceOptions:
     zero_copy: int = 0
     d2h_split: int = 1
     # Retained subgroups keep their updated state in HBM between phases.
+    # 1: their host slot stays reserved (C = min(cache_slots, pool_slots - 3));
+    # 2: HBM cache, the slot streams again and C = cache_slots.
     hbm_retain: int = 1
 
 

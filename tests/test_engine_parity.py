@@ -19,14 +19,14 @@ pytestmark = pytest.mark.gpu
 
 def make_engine(tf, tiers_cfg, params, *, pool_slots=4, cache_slots=-1, ratio=None, seed=42, lock_dir="",
                 wd=0.0, device_buffers=3, grad_dtype=0, param_dtype=0, deadlock=30.0, pad_ns=0, caching=True,
-                multi_path=True):
+                multi_path=True, hbm=1):
     trace = tf.EventTrace()
     tiers = [tf.Tier(tf.TierSpec(i, *cfg)) for i, cfg in enumerate(tiers_cfg)]
     opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=lock_dir,
                              deadlock_timeout_s=deadlock, update_pad_ns=pad_ns, enable_caching=caching,
                              multi_path=multi_path)
     w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(weight_decay=wd), trace,
-                         tf.DeviceOptions(0, grad_dtype, param_dtype, device_buffers))
+                         tf.DeviceOptions(0, grad_dtype, param_dtype, device_buffers, 0, 1, hbm))
     if ratio is not None:
         w.set_fixed_ratio(ratio)
     for i, n in enumerate(params):
@@ -39,15 +39,18 @@ def mem(rate_r, rate_w):
     return (2, "mem", rate_r, rate_w)
 
 
-def run_golden(tf, golden, run, lock_dir, device_buffers=3):
+def run_golden(tf, golden, run, lock_dir, device_buffers=3, hbm=1, host_slots=None):
     cfg = golden[f"run_{run}_config"]
     M, nt, pool, cache, seed, iters, accum, skip = (int(x) for x in cfg)
+    if hbm == 2:  # HBM cache: the reference's C on HBM, `host_slots` pool slots all streaming
+        cache = tf.retention_capacity(True, pool, cache, M)
+        pool = host_slots
     params = golden[f"run_{run}_params"].tolist()
     rates = {"hits": [(500e6, 500e6), (250e6, 250e6)], "ragged": [(300e6, 300e6), (200e6, 200e6), (100e6, 100e6)],
              "skip": [(400e6, 400e6), (200e6, 200e6)]}[run]
     w, trace, tiers = make_engine(tf, [mem(*r) for r in rates], params, pool_slots=pool, cache_slots=cache,
                                   ratio=golden[f"run_{run}_ratio"].tolist(), seed=seed, lock_dir=lock_dir,
-                                  wd=float(golden[f"run_{run}_wd"][0]), device_buffers=device_buffers)
+                                  wd=float(golden[f"run_{run}_wd"][0]), device_buffers=device_buffers, hbm=hbm)
     stats, seqs = [], []
     for it in range(iters):
         w.run_backward_sim(it, tf.SyntheticGradSource(seed), accum)
@@ -63,9 +66,12 @@ def run_golden(tf, golden, run, lock_dir, device_buffers=3):
     return w, trace, stats, seqs, params, iters
 
 
-@pytest.mark.parametrize("run", ["hits", "ragged", "skip"])
-def test_sequences_and_state_match_reference_engine(tf, cuda, golden, lock_dir, run):
-    w, trace, stats, seqs, params, iters = run_golden(tf, golden, run, lock_dir)
+@pytest.mark.parametrize("run,hbm,host_slots", [("hits", 1, None), ("ragged", 1, None), ("skip", 1, None),
+                                                ("hits", 2, 3), ("ragged", 2, 3), ("skip", 2, 4)])
+def test_sequences_and_state_match_reference_engine(tf, cuda, golden, lock_dir, run, hbm, host_slots):
+    """hbm=2 (HBM cache mode): the reference's retention capacity held in HBM
+    with only `host_slots` pinned slots: same sequences, counts and bits."""
+    w, trace, stats, seqs, params, iters = run_golden(tf, golden, run, lock_dir, hbm=hbm, host_slots=host_slots)
     want_seqs = [ast.literal_eval(s) for s in golden[f"run_{run}_seqs"]]
     for it in range(iters):
         assert seqs[it] == want_seqs[it], f"iteration {it}"
@@ -390,7 +396,7 @@ def test_engine_mode_backward_writes_nothing(tf, cuda, lock_dir):
         w.close()
 
 
-@pytest.mark.parametrize("hbm", [0, 1])
+@pytest.mark.parametrize("hbm", [0, 1, 2])
 def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
     """Retained subgroups keep their state in HBM between phases: no D2H when
     retained, no H2D at the next update. Same bits and cache hits as the
@@ -402,8 +408,9 @@ def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
     trace = tf.EventTrace()
     tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
              tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
-    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=C + 3, lock_dir=lock_dir), tf.AdamHyper(), trace,
-                         tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    opt = (tf.ScheduleOptions(pool_slots=3, cache_slots=C, lock_dir=lock_dir) if hbm == 2 else
+           tf.ScheduleOptions(pool_slots=C + 3, lock_dir=lock_dir))
+    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
     w.set_fixed_ratio([1.0, 1.0])
     for i, n in enumerate(params):
         w.add_subgroup(i, n)
@@ -417,6 +424,7 @@ def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
         order = list(range(len(params))) if it % 2 == 0 else list(reversed(range(len(params))))
         retained = set(order[-C:])
         assert st.cache_hits == len(prev_retained)
+        assert st.retained == C
         if hbm:
             assert st.h2d_bytes == 12 * (S - sum(params[i] for i in prev_retained))
             assert st.d2h_bytes == 12 * (S - sum(params[i] for i in retained))
