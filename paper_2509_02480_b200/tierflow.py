@@ -330,7 +330,7 @@ class EventTrace:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:  # not during interpreter teardown
             _lib.load().tfg_trace_destroy(self._h)
             self._h = None
 
@@ -380,7 +380,7 @@ class Tier:
         self._spec = spec
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:  # not during interpreter teardown
             _lib.load().tfg_tier_destroy(self._h)
             self._h = None
 
