@@ -137,7 +137,14 @@ struct StateIO {
 // DIVC selects the element math: 0 = div.rn quotients, 1 = constant-divisor
 // quotients, 2 = verified fast path (numerics.cuh adam_element_fast), 3 =
 // constant-divisor quotients with the quad's elements walked one at a time.
-template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0>
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// PF > 0: one thread per CTA asks the TMA unit to pull the CTA's chunk PF
+// grid-stride iterations ahead into L2 (cp.async.bulk.prefetch), so more bytes
+// are in flight than the registers of 32 warps per SM can hold.
+template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0, int PF = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                       unsigned long long* __restrict__ counters) {
@@ -154,6 +161,22 @@ __global__ void __launch_bounds__(kThreads, MINB)
         float4* mo4 = reinterpret_cast<float4*>(io.mo);
         float4* vo4 = reinterpret_cast<float4*>(io.vo);
         for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
+            if constexpr (PF > 0) {
+                if (threadIdx.x == 0) {
+                    const uint64_t cq = base + static_cast<uint64_t>(PF) * UNROLL * nthreads;
+                    if (cq < nq) {
+                        const uint64_t nqc = min(static_cast<uint64_t>(blockDim.x) * UNROLL, nq - cq);
+                        prefetch_l2(p4 + cq, static_cast<uint32_t>(16 * nqc));
+                        prefetch_l2(m4 + cq, static_cast<uint32_t>(16 * nqc));
+                        prefetch_l2(v4 + cq, static_cast<uint32_t>(16 * nqc));
+                        if constexpr (GMODE == 0) {
+                            const uint16_t* g = reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * cq;
+                            const uint32_t gb = static_cast<uint32_t>(8 * nqc) & ~15u;
+                            if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0 && gb > 0) prefetch_l2(g, gb);
+                        }
+                    }
+                }
+            }
             float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
             GradReg<GK, GMODE, NS> rg[UNROLL];
 #pragma unroll
@@ -234,11 +257,12 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
-template <int UNROLL, int DIVC, int MINB>
+template <int UNROLL, int DIVC, int MINB, int PF = 0>
 struct Cfg {
     static constexpr int kUnroll = UNROLL;
     static constexpr int kDivc = DIVC;
     static constexpr int kMinBlocks = MINB;
+    static constexpr int kPrefetch = PF;
 };
 
 GradSources sources_of(const AdamLaunch& a) {
@@ -276,7 +300,7 @@ cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     const GradSources gs = sources_of(a);
     if (is_vec(a)) {
         const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
-        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS>
+        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS, C::kPrefetch>
             <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
     } else {
         const unsigned grid = grid_for(a.n, B);
@@ -642,6 +666,12 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 23) return launch_scalar_wd<6>(a, stream);
     if constexpr (V == 24) return launch_wd<kF16, 0, kF16, Cfg<1, 3, 5>>(a, stream);
     if constexpr (V == 25) return launch_wd<kF16, 0, kF16, Cfg<1, 3, 6>>(a, stream);
+    if constexpr (V == 26) return launch_wd<kF16, 0, kF16, Cfg<1, 4, 4>>(a, stream);
+    if constexpr (V == 27) return launch_wd<kF16, 0, kF16, Cfg<1, 4, 5>>(a, stream);
+    if constexpr (V == 28) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 1>>(a, stream);
+    if constexpr (V == 29) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 2>>(a, stream);
+    if constexpr (V == 30) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 4>>(a, stream);
+    if constexpr (V == 31) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 3, 2>>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -710,11 +740,17 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 23: return launch_variant<23>(a, stream);
         case 24: return launch_variant<24>(a, stream);
         case 25: return launch_variant<25>(a, stream);
+        case 26: return launch_variant<26>(a, stream);
+        case 27: return launch_variant<27>(a, stream);
+        case 28: return launch_variant<28>(a, stream);
+        case 29: return launch_variant<29>(a, stream);
+        case 30: return launch_variant<30>(a, stream);
+        case 31: return launch_variant<31>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 26; }
+int adam_variant_count() { return 32; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {
