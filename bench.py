@@ -18,8 +18,14 @@ Legs of the `ours` line:
   e2e     the same metric through the engine's C ABI with the state on HOST
           tiers (pinned host DRAM + a local O_DIRECT directory tier): prefetch,
           H2D, fused kernel, D2H, flush/retain inside the timed region.
+  spill   the same metric with host DRAM capped to 8 pinned staging slots and
+          the state on two O_DIRECT directory tiers (local + remote, SURVEY
+          C4), the retention capacity in HBM; bounded sample (<= 12
+          subgroups). Roofline: the tiers' probed bandwidths.
   cpu_baseline  the reference CPU engine (oracle/_ref: the unmodified
           reference headers compiled in place) on a bounded sample, rank 0.
+--exchange fused|nccl: strong scaling over one model with the gradient
+reduce-scatter inside the update (fused: NVLink peer loads in the kernel).
 Multi-GPU (torchrun): weak scaling — every rank owns its own 68-subgroup shard
 (ids rank*68+k, ZeRO-3 contiguous blocks); value = all ranks' params / max
 rank time.
@@ -474,6 +480,71 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
 
 
 # ---------------------------------------------------------------------------
+# leg 3: spill (SURVEY C4 shape): host DRAM capped to a few pinned staging
+# slots, the state on two directory tiers (local "NVMe" + "remote"), the
+# retention capacity held in HBM (hbm_retain=2). Tier-bound; bounded sample.
+
+
+def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=3, pool=8, ring=4):
+    import torch
+    dev = torch.cuda.current_device()
+    root = Path(tier_root) / f"spill_rank{rank}"
+    shutil.rmtree(root, ignore_errors=True)
+    root.mkdir(parents=True)
+    # bounded by the disk the ranks share: at most half the free space
+    free = shutil.disk_usage(root).free
+    M = max(2, min(len(sizes), 12, int(0.5 * free / world // (12 * max(sizes) + 4096))))
+    sizes = sizes[:M]
+    cache = M // 2
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4))]
+    probes = [t.probe_bandwidth(256 << 20, 3) for t in tiers]
+    same_device = os.stat(root / "nvme").st_dev == os.stat(root / "remote").st_dev
+    trace = tf.EventTrace()
+    opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
+    w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, tf.F16, tf.F16, ring, 0, 1, 2))
+    for k, n in enumerate(sizes):
+        w.add_subgroup(base_id + k, n)
+    w.init_and_flush_all(seed)
+    src = tf.SyntheticGradSource(seed)
+    phases = []
+    for it in range(warmup + steps):
+        w.run_backward_sim(it, src, 1)
+        barrier(world)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        st = w.run_update(it)
+        b.record()
+        torch.cuda.synchronize()
+        barrier(world)
+        ms = a.elapsed_time(b)
+        log(f"[rank {rank}] spill phase {it}: {ms:.0f} ms, hits {st.cache_hits}, alloc {st.flush_allocation}")
+        if it >= warmup:
+            phases.append((ms, st))
+    w.close()
+    del w
+    shutil.rmtree(root, ignore_errors=True)
+    ms = statistics.mean(p[0] for p in phases)
+    # Tier roofline: each tier's I/O thread moves its reads and writes in turn,
+    # so a tier needs read/r + write/w; tiers on one physical device add up,
+    # independent devices overlap (the Eq. 1 model).
+    per_tier = []
+    for i, pr in enumerate(probes):
+        rb = statistics.mean(p[1].tier_obs[i].read_bytes for p in phases)
+        wb = statistics.mean(p[1].tier_obs[i].write_bytes for p in phases)
+        per_tier.append(dict(read_bytes=rb, write_bytes=wb, read_gbs=round(pr.read_bw / 1e9, 2),
+                             write_gbs=round(pr.write_bw / 1e9, 2), seconds=rb / pr.read_bw + wb / pr.write_bw))
+    serial_s = sum(t["seconds"] for t in per_tier)
+    parallel_s = max(t["seconds"] for t in per_tier)
+    bound_s = serial_s if same_device else parallel_s
+    return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, pool=pool, same_device=same_device,
+                bound_ms=bound_s * 1e3, independent_bound_ms=parallel_s * 1e3, per_tier=per_tier,
+                hits=statistics.mean(p[1].cache_hits for p in phases),
+                alloc=phases[-1][1].flush_allocation, launches=steps * M)
+
+
+# ---------------------------------------------------------------------------
 # reference CPU engine (oracle/_ref), bounded sample
 
 
@@ -533,6 +604,7 @@ def main(argv=None):
                          "(fused: peer loads in the Adam kernel; nccl: reduce_scatter then the kernel)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-spill", action="store_true", help="skip the directory-tier spill sample (SURVEY C4)")
     a = ap.parse_args(argv)
 
     wl = WORKLOADS[a.workload]
@@ -622,7 +694,25 @@ def main(argv=None):
             e2e = {"error": f"{type(exc).__name__}: {exc}"}
             log(f"e2e leg failed: {exc}")
 
-    e2e_launches = (e2e or {}).get("gpu_launches", 0)
+    spill = None
+    if a.exchange == "none" and not a.skip_e2e and not a.skip_spill:
+        try:
+            r = spill_leg(tf, sizes, base_id, rank, world, a.tier_root, a.seed)
+            s_ms = allmax(world, r["ms"])
+            spill = {"value": world * r["params"] / (s_ms / 1e3), "unit": "params/s", "ms_per_step": round(s_ms, 1),
+                     "tier_bound_ms": round(r["bound_ms"], 1), "tier_frac": round(r["bound_ms"] / s_ms, 4),
+                     "independent_tier_bound_ms": round(r["independent_bound_ms"], 1),
+                     "tiers_share_one_device": r["same_device"], "per_tier": r["per_tier"],
+                     "subgroups_per_rank": r["subgroups"], "hbm_cache_slots": r["cache"], "pool_slots": r["pool"],
+                     "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"],
+                     "gpu_launches": r["launches"],
+                     "path": "C ABI tfg_engine_run_update, tiers [local_dir O_DIRECT, remote_dir O_DIRECT], "
+                             "host DRAM = pinned staging slots only, retention in HBM (hbm_retain=2)"}
+        except Exception as exc:
+            spill = {"error": f"{type(exc).__name__}: {exc}"}
+            log(f"spill leg failed: {exc}")
+
+    e2e_launches = (e2e or {}).get("gpu_launches", 0) + (spill or {}).get("gpu_launches", 0)
     scaling = "strong" if a.exchange != "none" else "weak"
     parallelism = (f"zero3-shard x{world}, gradient reduce-scatter {a.exchange} (strong)" if a.exchange != "none"
                    else f"zero3-shard x{world} (weak)")
@@ -647,7 +737,7 @@ def main(argv=None):
                                   if ALG_BYTES_PER_PARAM * max(sizes) > 2 * 126e6 else
                                   "WARNING: launch working set fits in L2; not a roofline-valid size"),
                            "parallelism": parallelism},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "spill": spill,
                 "gpu_launches": dl["launches"] + e2e_launches,
                 "clocks": dl["clocks"]}
         print(json.dumps(line), flush=True)
