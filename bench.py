@@ -485,7 +485,8 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
 # retention capacity held in HBM (hbm_retain=2). Tier-bound; bounded sample.
 
 
-def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=3, pool=8, ring=4):
+def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=3, pool=8, ring=4,
+              lock_shared=True):
     import torch
     dev = torch.cuda.current_device()
     root = Path(tier_root) / f"spill_rank{rank}"
@@ -496,10 +497,18 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     M = max(2, min(len(sizes), 12, int(0.5 * free / world // (12 * max(sizes) + 4096))))
     sizes = sizes[:M]
     cache = M // 2
-    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4)),
-             tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4))]
-    probes = [t.probe_bandwidth(256 << 20, 3) for t in tiers]
+    for d in ("nvme", "remote"):
+        (root / d).mkdir()
+    # Tiers on one physical device share one semaphore (contention control
+    # per device, TierSpec.lock_device): their transfers take turns instead of
+    # seeking against each other.
     same_device = os.stat(root / "nvme").st_dev == os.stat(root / "remote").st_dev
+    lock_dev = 1 if same_device and lock_shared else 0
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4,
+                                 lock_device=lock_dev)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
+                                 lock_device=lock_dev))]
+    probes = [t.probe_bandwidth(256 << 20, 3) for t in tiers]
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
     w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, tf.F16, tf.F16, ring, 0, 1, 2))
@@ -539,6 +548,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     parallel_s = max(t["seconds"] for t in per_tier)
     bound_s = serial_s if same_device else parallel_s
     return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, pool=pool, same_device=same_device,
+                lock_device=lock_dev,
                 bound_ms=bound_s * 1e3, independent_bound_ms=parallel_s * 1e3, per_tier=per_tier,
                 hits=statistics.mean(p[1].cache_hits for p in phases),
                 alloc=phases[-1][1].flush_allocation, launches=steps * M)
@@ -702,7 +712,8 @@ def main(argv=None):
             spill = {"value": world * r["params"] / (s_ms / 1e3), "unit": "params/s", "ms_per_step": round(s_ms, 1),
                      "tier_bound_ms": round(r["bound_ms"], 1), "tier_frac": round(r["bound_ms"] / s_ms, 4),
                      "independent_tier_bound_ms": round(r["independent_bound_ms"], 1),
-                     "tiers_share_one_device": r["same_device"], "per_tier": r["per_tier"],
+                     "tiers_share_one_device": r["same_device"], "device_semaphore": bool(r["lock_device"]),
+                     "per_tier": r["per_tier"],
                      "subgroups_per_rank": r["subgroups"], "hbm_cache_slots": r["cache"], "pool_slots": r["pool"],
                      "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"],
                      "gpu_launches": r["launches"],

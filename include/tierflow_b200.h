@@ -73,6 +73,9 @@ typedef struct tfg_tier_spec {
     int32_t persistent;
     int32_t lock_width;      /* tier semaphore width; 1 = exclusive flock (the reference) */
     int32_t direct_io;       /* O_DIRECT on the engine path when the filesystem allows */
+    int32_t lock_device;     /* 0: the tier's own semaphore (the reference); k > 0: one semaphore
+                                shared by every tier with the same k, i.e. per physical device,
+                                so tiers on one disk do not contend with concurrent transfers */
 } tfg_tier_spec;
 
 /* ScheduleOptions, scheduler.hpp:32-50. */

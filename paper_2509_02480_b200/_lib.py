@@ -62,7 +62,7 @@ class AdamHyperC(C.Structure):
 class TierSpecC(C.Structure):
     _fields_ = [("tier_id", C.c_int32), ("kind", C.c_int32), ("root", C.c_char_p), ("read_bw", C.c_double),
                 ("write_bw", C.c_double), ("io_parallelism", C.c_int32), ("persistent", C.c_int32),
-                ("lock_width", C.c_int32), ("direct_io", C.c_int32)]
+                ("lock_width", C.c_int32), ("direct_io", C.c_int32), ("lock_device", C.c_int32)]
 
 
 class ScheduleOptionsC(C.Structure):

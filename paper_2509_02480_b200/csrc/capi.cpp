@@ -480,6 +480,8 @@ int tfg_tier_create(const tfg_tier_spec* spec, tfg_tier** out) {
         s.persistent = spec->persistent != 0;
         s.lock_width = spec->lock_width;
         s.direct_io = spec->direct_io != 0;
+        if (spec->lock_device < 0) throw tfb::ConfigError("lock_device must be >= 0");
+        s.lock_device = spec->lock_device;
         if ((s.kind == tfb::TierKind::local_dir || s.kind == tfb::TierKind::remote_dir) && s.root.empty())
             throw tfb::ConfigError("directory tiers need a root path");
         *out = new tfg_tier{std::make_shared<tfb::Tier>(s)};

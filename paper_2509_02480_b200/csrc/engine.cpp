@@ -247,7 +247,8 @@ void TierIoWorker::execute(Job& job) {
     const EventKind end = job.is_prefetch ? EventKind::prefetch_end : EventKind::flush_end;
     std::optional<TierLockGuard> guard;
     try {
-        if (use_lock_) guard.emplace(lock_dir_, tier_->id(), worker_, trace_, tier_->spec().lock_width);
+        if (use_lock_)
+            guard.emplace(lock_dir_, tier_->id(), worker_, trace_, tier_->spec().lock_width, tier_->spec().lock_device);
         Event ev;
         ev.timestamp_ns = now_ns();
         ev.worker_id = worker_;

@@ -117,7 +117,38 @@ Tier::Tier(TierSpec spec) : spec_(std::move(spec)) {
     }
 }
 
-Tier::~Tier() = default;
+Tier::~Tier() {
+    {
+        std::lock_guard<std::mutex> g(reap_mu_);
+        reap_stop_ = true;
+    }
+    reap_cv_.notify_all();
+    if (reaper_.joinable()) reaper_.join();
+}
+
+void Tier::reap_later(std::filesystem::path p) {
+    {
+        std::lock_guard<std::mutex> g(reap_mu_);
+        reap_q_.push_back(std::move(p));
+        if (!reaper_.joinable()) reaper_ = std::thread([this] { reap_loop(); });
+    }
+    reap_cv_.notify_one();
+}
+
+void Tier::reap_loop() {
+    for (;;) {
+        std::filesystem::path p;
+        {
+            std::unique_lock<std::mutex> l(reap_mu_);
+            reap_cv_.wait(l, [&] { return reap_stop_ || !reap_q_.empty(); });
+            if (reap_q_.empty()) return;  // stop requested and drained
+            p = std::move(reap_q_.front());
+            reap_q_.pop_front();
+        }
+        std::error_code ec;
+        std::filesystem::remove(p, ec);
+    }
+}
 
 std::string Tier::err_ctx() const {
     return "tier " + std::to_string(spec_.tier_id) + " (" + tier_kind_name(spec_.kind) + ")";
@@ -218,8 +249,17 @@ void Tier::remove_subgroup(SubgroupId id) {
                 break;
             }
             default: {
+                // rename (metadata only) under the tier mutex; unlink off-thread
+                const std::filesystem::path src = std::filesystem::path(spec_.root) / name;
+                std::filesystem::path trash;
+                {
+                    std::lock_guard<std::mutex> rg(reap_mu_);
+                    trash = src;
+                    trash += ".reap." + std::to_string(reap_seq_++);
+                }
                 std::error_code ec;
-                std::filesystem::remove(std::filesystem::path(spec_.root) / name, ec);
+                std::filesystem::rename(src, trash, ec);
+                if (!ec) reap_later(std::move(trash));
             }
         }
     }

@@ -18,9 +18,13 @@
 
 #include <array>
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <deque>
+#include <filesystem>
 #include <memory>
 #include <mutex>
+#include <thread>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -45,6 +49,7 @@ struct TierSpec {
     bool persistent = false;
     int lock_width = 1;      // tier semaphore width (1 = exclusive, the reference)
     bool direct_io = true;   // O_DIRECT on the engine path when the filesystem allows
+    int lock_device = 0;     // 0: own semaphore; k > 0: shared by all tiers with the same k
 };
 
 struct ProbeResult {
@@ -143,6 +148,17 @@ private:
     std::unordered_map<std::string, DramBlob> dram_store_;
     std::vector<HostBlock> spares_;
     std::size_t block_bytes_ = 0;
+    // directory tiers: removal renames the file out of the way at once and a
+    // reaper thread unlinks it, so dropping the stale copy of a subgroup that
+    // moved tier (reference scheduler.hpp:727-735) never stalls an I/O thread
+    void reap_later(std::filesystem::path p);
+    void reap_loop();
+    std::mutex reap_mu_;
+    std::condition_variable reap_cv_;
+    std::deque<std::filesystem::path> reap_q_;
+    bool reap_stop_ = false;
+    std::uint64_t reap_seq_ = 0;
+    std::thread reaper_;
 };
 
 }  // namespace tfb

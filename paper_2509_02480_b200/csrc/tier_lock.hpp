@@ -23,9 +23,13 @@
 
 namespace tfb {
 
-inline std::filesystem::path tier_lock_path(const std::filesystem::path& dir, TierId tier, int slot = 0) {
-    if (slot == 0) return dir / ("tier_" + std::to_string(tier) + ".lock");
-    return dir / ("tier_" + std::to_string(tier) + "." + std::to_string(slot) + ".lock");
+// `device` > 0 names a semaphore shared by every tier on one physical device
+// (TierSpec::lock_device); 0 is the reference's per-tier file.
+inline std::filesystem::path tier_lock_path(const std::filesystem::path& dir, TierId tier, int slot = 0,
+                                            int device = 0) {
+    const std::string stem = device > 0 ? "device_" + std::to_string(device) : "tier_" + std::to_string(tier);
+    if (slot == 0) return dir / (stem + ".lock");
+    return dir / (stem + "." + std::to_string(slot) + ".lock");
 }
 
 namespace detail {
@@ -36,8 +40,8 @@ inline thread_local int tier_locks_held = 0;
 class TierLockGuard {
 public:
     TierLockGuard(const std::filesystem::path& dir, TierId tier, WorkerId worker, EventTrace* trace,
-                  int width = 1)
-        : tier_(tier), worker_(worker), trace_(trace) {
+                  int width = 1, int device = 0)
+        : tier_(tier), device_(device), worker_(worker), trace_(trace) {
         if (detail::tier_locks_held != 0) throw Error("worker already holds a tier lock (no nesting allowed)");
         if (width < 1) throw ConfigError("tier lock width must be >= 1");
         std::error_code ec;
@@ -46,7 +50,7 @@ public:
         bool held = false;
         for (int k = 0; k < width && !held && width > 1; ++k) held = try_slot(dir, k, LOCK_EX | LOCK_NB);
         if (!held) held = try_slot(dir, width > 1 ? (worker % width + width) % width : 0, LOCK_EX);
-        if (!held) throw IoError("flock failed on " + tier_lock_path(dir, tier).string());
+        if (!held) throw IoError("flock failed on " + tier_lock_path(dir, tier, 0, device).string());
         ++detail::tier_locks_held;
         if (trace_) trace_->record(EventKind::lock_acquire, worker_, -1, tier_, 0);
     }
@@ -69,7 +73,7 @@ public:
 
 private:
     bool try_slot(const std::filesystem::path& dir, int slot, int op) {
-        const auto path = tier_lock_path(dir, tier_, slot);
+        const auto path = tier_lock_path(dir, tier_, slot, device_);
         const int fd = ::open(path.c_str(), O_CREAT | O_RDWR | O_CLOEXEC, 0644);
         if (fd < 0) throw ConfigError("cannot open lock file " + path.string() + ": " + std::strerror(errno));
         for (;;) {
@@ -87,6 +91,7 @@ private:
 
     int fd_ = -1;
     TierId tier_ = kNoTier;
+    int device_ = 0;
     WorkerId worker_ = 0;
     EventTrace* trace_ = nullptr;
 };

@@ -95,6 +95,9 @@ class TierSpec:
     persistent: bool = False
     lock_width: int = 1
     direct_io: bool = True
+    # 0: own semaphore (reference); k > 0: shared by all tiers with the same k
+    # (one physical device)
+    lock_device: int = 0
 
 
 @dataclass
@@ -373,7 +376,8 @@ class Tier:
     def __init__(self, spec: TierSpec):
         self._root = (spec.root or "").encode()
         cs = _lib.TierSpecC(spec.tier_id, int(spec.kind), self._root, spec.read_bw, spec.write_bw,
-                            spec.io_parallelism, int(spec.persistent), spec.lock_width, int(spec.direct_io))
+                            spec.io_parallelism, int(spec.persistent), spec.lock_width, int(spec.direct_io),
+                            spec.lock_device)
         h = C.c_void_p()
         _lib.call("tfg_tier_create", C.byref(cs), C.byref(h))
         self._h = h

@@ -19,9 +19,9 @@ pytestmark = pytest.mark.gpu
 
 def make_engine(tf, tiers_cfg, params, *, pool_slots=4, cache_slots=-1, ratio=None, seed=42, lock_dir="",
                 wd=0.0, device_buffers=3, grad_dtype=0, param_dtype=0, deadlock=30.0, pad_ns=0, caching=True,
-                multi_path=True, hbm=1):
+                multi_path=True, hbm=1, lock_device=0):
     trace = tf.EventTrace()
-    tiers = [tf.Tier(tf.TierSpec(i, *cfg)) for i, cfg in enumerate(tiers_cfg)]
+    tiers = [tf.Tier(tf.TierSpec(i, *cfg, lock_device=lock_device)) for i, cfg in enumerate(tiers_cfg)]
     opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=lock_dir,
                              deadlock_timeout_s=deadlock, update_pad_ns=pad_ns, enable_caching=caching,
                              multi_path=multi_path)
@@ -226,6 +226,32 @@ def test_flushes_to_distinct_tiers_overlap(tf, cuda, lock_dir):
             iv[e.subgroup_id][1] = e.timestamp_ns
     a, b = iv[0], iv[1]
     assert a[2] != b[2] and max(a[0], b[0]) < min(a[1], b[1])
+    w.close()
+
+
+def test_tiers_on_one_device_share_the_semaphore(tf, cuda, lock_dir):
+    """TierSpec.lock_device: two tiers keyed to one physical device take one
+    semaphore, so their transfers serialise (contention control per device)."""
+    w, trace, _ = make_engine(tf, [mem(150e6, 150e6), mem(150e6, 150e6)], [350_000] * 2, pool_slots=4,
+                              lock_dir=lock_dir, lock_device=7)
+    for i in (0, 1):
+        t = w.enqueue_prefetch(i)
+        if t:
+            t.get()
+    mark = trace.size()
+    f0, f1 = w.enqueue_flush(0, 0), w.enqueue_flush(1, 1)
+    f0.get()
+    f1.get()
+    iv = {}
+    for e in trace.snapshot(mark):
+        if e.kind == tf.EventKind.flush_start:
+            iv[e.subgroup_id] = [e.timestamp_ns, None]
+        elif e.kind == tf.EventKind.flush_end:
+            iv[e.subgroup_id][1] = e.timestamp_ns
+    a, b = sorted(iv.values())
+    assert a[1] <= b[0]
+    import os
+    assert os.path.exists(os.path.join(lock_dir, "device_7.lock"))
     w.close()
 
 
