@@ -92,3 +92,44 @@ def test_rebalance_after_bandwidth_drop(tf):
     tf.update_bandwidth_estimates(est, obs)
     after2 = tf.assign_subgroups(16, est.effective_all()).counts[1]
     assert after1 <= before and after2 < before
+
+
+def _paper_scale_cases():
+    """SURVEY §8 shapes: C2 68 subgroups, C3 200 over 1/2/4/8 ranks, C4 690
+    over 1/8 ranks (86/87 per rank), C5 sweep extremes; two- and three-tier
+    bandwidth vectors from the paper's testbeds (GB/s:
+    host DRAM ~25-55, NVMe 5.3-6.9, PFS 3.6-13.7)."""
+    from paper_2509_02480_b200 import parallel
+    Ms = {68, 200, 690, 9, 78}  # 9 = 1B at 125M per subgroup; 78 = 5B at 64M
+    for M, worlds in ((200, (2, 4, 8)), (690, (8,)), (68, (8,))):
+        for w in worlds:
+            Ms.update(parallel.shard(M, w, r)[1] for r in range(w))
+    bws = [[55.0, 5.3], [25.0, 6.9], [55.0, 5.3, 3.6], [6.9, 3.6], [5.3, 13.7], [25.0, 6.9, 4.8], [1.0, 1.0, 1.0]]
+    for M in sorted(Ms):
+        for bw in bws:
+            yield M, bw
+
+
+def test_paper_scale_placement_matches_oracle_and_reference(tf):
+    R = oracle.ref() if oracle.ref_available() else None
+    rng = np.random.default_rng(17)
+    for M, bw in _paper_scale_cases():
+        want = oracle.assign_subgroups(M, bw)
+        assert tf.assign_subgroups(M, bw).counts == want, (M, bw)
+        assert sum(want) == M
+        if R is not None:
+            counts = np.zeros(len(bw), np.int32)
+            assert R.ref_assign_subgroups(M, np.asarray(bw, np.float64), len(bw), counts) == 0
+            assert counts.tolist() == want, (M, bw)
+        for cap in (0, 5, 13, 29, M // 2):
+            order = list(range(M)) if rng.random() < 0.5 else list(reversed(range(M)))
+            plan = tf.DestinationPlan(order, cap, bw)
+            r, t, a = oracle.destination_plan(M, cap, bw)
+            got = [plan.assign_storage_tier(sg) for sg in order]
+            assert [(int(g.host_retain), g.tier) for g in got] == list(zip(r, t)), (M, bw, cap)
+            assert plan.flush_allocation().counts == a
+            if R is not None:
+                rr, tt, aa = (np.zeros(M, np.int32), np.zeros(M, np.int32), np.zeros(len(bw), np.int32))
+                assert R.ref_destination_plan(np.asarray(order, np.uint32), M, cap, np.asarray(bw, np.float64),
+                                              len(bw), rr, tt, aa) == 0
+                assert rr.tolist() == r and tt.tolist() == t and aa.tolist() == a
