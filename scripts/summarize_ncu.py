@@ -43,8 +43,10 @@ if launches.exists():
     (PROF / f"{tag}_launches.md").write_text("\n".join(lines) + "\n")
     print("\n".join(lines))
 
-rep = OUT / "prof_adam.ncu-rep"
-if rep.exists():
+import re  # noqa: E402
+
+
+def summarize(rep: Path, label: str, alg_bytes_per_param: int) -> None:
     raw = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, vals = rows[0], rows[1], rows[2]
@@ -56,18 +58,8 @@ if rep.exists():
             x = float(v.replace(",", ""))
         except ValueError:
             return None
-        if u in ("Gbyte",):
-            x *= 1e9
-        elif u in ("Mbyte",):
-            x *= 1e6
-        elif u in ("Kbyte",):
-            x *= 1e3
-        elif u in ("usecond", "us"):
-            x *= 1e-6
-        elif u in ("nsecond", "ns"):
-            x *= 1e-9
-        elif u in ("msecond", "ms"):
-            x *= 1e-3
+        x *= {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "usecond": 1e-6, "us": 1e-6, "nsecond": 1e-9, "ns": 1e-9,
+              "msecond": 1e-3, "ms": 1e-3}.get(u, 1.0)
         return x * scale
 
     keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -78,29 +70,41 @@ if rep.exists():
             "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
             "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__cycles_elapsed.avg.per_second",
             "launch__func_cache_config", "smsp__inst_executed.sum"]
-    text = [f"# ncu --set full, fused Adam kernel ({tag}); scripts/profile_kernel.py (100M params, f16 grads)"]
+    text = [f"# ncu --set full, {label} ({tag}); scripts/profile_kernel.py (100M params, f16 grads)"]
     for k in keys:
         if k in get:
             text.append(f"{k} = {get[k][0]} {get[k][1]}")
-    stalls = sorted(((h, v) for h, v in get.items() if "smsp__average_warp_latency_issue_stalled" in h
-                     or ("warp_issue_stalled" in h and "pct" in h)), key=lambda x: x[0])
-    for h, (v, u) in stalls[:40]:
-        text.append(f"{h} = {v} {u}")
+    text.append("# warp stall reasons, warps stalled per issued instruction")
+    stalls = sorted(((h, v) for h, v in get.items() if h.startswith("smsp__average_warps_issue_stalled_")
+                     and h.endswith("_per_issue_active.ratio")), key=lambda x: -float(x[1][0] or 0))
+    for h, (v, u) in stalls:
+        text.append(f"{h} = {v}")
     name = get.get("Kernel Name", ("?", ""))[0]
     dur = num("gpu__time_duration.sum")
     rd, wr = num("dram__bytes_read.sum"), num("dram__bytes_write.sum")
     n = 100_000_000
+    alg = alg_bytes_per_param * n
     summary = {"kernel": name, "params_per_launch": n, "duration_s": dur, "dram_bytes_read": rd,
                "dram_bytes_write": wr, "dram_bytes_per_launch": (rd or 0) + (wr or 0),
-               "algorithmic_bytes_per_launch": 28 * n,
-               "traffic_over_algorithmic": ((rd or 0) + (wr or 0)) / (28 * n),
+               "algorithmic_bytes_per_launch": alg,
+               "traffic_over_algorithmic": ((rd or 0) + (wr or 0)) / alg,
                "registers": num("launch__registers_per_thread"),
                "warps_active_pct": num("sm__warps_active.avg.pct_of_peak_sustained_active"),
                "fp64_pipe_pct": num("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
                "xu_pipe_pct": num("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
                "dram_throughput_pct": num("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
                "issue_active_pct": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
-               "tag": tag, "source": "gpurun_out/prof_adam.ncu-rep (ncu --set full --clock-control none)"}
-    (PROF / "ncu_adam_fused.json").write_text(json.dumps(summary, indent=1) + "\n")
-    (PROF / f"{tag}_ncu_adam_fused.txt").write_text("\n".join(text) + "\n")
+               "tag": tag, "source": f"gpurun_out/{rep.name} (ncu --set full --clock-control none)"}
+    stem = "adam_fused" if rep.stem == "prof_adam" else rep.stem.replace("prof_", "adam_")
+    (PROF / f"ncu_{stem}.json").write_text(json.dumps(summary, indent=1) + "\n")
+    (PROF / f"{tag}_ncu_{stem}.txt").write_text("\n".join(text) + "\n")
     print(json.dumps(summary, indent=1))
+
+
+for rep in sorted(OUT.glob("prof_*.ncu-rep")):
+    m = re.fullmatch(r"prof_multi(\d+)", rep.stem)
+    if rep.stem == "prof_adam":
+        summarize(rep, "fused Adam kernel", 28)
+    elif m:
+        k = int(m.group(1))
+        summarize(rep, f"fused reduce + update kernel, {k} gradient sources", 26 + 2 * k)
