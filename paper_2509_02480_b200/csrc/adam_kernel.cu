@@ -509,6 +509,131 @@ cudaError_t launch_tma(const AdamLaunch& a, cudaStream_t stream) {
 }
 
 // ---------------------------------------------------------------------------
+// TMA multistage pipeline without warp specialisation: every warp computes;
+// one elected thread keeps S-1 tiles (1024 params, 14 KiB) of P, m, v, g in
+// flight into a shared-memory ring with cp.async.bulk, so the bytes in flight
+// per SM (4 CTAs x (S-1) x 14 KiB) no longer depend on how long the FP64
+// chain of the current quad takes. One __syncthreads per tile retires a stage
+// before it is refilled.
+// REL = true: warps release a stage through a per-stage mbarrier (one
+// arrival per warp) instead of a CTA barrier, so only the issuing warp ever
+// waits for the slowest warp of a tile.
+template <int S, bool WD, int MINB, bool REL = false>
+__global__ void __launch_bounds__(kThreads, MINB)
+    adam_tma_pipe_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                         const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t ntiles, AdamConsts c,
+                         unsigned long long* __restrict__ counters) {
+    constexpr int T = 4 * kThreads;  // one quad per thread per tile
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* sp = reinterpret_cast<float*>(smem);
+    float* sm = sp + S * T;
+    float* sv = sm + S * T;
+    uint16_t* sg = reinterpret_cast<uint16_t*>(sv + S * T);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
+    uint64_t* empty = full + S;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            if constexpr (REL) mbar_init(&empty[s], kThreads / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](uint64_t k) {
+        const int s = static_cast<int>(k % S);
+        const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
+        mbar_arrive_expect_tx(&full[s], 14u * T);
+        bulk_load(sp + s * T, p + off, 4u * T, &full[s]);
+        bulk_load(sm + s * T, m + off, 4u * T, &full[s]);
+        bulk_load(sv + s * T, v + off, 4u * T, &full[s]);
+        bulk_load(sg + s * T, g + off, 2u * T, &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (uint64_t k = 0; k + 1 < static_cast<uint64_t>(S) && k < mine; ++k) issue(k);
+    unsigned nonfinite = 0, overflow = 0;
+    const int qi = threadIdx.x;
+    for (uint64_t k = 0; k < mine; ++k) {
+        if (threadIdx.x == 0 && k + S - 1 < mine) {  // refills the stage of tile k-1
+            if constexpr (REL)
+                if (k > 0) mbar_wait(&empty[(k - 1) % S], static_cast<uint32_t>((k - 1) / S) & 1u);
+            issue(k + S - 1);
+        }
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
+        const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
+        float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qi];
+        float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qi];
+        float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qi];
+        const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qi];
+        U16x4 gh;
+        gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
+        gh.y = static_cast<uint16_t>(graw.x >> 16);
+        gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
+        gh.w = static_cast<uint16_t>(graw.y >> 16);
+        nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
+                     nonfinite16<kF16>(gh.w);
+        adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
+        adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
+        adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
+        adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
+        U16x4 h;
+        h.x = narrow16<kF16>(rp.x);
+        h.y = narrow16<kF16>(rp.y);
+        h.z = narrow16<kF16>(rp.z);
+        h.w = narrow16<kF16>(rp.w);
+        overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
+        __stcs(reinterpret_cast<float4*>(p + off) + qi, rp);
+        __stcs(reinterpret_cast<float4*>(m + off) + qi, rm);
+        __stcs(reinterpret_cast<float4*>(v + off) + qi, rv);
+        store_u16x4(p16 + off + 4 * qi, h);
+        if constexpr (REL) {
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+        } else {
+            __syncthreads();  // stage s retired: it is refilled at iteration k + 1
+        }
+    }
+    if (counters != nullptr) {
+        warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+template <int S, int MINB, bool REL = false>
+cudaError_t launch_tma_pipe(const AdamLaunch& a, cudaStream_t stream) {
+    constexpr int T = 4 * kThreads;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
+                           reinterpret_cast<uintptr_t>(a.p16)) & 15u) == 0;
+    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
+        return cudaErrorInvalidValue;
+    const uint64_t ntiles = a.n / T;
+    constexpr size_t smem = static_cast<size_t>(S) * T * 14 + 2 * S * sizeof(uint64_t);
+    if (ntiles > 0) {
+        auto kern = a.c.lr_wd != 0.0 ? adam_tma_pipe_kernel<S, true, MINB, REL>
+                                     : adam_tma_pipe_kernel<S, false, MINB, REL>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
+        kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, ntiles, a.c,
+                                               a.counters);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t done = ntiles * T;
+    if (done == a.n) return cudaSuccess;
+    AdamLaunch tail = a;  // the n % T remainder through the register-streaming kernel
+    tail.p += done;
+    tail.m += done;
+    tail.v += done;
+    tail.g = static_cast<const uint16_t*>(a.g) + done;
+    tail.p16 += done;
+    tail.n = a.n - done;
+    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
+}
+
+// ---------------------------------------------------------------------------
 // cp.async double-buffered variant: each thread copies its NEXT quad of P, m,
 // v, g into its own shared-memory slots with cp.async (LDGSTS, no registers
 // held) before computing the current one, so memory latency overlaps the FP64
@@ -672,6 +797,12 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 29) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 2>>(a, stream);
     if constexpr (V == 30) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 4>>(a, stream);
     if constexpr (V == 31) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 3, 2>>(a, stream);
+    if constexpr (V == 32) return launch_tma_pipe<3, 4>(a, stream);
+    if constexpr (V == 33) return launch_tma_pipe<2, 4>(a, stream);
+    if constexpr (V == 34) return launch_tma_pipe<4, 3>(a, stream);
+    if constexpr (V == 35) return launch_tma_pipe<3, 3>(a, stream);
+    if constexpr (V == 36) return launch_tma_pipe<3, 4, true>(a, stream);
+    if constexpr (V == 37) return launch_tma_pipe<2, 4, true>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -746,11 +877,17 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 29: return launch_variant<29>(a, stream);
         case 30: return launch_variant<30>(a, stream);
         case 31: return launch_variant<31>(a, stream);
+        case 32: return launch_variant<32>(a, stream);
+        case 33: return launch_variant<33>(a, stream);
+        case 34: return launch_variant<34>(a, stream);
+        case 35: return launch_variant<35>(a, stream);
+        case 36: return launch_variant<36>(a, stream);
+        case 37: return launch_variant<37>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 32; }
+int adam_variant_count() { return 38; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {
