@@ -50,6 +50,7 @@ sys.path.insert(0, str(ROOT))
 BASE = json.loads((ROOT / "BASELINE.json").read_text())
 METRIC = BASE["metric"]
 ALG_BYTES_PER_PARAM = 28  # P,m,v fp32 read+write (24) + 16-bit grad read (2) + 16-bit params write (2)
+DT = 0  # 16-bit gradient / working-param kind: 0 f16 (the reference's), 1 bf16 (--dtype)
 
 WORKLOADS = {
     "llama2-7b": dict(total=6_738_415_616, sub=100_000_000,
@@ -201,7 +202,7 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
             st = torch.empty(3 * n, dtype=torch.float32, device=dev)
             g = torch.empty(n, dtype=torch.int16, device=dev)
             tf.synthetic_state(st[:n], st[n:2 * n], st[2 * n:], seed, base_id + k, stream=stream)
-            tf.synthetic_grads(g, seed, base_id + k, 0, stream=stream)
+            tf.synthetic_grads(g, seed, base_id + k, 0, dtype=DT, stream=stream)
             states.append(st)
             grads.append(g)
             p16s.append(torch.empty(n, dtype=torch.int16, device=dev))
@@ -214,7 +215,7 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
             st = states[k]
             if events is not None:
                 events[k][0].record(stream)
-            tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], grads[k], p16s[k], t, hyper, counters=counters,
+            tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], grads[k], p16s[k], t, hyper, DT, DT, counters=counters,
                           stream=stream)
             if events is not None:
                 events[k][1].record(stream)
@@ -281,7 +282,7 @@ def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
         if mode == "fused":
             pg = parallel.PeerGradients(sizes, world, rank, device=dev.index)
             for sg, n in enumerate(sizes):  # this rank's contribution to every subgroup
-                tf.synthetic_grads(pg.local(sg).view(torch.int16), seed + 100 * rank, sg, 0, stream=stream)
+                tf.synthetic_grads(pg.local(sg).view(torch.int16), seed + 100 * rank, sg, 0, dtype=DT, stream=stream)
         else:
             # padded layout: rank r's block = shard(r) subgroups x max subgroup size
             cmax = max(parallel.shard(M, world, r)[1] for r in range(world))
@@ -291,7 +292,8 @@ def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
                 b, c = parallel.shard(M, world, r)
                 for k in range(c):
                     off = (r * cmax + k) * sub
-                    tf.synthetic_grads(flat[off:off + sizes[b + k]], seed + 100 * rank, b + k, 0, stream=stream)
+                    tf.synthetic_grads(flat[off:off + sizes[b + k]], seed + 100 * rank, b + k, 0, dtype=DT,
+                                       stream=stream)
             mine = torch.empty(cmax * sub, dtype=torch.int16, device=dev) if world > 1 else flat
     stream.synchronize()
     barrier(world)  # every contribution written before any owner reads it
@@ -299,18 +301,19 @@ def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
     def step(t, events=None):
         if mode == "nccl" and world > 1:
             with torch.cuda.stream(stream):
-                dist.reduce_scatter_tensor(mine.view(torch.float16), flat.view(torch.float16), op=dist.ReduceOp.SUM)
+                ft = torch.bfloat16 if DT else torch.float16
+                dist.reduce_scatter_tensor(mine.view(ft), flat.view(ft), op=dist.ReduceOp.SUM)
         for k, sg in enumerate(owned):
             n = sizes[sg]
             st = states[sg]
             if events is not None:
                 events[k][0].record(stream)
             if mode == "fused":
-                tf.adam_fused_multi(st[:n], st[n:2 * n], st[2 * n:], pg.sources(sg), p16s[sg], t, hyper,
+                tf.adam_fused_multi(st[:n], st[n:2 * n], st[2 * n:], pg.sources(sg), p16s[sg], t, hyper, DT, DT,
                                     counters=counters, stream=stream)
             else:
                 off = k * max(sizes)
-                tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], mine[off:off + n], p16s[sg], t, hyper,
+                tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], mine[off:off + n], p16s[sg], t, hyper, DT, DT,
                               counters=counters, stream=stream)
             if events is not None:
                 events[k][1].record(stream)
@@ -424,7 +427,7 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=str(root / "locks"))
     w = tf.OffloadWorker(rank, [dram, nvme], opt, tf.AdamHyper(), trace,
-                         tf.DeviceOptions(dev, tf.F16, tf.F16, ring, 0, 1, hbm_retain))
+                         tf.DeviceOptions(dev, DT, DT, ring, 0, 1, hbm_retain))
     for k, n in enumerate(sizes):
         w.add_subgroup(base_id + k, n)
     t0 = time.time()
@@ -511,7 +514,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     probes = [t.probe_bandwidth(256 << 20, 3) for t in tiers]
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
-    w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, tf.F16, tf.F16, ring, 0, 1, 2))
+    w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2))
     for k, n in enumerate(sizes):
         w.add_subgroup(base_id + k, n)
     w.init_and_flush_all(seed)
@@ -609,6 +612,8 @@ def main(argv=None):
     ap.add_argument("--ring", type=int, default=12)
     ap.add_argument("--hbm-retain", type=int, default=1, help="retained subgroups stay in HBM between phases")
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--dtype", choices=["f16", "bf16"], default="f16",
+                    help="16-bit gradient and working-param kind (f16 = the reference's fp16)")
     ap.add_argument("--exchange", choices=["none", "fused", "nccl"], default="none",
                     help="strong scaling over one model with the gradient reduce-scatter in the update "
                          "(fused: peer loads in the Adam kernel; nccl: reduce_scatter then the kernel)")
@@ -618,6 +623,8 @@ def main(argv=None):
     a = ap.parse_args(argv)
 
     wl = WORKLOADS[a.workload]
+    global DT
+    DT = 1 if a.dtype == "bf16" else 0
     sizes = subgroup_sizes(wl["total"], wl["sub"])
 
     if a.impl == "reference":
@@ -742,7 +749,7 @@ def main(argv=None):
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded reference generators: synthetic_param_init, SyntheticGradSource)",
                 "config": {"workload": wl["desc"], "params_per_rank": params_rank, "subgroups_per_rank": launches_rank,
-                           "grad_dtype": "f16", "param_dtype": "f16", "state": "fp32 P/m/v resident in HBM",
+                           "grad_dtype": a.dtype, "param_dtype": a.dtype, "state": "fp32 P/m/v resident in HBM",
                            "l2": (f"inputs larger than L2 ({ALG_BYTES_PER_PARAM * max(sizes) / 1e9:.2f} GB per "
                                   "subgroup launch vs 126 MB L2; no flush needed)"
                                   if ALG_BYTES_PER_PARAM * max(sizes) > 2 * 126e6 else
