@@ -388,22 +388,41 @@ def pcie_probe():
     return out
 
 
-def e2e_shard(sizes, world, pool_slots, cache_slots):
+WRITEBACK_BLOCKS = 4  # engine.hpp kWritebackBlocks (HBM cache mode)
+
+
+def e2e_shard(sizes, world, pool_slots, cache_slots, hbm_retain=2):
     """(subgroups, pool_slots, cache_slots) each rank streams in the e2e leg.
-    Every subgroup pins one 12 B/param host block (a pool slot or a host-DRAM
-    tier blob); N ranks on one host share 70% of MemAvailable. When the
-    requested pool plus the shard does not fit, the pool shrinks first (to a
-    third of the rank's blocks, at least 4 slots) and then the shard."""
+    Host blocks of 12 B/param are pinned by the pool slots, by every subgroup
+    on the host-DRAM tier and (HBM cache mode) by the write-back lane; a
+    subgroup retained in HBM pins none in mode 2 but keeps its slot in mode 1.
+    N ranks on one host share 70% of MemAvailable. When the request does not
+    fit, the pool shrinks first (to a third of the rank's blocks, at least 4
+    slots) and then the shard."""
     try:
         avail = next(int(l.split()[1]) * 1024 for l in open("/proc/meminfo") if l.startswith("MemAvailable:"))
     except (OSError, StopIteration):
         return sizes, pool_slots, cache_slots
     blocks = int(0.7 * avail / world // (12 * max(sizes) + 4096))
+    hbm_cache = hbm_retain == 2 and cache_slots >= 0
+    extra = WRITEBACK_BLOCKS if hbm_cache else 0
+
+    def cache_for(n):  # a shrunk shard keeps the requested retained fraction
+        return min(cache_slots, n * cache_slots // len(sizes)) if hbm_cache else 0
+
+    def need(pool, n):  # retained in HBM: no host block
+        return pool + extra + n - cache_for(n)
+
     pool = pool_slots
-    if pool + len(sizes) > blocks:
+    if need(pool, len(sizes)) > blocks:
         pool = max(4, min(pool_slots, blocks // 3))
-    n = max(1, min(len(sizes), blocks - pool))
-    cache = cache_slots if cache_slots < 0 else min(cache_slots, max(0, pool - 3))
+    n = len(sizes)
+    while n > 1 and need(pool, n) > blocks:
+        n -= 1
+    if hbm_cache:
+        cache = cache_for(n)
+    else:
+        cache = cache_slots if cache_slots < 0 else min(cache_slots, max(0, pool - 3))
     return sizes[:n], pool, cache
 
 
@@ -604,13 +623,16 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama2-7b")
     ap.add_argument("--tier-root", default=os.environ.get("TFB_TIER_ROOT", str(ROOT / "gpurun_out" / "bench_tiers")))
-    # Pool 42 / C 29 / ring 12: 29 retained subgroups (35 GB) + 12 ring
-    # buffers (14 GB) of HBM beside the 27 GB of 16-bit gradients and working
-    # params, 76 GB of the 180 GB; 97 GB of pinned host memory.
-    ap.add_argument("--pool-slots", type=int, default=42)
-    ap.add_argument("--cache-slots", type=int, default=29, help="-1: C = pool_slots - 3 (reference default)")
+    # HBM cache (hbm_retain 2), C 29 / pool 16 / ring 12: 29 retained
+    # subgroups (35 GB) + 12 ring buffers (14 GB) of HBM beside the 27 GB of
+    # 16-bit gradients and working params, 76 GB of the 180 GB; 16 streaming
+    # slots + 4 write-back blocks + 39 host-DRAM tier blobs = 71 GB pinned.
+    ap.add_argument("--pool-slots", type=int, default=16)
+    ap.add_argument("--cache-slots", type=int, default=29,
+                    help="retention capacity C (HBM cache); -1: pool_slots - 3 (reference default)")
     ap.add_argument("--ring", type=int, default=12)
-    ap.add_argument("--hbm-retain", type=int, default=1, help="retained subgroups stay in HBM between phases")
+    ap.add_argument("--hbm-retain", type=int, default=2,
+                    help="0 host retention, 1 HBM retention with a reserved host slot, 2 HBM cache")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--dtype", choices=["f16", "bf16"], default="f16",
                     help="16-bit gradient and working-param kind (f16 = the reference's fp16)")
@@ -688,7 +710,7 @@ def main(argv=None):
         e2e = {"skipped": "the --exchange mode times the device-resident update with the in-phase reduce-scatter"}
     elif not a.skip_e2e:
         try:
-            e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots)
+            e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots, a.hbm_retain)
             if len(e_sizes) < len(sizes) or pool != a.pool_slots:
                 log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank, "
                     f"pool {pool}, cache {cache}")

@@ -312,6 +312,12 @@ OffloadWorker::~OffloadWorker() {
         cudaStreamSynchronize(s_d2h2_);
     }
     {
+        std::lock_guard<std::mutex> g(mu_);
+        wb_stop_ = true;
+    }
+    wb_cv_.notify_all();
+    if (wb_thread_.joinable()) wb_thread_.join();
+    {
         std::lock_guard<std::mutex> g(cq_mu_);
         cq_stop_ = true;
     }
@@ -409,6 +415,13 @@ void OffloadWorker::setup_device() {
             cuda_check(cudaEventCreateWithFlags(&hbm_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
             hbm_free_.push_back(static_cast<int>(b));
         }
+        if (dev_.hbm_retain == 2) {
+            const int nwb = std::min<int>(kWritebackBlocks, std::max<int>(1, cap));
+            for (int b = 0; b < nwb; ++b) {
+                wb_blocks_.push_back(HostBlock::allocate(state_block_bytes_ + annex_bytes_, true));
+                wb_free_.push_back(b);
+            }
+        }
     }
     grad_ptr_.clear();
     p16_ptr_.clear();
@@ -427,6 +440,7 @@ void OffloadWorker::setup_device() {
     }
     device_ready_ = true;
     completer_ = std::thread([this] { completion_loop(); });
+    if (!wb_blocks_.empty()) wb_thread_ = std::thread([this] { writeback_loop(); });
 }
 
 void OffloadWorker::release_device() {
@@ -448,6 +462,8 @@ void OffloadWorker::release_device() {
     hbm_ready_.clear();
     hbm_free_.clear();
     hbm_slot_.clear();
+    wb_blocks_.clear();
+    wb_free_.clear();
     for (float* r : ring_grad_) cudaFree(r);
     ring_grad_.clear();
     if (grad32_dev_) cudaFree(grad32_dev_);
@@ -801,8 +817,9 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
         trace_->record(EventKind::update_start, id_, id, kNoTier, 12 * pc);
         ++in_flight_;
     }
-    // slot < 0 only in HBM cache mode, for a subgroup held in HBM that the plan
-    // retains again: no host transfer either way.
+    // slot < 0 only in HBM cache mode, for a subgroup held in HBM: retained
+    // again it needs no host transfer; flushed, its D2H is deferred to the
+    // write-back thread (wb_pending_).
     static HostBlock no_block;
     const HostBlock& blk = slot >= 0 ? pool_->block(slot) : no_block;
     AdamLaunch a;
@@ -850,8 +867,14 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     int hslot = held;
     bool keep_in_hbm = false;
     if (!hbm_cache_.empty()) {
-        std::lock_guard<std::mutex> g(mu_);
+        std::unique_lock<std::mutex> l(mu_);
         const bool retain = dests_->assign_storage_tier(id).host_retain;
+        // HBM cache mode: a buffer is on its way back from a deferred
+        // write-back; wait for it rather than fall back to the host path.
+        while (retain && hslot < 0 && hbm_free_.empty() && wb_inflight_ > 0) {
+            if (completion_error_) std::rethrow_exception(completion_error_);
+            wb_cv_.wait_for(l, std::chrono::milliseconds(50));
+        }
         if (retain && hslot < 0 && !hbm_free_.empty()) {
             // FIFO: the buffer whose write-back was queued first drains first
             hslot = hbm_free_.front();
@@ -913,6 +936,15 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
     cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
 
+    if (slot < 0 && held >= 0 && !keep_in_hbm) {  // HBM cache mode: the write-back thread takes it
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            wb_pending_.push_back(PendingWriteback{id, k, held});
+            ++wb_inflight_;
+        }
+        wb_cv_.notify_all();
+        return {h2d_bytes, 12 * pc};
+    }
     cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
     cuda_check(cudaEventRecord(e.d2h_start, s_d2h_), "cudaEventRecord");
     if (keep_in_hbm) {
@@ -1002,7 +1034,7 @@ void OffloadWorker::completion_loop() {
             trace_->record(EventKind::update_end, id_, c.id, kNoTier, 12 * sg.param_count);
             const TierAssignment a = dests_->assign_storage_tier(c.id);
             if (!a.host_retain) {
-                start_flush_locked(c.id, a.tier, c.slot);
+                start_flush_locked(c.id, a.tier, c.slot, c.wb);
             } else if (hbm_cache_mode() && hbm_slot_[k] >= 0 && c.slot >= 0) {
                 pool_->evict(c.slot);  // the state lives in HBM: the slot streams again
                 sg.slot = -1;
@@ -1029,15 +1061,6 @@ int OffloadWorker::wait_host_resident(SubgroupId id) {
                 break;
             }
             if (sg.residency == Residency::host_cached) {
-                // HBM cache mode: an HBM-held subgroup this plan flushes needs a
-                // slot to write back into (normally pump_locked reserved it).
-                if (sg.slot < 0 && hbm_cache_mode() && dests_ && !dests_->assign_storage_tier(id).host_retain &&
-                    reserve_writeback_slot_locked(id) < 0) {
-                    l.unlock();
-                    wait_pool_free();
-                    l.lock();
-                    continue;
-                }
                 ++cache_hits_this_phase_;
                 trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
                 need_grad_fetch = !opt_.skip_gradients && grad_tier_.count(id) != 0;
@@ -1144,13 +1167,6 @@ void OffloadWorker::pump_locked() {
     while (frontier_ < order_.size()) {
         const SubgroupId id = order_[frontier_];
         Subgroup& sg = subgroups_.at(id);
-        if (sg.residency == Residency::host_cached && sg.slot < 0 && hbm_cache_mode() && dests_ &&
-            !dests_->assign_storage_tier(id).host_retain) {
-            // HBM-held, flushed this phase: its write-back slot, in plan order
-            if (reserve_writeback_slot_locked(id) < 0) break;
-            ++frontier_;
-            continue;
-        }
         if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) {
             ++frontier_;
             continue;
@@ -1203,30 +1219,53 @@ std::shared_future<IoStats> OffloadWorker::start_prefetch_locked(SubgroupId id, 
     return fut;
 }
 
-std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, TierId dest, int slot) {
+std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, TierId dest, int slot, int wb) {
     if (dest < 0 || static_cast<std::size_t>(dest) >= tiers_.size()) throw Error("flush destination out of range");
     Subgroup& sg = subgroups_.at(id);
     const TierId origin = sg.tier;  // differs from dest when the allocation shifted
     sg.begin_flush();
-    pool_->begin_flush(slot);
+    if (wb < 0) pool_->begin_flush(slot);
     const std::uint64_t pc = sg.param_count;
     auto tier = tiers_[static_cast<std::size_t>(dest)];
-    HostBufferPool* pool = pool_.get();
-    auto transfer = [tier, id, pc, pool, slot] { return tier->write_from(id, pc, pool->block(slot)); };
-    auto completion = [this, id, slot, dest, origin](bool ok, const IoStats& st) {
+    HostBlock* src = wb >= 0 ? &wb_blocks_[static_cast<std::size_t>(wb)] : &pool_->block(slot);
+    // The pool slot's block may be exchanged with a host_dram tier's blob by
+    // write_from; a write-back block likewise (both are owned by the lane /
+    // pool object, not by the pointer's referent).
+    auto transfer = [tier, id, pc, src] { return tier->write_from(id, pc, *src); };
+    auto completion = [this, id, slot, wb, dest, origin](bool ok, const IoStats& st) {
         std::shared_ptr<Tier> stale;
         {
             std::lock_guard<std::mutex> g(mu_);
             Subgroup& s = subgroups_.at(id);
             if (ok) {
                 s.finish_flush(dest);
-                pool_->flush_done(slot);
+                if (wb >= 0) {
+                    wb_free_.push_back(wb);
+                    wb_cv_.notify_all();
+                } else {
+                    pool_->flush_done(slot);
+                }
                 record_write_locked(id, dest, st);
                 if (origin >= 0 && origin != dest) stale = tiers_[static_cast<std::size_t>(origin)];
                 pump_locked();
-            } else {
+            } else if (wb < 0) {
                 s.residency = Residency::host_cached;  // flush failed: the state stays in its slot
                 pool_->flush_failed(slot);
+            } else {
+                // Write-back failed: the state is only in the write-back block.
+                // Adopt it into a free pool slot (block exchange) if one is free.
+                s.residency = Residency::host_cached;
+                const int ps = pool_->try_reserve(id);
+                if (ps >= 0) {
+                    std::swap(pool_->block(ps), wb_blocks_[static_cast<std::size_t>(wb)]);
+                    pool_->prefetch_done(ps);
+                    s.slot = ps;
+                    wb_free_.push_back(wb);
+                    wb_cv_.notify_all();
+                } else if (!completion_error_) {
+                    completion_error_ = std::make_exception_ptr(IoError(
+                        "write-back of subgroup " + std::to_string(id) + " failed and no pool slot is free to hold it"));
+                }
             }
         }
         if (stale) stale->remove_subgroup(id);
@@ -1236,6 +1275,53 @@ std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, Tie
                    .share();
     flush_futures_.emplace_back(id, fut);
     return fut;
+}
+
+// HBM cache mode write-back thread: pairs each deferred hit (kernel issued,
+// state updated in its HBM buffer) with a free write-back block, issues the
+// D2H on its own stream, frees the HBM buffer behind it, and hands the
+// subgroup to the completion thread, which flushes it from the block.
+void OffloadWorker::writeback_loop() {
+    cudaSetDevice(dev_.device);
+    for (;;) {
+        PendingWriteback p{};
+        int wb = -1;
+        {
+            std::unique_lock<std::mutex> l(mu_);
+            wb_cv_.wait(l, [&] { return wb_stop_ || (!wb_pending_.empty() && !wb_free_.empty()); });
+            if (wb_stop_) return;
+            p = wb_pending_.front();
+            wb_pending_.pop_front();
+            wb = wb_free_.front();
+            wb_free_.pop_front();
+        }
+        try {
+            const DeviceEvents& e = events_[p.k];
+            const std::uint64_t pc = subgroups_.at(p.id).param_count;
+            cuda_check(cudaStreamWaitEvent(s_d2h2_, e.k_end, 0), "wait");
+            cuda_check(cudaEventRecord(e.d2h_start, s_d2h2_), "cudaEventRecord");
+            copy_state(hbm_cache_[static_cast<std::size_t>(p.hslot)], wb_blocks_[static_cast<std::size_t>(wb)], pc,
+                       false, s_d2h2_);
+            cuda_check(cudaEventRecord(e.d2h_end, s_d2h2_), "cudaEventRecord");
+            cuda_check(cudaEventRecord(hbm_ready_[static_cast<std::size_t>(p.hslot)], s_d2h2_), "cudaEventRecord");
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                hbm_free_.push_back(p.hslot);
+                hbm_slot_[p.k] = -1;
+                --wb_inflight_;
+            }
+            wb_cv_.notify_all();
+            auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{p.id, -1, wb});
+            cuda_check(cudaLaunchHostFunc(s_d2h2_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
+        } catch (...) {
+            std::lock_guard<std::mutex> g(mu_);
+            if (!completion_error_) completion_error_ = std::current_exception();
+            --wb_inflight_;
+            --in_flight_;
+            inflight_cv_.notify_all();
+            wb_cv_.notify_all();
+        }
+    }
 }
 
 void OffloadWorker::record_read_locked(SubgroupId id, TierId tier, const IoStats& st, bool state_fetch) {

@@ -89,6 +89,9 @@ struct DeviceOptions {
     int hbm_retain = 1;
 };
 
+// HBM cache mode: pinned blocks in the write-back lane.
+constexpr int kWritebackBlocks = 4;
+
 enum class Residency : int { host_cached = 0, in_flight = 1, on_tier = 2 };
 
 struct Subgroup {
@@ -291,17 +294,21 @@ private:
     struct Completion {
         SubgroupId id;
         int slot;
+        int wb = -1;  // HBM cache mode: the write-back block the D2H went to
     };
 
     std::vector<double> placement_bandwidths() const;
     int retention_capacity() const;
     bool hbm_cache_mode() const { return !hbm_cache_.empty() && dev_.hbm_retain == 2; }
-    // HBM cache mode: a slot for an HBM-held subgroup's write-back (no I/O;
-    // the slot goes straight to cached). Called with mu_ held; -1 if none free.
+    // HBM cache mode, op-level flush: a pool slot for an HBM-held subgroup's
+    // write-back (no I/O; the slot goes straight to cached). Called with mu_
+    // held; -1 if none free.
     int reserve_writeback_slot_locked(SubgroupId id);
     void pump_locked();
     std::shared_future<IoStats> start_prefetch_locked(SubgroupId id, int slot);
-    std::shared_future<IoStats> start_flush_locked(SubgroupId id, TierId dest, int slot);
+    // slot >= 0: flush from a pool slot; wb >= 0: from a write-back block.
+    std::shared_future<IoStats> start_flush_locked(SubgroupId id, TierId dest, int slot, int wb = -1);
+    void writeback_loop();
     void record_read_locked(SubgroupId id, TierId tier, const IoStats& st, bool state_fetch);
     void record_write_locked(SubgroupId id, TierId tier, const IoStats& st);
     // ZeRO-3 baseline flow (skip_gradients = false): fp32 gradients through storage.
@@ -365,6 +372,24 @@ private:
     std::vector<cudaEvent_t> hbm_ready_;
     std::deque<int> hbm_free_;
     std::vector<int> hbm_slot_;
+    // HBM cache mode: an HBM-held subgroup the plan flushes is written back
+    // through its own small lane of pinned blocks (D2H -> block -> tier), so
+    // the pool's slots serve only prefetches and the two directions overlap.
+    // The coordinator only issues such a subgroup's kernel; the write-back
+    // thread issues its D2H (on its own stream) once a block is free, then
+    // releases the HBM buffer. Misses' H2D therefore start at phase begin.
+    struct PendingWriteback {
+        SubgroupId id;
+        std::size_t k;
+        int hslot;
+    };
+    std::vector<HostBlock> wb_blocks_;
+    std::deque<int> wb_free_;
+    std::deque<PendingWriteback> wb_pending_;
+    std::condition_variable wb_cv_;   // wb_free_ / wb_pending_ / hbm_free_ changed (with mu_)
+    bool wb_stop_ = false;
+    int wb_inflight_ = 0;  // deferred write-backs whose HBM buffer is not yet free
+    std::thread wb_thread_;
     float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H
     HostBlock grad_stage_;           // baseline flow: pinned D2H staging of fp32 gradients
     std::size_t state_block_bytes_ = 0;  // header + P||m||v of the largest subgroup, 4 KiB multiple

@@ -39,13 +39,21 @@ def test_e2e_shard_fits_host_memory(monkeypatch, world):
     sizes = bench.subgroup_sizes(6_738_415_616, 100_000_000)
     avail = 205 * 2**30
     _meminfo(monkeypatch, avail)
-    sub, pool, cache = bench.e2e_shard(sizes, world, 42, 29)
     block = 12 * max(sizes) + 4096
+    # mode 1: retained subgroups keep a slot, C <= pool - 3
+    sub, pool, cache = bench.e2e_shard(sizes, world, 42, 29, 1)
     assert (pool + len(sub)) * block <= 0.7 * avail / world + block  # every pinned block fits
     assert 1 <= len(sub) <= len(sizes) and sub == sizes[:len(sub)]
-    assert pool >= 4 and 0 <= cache <= max(0, pool - 3) if cache >= 0 else True
+    assert pool >= 4 and 0 <= cache <= max(0, pool - 3)
     if world == 1:
-        assert (len(sub), pool, cache) == (68, 42, 29)  # the bench default fits one rank's host share
+        assert (len(sub), pool, cache) == (68, 42, 29)
+    # mode 2 (HBM cache, the bench default): C in HBM, no host block for it
+    sub, pool, cache = bench.e2e_shard(sizes, world, 16, 29, 2)
+    pinned = pool + bench.WRITEBACK_BLOCKS + len(sub) - cache
+    assert pinned * block <= 0.7 * avail / world + block
+    assert pool >= 4 and cache == len(sub) * 29 // 68  # the retained fraction stays that of the full shard
+    if world == 1:
+        assert (len(sub), pool) == (68, 16)
 
 
 def test_e2e_shard_without_meminfo_keeps_request(monkeypatch):
