@@ -18,10 +18,11 @@ Legs of the `ours` line:
   e2e     the same metric through the engine's C ABI with the state on HOST
           tiers (pinned host DRAM + a local O_DIRECT directory tier): prefetch,
           H2D, fused kernel, D2H, flush/retain inside the timed region.
-  spill   the same metric with host DRAM capped to 8 pinned staging slots and
-          the state on two O_DIRECT directory tiers (local + remote, SURVEY
-          C4), the retention capacity in HBM; bounded sample (<= 12
-          subgroups). Roofline: the tiers' probed bandwidths.
+  spill   the same metric with host DRAM capped (a capacity-capped DRAM tier,
+          8 pinned staging slots) so the state spills to two O_DIRECT
+          directory tiers (local + remote), the retention capacity
+          in HBM; bounded sample (<= 12 subgroups). Roofline: the directory
+          tiers' probed bandwidths.
   cpu_baseline  the reference CPU engine (oracle/_ref: the unmodified
           reference headers compiled in place) on a bounded sample, rank 0.
 --exchange fused|nccl: strong scaling over one model with the gradient
@@ -502,9 +503,10 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
 
 
 # ---------------------------------------------------------------------------
-# leg 3: spill (SURVEY C4 shape): host DRAM capped to a few pinned staging
-# slots, the state on two directory tiers (local "NVMe" + "remote"), the
-# retention capacity held in HBM (hbm_retain=2). Tier-bound; bounded sample.
+# leg 3: spill (SURVEY C4 shape): a capacity-capped host-DRAM tier and a few
+# pinned staging slots, so Eq. 1 spills the state to two directory tiers
+# (local "NVMe" + "remote"); the retention capacity held in HBM
+# (hbm_retain=2). Tier-bound; bounded sample.
 
 
 def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=3, pool=8, ring=4,
@@ -519,6 +521,8 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     M = max(2, min(len(sizes), 12, int(0.5 * free / world // (12 * max(sizes) + 4096))))
     sizes = sizes[:M]
     cache = M // 2
+    dram_cap = max(1, (M - cache) // 3)  # host DRAM capped: Eq. 1 spills the rest to the directory tiers
+    block = 4096 * ((32 + 12 * max(sizes) + 4095) // 4096)
     for d in ("nvme", "remote"):
         (root / d).mkdir()
     # Tiers on one physical device share one semaphore (contention control
@@ -526,11 +530,13 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     # seeking against each other.
     same_device = os.stat(root / "nvme").st_dev == os.stat(root / "remote").st_dev
     lock_dev = 1 if same_device and lock_shared else 0
-    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4,
-                                 lock_device=lock_dev)),
-             tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
-                                 lock_device=lock_dev))]
-    probes = [t.probe_bandwidth(256 << 20, 3) for t in tiers]
+    dirs = [tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4,
+                                lock_device=lock_dev)),
+            tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
+                                lock_device=lock_dev))]
+    probes = [t.probe_bandwidth(256 << 20, 3) for t in dirs]
+    dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=dram_cap * block))
+    tiers = [dram] + dirs
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
     w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2))
@@ -561,7 +567,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     # so a tier needs read/r + write/w; tiers on one physical device add up,
     # independent devices overlap (the Eq. 1 model).
     per_tier = []
-    for i, pr in enumerate(probes):
+    for i, pr in enumerate(probes, start=1):  # tier 0 (host DRAM) moves blocks by exchange: no tier time
         rb = statistics.mean(p[1].tier_obs[i].read_bytes for p in phases)
         wb = statistics.mean(p[1].tier_obs[i].write_bytes for p in phases)
         per_tier.append(dict(read_bytes=rb, write_bytes=wb, read_gbs=round(pr.read_bw / 1e9, 2),
@@ -570,7 +576,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     parallel_s = max(t["seconds"] for t in per_tier)
     bound_s = serial_s if same_device else parallel_s
     return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, pool=pool, same_device=same_device,
-                lock_device=lock_dev,
+                lock_device=lock_dev, dram_cap=dram_cap,
                 bound_ms=bound_s * 1e3, independent_bound_ms=parallel_s * 1e3, per_tier=per_tier,
                 hits=statistics.mean(p[1].cache_hits for p in phases),
                 alloc=phases[-1][1].flush_allocation, launches=steps * M)
@@ -744,10 +750,11 @@ def main(argv=None):
                      "tiers_share_one_device": r["same_device"], "device_semaphore": bool(r["lock_device"]),
                      "per_tier": r["per_tier"],
                      "subgroups_per_rank": r["subgroups"], "hbm_cache_slots": r["cache"], "pool_slots": r["pool"],
+                     "dram_tier_capacity_subgroups": r["dram_cap"],
                      "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"],
                      "gpu_launches": r["launches"],
-                     "path": "C ABI tfg_engine_run_update, tiers [local_dir O_DIRECT, remote_dir O_DIRECT], "
-                             "host DRAM = pinned staging slots only, retention in HBM (hbm_retain=2)"}
+                     "path": "C ABI tfg_engine_run_update, tiers [host_dram capped, local_dir O_DIRECT, "
+                             "remote_dir O_DIRECT], retention in HBM (hbm_retain=2)"}
         except Exception as exc:
             spill = {"error": f"{type(exc).__name__}: {exc}"}
             log(f"spill leg failed: {exc}")

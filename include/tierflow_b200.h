@@ -76,6 +76,8 @@ typedef struct tfg_tier_spec {
     int32_t lock_device;     /* 0: the tier's own semaphore (the reference); k > 0: one semaphore
                                 shared by every tier with the same k, i.e. per physical device,
                                 so tiers on one disk do not contend with concurrent transfers */
+    uint64_t capacity_bytes; /* 0: unlimited (the reference); else the state bytes the tier may hold:
+                                Eq. 1 is capped at capacity / state block bytes subgroups per tier */
 } tfg_tier_spec;
 
 /* ScheduleOptions, scheduler.hpp:32-50. */
@@ -254,6 +256,10 @@ int tfg_synthetic_state(float* p, float* m, float* v, uint64_t n, uint64_t seed,
 /* ---- placement (host, pure) --------------------------------------------- */
 /* assign_subgroups, placement.hpp:30-100. counts_out[n_tiers]. */
 int tfg_assign_subgroups(int M, const double* bandwidths, int n_tiers, int* counts_out);
+/* Capacity-aware Eq. 1 (beyond the reference): caps[i] < 0 unlimited; the
+   reference allocation whenever it fits every cap, else the min-max of T_i/B_i
+   subject to T_i <= caps[i] (water filling). ConfigError if the caps cannot hold M. */
+int tfg_assign_subgroups_capped(int M, const double* bandwidths, const int* caps, int n_tiers, int* counts_out);
 /* DestinationPlan, placement.hpp:178-225: per order position, retain flag and tier. */
 int tfg_destination_plan(const uint32_t* order, int M, int capacity, const double* bandwidths, int n_tiers,
                          int* retain_out, int* tier_out, int* flush_allocation_out);

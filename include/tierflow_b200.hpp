@@ -64,6 +64,7 @@ struct TierSpec {
     int lock_width = 1;
     bool direct_io = true;
     int lock_device = 0;  // > 0: semaphore shared with every tier of the same physical device
+    std::uint64_t capacity_bytes = 0;  // 0: unlimited; caps the subgroups Eq. 1 places here
 };
 
 struct IoStats {
@@ -115,7 +116,7 @@ public:
     explicit Tier(TierSpec spec) : spec_(std::move(spec)) {
         tfg_tier_spec s{spec_.tier_id, static_cast<int32_t>(spec_.kind), spec_.root.c_str(), spec_.read_bw,
                         spec_.write_bw, spec_.io_parallelism, spec_.persistent ? 1 : 0, spec_.lock_width,
-                        spec_.direct_io ? 1 : 0, spec_.lock_device};
+                        spec_.direct_io ? 1 : 0, spec_.lock_device, spec_.capacity_bytes};
         check(tfg_tier_create(&s, &h_));
     }
     ~Tier() { tfg_tier_destroy(h_); }

@@ -62,7 +62,8 @@ class AdamHyperC(C.Structure):
 class TierSpecC(C.Structure):
     _fields_ = [("tier_id", C.c_int32), ("kind", C.c_int32), ("root", C.c_char_p), ("read_bw", C.c_double),
                 ("write_bw", C.c_double), ("io_parallelism", C.c_int32), ("persistent", C.c_int32),
-                ("lock_width", C.c_int32), ("direct_io", C.c_int32), ("lock_device", C.c_int32)]
+                ("lock_width", C.c_int32), ("direct_io", C.c_int32), ("lock_device", C.c_int32),
+                ("capacity_bytes", C.c_uint64)]
 
 
 class ScheduleOptionsC(C.Structure):
@@ -141,6 +142,7 @@ _SIGS = {
     "tfg_synthetic_grads": (_i, [_vp, _u64, _i, _u64, C.c_uint32, _i, _i, _i, _vp]),
     "tfg_synthetic_state": (_i, [_vp, _vp, _vp, _u64, _u64, C.c_uint32, _vp]),
     "tfg_assign_subgroups": (_i, [_i, C.POINTER(_d), _i, C.POINTER(_i)]),
+    "tfg_assign_subgroups_capped": (_i, [_i, C.POINTER(_d), C.POINTER(_i), _i, C.POINTER(_i)]),
     "tfg_destination_plan": (_i, [C.POINTER(C.c_uint32), _i, _i, C.POINTER(_d), _i, C.POINTER(_i), C.POINTER(_i),
                                   C.POINTER(_i)]),
     "tfg_update_order": (_i, [_i, C.POINTER(C.c_uint32), _i, _i, C.POINTER(C.c_uint32)]),

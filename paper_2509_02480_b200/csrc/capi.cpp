@@ -345,6 +345,20 @@ int tfg_assign_subgroups(int M, const double* bandwidths, int n_tiers, int* coun
     });
 }
 
+int tfg_assign_subgroups_capped(int M, const double* bandwidths, const int* caps, int n_tiers, int* counts_out) {
+    return guarded([&] {
+        if (n_tiers > 0) {
+            need(bandwidths, "bandwidths");
+            need(caps, "caps");
+            need(counts_out, "counts_out");
+        }
+        const std::vector<double> b(bandwidths, bandwidths + std::max(n_tiers, 0));
+        const std::vector<int> c(caps, caps + std::max(n_tiers, 0));
+        const auto a = tfb::assign_subgroups_capped(M, b, c);
+        for (int i = 0; i < n_tiers; ++i) counts_out[i] = a.counts[static_cast<std::size_t>(i)];
+    });
+}
+
 int tfg_destination_plan(const uint32_t* order, int M, int capacity, const double* bandwidths, int n_tiers,
                          int* retain_out, int* tier_out, int* flush_allocation_out) {
     return guarded([&] {
@@ -482,6 +496,7 @@ int tfg_tier_create(const tfg_tier_spec* spec, tfg_tier** out) {
         s.direct_io = spec->direct_io != 0;
         if (spec->lock_device < 0) throw tfb::ConfigError("lock_device must be >= 0");
         s.lock_device = spec->lock_device;
+        s.capacity_bytes = spec->capacity_bytes;
         if ((s.kind == tfb::TierKind::local_dir || s.kind == tfb::TierKind::remote_dir) && s.root.empty())
             throw tfb::ConfigError("directory tiers need a root path");
         *out = new tfg_tier{std::make_shared<tfb::Tier>(s)};

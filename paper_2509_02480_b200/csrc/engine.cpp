@@ -354,6 +354,17 @@ std::vector<double> OffloadWorker::placement_bandwidths() const {
     return b;
 }
 
+// Per-tier subgroup capacity for the capacity-aware Eq. 1: the tier's
+// capacity_bytes over the state block of the largest subgroup (-1: unlimited).
+std::vector<int> OffloadWorker::tier_caps() const {
+    std::vector<int> caps;
+    for (const auto& t : tiers_) {
+        const std::uint64_t cb = t->spec().capacity_bytes;
+        caps.push_back(cb == 0 || state_block_bytes_ == 0 ? -1 : static_cast<int>(cb / state_block_bytes_));
+    }
+    return caps;
+}
+
 int OffloadWorker::retention_capacity() const {
     const int M = static_cast<int>(ids_.size());
     if (dev_.hbm_retain == 2 && dev_.zero_copy == 0 && opt_.skip_gradients && opt_.enable_caching) {
@@ -513,7 +524,7 @@ void OffloadWorker::init_and_flush_all(std::uint64_t seed) {
     setup_device();
 
     const std::vector<SubgroupId> order = update_order(0, ids_, false);
-    const DestinationPlan dests(order, 0, placement_bandwidths());
+    const DestinationPlan dests(order, 0, placement_bandwidths(), tier_caps());
     // Generate on the GPU into the ring, copy into a staging slot, persist.
     HostBlock staging = HostBlock::allocate(state_block_bytes_ + annex_bytes_, true);
     for (const SubgroupId id : order) {
@@ -697,7 +708,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
     {
         std::lock_guard<std::mutex> g(mu_);
         const int cap = retention_capacity();
-        dests_ = std::make_unique<DestinationPlan>(order_, cap, placement_bandwidths());
+        dests_ = std::make_unique<DestinationPlan>(order_, cap, placement_bandwidths(), tier_caps());
         stats.retained = dests_->retained_count();
         stats.flush_allocation = dests_->flush_allocation().counts;
         frontier_ = 0;

@@ -299,6 +299,7 @@ private:
 
     std::vector<double> placement_bandwidths() const;
     int retention_capacity() const;
+    std::vector<int> tier_caps() const;
     bool hbm_cache_mode() const { return !hbm_cache_.empty() && dev_.hbm_retain == 2; }
     // HBM cache mode, op-level flush: a pool slot for an HBM-held subgroup's
     // write-back (no I/O; the slot goes straight to cached). Called with mu_

@@ -93,6 +93,42 @@ inline AllocationVector assign_subgroups(int M, const std::vector<double>& bw) {
     return a;
 }
 
+// Capacity-aware Eq. 1, beyond the reference (whose harness instead requires
+// every tier to hold the whole state, harness.hpp:136-150): caps[i] < 0 is
+// unlimited. When the reference allocation fits every cap it is returned
+// unchanged, so placement stays bit-identical to the reference whenever no cap
+// binds. Otherwise max T_i/B_i is minimised subject to T_i <= cap_i by water
+// filling: each subgroup goes to the tier with room whose (T_i+1)/B_i is
+// smallest (ties: higher bandwidth, then lower id), which is optimal for this
+// bottleneck objective.
+inline AllocationVector assign_subgroups_capped(int M, const std::vector<double>& bw, const std::vector<int>& caps) {
+    AllocationVector a = assign_subgroups(M, bw);
+    const std::size_t N = bw.size();
+    auto room = [&](std::size_t i) {
+        return i < caps.size() && caps[i] >= 0 ? caps[i] : std::numeric_limits<int>::max();
+    };
+    bool fits = true;
+    for (std::size_t i = 0; i < N; ++i) fits = fits && a.counts[i] <= room(i);
+    if (fits) return a;
+    a.counts.assign(N, 0);
+    for (int k = 0; k < M; ++k) {
+        std::size_t pick = N;
+        double best = std::numeric_limits<double>::infinity();
+        for (std::size_t i = 0; i < N; ++i) {
+            if (!(bw[i] > 0.0) || a.counts[i] >= room(i)) continue;
+            const double r = (a.counts[i] + 1) / bw[i];
+            if (r < best || (r == best && bw[i] > bw[pick])) {
+                pick = i;
+                best = r;
+            }
+        }
+        if (pick == N)
+            throw ConfigError("tier capacities cannot hold " + std::to_string(M) + " subgroups");
+        ++a.counts[pick];
+    }
+    return a;
+}
+
 struct TierObservation {
     std::uint64_t read_transfers = 0;
     double read_bytes = 0.0;
@@ -151,13 +187,15 @@ struct TierAssignment {
 
 class DestinationPlan {
 public:
-    DestinationPlan(const std::vector<SubgroupId>& order, int capacity, const std::vector<double>& bw) {
+    // tier_caps: per-tier subgroup capacity (< 0 or absent: unlimited).
+    DestinationPlan(const std::vector<SubgroupId>& order, int capacity, const std::vector<double>& bw,
+                    const std::vector<int>& tier_caps = {}) {
         const int M = static_cast<int>(order.size());
         retained_ = std::clamp(capacity, 0, M);
         const int flushed = M - retained_;
         alloc_.counts.assign(bw.size(), 0);
         alloc_.total = flushed;
-        if (flushed > 0) alloc_ = assign_subgroups(flushed, bw);
+        if (flushed > 0) alloc_ = assign_subgroups_capped(flushed, bw, tier_caps);
         std::vector<int> quota = alloc_.counts;
         for (int k = 0; k < M; ++k) {
             const SubgroupId sg = order[static_cast<std::size_t>(k)];

@@ -50,6 +50,7 @@ struct TierSpec {
     int lock_width = 1;      // tier semaphore width (1 = exclusive, the reference)
     bool direct_io = true;   // O_DIRECT on the engine path when the filesystem allows
     int lock_device = 0;     // 0: own semaphore; k > 0: shared by all tiers with the same k
+    std::uint64_t capacity_bytes = 0;  // 0: unlimited; caps the subgroups Eq. 1 places here
 };
 
 struct ProbeResult {

@@ -98,6 +98,8 @@ class TierSpec:
     # 0: own semaphore (reference); k > 0: shared by all tiers with the same k
     # (one physical device)
     lock_device: int = 0
+    # 0: unlimited (reference); else the state bytes the tier may hold
+    capacity_bytes: int = 0
 
 
 @dataclass
@@ -231,6 +233,19 @@ def assign_subgroups(M: int, bandwidths: Sequence[float]) -> AllocationVector:
     bw = (C.c_double * max(n, 1))(*bandwidths)
     out = (C.c_int * max(n, 1))()
     _lib.call("tfg_assign_subgroups", M, bw, n, out)
+    return AllocationVector(list(out)[:n], M)
+
+
+def assign_subgroups_capped(M: int, bandwidths: Sequence[float], caps: Sequence[int]) -> AllocationVector:
+    """Capacity-aware Eq. 1 (caps[i] < 0: unlimited); the reference allocation
+    whenever it fits every cap."""
+    n = len(bandwidths)
+    if len(caps) != n:
+        raise ConfigError("one cap per tier")
+    bw = (C.c_double * max(n, 1))(*bandwidths)
+    cp = (C.c_int * max(n, 1))(*caps)
+    out = (C.c_int * max(n, 1))()
+    _lib.call("tfg_assign_subgroups_capped", M, bw, cp, n, out)
     return AllocationVector(list(out)[:n], M)
 
 
@@ -377,7 +392,7 @@ class Tier:
         self._root = (spec.root or "").encode()
         cs = _lib.TierSpecC(spec.tier_id, int(spec.kind), self._root, spec.read_bw, spec.write_bw,
                             spec.io_parallelism, int(spec.persistent), spec.lock_width, int(spec.direct_io),
-                            spec.lock_device)
+                            spec.lock_device, spec.capacity_bytes)
         h = C.c_void_p()
         _lib.call("tfg_tier_create", C.byref(cs), C.byref(h))
         self._h = h

@@ -473,3 +473,40 @@ def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
     assert np.array_equal(got.view(np.uint32), want[3][0])
     assert np.array_equal(w.read_current_state(3).view(np.uint32), want[3][0])
     w.close()
+
+
+def test_capacity_capped_tier_spills_and_keeps_bits(tf, cuda, lock_dir, tmp_path):
+    """TierSpec.capacity_bytes ("host DRAM capped"): the host-DRAM
+    tier holds at most its capacity in subgroups; Eq. 1 spills the rest to
+    the other tiers by bandwidth; the state bits do not depend on placement."""
+    params = [60_000] * 7 + [33_333]
+    seed = 41
+    block = 4096 * ((32 + 12 * 60_000 + 4095) // 4096)  # header + P||m||v of the largest, 4 KiB pages
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=2 * block)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.mem_throttled, "nvme", 400e6, 400e6)),
+             tf.Tier(tf.TierSpec(2, tf.TierKind.local_dir, str(tmp_path / "remote"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=4, lock_dir=lock_dir), tf.AdamHyper(), trace,
+                         tf.DeviceOptions(0, 0, 0, 3))
+    w.set_fixed_ratio([10.0, 2.0, 1.0])  # uncapped Eq. 1 would put most of the state on tier 0
+    assert tf.assign_subgroups(7, [10.0, 2.0, 1.0]).counts[0] > 2
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    host, per_tier = w.residency_census()
+    assert per_tier[0] <= 2 * 60_000 and sum(per_tier) == sum(params)
+    for it in range(3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        st = w.run_update(it)
+        assert st.flush_allocation == tf.assign_subgroups_capped(len(params) - st.retained, [10.0, 2.0, 1.0],
+                                                                 [2, -1, -1]).counts
+        assert st.flush_allocation[0] <= 2
+        host, per_tier = w.residency_census()
+        assert per_tier[0] <= 2 * 60_000
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(3):
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32))
+        assert np.array_equal(w.read_params16(sg), p16)
+    w.close()

@@ -1,6 +1,7 @@
 """Product placement/ordering functions (C ABI, host) against the oracle and
 the reference known answers. CPU only."""
 import numpy as np
+import pytest
 
 import oracle
 
@@ -133,3 +134,52 @@ def test_paper_scale_placement_matches_oracle_and_reference(tf):
                 assert R.ref_destination_plan(np.asarray(order, np.uint32), M, cap, np.asarray(bw, np.float64),
                                               len(bw), rr, tt, aa) == 0
                 assert rr.tolist() == r and tt.tolist() == t and aa.tolist() == a
+
+
+def _brute_capped(M, bw, caps):
+    """min over T (sum M, T_i <= caps_i, T_i = 0 where B_i = 0) of max T_i/B_i."""
+    import itertools
+    N = len(bw)
+    best = None
+    ranges = [range(0, (min(M, c) if c >= 0 else M) + 1) if b > 0 else range(1) for b, c in zip(bw, caps)]
+    for T in itertools.product(*ranges):
+        if sum(T) != M:
+            continue
+        v = max(T[i] / bw[i] for i in range(N) if bw[i] > 0)
+        best = v if best is None else min(best, v)
+    return best
+
+
+def test_capped_eq1_equals_reference_when_caps_do_not_bind(tf):
+    rng = np.random.default_rng(23)
+    for _ in range(300):
+        N = int(rng.integers(1, 4))
+        M = int(rng.integers(1, 120))
+        bw = [float(x) for x in 10 ** rng.uniform(-1, 1, N)]
+        ref = oracle.assign_subgroups(M, bw)
+        caps = [c + int(rng.integers(0, 5)) if rng.random() < 0.7 else -1 for c in ref]
+        assert tf.assign_subgroups_capped(M, bw, caps).counts == ref
+
+
+def test_capped_eq1_respects_caps_and_is_minmax_optimal(tf):
+    rng = np.random.default_rng(29)
+    checked = 0
+    for _ in range(400):
+        N = int(rng.integers(2, 4))
+        M = int(rng.integers(1, 25))
+        bw = [float(x) for x in 10 ** rng.uniform(-1, 1, N)]
+        caps = [int(rng.integers(0, M + 1)) if rng.random() < 0.6 else -1 for _ in range(N)]
+        room = sum(M if c < 0 else c for c in caps)
+        if room < M:
+            with pytest.raises(tf.ConfigError):
+                tf.assign_subgroups_capped(M, bw, caps)
+            continue
+        got = tf.assign_subgroups_capped(M, bw, caps).counts
+        assert sum(got) == M
+        assert all(c < 0 or g <= c for g, c in zip(got, caps))
+        opt = _brute_capped(M, bw, caps)
+        assert max(g / b for g, b in zip(got, bw) if b > 0) == pytest.approx(opt, rel=1e-12)
+        checked += 1
+    assert checked > 100
+    # C4-style: a fast host-DRAM tier capped, the rest spills to NVMe and remote by bandwidth
+    assert tf.assign_subgroups_capped(690, [50.0, 6.9, 3.6], [100, -1, -1]).counts == [100, 388, 202]
