@@ -104,3 +104,68 @@ int main() {
                     "-L", str(lib), "-ltierflow_b200", f"-Wl,-rpath,{lib}"], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0 and "adapter ok" in out.stdout, (out.returncode, out.stdout, out.stderr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("hbm", [1, 2])
+def test_cxx_adapter_runs_the_engine_on_the_gpu(tf, cuda, tmp_path, hbm):
+    """The drop-in as a reference-style C++ caller would use it: tiers, the
+    engine, add_subgroup, init_and_flush_all, backward + run_update per
+    iteration, read_current_state; the state bits equal the oracle's."""
+    import numpy as np
+
+    import oracle
+    lib = ROOT / "paper_2509_02480_b200" / "lib"
+    params = [70_001, 40_000, 65_536, 12_345]
+    seed, iters = 9, 3
+    src = tmp_path / "engine.cpp"
+    src.write_text(r'''
+#include "tierflow_b200.hpp"
+#include <cstdio>
+#include <memory>
+using namespace tierflow_b200;
+int main(int argc, char** argv) {
+    const std::uint64_t params[] = {70001, 40000, 65536, 12345};
+    TierSpec d; d.tier_id = 0; d.kind = TierKind::host_dram; d.root = "dram"; d.read_bw = 20e9; d.write_bw = 20e9;
+    TierSpec n; n.tier_id = 1; n.kind = TierKind::local_dir; n.root = argv[1]; n.read_bw = 2e9; n.write_bw = 2e9;
+    std::vector<std::shared_ptr<Tier>> tiers{std::make_shared<Tier>(d), std::make_shared<Tier>(n)};
+    ScheduleOptions o; o.pool_slots = 4; o.cache_slots = 2; o.lock_dir = argv[2];
+    DeviceOptions dev; dev.hbm_retain = ''' + str(hbm) + r''';
+    EventTrace trace;
+    OffloadWorker w(0, tiers, o, AdamHyper{}, trace, dev);
+    w.set_fixed_ratio({1.0, 1.0});
+    for (int i = 0; i < 4; ++i) w.add_subgroup(i, params[i]);
+    w.init_and_flush_all(''' + str(seed) + r''');
+    unsigned long long hits = 0;
+    for (int it = 0; it < ''' + str(iters) + r'''; ++it) {
+        w.run_backward_sim(it, ''' + str(seed) + r''', 1);
+        if (!w.gradients_finite()) return 5;
+        hits += w.run_update(it).cache_hits;
+    }
+    FILE* f = std::fopen(argv[3], "wb");
+    for (int i = 0; i < 4; ++i) {
+        const auto s = w.read_current_state(i);
+        std::fwrite(s.data(), sizeof(float), s.size(), f);
+    }
+    std::fclose(f);
+    std::printf("hits %llu\n", hits);
+    return 0;
+}
+''')
+    exe = tmp_path / "engine"
+    subprocess.run(["g++", "-std=c++20", "-Wall", "-Werror", "-I", str(ROOT / "include"), str(src), "-o", str(exe),
+                    "-L", str(lib), "-ltierflow_b200", f"-Wl,-rpath,{lib}"], check=True)
+    out_bin = tmp_path / "state.bin"
+    (tmp_path / "locks").mkdir()
+    r = subprocess.run([str(exe), str(tmp_path / "nvme"), str(tmp_path / "locks"), str(out_bin)],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
+    assert r.stdout.strip() == "hits 4"  # C = 2 hits in each of the last two phases
+    got = np.fromfile(out_bin, dtype=np.uint32)
+    want = []
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(iters):
+            p, m, v, _, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        want.append(np.concatenate([p, m, v]).view(np.uint32))
+    assert np.array_equal(got, np.concatenate(want))
