@@ -129,7 +129,7 @@ int main(int argc, char** argv) {
     TierSpec d; d.tier_id = 0; d.kind = TierKind::host_dram; d.root = "dram"; d.read_bw = 20e9; d.write_bw = 20e9;
     TierSpec n; n.tier_id = 1; n.kind = TierKind::local_dir; n.root = argv[1]; n.read_bw = 2e9; n.write_bw = 2e9;
     std::vector<std::shared_ptr<Tier>> tiers{std::make_shared<Tier>(d), std::make_shared<Tier>(n)};
-    ScheduleOptions o; o.pool_slots = 4; o.cache_slots = 2; o.lock_dir = argv[2];
+    ScheduleOptions o; o.pool_slots = 5; o.cache_slots = 2; o.lock_dir = argv[2];
     DeviceOptions dev; dev.hbm_retain = ''' + str(hbm) + r''';
     EventTrace trace;
     OffloadWorker w(0, tiers, o, AdamHyper{}, trace, dev);
