@@ -510,3 +510,38 @@ def test_capacity_capped_tier_spills_and_keeps_bits(tf, cuda, lock_dir, tmp_path
         assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32))
         assert np.array_equal(w.read_params16(sg), p16)
     w.close()
+
+
+@pytest.mark.parametrize("hbm", [2])
+def test_full_size_subgroups_bit_exact(tf, cuda, lock_dir, tmp_path, hbm):
+    """BASELINE shapes at full size: a 100M-param subgroup and the 7B shape's
+    ragged last one (38,415,616), through host DRAM and an O_DIRECT directory
+    tier with HBM retention, bit-exact against the oracle after 3 phases."""
+    params = [100_000_000, 38_415_616]
+    seed, iters = 42, 3
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "nvme"), 4e9, 4e9, io_parallelism=4))]
+    opt = (tf.ScheduleOptions(pool_slots=3, cache_slots=1, lock_dir=lock_dir) if hbm == 2 else
+           tf.ScheduleOptions(pool_slots=4, lock_dir=lock_dir))
+    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    w.set_fixed_ratio([1.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    hits = []
+    for it in range(iters):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        hits.append(w.run_update(it).cache_hits)
+    assert hits == [0, 1, 1]
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(iters):
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        got = w.read_current_state(sg).view(np.uint32)
+        assert np.array_equal(got[:n], p.view(np.uint32)), f"subgroup {sg} P"
+        assert np.array_equal(got[n:2 * n], m.view(np.uint32)), f"subgroup {sg} m"
+        assert np.array_equal(got[2 * n:], v.view(np.uint32)), f"subgroup {sg} v"
+        assert np.array_equal(w.read_params16(sg), p16), f"subgroup {sg} params16"
+        del p, m, v, p16, got
+    w.close()
