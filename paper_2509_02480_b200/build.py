@@ -26,7 +26,7 @@ CUDA_HOME = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
-CU_SOURCES = ["kernels.cu", "adam_kernel.cu"]
+CU_SOURCES = ["kernels.cu", "adam_kernel.cu", "adam_variants.cu"]
 CXX_SOURCES = ["tier.cpp", "engine.cpp", "capi.cpp"]
 
 

@@ -1,0 +1,356 @@
+// The fused update-phase kernel as a template, shared by the shipped launch
+// path (adam_kernel.cu) and the tuning variants (adam_variants.cu).
+//
+// One HBM pass per subgroup replaces upscale_f16_to_f32 -> adam_step ->
+// downscale_f32_to_f16 (reference scheduler.hpp:467, 479, 490): read P, m, v
+// (fp32) and the 16-bit gradient, widen, bias-corrected Adam/AdamW in binary64
+// (bit-exact with optimizer.hpp:91-108), write P, m, v and the 16-bit working
+// params, and count non-finite gradients and narrowing overflows.
+// 28 algorithmic bytes per parameter. Everything here has internal linkage
+// (anonymous namespace): each including translation unit instantiates its own.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+#include "launch_util.cuh"
+#include "numerics.cuh"
+
+namespace tfb {
+namespace {
+
+using namespace detail;
+
+// Gradient sources of one launch. GMODE 0: one 16-bit buffer (GK = F16 or
+// BF16). GMODE 1: one fp32 buffer (GK = F32; the ZeRO-3 baseline flow that
+// fetches fp32 gradients from storage). GMODE 2: the sum of n 16-bit buffers,
+// e.g. the same subgroup's gradient contributions in every data-parallel
+// peer's memory over NVLink: summed in fp32 in source order, rounded once to
+// GK — the reduce-scatter fused into the update. NS > 0 fixes n at compile
+// time (the 2/4/8-rank cases: unrolled loads, no per-source predicates);
+// NS = 0 reads gs.n at run time.
+struct GradSources {
+    const void* src[kMaxGradSources];
+    int n;
+};
+
+// In-order fp32 sum of one quad over the sources, rounded once to GK.
+template <int GK, int NS>
+__device__ __forceinline__ U16x4 sum_quad16(const GradSources& gs, uint64_t q) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    auto add = [&](const U16x4& x) {
+        acc.x = __fadd_rn(acc.x, widen16<GK>(x.x));
+        acc.y = __fadd_rn(acc.y, widen16<GK>(x.y));
+        acc.z = __fadd_rn(acc.z, widen16<GK>(x.z));
+        acc.w = __fadd_rn(acc.w, widen16<GK>(x.w));
+    };
+    if constexpr (NS > 0) {
+        U16x4 x[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)  // all loads first: NS independent streams in flight
+            x[s] = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) add(x[s]);
+    } else {
+#pragma unroll
+        for (int s = 0; s < kMaxGradSources; ++s)
+            if (s < gs.n) add(load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q));
+    }
+    U16x4 h;
+    h.x = narrow16<GK>(acc.x);
+    h.y = narrow16<GK>(acc.y);
+    h.z = narrow16<GK>(acc.z);
+    h.w = narrow16<GK>(acc.w);
+    return h;
+}
+
+// Register form of one gradient quad: 16-bit sources stay packed (2
+// registers; a summed quad is held already rounded) and are widened at use;
+// fp32 sources (GMODE 1) hold floats.
+template <int GK, int GMODE, int NS>
+struct GradReg {
+    U16x4 h;
+    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
+        if constexpr (GMODE == 0)
+            h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
+        else
+            h = sum_quad16<GK, NS>(gs, q);
+        nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
+    }
+    __device__ __forceinline__ float get(int k) const {
+        return widen16<GK>(k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w);
+    }
+};
+
+template <int GK, int NS>
+struct GradReg<GK, 1, NS> {
+    float4 f;
+    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
+        f = __ldcs(reinterpret_cast<const float4*>(gs.src[0]) + q);
+        nonfinite += !isfinite(f.x) + !isfinite(f.y) + !isfinite(f.z) + !isfinite(f.w);
+    }
+    __device__ __forceinline__ float get(int k) const { return k == 0 ? f.x : k == 1 ? f.y : k == 2 ? f.z : f.w; }
+};
+
+template <int GK, int GMODE>
+__device__ __forceinline__ float load_grad1(const GradSources& gs, uint64_t i, unsigned& nonfinite) {
+    if constexpr (GMODE == 1) {
+        const float f = __ldcs(reinterpret_cast<const float*>(gs.src[0]) + i);
+        nonfinite += !isfinite(f);
+        return f;
+    } else {
+        uint16_t h;
+        if constexpr (GMODE == 0) {
+            h = __ldcs(reinterpret_cast<const uint16_t*>(gs.src[0]) + i);
+        } else {
+            float acc = 0.f;
+#pragma unroll
+            for (int s = 0; s < kMaxGradSources; ++s)
+                if (s < gs.n) acc = __fadd_rn(acc, widen16<GK>(__ldcs(reinterpret_cast<const uint16_t*>(gs.src[s]) + i)));
+            h = narrow16<GK>(acc);
+        }
+        nonfinite += nonfinite16<GK>(h);
+        return widen16<GK>(h);
+    }
+}
+
+// Where one launch reads and writes the fp32 state. In place (in == out) for
+// the device ring and the HBM-resident path; out may instead be mapped pinned
+// host memory, which fuses the D2H write-back into the kernel's epilogue.
+struct StateIO {
+    const float* p;
+    const float* m;
+    const float* v;
+    float* po;
+    float* mo;
+    float* vo;
+};
+
+// VEC = true: P, m, v 16-byte aligned and the gradient / p16 streams 8-byte
+// (16-bit) or 16-byte (fp32) aligned; the body walks quads (float4 / 4 x
+// 16-bit) and the n % 4 tail is scalar. VEC = false: scalar everywhere (e.g.
+// a contiguous P||m||v with P % 4 != 0). Loads and stores are explicit
+// evict-first intrinsics, issued in program order per element, so in-place
+// aliasing of in and out is well defined.
+// DIVC selects the element math: 0 = div.rn quotients, 1 = constant-divisor
+// quotients, 2 = verified fast path (numerics.cuh adam_element_fast), 3 =
+// constant-divisor quotients with the quad's elements walked one at a time.
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// PF > 0: one thread per CTA asks the TMA unit to pull the CTA's chunk PF
+// grid-stride iterations ahead into L2 (cp.async.bulk.prefetch), so more bytes
+// are in flight than the registers of 32 warps per SM can hold.
+template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0, int PF = 0>
+__global__ void __launch_bounds__(kThreads, MINB)
+    adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
+                      unsigned long long* __restrict__ counters) {
+    unsigned nonfinite = 0, overflow = 0;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+
+    if constexpr (VEC) {
+        const uint64_t nq = n / 4;
+        const float4* p4 = reinterpret_cast<const float4*>(io.p);
+        const float4* m4 = reinterpret_cast<const float4*>(io.m);
+        const float4* v4 = reinterpret_cast<const float4*>(io.v);
+        float4* po4 = reinterpret_cast<float4*>(io.po);
+        float4* mo4 = reinterpret_cast<float4*>(io.mo);
+        float4* vo4 = reinterpret_cast<float4*>(io.vo);
+        for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
+            if constexpr (PF > 0) {
+                if (threadIdx.x == 0) {
+                    const uint64_t cq = base + static_cast<uint64_t>(PF) * UNROLL * nthreads;
+                    if (cq < nq) {
+                        const uint64_t nqc = min(static_cast<uint64_t>(blockDim.x) * UNROLL, nq - cq);
+                        prefetch_l2(p4 + cq, static_cast<uint32_t>(16 * nqc));
+                        prefetch_l2(m4 + cq, static_cast<uint32_t>(16 * nqc));
+                        prefetch_l2(v4 + cq, static_cast<uint32_t>(16 * nqc));
+                        if constexpr (GMODE == 0) {
+                            const uint16_t* g = reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * cq;
+                            const uint32_t gb = static_cast<uint32_t>(8 * nqc) & ~15u;
+                            if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0 && gb > 0) prefetch_l2(g, gb);
+                        }
+                    }
+                }
+            }
+            float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
+            GradReg<GK, GMODE, NS> rg[UNROLL];
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {  // all loads first: UNROLL quads in flight
+                const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
+                if (q < nq) {
+                    rp[u] = __ldcs(p4 + q);
+                    rm[u] = __ldcs(m4 + q);
+                    rv[u] = __ldcs(v4 + q);
+                    rg[u].load(gs, q, nonfinite);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < UNROLL; ++u) {
+                const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
+                if (q < nq) {
+                    if constexpr (DIVC == 3) {
+                        // one element at a time (no cross-element ILP, fewer
+                        // live registers): rotate the quad through .x
+                        float g4[4] = {rg[u].get(0), rg[u].get(1), rg[u].get(2), rg[u].get(3)};
+                        float gx = g4[0], gy = g4[1], gz = g4[2], gw = g4[3];
+#pragma unroll 1
+                        for (int k = 0; k < 4; ++k) {
+                            adam_math<WD, 1>(rp[u].x, rm[u].x, rv[u].x, gx, c);
+                            const float tp = rp[u].x, tm = rm[u].x, tv = rv[u].x, tg = gx;
+                            rp[u].x = rp[u].y; rp[u].y = rp[u].z; rp[u].z = rp[u].w; rp[u].w = tp;
+                            rm[u].x = rm[u].y; rm[u].y = rm[u].z; rm[u].z = rm[u].w; rm[u].w = tm;
+                            rv[u].x = rv[u].y; rv[u].y = rv[u].z; rv[u].z = rv[u].w; rv[u].w = tv;
+                            gx = gy; gy = gz; gz = gw; gw = tg;
+                        }
+                    } else {
+                        adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
+                        adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
+                        adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
+                        adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
+                    }
+                    U16x4 h;
+                    h.x = narrow16<OK>(rp[u].x);
+                    h.y = narrow16<OK>(rp[u].y);
+                    h.z = narrow16<OK>(rp[u].z);
+                    h.w = narrow16<OK>(rp[u].w);
+                    overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
+                    __stcs(po4 + q, rp[u]);
+                    __stcs(mo4 + q, rm[u]);
+                    __stcs(vo4 + q, rv[u]);
+                    store_u16x4(p16 + 4 * q, h);
+                }
+            }
+        }
+        const uint64_t i = nq * 4 + tid;  // scalar tail: n % 4 elements
+        if (i < n) {
+            float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
+            const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
+            adam_math<WD, DIVC == 3 ? 1 : DIVC>(pf, mf, vf, gf, c);
+            const uint16_t h = narrow16<OK>(pf);
+            overflow += is_inf16<OK>(h);
+            __stcs(io.po + i, pf);
+            __stcs(io.mo + i, mf);
+            __stcs(io.vo + i, vf);
+            p16[i] = h;
+        }
+    } else {
+        for (uint64_t i = tid; i < n; i += nthreads) {
+            float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
+            const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
+            adam_math<WD, DIVC == 3 ? 1 : DIVC>(pf, mf, vf, gf, c);
+            const uint16_t h = narrow16<OK>(pf);
+            overflow += is_inf16<OK>(h);
+            __stcs(io.po + i, pf);
+            __stcs(io.mo + i, mf);
+            __stcs(io.vo + i, vf);
+            p16[i] = h;
+        }
+    }
+    if (counters != nullptr) {
+        warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+template <int UNROLL, int DIVC, int MINB, int PF = 0>
+struct Cfg {
+    static constexpr int kUnroll = UNROLL;
+    static constexpr int kDivc = DIVC;
+    static constexpr int kMinBlocks = MINB;
+    static constexpr int kPrefetch = PF;
+};
+
+GradSources sources_of(const AdamLaunch& a) {
+    GradSources gs{};
+    if (a.n_peers > 0) {
+        for (int s = 0; s < a.n_peers; ++s) gs.src[s] = a.peers[s];
+        gs.n = a.n_peers;
+    } else {
+        gs.src[0] = a.g;
+        gs.n = 1;
+    }
+    return gs;
+}
+
+StateIO state_io(const AdamLaunch& a) {
+    return StateIO{a.p, a.m, a.v, a.p_out ? a.p_out : a.p, a.m_out ? a.m_out : a.m, a.v_out ? a.v_out : a.v};
+}
+
+bool is_vec(const AdamLaunch& a) {
+    const StateIO io = state_io(a);
+    const uintptr_t state = reinterpret_cast<uintptr_t>(io.p) | reinterpret_cast<uintptr_t>(io.m) |
+                            reinterpret_cast<uintptr_t>(io.v) | reinterpret_cast<uintptr_t>(io.po) |
+                            reinterpret_cast<uintptr_t>(io.mo) | reinterpret_cast<uintptr_t>(io.vo);
+    uintptr_t grads = 0;
+    const GradSources gs = sources_of(a);
+    for (int s = 0; s < gs.n; ++s) grads |= reinterpret_cast<uintptr_t>(gs.src[s]);
+    const uintptr_t galign = a.grad_kind == kF32 ? 15u : 7u;
+    return (state & 15u) == 0 && (grads & galign) == 0 && (reinterpret_cast<uintptr_t>(a.p16) & 7u) == 0;
+}
+
+template <int GK, int GMODE, int OK, bool WD, class C, int NS = 0>
+cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
+    constexpr int U = C::kUnroll;
+    constexpr int B = C::kMinBlocks;
+    const GradSources gs = sources_of(a);
+    if (is_vec(a)) {
+        const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
+        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS, C::kPrefetch>
+            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
+    } else {
+        const unsigned grid = grid_for(a.n, B);
+        adam_fused_kernel<GK, GMODE, OK, WD, false, 1, C::kDivc, B>
+            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
+    }
+    return cudaGetLastError();
+}
+
+template <int GK, int GMODE, int OK, class C, int NS = 0>
+cudaError_t launch_wd(const AdamLaunch& a, cudaStream_t stream) {
+    return a.c.lr_wd != 0.0 ? launch_cfg<GK, GMODE, OK, true, C, NS>(a, stream)
+                            : launch_cfg<GK, GMODE, OK, false, C, NS>(a, stream);
+}
+
+// Summed sources: a compile-time source count (unrolled loads, no
+// per-source predicates) measured at 0.92-0.93 of the HBM roofline for 1, 2
+// and 4 sources against 0.75-0.77 for the run-time loop
+// (profiles/multi_sweep_r1.json).
+template <int GK, int OK, class C>
+cudaError_t launch_sum(const AdamLaunch& a, cudaStream_t stream) {
+    switch (a.n_peers) {
+        case 1: return launch_wd<GK, 2, OK, C, 1>(a, stream);
+        case 2: return launch_wd<GK, 2, OK, C, 2>(a, stream);
+        case 3: return launch_wd<GK, 2, OK, C, 3>(a, stream);
+        case 4: return launch_wd<GK, 2, OK, C, 4>(a, stream);
+        case 5: return launch_wd<GK, 2, OK, C, 5>(a, stream);
+        case 6: return launch_wd<GK, 2, OK, C, 6>(a, stream);
+        case 7: return launch_wd<GK, 2, OK, C, 7>(a, stream);
+        case 8: return launch_wd<GK, 2, OK, C, 8>(a, stream);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <class C>
+cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
+    if (a.out_kind != kF16 && a.out_kind != kBF16) return cudaErrorInvalidValue;
+    if (a.n_peers > 0) {  // fused multi-source reduction: 16-bit sources, same kind in and out
+        if (a.n_peers > kMaxGradSources || a.grad_kind == kF32) return cudaErrorInvalidValue;
+        if (a.grad_kind == kF16)
+            return a.out_kind == kF16 ? launch_sum<kF16, kF16, C>(a, stream) : launch_sum<kF16, kBF16, C>(a, stream);
+        return a.out_kind == kF16 ? launch_sum<kBF16, kF16, C>(a, stream) : launch_sum<kBF16, kBF16, C>(a, stream);
+    }
+    if (a.grad_kind == kF32)
+        return a.out_kind == kF16 ? launch_wd<kF32, 1, kF16, C>(a, stream) : launch_wd<kF32, 1, kBF16, C>(a, stream);
+    if (a.grad_kind == kF16 && a.out_kind == kF16) return launch_wd<kF16, 0, kF16, C>(a, stream);
+    if (a.grad_kind == kF16 && a.out_kind == kBF16) return launch_wd<kF16, 0, kBF16, C>(a, stream);
+    if (a.grad_kind == kBF16 && a.out_kind == kF16) return launch_wd<kBF16, 0, kF16, C>(a, stream);
+    return launch_wd<kBF16, 0, kBF16, C>(a, stream);
+}
+
+}  // namespace
+}  // namespace tfb

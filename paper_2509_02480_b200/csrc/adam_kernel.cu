@@ -1,761 +1,18 @@
-// The hot kernel of the update phase: fused upscale -> Adam -> downscale.
+// The hot kernel of the update phase: fused upscale -> Adam -> downscale,
+// launched in its shipped configuration (adam_fused.cuh holds the template;
+// the measured alternatives live in adam_variants.cu).
 //
-// One HBM pass per subgroup replaces upscale_f16_to_f32 -> adam_step ->
-// downscale_f32_to_f16 (reference scheduler.hpp:467, 479, 490): read P, m, v
-// (fp32) and the 16-bit gradient, widen, bias-corrected Adam/AdamW in binary64
-// (bit-exact with optimizer.hpp:91-108), write P, m, v and the 16-bit working
-// params, and count non-finite gradients and narrowing overflows.
 // 28 algorithmic bytes per parameter; the kernel is HBM-bound when the
 // binary64 element math (~45 FP64 + ~12 XU instructions per element) and
-// the memory latency are both hidden — hence the variants below, which trade
-// per-thread unroll (independent loads in flight) against occupancy.
+// the memory latency are both hidden.
 #include <cuda_runtime.h>
 
 #include <cstdint>
 
-#include "kernels.hpp"
-#include "launch_util.cuh"
-#include "numerics.cuh"
+#include "adam_fused.cuh"
 
 namespace tfb {
-
-using namespace detail;
-
 namespace {
-
-// Gradient sources of one launch. GMODE 0: one 16-bit buffer (GK = F16 or
-// BF16). GMODE 1: one fp32 buffer (GK = F32; the ZeRO-3 baseline flow that
-// fetches fp32 gradients from storage). GMODE 2: the sum of n 16-bit buffers,
-// e.g. the same subgroup's gradient contributions in every data-parallel
-// peer's memory over NVLink: summed in fp32 in source order, rounded once to
-// GK — the reduce-scatter fused into the update. NS > 0 fixes n at compile
-// time (the 2/4/8-rank cases: unrolled loads, no per-source predicates);
-// NS = 0 reads gs.n at run time.
-struct GradSources {
-    const void* src[kMaxGradSources];
-    int n;
-};
-
-// In-order fp32 sum of one quad over the sources, rounded once to GK.
-template <int GK, int NS>
-__device__ __forceinline__ U16x4 sum_quad16(const GradSources& gs, uint64_t q) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    auto add = [&](const U16x4& x) {
-        acc.x = __fadd_rn(acc.x, widen16<GK>(x.x));
-        acc.y = __fadd_rn(acc.y, widen16<GK>(x.y));
-        acc.z = __fadd_rn(acc.z, widen16<GK>(x.z));
-        acc.w = __fadd_rn(acc.w, widen16<GK>(x.w));
-    };
-    if constexpr (NS > 0) {
-        U16x4 x[NS];
-#pragma unroll
-        for (int s = 0; s < NS; ++s)  // all loads first: NS independent streams in flight
-            x[s] = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q);
-#pragma unroll
-        for (int s = 0; s < NS; ++s) add(x[s]);
-    } else {
-#pragma unroll
-        for (int s = 0; s < kMaxGradSources; ++s)
-            if (s < gs.n) add(load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[s]) + 4 * q));
-    }
-    U16x4 h;
-    h.x = narrow16<GK>(acc.x);
-    h.y = narrow16<GK>(acc.y);
-    h.z = narrow16<GK>(acc.z);
-    h.w = narrow16<GK>(acc.w);
-    return h;
-}
-
-// Register form of one gradient quad: 16-bit sources stay packed (2
-// registers; a summed quad is held already rounded) and are widened at use;
-// fp32 sources (GMODE 1) hold floats.
-template <int GK, int GMODE, int NS>
-struct GradReg {
-    U16x4 h;
-    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
-        if constexpr (GMODE == 0)
-            h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
-        else
-            h = sum_quad16<GK, NS>(gs, q);
-        nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
-    }
-    __device__ __forceinline__ float get(int k) const {
-        return widen16<GK>(k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w);
-    }
-};
-
-template <int GK, int NS>
-struct GradReg<GK, 1, NS> {
-    float4 f;
-    __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
-        f = __ldcs(reinterpret_cast<const float4*>(gs.src[0]) + q);
-        nonfinite += !isfinite(f.x) + !isfinite(f.y) + !isfinite(f.z) + !isfinite(f.w);
-    }
-    __device__ __forceinline__ float get(int k) const { return k == 0 ? f.x : k == 1 ? f.y : k == 2 ? f.z : f.w; }
-};
-
-template <int GK, int GMODE>
-__device__ __forceinline__ float load_grad1(const GradSources& gs, uint64_t i, unsigned& nonfinite) {
-    if constexpr (GMODE == 1) {
-        const float f = __ldcs(reinterpret_cast<const float*>(gs.src[0]) + i);
-        nonfinite += !isfinite(f);
-        return f;
-    } else {
-        uint16_t h;
-        if constexpr (GMODE == 0) {
-            h = __ldcs(reinterpret_cast<const uint16_t*>(gs.src[0]) + i);
-        } else {
-            float acc = 0.f;
-#pragma unroll
-            for (int s = 0; s < kMaxGradSources; ++s)
-                if (s < gs.n) acc = __fadd_rn(acc, widen16<GK>(__ldcs(reinterpret_cast<const uint16_t*>(gs.src[s]) + i)));
-            h = narrow16<GK>(acc);
-        }
-        nonfinite += nonfinite16<GK>(h);
-        return widen16<GK>(h);
-    }
-}
-
-// Where one launch reads and writes the fp32 state. In place (in == out) for
-// the device ring and the HBM-resident path; out may instead be mapped pinned
-// host memory, which fuses the D2H write-back into the kernel's epilogue.
-struct StateIO {
-    const float* p;
-    const float* m;
-    const float* v;
-    float* po;
-    float* mo;
-    float* vo;
-};
-
-// VEC = true: P, m, v 16-byte aligned and the gradient / p16 streams 8-byte
-// (16-bit) or 16-byte (fp32) aligned; the body walks quads (float4 / 4 x
-// 16-bit) and the n % 4 tail is scalar. VEC = false: scalar everywhere (e.g.
-// a contiguous P||m||v with P % 4 != 0). Loads and stores are explicit
-// evict-first intrinsics, issued in program order per element, so in-place
-// aliasing of in and out is well defined.
-// DIVC selects the element math: 0 = div.rn quotients, 1 = constant-divisor
-// quotients, 2 = verified fast path (numerics.cuh adam_element_fast), 3 =
-// constant-divisor quotients with the quad's elements walked one at a time.
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-// PF > 0: one thread per CTA asks the TMA unit to pull the CTA's chunk PF
-// grid-stride iterations ahead into L2 (cp.async.bulk.prefetch), so more bytes
-// are in flight than the registers of 32 warps per SM can hold.
-template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0, int PF = 0>
-__global__ void __launch_bounds__(kThreads, MINB)
-    adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
-                      unsigned long long* __restrict__ counters) {
-    unsigned nonfinite = 0, overflow = 0;
-    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-
-    if constexpr (VEC) {
-        const uint64_t nq = n / 4;
-        const float4* p4 = reinterpret_cast<const float4*>(io.p);
-        const float4* m4 = reinterpret_cast<const float4*>(io.m);
-        const float4* v4 = reinterpret_cast<const float4*>(io.v);
-        float4* po4 = reinterpret_cast<float4*>(io.po);
-        float4* mo4 = reinterpret_cast<float4*>(io.mo);
-        float4* vo4 = reinterpret_cast<float4*>(io.vo);
-        for (uint64_t base = tid; base < nq; base += nthreads * UNROLL) {
-            if constexpr (PF > 0) {
-                if (threadIdx.x == 0) {
-                    const uint64_t cq = base + static_cast<uint64_t>(PF) * UNROLL * nthreads;
-                    if (cq < nq) {
-                        const uint64_t nqc = min(static_cast<uint64_t>(blockDim.x) * UNROLL, nq - cq);
-                        prefetch_l2(p4 + cq, static_cast<uint32_t>(16 * nqc));
-                        prefetch_l2(m4 + cq, static_cast<uint32_t>(16 * nqc));
-                        prefetch_l2(v4 + cq, static_cast<uint32_t>(16 * nqc));
-                        if constexpr (GMODE == 0) {
-                            const uint16_t* g = reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * cq;
-                            const uint32_t gb = static_cast<uint32_t>(8 * nqc) & ~15u;
-                            if ((reinterpret_cast<uintptr_t>(g) & 15u) == 0 && gb > 0) prefetch_l2(g, gb);
-                        }
-                    }
-                }
-            }
-            float4 rp[UNROLL], rm[UNROLL], rv[UNROLL];
-            GradReg<GK, GMODE, NS> rg[UNROLL];
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {  // all loads first: UNROLL quads in flight
-                const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
-                if (q < nq) {
-                    rp[u] = __ldcs(p4 + q);
-                    rm[u] = __ldcs(m4 + q);
-                    rv[u] = __ldcs(v4 + q);
-                    rg[u].load(gs, q, nonfinite);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < UNROLL; ++u) {
-                const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
-                if (q < nq) {
-                    if constexpr (DIVC == 3) {
-                        // one element at a time (no cross-element ILP, fewer
-                        // live registers): rotate the quad through .x
-                        float g4[4] = {rg[u].get(0), rg[u].get(1), rg[u].get(2), rg[u].get(3)};
-                        float gx = g4[0], gy = g4[1], gz = g4[2], gw = g4[3];
-#pragma unroll 1
-                        for (int k = 0; k < 4; ++k) {
-                            adam_math<WD, 1>(rp[u].x, rm[u].x, rv[u].x, gx, c);
-                            const float tp = rp[u].x, tm = rm[u].x, tv = rv[u].x, tg = gx;
-                            rp[u].x = rp[u].y; rp[u].y = rp[u].z; rp[u].z = rp[u].w; rp[u].w = tp;
-                            rm[u].x = rm[u].y; rm[u].y = rm[u].z; rm[u].z = rm[u].w; rm[u].w = tm;
-                            rv[u].x = rv[u].y; rv[u].y = rv[u].z; rv[u].z = rv[u].w; rv[u].w = tv;
-                            gx = gy; gy = gz; gz = gw; gw = tg;
-                        }
-                    } else {
-                        adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
-                        adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
-                        adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
-                        adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
-                    }
-                    U16x4 h;
-                    h.x = narrow16<OK>(rp[u].x);
-                    h.y = narrow16<OK>(rp[u].y);
-                    h.z = narrow16<OK>(rp[u].z);
-                    h.w = narrow16<OK>(rp[u].w);
-                    overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
-                    __stcs(po4 + q, rp[u]);
-                    __stcs(mo4 + q, rm[u]);
-                    __stcs(vo4 + q, rv[u]);
-                    store_u16x4(p16 + 4 * q, h);
-                }
-            }
-        }
-        const uint64_t i = nq * 4 + tid;  // scalar tail: n % 4 elements
-        if (i < n) {
-            float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
-            const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
-            adam_math<WD, DIVC == 3 ? 1 : DIVC>(pf, mf, vf, gf, c);
-            const uint16_t h = narrow16<OK>(pf);
-            overflow += is_inf16<OK>(h);
-            __stcs(io.po + i, pf);
-            __stcs(io.mo + i, mf);
-            __stcs(io.vo + i, vf);
-            p16[i] = h;
-        }
-    } else {
-        for (uint64_t i = tid; i < n; i += nthreads) {
-            float pf = __ldcs(io.p + i), mf = __ldcs(io.m + i), vf = __ldcs(io.v + i);
-            const float gf = load_grad1<GK, GMODE>(gs, i, nonfinite);
-            adam_math<WD, DIVC == 3 ? 1 : DIVC>(pf, mf, vf, gf, c);
-            const uint16_t h = narrow16<OK>(pf);
-            overflow += is_inf16<OK>(h);
-            __stcs(io.po + i, pf);
-            __stcs(io.mo + i, mf);
-            __stcs(io.vo + i, vf);
-            p16[i] = h;
-        }
-    }
-    if (counters != nullptr) {
-        warp_count_add(counters + 0, nonfinite);
-        warp_count_add(counters + 1, overflow);
-    }
-}
-
-template <int UNROLL, int DIVC, int MINB, int PF = 0>
-struct Cfg {
-    static constexpr int kUnroll = UNROLL;
-    static constexpr int kDivc = DIVC;
-    static constexpr int kMinBlocks = MINB;
-    static constexpr int kPrefetch = PF;
-};
-
-GradSources sources_of(const AdamLaunch& a) {
-    GradSources gs{};
-    if (a.n_peers > 0) {
-        for (int s = 0; s < a.n_peers; ++s) gs.src[s] = a.peers[s];
-        gs.n = a.n_peers;
-    } else {
-        gs.src[0] = a.g;
-        gs.n = 1;
-    }
-    return gs;
-}
-
-StateIO state_io(const AdamLaunch& a) {
-    return StateIO{a.p, a.m, a.v, a.p_out ? a.p_out : a.p, a.m_out ? a.m_out : a.m, a.v_out ? a.v_out : a.v};
-}
-
-bool is_vec(const AdamLaunch& a) {
-    const StateIO io = state_io(a);
-    const uintptr_t state = reinterpret_cast<uintptr_t>(io.p) | reinterpret_cast<uintptr_t>(io.m) |
-                            reinterpret_cast<uintptr_t>(io.v) | reinterpret_cast<uintptr_t>(io.po) |
-                            reinterpret_cast<uintptr_t>(io.mo) | reinterpret_cast<uintptr_t>(io.vo);
-    uintptr_t grads = 0;
-    const GradSources gs = sources_of(a);
-    for (int s = 0; s < gs.n; ++s) grads |= reinterpret_cast<uintptr_t>(gs.src[s]);
-    const uintptr_t galign = a.grad_kind == kF32 ? 15u : 7u;
-    return (state & 15u) == 0 && (grads & galign) == 0 && (reinterpret_cast<uintptr_t>(a.p16) & 7u) == 0;
-}
-
-template <int GK, int GMODE, int OK, bool WD, class C, int NS = 0>
-cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
-    constexpr int U = C::kUnroll;
-    constexpr int B = C::kMinBlocks;
-    const GradSources gs = sources_of(a);
-    if (is_vec(a)) {
-        const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
-        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS, C::kPrefetch>
-            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
-    } else {
-        const unsigned grid = grid_for(a.n, B);
-        adam_fused_kernel<GK, GMODE, OK, WD, false, 1, C::kDivc, B>
-            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
-    }
-    return cudaGetLastError();
-}
-
-template <int GK, int GMODE, int OK, class C, int NS = 0>
-cudaError_t launch_wd(const AdamLaunch& a, cudaStream_t stream) {
-    return a.c.lr_wd != 0.0 ? launch_cfg<GK, GMODE, OK, true, C, NS>(a, stream)
-                            : launch_cfg<GK, GMODE, OK, false, C, NS>(a, stream);
-}
-
-// Summed sources: a compile-time source count (unrolled loads, no
-// per-source predicates) measured at 0.92-0.93 of the HBM roofline for 1, 2
-// and 4 sources against 0.75-0.77 for the run-time loop
-// (profiles/multi_sweep_r1.json).
-template <int GK, int OK, class C>
-cudaError_t launch_sum(const AdamLaunch& a, cudaStream_t stream) {
-    switch (a.n_peers) {
-        case 1: return launch_wd<GK, 2, OK, C, 1>(a, stream);
-        case 2: return launch_wd<GK, 2, OK, C, 2>(a, stream);
-        case 3: return launch_wd<GK, 2, OK, C, 3>(a, stream);
-        case 4: return launch_wd<GK, 2, OK, C, 4>(a, stream);
-        case 5: return launch_wd<GK, 2, OK, C, 5>(a, stream);
-        case 6: return launch_wd<GK, 2, OK, C, 6>(a, stream);
-        case 7: return launch_wd<GK, 2, OK, C, 7>(a, stream);
-        case 8: return launch_wd<GK, 2, OK, C, 8>(a, stream);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-template <class C>
-cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
-    if (a.out_kind != kF16 && a.out_kind != kBF16) return cudaErrorInvalidValue;
-    if (a.n_peers > 0) {  // fused multi-source reduction: 16-bit sources, same kind in and out
-        if (a.n_peers > kMaxGradSources || a.grad_kind == kF32) return cudaErrorInvalidValue;
-        if (a.grad_kind == kF16)
-            return a.out_kind == kF16 ? launch_sum<kF16, kF16, C>(a, stream) : launch_sum<kF16, kBF16, C>(a, stream);
-        return a.out_kind == kF16 ? launch_sum<kBF16, kF16, C>(a, stream) : launch_sum<kBF16, kBF16, C>(a, stream);
-    }
-    if (a.grad_kind == kF32)
-        return a.out_kind == kF16 ? launch_wd<kF32, 1, kF16, C>(a, stream) : launch_wd<kF32, 1, kBF16, C>(a, stream);
-    if (a.grad_kind == kF16 && a.out_kind == kF16) return launch_wd<kF16, 0, kF16, C>(a, stream);
-    if (a.grad_kind == kF16 && a.out_kind == kBF16) return launch_wd<kF16, 0, kBF16, C>(a, stream);
-    if (a.grad_kind == kBF16 && a.out_kind == kF16) return launch_wd<kBF16, 0, kF16, C>(a, stream);
-    return launch_wd<kBF16, 0, kBF16, C>(a, stream);
-}
-
-// ---------------------------------------------------------------------------
-// TMA-staged variant: one producer warp streams tiles of P, m, v and g into a
-// ring of shared-memory stages with 1D bulk copies (cp.async.bulk, completion
-// counted on an mbarrier), the consumer warps compute from shared memory and
-// store straight to global. Memory parallelism comes from the stage ring
-// (S x 14 KiB per CTA in flight) instead of registers.
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
-
-constexpr int kTmaConsumerWarps = 8;
-
-template <int T, int S, bool WD, int MINB>
-__global__ void __launch_bounds__((kTmaConsumerWarps + 1) * 32, MINB)
-    adam_tma_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                    const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t ntiles, AdamConsts c,
-                    unsigned long long* __restrict__ counters) {
-    extern __shared__ __align__(128) unsigned char smem[];
-    float* sp = reinterpret_cast<float*>(smem);
-    float* sm = sp + S * T;
-    float* sv = sm + S * T;
-    uint16_t* sg = reinterpret_cast<uint16_t*>(sv + S * T);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
-    uint64_t* empty = full + S;
-    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kTmaConsumerWarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (warp == kTmaConsumerWarps) {  // producer warp: one lane issues the bulk copies
-        if (lane == 0) {
-            uint64_t k = 0;
-            for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-                const int s = static_cast<int>(k % S);
-                const uint32_t round = static_cast<uint32_t>(k / S);
-                if (k >= static_cast<uint64_t>(S)) mbar_wait(&empty[s], (round - 1) & 1u);
-                mbar_arrive_expect_tx(&full[s], 14u * T);
-                const uint64_t off = tile * T;
-                bulk_load(sp + s * T, p + off, 4u * T, &full[s]);
-                bulk_load(sm + s * T, m + off, 4u * T, &full[s]);
-                bulk_load(sv + s * T, v + off, 4u * T, &full[s]);
-                bulk_load(sg + s * T, g + off, 2u * T, &full[s]);
-            }
-        }
-        return;
-    }
-    unsigned nonfinite = 0, overflow = 0;
-    uint64_t k = 0;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
-        const int s = static_cast<int>(k % S);
-        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
-        const uint64_t off = tile * T;
-        const float4* tp = reinterpret_cast<const float4*>(sp + s * T);
-        const float4* tm = reinterpret_cast<const float4*>(sm + s * T);
-        const float4* tv = reinterpret_cast<const float4*>(sv + s * T);
-        const uint2* tg = reinterpret_cast<const uint2*>(sg + s * T);
-#pragma unroll 1
-        for (int qi = threadIdx.x; qi < T / 4; qi += kTmaConsumerWarps * 32) {
-            float4 rp = tp[qi], rm = tm[qi], rv = tv[qi];
-            const uint2 graw = tg[qi];
-            U16x4 gh;
-            gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
-            gh.y = static_cast<uint16_t>(graw.x >> 16);
-            gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
-            gh.w = static_cast<uint16_t>(graw.y >> 16);
-            nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
-                         nonfinite16<kF16>(gh.w);
-            adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
-            adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
-            adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
-            adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
-            U16x4 h;
-            h.x = narrow16<kF16>(rp.x);
-            h.y = narrow16<kF16>(rp.y);
-            h.z = narrow16<kF16>(rp.z);
-            h.w = narrow16<kF16>(rp.w);
-            overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
-            __stcs(reinterpret_cast<float4*>(p + off) + qi, rp);
-            __stcs(reinterpret_cast<float4*>(m + off) + qi, rm);
-            __stcs(reinterpret_cast<float4*>(v + off) + qi, rv);
-            store_u16x4(p16 + off + 4 * qi, h);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    if (counters != nullptr) {
-        warp_count_add(counters + 0, nonfinite);
-        warp_count_add(counters + 1, overflow);
-    }
-}
-
-template <int T, int S, int MINB>
-cudaError_t launch_tma(const AdamLaunch& a, cudaStream_t stream) {
-    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
-                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
-                           reinterpret_cast<uintptr_t>(a.p16)) & 15u) == 0;
-    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
-        return cudaErrorInvalidValue;
-    const uint64_t ntiles = a.n / T;
-    constexpr size_t smem = static_cast<size_t>(S) * T * 14 + 2 * S * sizeof(uint64_t);
-    if (ntiles > 0) {
-        auto kern = a.c.lr_wd != 0.0 ? adam_tma_kernel<T, S, true, MINB> : adam_tma_kernel<T, S, false, MINB>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
-        kern<<<grid, (kTmaConsumerWarps + 1) * 32, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g),
-                                                                   a.p16, ntiles, a.c, a.counters);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    const uint64_t done = ntiles * T;
-    if (done == a.n) return cudaSuccess;
-    AdamLaunch tail = a;  // the n % T remainder through the register-streaming kernel
-    tail.p += done;
-    tail.m += done;
-    tail.v += done;
-    tail.g = static_cast<const uint16_t*>(a.g) + done;
-    tail.p16 += done;
-    tail.n = a.n - done;
-    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
-}
-
-// ---------------------------------------------------------------------------
-// TMA multistage pipeline without warp specialisation: every warp computes;
-// one elected thread keeps S-1 tiles (1024 params, 14 KiB) of P, m, v, g in
-// flight into a shared-memory ring with cp.async.bulk, so the bytes in flight
-// per SM (4 CTAs x (S-1) x 14 KiB) no longer depend on how long the FP64
-// chain of the current quad takes. One __syncthreads per tile retires a stage
-// before it is refilled.
-// REL = true: warps release a stage through a per-stage mbarrier (one
-// arrival per warp) instead of a CTA barrier, so only the issuing warp ever
-// waits for the slowest warp of a tile.
-template <int S, bool WD, int MINB, bool REL = false>
-__global__ void __launch_bounds__(kThreads, MINB)
-    adam_tma_pipe_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                         const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t ntiles, AdamConsts c,
-                         unsigned long long* __restrict__ counters) {
-    constexpr int T = 4 * kThreads;  // one quad per thread per tile
-    extern __shared__ __align__(128) unsigned char smem[];
-    float* sp = reinterpret_cast<float*>(smem);
-    float* sm = sp + S * T;
-    float* sv = sm + S * T;
-    uint16_t* sg = reinterpret_cast<uint16_t*>(sv + S * T);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
-    uint64_t* empty = full + S;
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            if constexpr (REL) mbar_init(&empty[s], kThreads / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    const uint64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-    auto issue = [&](uint64_t k) {
-        const int s = static_cast<int>(k % S);
-        const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
-        mbar_arrive_expect_tx(&full[s], 14u * T);
-        bulk_load(sp + s * T, p + off, 4u * T, &full[s]);
-        bulk_load(sm + s * T, m + off, 4u * T, &full[s]);
-        bulk_load(sv + s * T, v + off, 4u * T, &full[s]);
-        bulk_load(sg + s * T, g + off, 2u * T, &full[s]);
-    };
-    if (threadIdx.x == 0)
-        for (uint64_t k = 0; k + 1 < static_cast<uint64_t>(S) && k < mine; ++k) issue(k);
-    unsigned nonfinite = 0, overflow = 0;
-    const int qi = threadIdx.x;
-    for (uint64_t k = 0; k < mine; ++k) {
-        if (threadIdx.x == 0 && k + S - 1 < mine) {  // refills the stage of tile k-1
-            if constexpr (REL)
-                if (k > 0) mbar_wait(&empty[(k - 1) % S], static_cast<uint32_t>((k - 1) / S) & 1u);
-            issue(k + S - 1);
-        }
-        const int s = static_cast<int>(k % S);
-        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
-        const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
-        float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qi];
-        float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qi];
-        float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qi];
-        const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qi];
-        U16x4 gh;
-        gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
-        gh.y = static_cast<uint16_t>(graw.x >> 16);
-        gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
-        gh.w = static_cast<uint16_t>(graw.y >> 16);
-        nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
-                     nonfinite16<kF16>(gh.w);
-        adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
-        adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
-        adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
-        adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
-        U16x4 h;
-        h.x = narrow16<kF16>(rp.x);
-        h.y = narrow16<kF16>(rp.y);
-        h.z = narrow16<kF16>(rp.z);
-        h.w = narrow16<kF16>(rp.w);
-        overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
-        __stcs(reinterpret_cast<float4*>(p + off) + qi, rp);
-        __stcs(reinterpret_cast<float4*>(m + off) + qi, rm);
-        __stcs(reinterpret_cast<float4*>(v + off) + qi, rv);
-        store_u16x4(p16 + off + 4 * qi, h);
-        if constexpr (REL) {
-            __syncwarp();
-            if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
-        } else {
-            __syncthreads();  // stage s retired: it is refilled at iteration k + 1
-        }
-    }
-    if (counters != nullptr) {
-        warp_count_add(counters + 0, nonfinite);
-        warp_count_add(counters + 1, overflow);
-    }
-}
-
-template <int S, int MINB, bool REL = false>
-cudaError_t launch_tma_pipe(const AdamLaunch& a, cudaStream_t stream) {
-    constexpr int T = 4 * kThreads;
-    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
-                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
-                           reinterpret_cast<uintptr_t>(a.p16)) & 15u) == 0;
-    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
-        return cudaErrorInvalidValue;
-    const uint64_t ntiles = a.n / T;
-    constexpr size_t smem = static_cast<size_t>(S) * T * 14 + 2 * S * sizeof(uint64_t);
-    if (ntiles > 0) {
-        auto kern = a.c.lr_wd != 0.0 ? adam_tma_pipe_kernel<S, true, MINB, REL>
-                                     : adam_tma_pipe_kernel<S, false, MINB, REL>;
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
-        kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, ntiles, a.c,
-                                               a.counters);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    const uint64_t done = ntiles * T;
-    if (done == a.n) return cudaSuccess;
-    AdamLaunch tail = a;  // the n % T remainder through the register-streaming kernel
-    tail.p += done;
-    tail.m += done;
-    tail.v += done;
-    tail.g = static_cast<const uint16_t*>(a.g) + done;
-    tail.p16 += done;
-    tail.n = a.n - done;
-    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
-}
-
-// ---------------------------------------------------------------------------
-// cp.async double-buffered variant: each thread copies its NEXT quad of P, m,
-// v, g into its own shared-memory slots with cp.async (LDGSTS, no registers
-// held) before computing the current one, so memory latency overlaps the FP64
-// chain without giving up occupancy. Same element math and stores as the
-// register kernel; F16 in and out.
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <bool WD, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-    adam_cpasync_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                        const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t nq, AdamConsts c,
-                        unsigned long long* __restrict__ counters) {
-    __shared__ float4 sbuf[2][3][kThreads];
-    __shared__ uint2 sgrad[2][kThreads];
-    unsigned nonfinite = 0, overflow = 0;
-    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-    uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int t = threadIdx.x;
-    float4* p4 = reinterpret_cast<float4*>(p);
-    float4* m4 = reinterpret_cast<float4*>(m);
-    float4* v4 = reinterpret_cast<float4*>(v);
-    const uint2* g2 = reinterpret_cast<const uint2*>(g);
-    auto issue = [&](uint64_t qq, int s) {
-        cp_async16(&sbuf[s][0][t], p4 + qq);
-        cp_async16(&sbuf[s][1][t], m4 + qq);
-        cp_async16(&sbuf[s][2][t], v4 + qq);
-        cp_async8(&sgrad[s][t], g2 + qq);
-    };
-    int s = 0;
-    if (q < nq) issue(q, 0);
-    cp_async_commit();
-    for (; q < nq; q += nthreads, s ^= 1) {
-        const uint64_t nxt = q + nthreads;
-        if (nxt < nq) issue(nxt, s ^ 1);
-        cp_async_commit();
-        cp_async_wait<1>();  // the current quad has landed; the next stays in flight
-        float4 rp = sbuf[s][0][t], rm = sbuf[s][1][t], rv = sbuf[s][2][t];
-        const uint2 graw = sgrad[s][t];
-        U16x4 gh;
-        gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
-        gh.y = static_cast<uint16_t>(graw.x >> 16);
-        gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
-        gh.w = static_cast<uint16_t>(graw.y >> 16);
-        nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
-                     nonfinite16<kF16>(gh.w);
-        adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
-        adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
-        adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
-        adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
-        U16x4 h;
-        h.x = narrow16<kF16>(rp.x);
-        h.y = narrow16<kF16>(rp.y);
-        h.z = narrow16<kF16>(rp.z);
-        h.w = narrow16<kF16>(rp.w);
-        overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
-        __stcs(p4 + q, rp);
-        __stcs(m4 + q, rm);
-        __stcs(v4 + q, rv);
-        store_u16x4(p16 + 4 * q, h);
-    }
-    cp_async_wait<0>();
-    if (counters != nullptr) {
-        warp_count_add(counters + 0, nonfinite);
-        warp_count_add(counters + 1, overflow);
-    }
-}
-
-template <int MINB>
-cudaError_t launch_cpasync(const AdamLaunch& a, cudaStream_t stream) {
-    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
-                           reinterpret_cast<uintptr_t>(a.v)) & 15u) == 0 &&
-                         ((reinterpret_cast<uintptr_t>(a.g) | reinterpret_cast<uintptr_t>(a.p16)) & 7u) == 0;
-    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
-        return cudaErrorInvalidValue;
-    const uint64_t nq = a.n / 4;
-    if (nq > 0) {
-        const unsigned grid = grid_for(nq, MINB);
-        if (a.c.lr_wd != 0.0)
-            adam_cpasync_kernel<true, MINB><<<grid, kThreads, 0, stream>>>(
-                a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, nq, a.c, a.counters);
-        else
-            adam_cpasync_kernel<false, MINB><<<grid, kThreads, 0, stream>>>(
-                a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, nq, a.c, a.counters);
-        const cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
-    if (nq * 4 == a.n) return cudaSuccess;
-    AdamLaunch tail = a;  // the n % 4 remainder through the register-streaming kernel
-    const uint64_t done = nq * 4;
-    tail.p += done;
-    tail.m += done;
-    tail.v += done;
-    tail.g = static_cast<const uint16_t*>(a.g) + done;
-    tail.p16 += done;
-    tail.n = a.n - done;
-    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
-}
-
-// Scalar-element form at a given occupancy (tuning variants): 4-byte
-// coalesced streams, one element per thread per iteration.
-template <bool WD, int MINB>
-cudaError_t launch_scalar(const AdamLaunch& a, cudaStream_t stream) {
-    const unsigned grid = grid_for(a.n, MINB);
-    adam_fused_kernel<kF16, 0, kF16, WD, false, 1, 1, MINB>
-        <<<grid, kThreads, 0, stream>>>(state_io(a), sources_of(a), a.p16, a.n, a.c, a.counters);
-    return cudaGetLastError();
-}
-template <int MINB>
-cudaError_t launch_scalar_wd(const AdamLaunch& a, cudaStream_t stream) {
-    return a.c.lr_wd != 0.0 ? launch_scalar<true, MINB>(a, stream) : launch_scalar<false, MINB>(a, stream);
-}
 
 // Shipped configuration: one quad per thread per iteration, constant-divisor
 // quotients, <= 64 registers for 4 resident CTAs (32 warps) per SM. The
@@ -764,47 +21,6 @@ cudaError_t launch_scalar_wd(const AdamLaunch& a, cudaStream_t stream) {
 // peak, against 1045 us for the register-heavy unroll-2 form (variant 1).
 using VariantDefault = Cfg<1, true, 4>;
 // Tuning variants (F16 gradients and params only), for the kernel sweep.
-template <int V>
-cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
-    if constexpr (V == 1) return launch_wd<kF16, 0, kF16, Cfg<2, false, 1>>(a, stream);
-    if constexpr (V == 2) return launch_wd<kF16, 0, kF16, Cfg<1, false, 4>>(a, stream);
-    if constexpr (V == 3) return launch_wd<kF16, 0, kF16, Cfg<2, false, 3>>(a, stream);
-    if constexpr (V == 4) return launch_wd<kF16, 0, kF16, Cfg<1, true, 4>>(a, stream);
-    if constexpr (V == 5) return launch_wd<kF16, 0, kF16, Cfg<2, true, 3>>(a, stream);
-    if constexpr (V == 6) return launch_wd<kF16, 0, kF16, Cfg<2, true, 2>>(a, stream);
-    if constexpr (V == 7) return launch_wd<kF16, 0, kF16, Cfg<1, true, 3>>(a, stream);
-    if constexpr (V == 8) return launch_wd<kF16, 0, kF16, Cfg<4, true, 2>>(a, stream);
-    if constexpr (V == 9) return launch_wd<kF16, 0, kF16, Cfg<1, true, 5>>(a, stream);
-    if constexpr (V == 10) return launch_wd<kF16, 0, kF16, Cfg<2, true, 4>>(a, stream);
-    if constexpr (V == 11) return launch_wd<kF16, 0, kF16, Cfg<1, true, 6>>(a, stream);
-    if constexpr (V == 12) return launch_tma<1024, 4, 2>(a, stream);
-    if constexpr (V == 13) return launch_tma<1024, 3, 3>(a, stream);
-    if constexpr (V == 14) return launch_tma<2048, 3, 2>(a, stream);
-    if constexpr (V == 15) return launch_tma<512, 4, 4>(a, stream);
-    if constexpr (V == 16) return launch_cpasync<4>(a, stream);
-    if constexpr (V == 17) return launch_cpasync<3>(a, stream);
-    if constexpr (V == 18) return launch_wd<kF16, 0, kF16, Cfg<1, 2, 4>>(a, stream);
-    if constexpr (V == 19) return launch_wd<kF16, 0, kF16, Cfg<2, 2, 3>>(a, stream);
-    if constexpr (V == 20) return launch_wd<kF16, 0, kF16, Cfg<1, 2, 5>>(a, stream);
-    if constexpr (V == 21) return launch_scalar_wd<4>(a, stream);
-    if constexpr (V == 22) return launch_scalar_wd<5>(a, stream);
-    if constexpr (V == 23) return launch_scalar_wd<6>(a, stream);
-    if constexpr (V == 24) return launch_wd<kF16, 0, kF16, Cfg<1, 3, 5>>(a, stream);
-    if constexpr (V == 25) return launch_wd<kF16, 0, kF16, Cfg<1, 3, 6>>(a, stream);
-    if constexpr (V == 26) return launch_wd<kF16, 0, kF16, Cfg<1, 4, 4>>(a, stream);
-    if constexpr (V == 27) return launch_wd<kF16, 0, kF16, Cfg<1, 4, 5>>(a, stream);
-    if constexpr (V == 28) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 1>>(a, stream);
-    if constexpr (V == 29) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 2>>(a, stream);
-    if constexpr (V == 30) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 4>>(a, stream);
-    if constexpr (V == 31) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 3, 2>>(a, stream);
-    if constexpr (V == 32) return launch_tma_pipe<3, 4>(a, stream);
-    if constexpr (V == 33) return launch_tma_pipe<2, 4>(a, stream);
-    if constexpr (V == 34) return launch_tma_pipe<4, 3>(a, stream);
-    if constexpr (V == 35) return launch_tma_pipe<3, 3>(a, stream);
-    if constexpr (V == 36) return launch_tma_pipe<3, 4, true>(a, stream);
-    if constexpr (V == 37) return launch_tma_pipe<2, 4, true>(a, stream);
-    return cudaErrorInvalidValue;
-}
 
 // ---------------------------------------------------------------------------
 // Self-test of div_by_const against div.rn.f64: numerators with random 52-bit
@@ -840,54 +56,6 @@ cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
     return launch_dtypes<VariantDefault>(a, stream);
 }
-
-cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStream_t stream) {
-    if (a.n == 0) return cudaSuccess;
-    if (variant == 0) return launch_adam_fused(a, stream);
-    if (a.grad_kind != kF16 || a.out_kind != kF16 || a.n_peers > 0) return cudaErrorInvalidValue;
-    switch (variant) {
-        case 1: return launch_variant<1>(a, stream);
-        case 2: return launch_variant<2>(a, stream);
-        case 3: return launch_variant<3>(a, stream);
-        case 4: return launch_variant<4>(a, stream);
-        case 5: return launch_variant<5>(a, stream);
-        case 6: return launch_variant<6>(a, stream);
-        case 7: return launch_variant<7>(a, stream);
-        case 8: return launch_variant<8>(a, stream);
-        case 9: return launch_variant<9>(a, stream);
-        case 10: return launch_variant<10>(a, stream);
-        case 11: return launch_variant<11>(a, stream);
-        case 12: return launch_variant<12>(a, stream);
-        case 13: return launch_variant<13>(a, stream);
-        case 14: return launch_variant<14>(a, stream);
-        case 15: return launch_variant<15>(a, stream);
-        case 16: return launch_variant<16>(a, stream);
-        case 17: return launch_variant<17>(a, stream);
-        case 18: return launch_variant<18>(a, stream);
-        case 19: return launch_variant<19>(a, stream);
-        case 20: return launch_variant<20>(a, stream);
-        case 21: return launch_variant<21>(a, stream);
-        case 22: return launch_variant<22>(a, stream);
-        case 23: return launch_variant<23>(a, stream);
-        case 24: return launch_variant<24>(a, stream);
-        case 25: return launch_variant<25>(a, stream);
-        case 26: return launch_variant<26>(a, stream);
-        case 27: return launch_variant<27>(a, stream);
-        case 28: return launch_variant<28>(a, stream);
-        case 29: return launch_variant<29>(a, stream);
-        case 30: return launch_variant<30>(a, stream);
-        case 31: return launch_variant<31>(a, stream);
-        case 32: return launch_variant<32>(a, stream);
-        case 33: return launch_variant<33>(a, stream);
-        case 34: return launch_variant<34>(a, stream);
-        case 35: return launch_variant<35>(a, stream);
-        case 36: return launch_variant<36>(a, stream);
-        case 37: return launch_variant<37>(a, stream);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-int adam_variant_count() { return 38; }
 
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream) {
