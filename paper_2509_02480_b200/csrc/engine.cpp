@@ -401,7 +401,12 @@ void OffloadWorker::setup_device() {
         for (auto& r : ring_grad_)
             cuda_check(cudaMalloc(reinterpret_cast<void**>(&r), ring_stride_ * sizeof(float)), "cudaMalloc(ring grads)");
         cuda_check(cudaMalloc(reinterpret_cast<void**>(&grad32_dev_), ring_stride_ * sizeof(float)), "cudaMalloc");
-        grad_stage_ = HostBlock::allocate(4 * static_cast<std::size_t>(max_params_), true);
+        for (int b = 0; b < kGradStages; ++b) {
+            grad_stages_.push_back(HostBlock::allocate(4 * static_cast<std::size_t>(max_params_), true));
+            grad_stage_ready_.push_back(nullptr);
+            cuda_check(cudaEventCreateWithFlags(&grad_stage_ready_.back(), cudaEventDisableTiming), "cudaEventCreate");
+            grad_stage_free_.push_back(b);
+        }
     }
     std::size_t arena = 0;
     std::vector<std::size_t> offs;
@@ -479,6 +484,11 @@ void OffloadWorker::release_device() {
     ring_grad_.clear();
     if (grad32_dev_) cudaFree(grad32_dev_);
     grad32_dev_ = nullptr;
+    for (cudaEvent_t ev : grad_stage_ready_)
+        if (ev) cudaEventDestroy(ev);
+    grad_stage_ready_.clear();
+    grad_stages_.clear();
+    grad_stage_free_.clear();
     cudaFree(grad_arena_);
     cudaFree(p16_arena_);
     cudaFree(counters_);
@@ -570,13 +580,19 @@ void OffloadWorker::flush_grads_to_storage() {
     for (std::size_t k = 0; k < ids_.size(); ++k) {
         const SubgroupId id = ids_[k];
         const std::uint64_t pc = subgroups_.at(id).param_count;
+        int b;
+        {
+            std::unique_lock<std::mutex> l(mu_);
+            while (grad_stage_free_.empty()) grad_stage_cv_.wait_for(l, std::chrono::milliseconds(50));
+            b = grad_stage_free_.front();
+            grad_stage_free_.pop_front();
+        }
+        float* stage = reinterpret_cast<float*>(grad_stages_[static_cast<std::size_t>(b)].base());
+        const cudaEvent_t ready = grad_stage_ready_[static_cast<std::size_t>(b)];
         trace_->record(EventKind::grad_upscale_start, id_, id, kNoTier, 4 * pc);
         cuda_check(launch_widen16(grad_ptr_[k], grad32_dev_, pc, dev_.grad_kind, nullptr, s_k_), "widen16");
-        cuda_check(cudaMemcpyAsync(grad_stage_.base(), grad32_dev_, 4 * pc, cudaMemcpyDeviceToHost, s_k_),
-                   "cudaMemcpyAsync(grads)");
-        cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
-        auto grads32 = std::make_shared<std::vector<float>>(reinterpret_cast<const float*>(grad_stage_.base()),
-                                                             reinterpret_cast<const float*>(grad_stage_.base()) + pc);
+        cuda_check(cudaMemcpyAsync(stage, grad32_dev_, 4 * pc, cudaMemcpyDeviceToHost, s_k_), "cudaMemcpyAsync(grads)");
+        cuda_check(cudaEventRecord(ready, s_k_), "cudaEventRecord");
         trace_->record(EventKind::grad_upscale_end, id_, id, kNoTier, 4 * pc);
         TierId dest;
         {
@@ -586,9 +602,23 @@ void OffloadWorker::flush_grads_to_storage() {
             grad_tier_[id] = dest;
         }
         auto tier = tiers_[static_cast<std::size_t>(dest)];
-        pending.push_back(io_[static_cast<std::size_t>(dest)]->submit(
-            false, id, 4 * pc, [tier, id, pc, grads32] { return tier->write_grads(id, pc, grads32->data()); },
-            nullptr));
+        const int device = dev_.device;
+        // The write waits for the D2H on the tier's I/O thread; the stage goes
+        // back to the rotation when the write completes (or fails).
+        auto transfer = [tier, id, pc, stage, ready, device] {
+            cudaSetDevice(device);
+            cuda_check(cudaEventSynchronize(ready), "cudaEventSynchronize(grads)");
+            return tier->write_grads(id, pc, stage);
+        };
+        auto release = [this, b](bool, const IoStats&) {
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                grad_stage_free_.push_back(b);
+            }
+            grad_stage_cv_.notify_all();
+        };
+        pending.push_back(io_[static_cast<std::size_t>(dest)]->submit(false, id, 4 * pc, std::move(transfer),
+                                                                      std::move(release)));
     }
     for (auto& f : pending) {
         std::shared_future<IoStats> s = f.share();

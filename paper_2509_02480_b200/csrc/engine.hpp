@@ -91,6 +91,8 @@ struct DeviceOptions {
 
 // HBM cache mode: pinned blocks in the write-back lane.
 constexpr int kWritebackBlocks = 4;
+// Baseline flow: pinned fp32-gradient staging blocks in rotation.
+constexpr int kGradStages = 4;
 
 enum class Residency : int { host_cached = 0, in_flight = 1, on_tier = 2 };
 
@@ -392,7 +394,12 @@ private:
     int wb_inflight_ = 0;  // deferred write-backs whose HBM buffer is not yet free
     std::thread wb_thread_;
     float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H
-    HostBlock grad_stage_;           // baseline flow: pinned D2H staging of fp32 gradients
+    // baseline flow: pinned D2H staging of fp32 gradients, a few in rotation so
+    // the D2H of one subgroup overlaps the storage write of the previous ones
+    std::vector<HostBlock> grad_stages_;
+    std::vector<cudaEvent_t> grad_stage_ready_;
+    std::deque<int> grad_stage_free_;
+    std::condition_variable grad_stage_cv_;
     std::size_t state_block_bytes_ = 0;  // header + P||m||v of the largest subgroup, 4 KiB multiple
     std::size_t annex_bytes_ = 0;        // baseline flow: fp32 gradient annex after the state
     std::unordered_map<SubgroupId, TierId> grad_tier_;  // tier holding each subgroup's fp32 gradients
