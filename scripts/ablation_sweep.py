@@ -60,14 +60,22 @@ else:
             r["update_speedup_vs_zero3"] = base["update_s"] / r["update_s"]
             r["iteration_speedup_vs_zero3"] = base["iteration_s"] / r["iteration_s"]
     print(json.dumps(out, indent=1))
-    Path("gpurun_out/ablation_sweep.json").write_text(json.dumps(out, indent=1))
+    Path(os.environ.get("TFB_SWEEP_OUT", "gpurun_out/ablation_sweep.json")).write_text(json.dumps(out, indent=1))
     sys.exit(0)
 
 for name, caching, skip, atomic, multi, pool, cache, hbm in ladder:
     shutil.rmtree(root, ignore_errors=True)
-    dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9))
-    nvme = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4))
-    nvme.probe_bandwidth(256 << 20, 3)
+    if os.environ.get("TFB_TIERS", "dram,nvme") == "nvme,remote":  # disk-bound: the paper's NVMe + PFS setting
+        t0_ = tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4,
+                                  lock_device=1))
+        t1_ = tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0, 0, io_parallelism=4,
+                                  lock_device=1))
+        t1_.probe_bandwidth(256 << 20, 3)
+    else:
+        t0_ = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9))
+        t1_ = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4))
+    t1_.probe_bandwidth(256 << 20, 3)
+    dram, nvme = t0_, t1_
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, enable_caching=caching, skip_gradients=skip,
                              atomic_rw=atomic, multi_path=multi, lock_dir=str(root / "locks"))
     w = tf.OffloadWorker(0, [dram, nvme], opt, tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 12, 0, 1, hbm))
