@@ -70,7 +70,7 @@ for name, caching, skip, atomic, multi, pool, cache, hbm in ladder:
                                   lock_device=1))
         t1_ = tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0, 0, io_parallelism=4,
                                   lock_device=1))
-        t1_.probe_bandwidth(256 << 20, 3)
+        t0_.probe_bandwidth(256 << 20, 3)
     else:
         t0_ = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9))
         t1_ = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4))
