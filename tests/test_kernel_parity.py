@@ -323,3 +323,43 @@ def test_fast_path_fallback_on_midpoint_cases(tf, cuda, variant):
     assert_bits(Mm.cpu().numpy(), want[1], "m")
     assert_bits(V.cpu().numpy(), want[2], "v")
     assert np.array_equal(_np16(p16), want[3])
+
+
+def test_one_billion_param_subgroup_is_chunk_invariant(tf, cuda):
+    """SURVEY C5 upper end (1B params per subgroup, 12 GB of state): one launch
+    over the whole subgroup equals ten launches over 100M-param slices, bit
+    for bit (element-wise op; exercises 64-bit indexing past 2^32 bytes), and
+    the counters agree."""
+    import torch
+    n = 1_000_000_000
+    st = torch.empty(3 * n, dtype=torch.float32, device=cuda)
+    g = torch.empty(n, dtype=torch.int16, device=cuda)
+    tf.synthetic_state(st[:n], st[n:2 * n], st[2 * n:], 7, 3)
+    tf.synthetic_grads(g, 7, 3, 0)
+    ref = st.clone()
+    idx = np.random.default_rng(1).integers(0, n, 4096)
+    ti = torch.from_numpy(idx).to(cuda)
+    p0 = st[ti].cpu().numpy()
+    m0 = st[n + ti].cpu().numpy()
+    v0 = st[2 * n + ti].cpu().numpy()
+    g0 = g[ti].cpu().numpy().view(np.uint16)
+    p16a = torch.empty(n, dtype=torch.int16, device=cuda)
+    p16b = torch.empty(n, dtype=torch.int16, device=cuda)
+    ca = torch.zeros(2, dtype=torch.int64, device=cuda)
+    cb = torch.zeros(2, dtype=torch.int64, device=cuda)
+    hy = tf.AdamHyper(weight_decay=0.01)
+    tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], g, p16a, 5, hy, counters=ca)
+    c = 100_000_000
+    for k in range(0, n, c):
+        tf.adam_fused(ref[k:k + c], ref[n + k:n + k + c], ref[2 * n + k:2 * n + k + c], g[k:k + c], p16b[k:k + c],
+                      5, hy, counters=cb)
+    torch.cuda.synchronize()
+    assert torch.equal(st.view(torch.int32), ref.view(torch.int32))
+    assert torch.equal(p16a, p16b)
+    assert ca.tolist() == cb.tolist()
+    # and a sample of elements, far into the buffer, against the CPU oracle
+    want = oracle.adam_fused(p0, m0, v0, g0, 0, 0, 5, weight_decay=0.01)
+    assert np.array_equal(st[ti].cpu().numpy().view(np.uint32), want[0].view(np.uint32))
+    assert np.array_equal(st[n + ti].cpu().numpy().view(np.uint32), want[1].view(np.uint32))
+    assert np.array_equal(st[2 * n + ti].cpu().numpy().view(np.uint32), want[2].view(np.uint32))
+    assert np.array_equal(p16a[ti].cpu().numpy().view(np.uint16), want[3])
