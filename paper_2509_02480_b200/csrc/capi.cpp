@@ -333,6 +333,13 @@ int tfg_synthetic_state(float* p, float* m, float* v, uint64_t n, uint64_t seed,
 
 // ---- placement -------------------------------------------------------------------
 
+int tfg_host_blocks_live(int64_t* blocks_out, int64_t* bytes_out) {
+    return guarded([&] {
+        if (blocks_out) *blocks_out = tfb::g_host_blocks_live.load();
+        if (bytes_out) *bytes_out = tfb::g_host_bytes_live.load();
+    });
+}
+
 int tfg_assign_subgroups(int M, const double* bandwidths, int n_tiers, int* counts_out) {
     return guarded([&] {
         if (n_tiers > 0) {

@@ -8,6 +8,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <utility>
@@ -20,6 +21,10 @@ constexpr std::size_t kHeaderBytes = 32;
 constexpr std::size_t kPageBytes = 4096;
 
 inline std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) / a * a; }
+
+// Live host blocks (count, bytes) in the process: leak accounting for tests.
+inline std::atomic<std::int64_t> g_host_blocks_live{0};
+inline std::atomic<std::int64_t> g_host_bytes_live{0};
 
 // Bytes a block needs for a subgroup of `params` parameters.
 inline std::size_t block_bytes_for(std::uint64_t params) {
@@ -61,6 +66,8 @@ public:
         }
         b.base_ = static_cast<std::uint8_t*>(p);
         b.bytes_ = bytes;
+        g_host_blocks_live.fetch_add(1, std::memory_order_relaxed);
+        g_host_bytes_live.fetch_add(static_cast<std::int64_t>(bytes), std::memory_order_relaxed);
         return b;
     }
 
@@ -74,6 +81,8 @@ public:
 private:
     void release() {
         if (base_ == nullptr) return;
+        g_host_blocks_live.fetch_sub(1, std::memory_order_relaxed);
+        g_host_bytes_live.fetch_sub(static_cast<std::int64_t>(bytes_), std::memory_order_relaxed);
         if (pinned_)
             cudaFreeHost(base_);
         else

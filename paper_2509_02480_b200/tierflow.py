@@ -236,6 +236,13 @@ def assign_subgroups(M: int, bandwidths: Sequence[float]) -> AllocationVector:
     return AllocationVector(list(out)[:n], M)
 
 
+def host_blocks_live() -> tuple:
+    """(blocks, bytes) of host blocks alive in the process (leak accounting)."""
+    b, n = C.c_int64(), C.c_int64()
+    _lib.call("tfg_host_blocks_live", C.byref(b), C.byref(n))
+    return b.value, n.value
+
+
 def assign_subgroups_capped(M: int, bandwidths: Sequence[float], caps: Sequence[int]) -> AllocationVector:
     """Capacity-aware Eq. 1 (caps[i] < 0: unlimited); the reference allocation
     whenever it fits every cap."""

@@ -1,0 +1,37 @@
+#!/bin/bash
+# compute-sanitizer passes: memcheck over the engine smoke run (pipeline, HBM
+# cache, directory tier) and over the fused reduce + update kernel; racecheck
+# and synccheck over the shared-memory kernel variants (TMA, cp.async).
+set -u
+mkdir -p gpurun_out
+CS=/usr/local/cuda/bin/compute-sanitizer
+python -m paper_2509_02480_b200.build > gpurun_out/build.log 2>&1 || exit 1
+make -s -C oracle >> gpurun_out/build.log 2>&1
+timeout 900 $CS --tool memcheck --leak-check full --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/san_memcheck_smoke.log 2>&1
+echo "memcheck smoke rc=$?"; tail -3 gpurun_out/san_memcheck_smoke.log
+cat > /tmp/san_kernels.py <<'PY'
+import sys
+sys.path.insert(0, ".")
+import torch
+from paper_2509_02480_b200 import tierflow as tf
+n = 1_000_003
+variants = [int(v) for v in sys.argv[1].split(",")]
+for v in variants:
+    st = torch.empty(3 * n, device="cuda"); g = torch.empty(n, dtype=torch.int16, device="cuda")
+    tf.synthetic_state(st[:n], st[n:2*n], st[2*n:], 1, 0); tf.synthetic_grads(g, 1, 0, 0)
+    p16 = torch.empty(n, dtype=torch.int16, device="cuda")
+    nn = n - n % 4096 if v >= 12 else n
+    tf.adam_fused_variant(v, st[:nn], st[n:n+nn], st[2*n:2*n+nn], g[:nn], p16[:nn], 1, tf.AdamHyper())
+    torch.cuda.synchronize()
+srcs = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(3)]
+for s_ in srcs: tf.synthetic_grads(s_, 2, 0, 0)
+tf.adam_fused_multi(st[:n], st[n:2*n], st[2*n:], srcs, p16, 2, tf.AdamHyper())
+torch.cuda.synchronize()
+print("kernels ok")
+PY
+timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,1,12,16,32,36 > gpurun_out/san_memcheck_kernels.log 2>&1
+echo "memcheck kernels rc=$?"; tail -3 gpurun_out/san_memcheck_kernels.log
+timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 12,13,16,32,33,36 > gpurun_out/san_racecheck.log 2>&1
+echo "racecheck rc=$?"; tail -3 gpurun_out/san_racecheck.log
+timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 12,16,32,36 > gpurun_out/san_synccheck.log 2>&1
+echo "synccheck rc=$?"; tail -3 gpurun_out/san_synccheck.log

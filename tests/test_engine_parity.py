@@ -545,3 +545,30 @@ def test_full_size_subgroups_bit_exact(tf, cuda, lock_dir, tmp_path, hbm):
         assert np.array_equal(w.read_params16(sg), p16), f"subgroup {sg} params16"
         del p, m, v, p16, got
     w.close()
+
+
+@pytest.mark.parametrize("hbm,skip", [(0, True), (1, True), (2, True), (0, False)])
+def test_engine_returns_every_host_block(tf, cuda, lock_dir, tmp_path, hbm, skip):
+    """Pool slots, host-DRAM blobs and spares, the write-back lane and the
+    baseline flow's gradient stages are all freed once the engine and its
+    tiers are gone."""
+    import gc
+    gc.collect()
+    base = tf.host_blocks_live()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=4, cache_slots=2, lock_dir=lock_dir,
+                                                      skip_gradients=skip),
+                         tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    w.set_fixed_ratio([1.0, 1.0])
+    for i in range(5):
+        w.add_subgroup(i, 50_000 + 7 * i)
+    w.init_and_flush_all(3)
+    for it in range(3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(3))
+        w.run_update(it)
+    assert tf.host_blocks_live()[0] > base[0]
+    w.close()
+    del w, tiers
+    gc.collect()
+    assert tf.host_blocks_live() == base

@@ -171,3 +171,22 @@ def test_semaphore_width_admits_two(tf, lock_dir):
     assert done.wait(5.0)
     th.join()
     a.release()
+
+
+def test_host_dram_tier_blocks_are_freed(tf):
+    """Host-block accounting: a host-DRAM tier's blobs and spares are returned
+    when the tier goes away (no pinned memory leaks across engines)."""
+    import gc
+    gc.collect()
+    base = tf.host_blocks_live()
+    t = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 1e9, 1e9))
+    P = 10_000
+    for sg in range(5):
+        t.write_subgroup(sg, P, _state(P, sg))
+    back = np.empty(3 * P, np.float32)
+    t.read_subgroup(3, P, back)
+    t.remove_subgroup(2)
+    assert tf.host_blocks_live()[0] > base[0]
+    del t
+    gc.collect()
+    assert tf.host_blocks_live() == base
