@@ -14,14 +14,13 @@ import sys
 sys.path.insert(0, ".")
 import torch
 from paper_2509_02480_b200 import tierflow as tf
-n = 1_000_003
+n = 1_003_520  # multiple of the TMA tile so every variant takes its main path
 variants = [int(v) for v in sys.argv[1].split(",")]
 for v in variants:
     st = torch.empty(3 * n, device="cuda"); g = torch.empty(n, dtype=torch.int16, device="cuda")
     tf.synthetic_state(st[:n], st[n:2*n], st[2*n:], 1, 0); tf.synthetic_grads(g, 1, 0, 0)
     p16 = torch.empty(n, dtype=torch.int16, device="cuda")
-    nn = n - n % 4096 if v >= 12 else n
-    tf.adam_fused_variant(v, st[:nn], st[n:n+nn], st[2*n:2*n+nn], g[:nn], p16[:nn], 1, tf.AdamHyper())
+    tf.adam_fused_variant(v, st[:n], st[n:2*n], st[2*n:], g, p16, 1, tf.AdamHyper())
     torch.cuda.synchronize()
 srcs = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(3)]
 for s_ in srcs: tf.synthetic_grads(s_, 2, 0, 0)
