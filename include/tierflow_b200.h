@@ -257,7 +257,7 @@ int tfg_synthetic_state(float* p, float* m, float* v, uint64_t n, uint64_t seed,
 /* assign_subgroups, placement.hpp:30-100. counts_out[n_tiers]. */
 int tfg_assign_subgroups(int M, const double* bandwidths, int n_tiers, int* counts_out);
 /* Host blocks (pinned slots, tier blobs, staging) alive in the process: leak accounting. */
-int tfg_host_blocks_live(int64_t* blocks_out, int64_t* bytes_out);
+int tfg_host_blocks_live(int64_t* blocks_out, int64_t* bytes_out, int64_t* free_failures_out);
 /* Capacity-aware Eq. 1 (beyond the reference): caps[i] < 0 unlimited; the
    reference allocation whenever it fits every cap, else the min-max of T_i/B_i
    subject to T_i <= caps[i] (water filling). ConfigError if the caps cannot hold M. */

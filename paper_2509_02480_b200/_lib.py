@@ -142,7 +142,7 @@ _SIGS = {
     "tfg_synthetic_grads": (_i, [_vp, _u64, _i, _u64, C.c_uint32, _i, _i, _i, _vp]),
     "tfg_synthetic_state": (_i, [_vp, _vp, _vp, _u64, _u64, C.c_uint32, _vp]),
     "tfg_assign_subgroups": (_i, [_i, C.POINTER(_d), _i, C.POINTER(_i)]),
-    "tfg_host_blocks_live": (_i, [C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tfg_host_blocks_live": (_i, [C.POINTER(C.c_int64), C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tfg_assign_subgroups_capped": (_i, [_i, C.POINTER(_d), C.POINTER(_i), _i, C.POINTER(_i)]),
     "tfg_destination_plan": (_i, [C.POINTER(C.c_uint32), _i, _i, C.POINTER(_d), _i, C.POINTER(_i), C.POINTER(_i),
                                   C.POINTER(_i)]),

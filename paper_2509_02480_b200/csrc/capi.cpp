@@ -333,10 +333,11 @@ int tfg_synthetic_state(float* p, float* m, float* v, uint64_t n, uint64_t seed,
 
 // ---- placement -------------------------------------------------------------------
 
-int tfg_host_blocks_live(int64_t* blocks_out, int64_t* bytes_out) {
+int tfg_host_blocks_live(int64_t* blocks_out, int64_t* bytes_out, int64_t* free_failures_out) {
     return guarded([&] {
         if (blocks_out) *blocks_out = tfb::g_host_blocks_live.load();
         if (bytes_out) *bytes_out = tfb::g_host_bytes_live.load();
+        if (free_failures_out) *free_failures_out = tfb::g_host_free_failures.load();
     });
 }
 

@@ -25,6 +25,7 @@ inline std::size_t round_up(std::size_t x, std::size_t a) { return (x + a - 1) /
 // Live host blocks (count, bytes) in the process: leak accounting for tests.
 inline std::atomic<std::int64_t> g_host_blocks_live{0};
 inline std::atomic<std::int64_t> g_host_bytes_live{0};
+inline std::atomic<std::int64_t> g_host_free_failures{0};
 
 // Bytes a block needs for a subgroup of `params` parameters.
 inline std::size_t block_bytes_for(std::uint64_t params) {
@@ -83,9 +84,12 @@ private:
         if (base_ == nullptr) return;
         g_host_blocks_live.fetch_sub(1, std::memory_order_relaxed);
         g_host_bytes_live.fetch_sub(static_cast<std::int64_t>(bytes_), std::memory_order_relaxed);
-        if (pinned_)
-            cudaFreeHost(base_);
-        else
+        if (pinned_) {
+            if (cudaFreeHost(base_) != cudaSuccess) {
+                (void)cudaGetLastError();
+                g_host_free_failures.fetch_add(1, std::memory_order_relaxed);
+            }
+        } else
             std::free(base_);
         base_ = nullptr;
         bytes_ = 0;

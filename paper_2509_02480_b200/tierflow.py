@@ -238,9 +238,16 @@ def assign_subgroups(M: int, bandwidths: Sequence[float]) -> AllocationVector:
 
 def host_blocks_live() -> tuple:
     """(blocks, bytes) of host blocks alive in the process (leak accounting)."""
-    b, n = C.c_int64(), C.c_int64()
-    _lib.call("tfg_host_blocks_live", C.byref(b), C.byref(n))
+    b, n, f = C.c_int64(), C.c_int64(), C.c_int64()
+    _lib.call("tfg_host_blocks_live", C.byref(b), C.byref(n), C.byref(f))
     return b.value, n.value
+
+
+def host_block_free_failures() -> int:
+    """cudaFreeHost calls that failed (pinned memory the process could not return)."""
+    b, n, f = C.c_int64(), C.c_int64(), C.c_int64()
+    _lib.call("tfg_host_blocks_live", C.byref(b), C.byref(n), C.byref(f))
+    return f.value
 
 
 def assign_subgroups_capped(M: int, bandwidths: Sequence[float], caps: Sequence[int]) -> AllocationVector:

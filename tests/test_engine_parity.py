@@ -572,3 +572,4 @@ def test_engine_returns_every_host_block(tf, cuda, lock_dir, tmp_path, hbm, skip
     del w, tiers
     gc.collect()
     assert tf.host_blocks_live() == base
+    assert tf.host_block_free_failures() == 0
