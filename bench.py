@@ -244,7 +244,31 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
         raise RuntimeError("non-finite gradients in the device leg")
     del states, grads, p16s
     torch.cuda.empty_cache()
-    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(sizes), clocks=clk.summary())
+    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(sizes), clocks=clk.summary(),
+                copy_sustained_gbs=sustained_copy_gbs(stream, total_ms))
+
+
+def sustained_copy_gbs(stream, busy_ms):
+    """Context for the roofline denominator: a device-to-device copy (read +
+    write bytes) run back to back for as long as the timed region, i.e. under
+    the same power cap the update phase sees. Not the reported peak."""
+    import torch
+    n = 1 << 30  # 2 GiB of bf16 each way
+    a = torch.empty(n, dtype=torch.bfloat16, device=stream.device)
+    b = torch.empty_like(a)
+    with torch.cuda.stream(stream):
+        b.copy_(a)
+        reps = max(4, int(busy_ms / 0.7))  # ~0.7 ms per 4 GiB copy
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            b.copy_(a)
+        e1.record(stream)
+    stream.synchronize()
+    gbs = reps * 4 * n / (e0.elapsed_time(e1) / 1e3) / 1e9
+    del a, b
+    torch.cuda.empty_cache()
+    return round(gbs, 1)
 
 
 # ---------------------------------------------------------------------------
@@ -709,7 +733,10 @@ def main(argv=None):
                           "quotients, 4 CTAs x 256 threads per SM)"
                           + (f"; {world} gradient sources summed in-kernel, {world - 1} over NVLink peer loads"
                              if a.exchange == "fused" else ""),
-                "traffic_source": "profiles/ncu_adam_fused.json (ncu --set full, dram bytes per 100M-param launch)"}
+                "traffic_source": "profiles/ncu_adam_fused.json (ncu --set full, dram bytes per 100M-param launch)",
+                "copy_sustained_gbs": dl.get("copy_sustained_gbs"),
+                "frac_of_copy_sustained": (round(achieved / dl["copy_sustained_gbs"], 4)
+                                           if dl.get("copy_sustained_gbs") else None)}
 
     e2e = None
     if a.exchange != "none":
