@@ -109,6 +109,7 @@ typedef struct tfg_device_options {
                                 1: the host slot stays reserved, C = min(cache_slots, pool_slots-3)
                                 as in the reference; 2 (HBM cache): the slot streams again and
                                 C = cache_slots (or pool_slots-3 if < 0), bounded by HBM only */
+    int32_t h2d_split;       /* copy mode: concurrent H2D streams per subgroup (0 or 1: one; 2: two) */
 } tfg_device_options;
 
 typedef struct tfg_tier_observation { /* placement.hpp:138-145 */

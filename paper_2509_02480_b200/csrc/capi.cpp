@@ -644,6 +644,7 @@ int tfg_engine_create(int worker_id, tfg_tier* const* tiers, int n_tiers, const 
             d.device_buffers = device->device_buffers;
             d.zero_copy = device->zero_copy;
             d.d2h_split = device->d2h_split;
+            d.h2d_split = device->h2d_split > 1 ? 2 : 1;
             d.hbm_retain = device->hbm_retain;
         }
         int ndev = 0;

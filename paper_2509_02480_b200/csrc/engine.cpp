@@ -310,6 +310,7 @@ OffloadWorker::~OffloadWorker() {
         cudaStreamSynchronize(s_k_);
         cudaStreamSynchronize(s_d2h_);
         cudaStreamSynchronize(s_d2h2_);
+        cudaStreamSynchronize(s_h2d2_);
     }
     {
         std::lock_guard<std::mutex> g(mu_);
@@ -388,6 +389,7 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaStreamCreateWithFlags(&s_k_, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&s_d2h_, cudaStreamNonBlocking), "cudaStreamCreate");
     cuda_check(cudaStreamCreateWithFlags(&s_d2h2_, cudaStreamNonBlocking), "cudaStreamCreate");
+    cuda_check(cudaStreamCreateWithFlags(&s_h2d2_, cudaStreamNonBlocking), "cudaStreamCreate");
     ring_stride_ = seg_stride(max_params_);
     ring_.assign(static_cast<std::size_t>(dev_.device_buffers), nullptr);
     ring_ready_.assign(ring_.size(), nullptr);
@@ -453,6 +455,7 @@ void OffloadWorker::setup_device() {
         for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_start, &e.d2h_end})
             cuda_check(cudaEventCreate(ev), "cudaEventCreate");
         cuda_check(cudaEventCreateWithFlags(&e.d2h_half, cudaEventDisableTiming), "cudaEventCreate");
+        cuda_check(cudaEventCreateWithFlags(&e.h2d_half, cudaEventDisableTiming), "cudaEventCreate");
     }
     device_ready_ = true;
     completer_ = std::thread([this] { completion_loop(); });
@@ -463,7 +466,8 @@ void OffloadWorker::release_device() {
     if (!device_ready_) return;
     cudaSetDevice(dev_.device);
     for (auto& e : events_)
-        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_start, e.d2h_end, e.d2h_half})
+        for (cudaEvent_t ev : {e.h2d_start, e.h2d_done, e.k_start, e.k_end, e.d2h_start, e.d2h_end, e.d2h_half,
+                               e.h2d_half})
             if (ev) cudaEventDestroy(ev);
     events_.clear();
     for (float* r : ring_) cudaFree(r);
@@ -497,6 +501,7 @@ void OffloadWorker::release_device() {
     cudaStreamDestroy(s_k_);
     cudaStreamDestroy(s_d2h_);
     cudaStreamDestroy(s_d2h2_);
+    cudaStreamDestroy(s_h2d2_);
     device_ready_ = false;
 }
 
@@ -938,7 +943,22 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     if (held < 0) {
         if (hslot >= 0)  // the buffer's previous occupant has been written back
             cuda_check(cudaStreamWaitEvent(s_h2d_, hbm_ready_[static_cast<std::size_t>(hslot)], 0), "wait");
-        copy_state(d, blk, pc, true, s_h2d_);
+        if (dev_.h2d_split > 1 && ds == pc) {
+            // Two concurrent halves on two copy engines: the H2D side of the
+            // duplex link arbitration gets a second queue, like d2h_split.
+            const std::size_t bytes = 12 * pc;
+            const std::size_t half = (bytes / 2) & ~static_cast<std::size_t>(4095);
+            auto* host = reinterpret_cast<const char*>(blk.payload());
+            auto* dev = reinterpret_cast<char*>(d);
+            cuda_check(cudaStreamWaitEvent(s_h2d2_, e.h2d_start, 0), "wait");
+            cuda_check(cudaMemcpyAsync(dev, host, half, cudaMemcpyHostToDevice, s_h2d_), "cudaMemcpyAsync");
+            cuda_check(cudaMemcpyAsync(dev + half, host + half, bytes - half, cudaMemcpyHostToDevice, s_h2d2_),
+                       "cudaMemcpyAsync");
+            cuda_check(cudaEventRecord(e.h2d_half, s_h2d2_), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(s_h2d_, e.h2d_half, 0), "wait");
+        } else {
+            copy_state(d, blk, pc, true, s_h2d_);
+        }
         h2d_bytes += 12 * pc;
     }
     if (!opt_.skip_gradients) {  // baseline flow: fp32 gradients fetched with the state

@@ -78,6 +78,7 @@ struct DeviceOptions {
     int device_buffers = 3;  // depth of the H2D -> kernel -> D2H ring
     int zero_copy = 0;       // 1: the kernel reads/writes the pinned slot over PCIe (no ring, no DMA)
     int d2h_split = 1;       // concurrent D2H copy streams per subgroup (1 or 2)
+    int h2d_split = 1;       // concurrent H2D copy streams per subgroup (1 or 2)
     // Copy mode, 16-bit gradient flow: a subgroup the destination plan retains
     // keeps its updated state in HBM until its next update (no D2H now, no H2D
     // then). 1: the host slot stays reserved and is refreshed on demand, C is
@@ -291,7 +292,7 @@ public:
 private:
     struct DeviceEvents {
         cudaEvent_t h2d_start = nullptr, h2d_done = nullptr, k_start = nullptr, k_end = nullptr,
-                    d2h_start = nullptr, d2h_end = nullptr, d2h_half = nullptr;
+                    d2h_start = nullptr, d2h_end = nullptr, d2h_half = nullptr, h2d_half = nullptr;
     };
     struct Completion {
         SubgroupId id;
@@ -362,7 +363,7 @@ private:
 
     // Device resources.
     bool device_ready_ = false;
-    cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr, s_d2h2_ = nullptr;
+    cudaStream_t s_h2d_ = nullptr, s_k_ = nullptr, s_d2h_ = nullptr, s_d2h2_ = nullptr, s_h2d2_ = nullptr;
     std::vector<float*> ring_;
     std::vector<cudaEvent_t> ring_ready_;  // last D2H out of each ring buffer
     std::size_t ring_next_ = 0;           // round-robin ring cursor

@@ -146,6 +146,8 @@ class DeviceOptions:
     # 1: their host slot stays reserved (C = min(cache_slots, pool_slots - 3));
     # 2: HBM cache, the slot streams again and C = cache_slots.
     hbm_retain: int = 1
+    # concurrent H2D copy streams per subgroup (1 or 2)
+    h2d_split: int = 1
 
 
 @dataclass
@@ -549,7 +551,8 @@ class OffloadWorker:
         h = C.c_void_p()
         o, hy = opt.c(), hyper.c()
         d = _lib.DeviceOptionsC(device.device, device.grad_dtype, device.param_dtype, device.device_buffers,
-                                int(device.zero_copy), device.d2h_split, int(device.hbm_retain))
+                                int(device.zero_copy), device.d2h_split, int(device.hbm_retain),
+                                device.h2d_split)
         _lib.call("tfg_engine_create", worker_id, arr, len(self._tiers), C.byref(o), C.byref(hy),
                   trace.handle if trace else None, C.byref(d), C.byref(h))
         self._h = h

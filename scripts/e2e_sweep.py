@@ -4,7 +4,7 @@ Prints per-phase time, PCIe-stream busy fractions and pipeline gaps from the
 engine's per-subgroup timeline, and writes gpurun_out/e2e_sweep.json.
 
     python scripts/e2e_sweep.py [total_params] [configs...]
-        config = pool:cache:ring:zero_copy:d2h_split[:hbm_retain]
+        config = pool:cache:ring:zero_copy:d2h_split[:hbm_retain[:h2d_split]]
 """
 import json
 import shutil
@@ -21,7 +21,8 @@ from paper_2509_02480_b200 import tierflow as tf  # noqa: E402
 
 total = int(sys.argv[1]) if len(sys.argv) > 1 else 6_738_415_616
 configs = [tuple(int(x) for x in c.split(":")) for c in sys.argv[2:]] or [(12, 5, 3, 0, 1, 1), (12, 5, 3, 0, 1, 0)]
-configs = [c if len(c) == 6 else c + (1,) for c in configs]
+configs = [c if len(c) >= 6 else c + (1,) for c in configs]
+configs = [c if len(c) == 7 else c + (1,) for c in configs]
 sub = 100_000_000
 sizes = [min(sub, total - k * sub) for k in range((total + sub - 1) // sub)]
 import os
@@ -47,11 +48,11 @@ for name in tier_set:
         pr = tiers[-1].probe_bandwidth(256 << 20, 3)
         print(f"{name} probe r={pr.read_bw/1e9:.2f} w={pr.write_bw/1e9:.2f} GB/s", flush=True)
 out = []
-for pool, cache, ring, zc, split, hbm in configs:
+for pool, cache, ring, zc, split, hbm, hsplit in configs:
     trace = tf.EventTrace()
     w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=pool, cache_slots=cache,
                                                             lock_dir=str(root / "locks")),
-                         tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, ring, zc, split, hbm))
+                         tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, ring, zc, split, hbm, hsplit))
     for k, n in enumerate(sizes):
         w.add_subgroup(k, n)
     t0 = time.time()
@@ -72,14 +73,15 @@ for pool, cache, ring, zc, split, hbm in configs:
         phases.append(dict(ms=ms, span=span, h2d_busy=h2d_busy, d2h_busy=d2h_busy, h2d_gaps=h2d_gaps,
                            hits=st.cache_hits, alloc=st.flush_allocation, kernel_ms=st.kernel_seconds * 1e3,
                            h2d_bytes=st.h2d_bytes, d2h_bytes=st.d2h_bytes))
-        print(f"pool={pool} cache={cache} ring={ring} zc={zc} split={split} hbm={hbm} phase {it}: {ms:7.1f} ms (device span {span:7.1f}) "
+        print(f"pool={pool} cache={cache} ring={ring} zc={zc} split={split} hbm={hbm} h2dsplit={hsplit} phase {it}: {ms:7.1f} ms (device span {span:7.1f}) "
               f"h2d busy {h2d_busy:7.1f} gaps {h2d_gaps:6.1f} d2h busy {d2h_busy:7.1f} hits {st.cache_hits} "
               f"alloc {st.flush_allocation} h2d {st.h2d_bytes/1e9:.1f} GB d2h {st.d2h_bytes/1e9:.1f} GB", flush=True)
         if it == 6:
             Path("gpurun_out").mkdir(exist_ok=True)
-            Path(f"gpurun_out/timeline_{'_'.join(tier_set)}_p{pool}_c{cache}_r{ring}_z{zc}_s{split}_h{hbm}.json").write_text(json.dumps(tl))
+            Path(f"gpurun_out/timeline_{'_'.join(tier_set)}_p{pool}_c{cache}_r{ring}_z{zc}_s{split}_h{hbm}_u{hsplit}.json").write_text(json.dumps(tl))
     steady = phases[3:]
-    out.append(dict(pool=pool, cache=cache, ring=ring, zero_copy=zc, d2h_split=split, hbm_retain=hbm, init_s=init_s,
+    out.append(dict(pool=pool, cache=cache, ring=ring, zero_copy=zc, d2h_split=split, hbm_retain=hbm, h2d_split=hsplit,
+                    init_s=init_s,
                     ms=statistics.mean(p["ms"] for p in steady), phases=phases))
     w.close()
     del w
