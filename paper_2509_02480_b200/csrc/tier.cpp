@@ -693,8 +693,11 @@ ProbeResult Tier::probe_bandwidth(std::uint64_t probe_bytes, int repetitions) {
             std::memcpy(buf.base(), mirror.base(), bytes);
             rsec = clamp(since(t0));
         } else {
+            // The warm-up repetition creates the file; the measured ones overwrite
+            // its blocks in place, the pattern of the engine's steady state
+            // (subgroup files are rewritten or recycled, not re-created).
             bool direct = false;
-            int fd = open_file(path, O_WRONLY | O_CREAT | O_TRUNC, true, direct);
+            int fd = open_file(path, O_WRONLY | O_CREAT | (rep == 0 ? O_TRUNC : 0), true, direct);
             if (fd < 0) throw IoError(err_ctx() + ": probe failure, cannot write under " + spec_.root);
             auto t0 = Clock::now();
             try {
