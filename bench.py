@@ -464,7 +464,7 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
         shutil.rmtree(root)
     root.mkdir(parents=True)
     nvme = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4))
-    probe = nvme.probe_bandwidth(256 << 20, 3)
+    probe = nvme.probe_bandwidth(1 << 30, 3)
     # Host DRAM tier: data moves by block exchange, its transfer cost is the PCIe leg.
     dram_bw = min(pcie["h2d"], pcie["d2h"])
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", dram_bw, dram_bw))
@@ -558,7 +558,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
                                 lock_device=lock_dev)),
             tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
                                 lock_device=lock_dev))]
-    probes = [t.probe_bandwidth(256 << 20, 3) for t in dirs]
+    probes = [t.probe_bandwidth(1 << 30, 3) for t in dirs]
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=dram_cap * block))
     tiers = [dram] + dirs
     trace = tf.EventTrace()

@@ -701,7 +701,7 @@ ProbeResult Tier::probe_bandwidth(std::uint64_t probe_bytes, int repetitions) {
             if (fd < 0) throw IoError(err_ctx() + ": probe failure, cannot write under " + spec_.root);
             auto t0 = Clock::now();
             try {
-                io_all(fd, buf.base(), bytes, 0, true, err_ctx());
+                striped(fd, buf.base(), bytes, 0, true, kPageBytes);  // as the engine moves a subgroup
                 if (::fdatasync(fd) != 0) throw IoError(err_ctx() + ": probe fdatasync failed");
             } catch (...) {
                 ::close(fd);
@@ -714,7 +714,7 @@ ProbeResult Tier::probe_bandwidth(std::uint64_t probe_bytes, int repetitions) {
             if (fd < 0) throw IoError(err_ctx() + ": probe failure, cannot read back probe file");
             t0 = Clock::now();
             try {
-                io_all(fd, buf.base(), bytes, 0, false, err_ctx());
+                striped(fd, buf.base(), bytes, 0, false, kPageBytes);
             } catch (...) {
                 ::close(fd);
                 throw;

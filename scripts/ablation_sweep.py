@@ -70,11 +70,11 @@ for name, caching, skip, atomic, multi, pool, cache, hbm in ladder:
                                   lock_device=1))
         t1_ = tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0, 0, io_parallelism=4,
                                   lock_device=1))
-        t0_.probe_bandwidth(256 << 20, 3)
+        t0_.probe_bandwidth(1 << 30, 3)
     else:
         t0_ = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9))
         t1_ = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=4))
-    t1_.probe_bandwidth(256 << 20, 3)
+    t1_.probe_bandwidth(1 << 30, 3)
     dram, nvme = t0_, t1_
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, enable_caching=caching, skip_gradients=skip,
                              atomic_rw=atomic, multi_path=multi, lock_dir=str(root / "locks"))

@@ -45,7 +45,7 @@ for name in tier_set:
     else:
         raise SystemExit(f"unknown tier {name}")
     if name != "dram":
-        pr = tiers[-1].probe_bandwidth(256 << 20, 3)
+        pr = tiers[-1].probe_bandwidth(1 << 30, 3)
         print(f"{name} probe r={pr.read_bw/1e9:.2f} w={pr.write_bw/1e9:.2f} GB/s", flush=True)
 out = []
 for pool, cache, ring, zc, split, hbm, hsplit in configs:

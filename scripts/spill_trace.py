@@ -29,7 +29,7 @@ tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0, 0,
          tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0, 0, io_parallelism=iopar,
                              lock_device=lock_device))]
 for t in tiers:
-    pr = t.probe_bandwidth(256 << 20, 3)
+    pr = t.probe_bandwidth(1 << 30, 3)
     print(f"tier {t.id()} probe r={pr.read_bw / 1e9:.2f} w={pr.write_bw / 1e9:.2f}", flush=True)
 trace = tf.EventTrace()
 w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks")),
