@@ -22,13 +22,20 @@ cache = int(sys.argv[3]) if len(sys.argv) > 3 else 6
 iopar = int(sys.argv[4]) if len(sys.argv) > 4 else 4
 hbm = int(sys.argv[5]) if len(sys.argv) > 5 else 2
 lock_device = int(sys.argv[6]) if len(sys.argv) > 6 else 0
+dram_cap = int(sys.argv[7]) if len(sys.argv) > 7 else 0  # > 0: a host-DRAM tier capped at this many subgroups
 root = ROOT / "gpurun_out" / "spill_trace_tiers"
 shutil.rmtree(root, ignore_errors=True)
-tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=iopar,
+off = 1 if dram_cap > 0 else 0
+tiers = [tf.Tier(tf.TierSpec(off, tf.TierKind.local_dir, str(root / "nvme"), 0, 0, io_parallelism=iopar,
                              lock_device=lock_device)),
-         tf.Tier(tf.TierSpec(1, tf.TierKind.remote_dir, str(root / "remote"), 0, 0, io_parallelism=iopar,
+         tf.Tier(tf.TierSpec(off + 1, tf.TierKind.remote_dir, str(root / "remote"), 0, 0, io_parallelism=iopar,
                              lock_device=lock_device))]
+if dram_cap > 0:
+    block = 4096 * ((32 + 12 * 100_000_000 + 4095) // 4096)
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=dram_cap * block))] + tiers
 for t in tiers:
+    if t.spec().kind == tf.TierKind.host_dram:
+        continue
     pr = t.probe_bandwidth(1 << 30, 3)
     print(f"tier {t.id()} probe r={pr.read_bw / 1e9:.2f} w={pr.write_bw / 1e9:.2f}", flush=True)
 trace = tf.EventTrace()
