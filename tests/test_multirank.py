@@ -58,10 +58,13 @@ def _worker(rank, world, port, sizes, seed, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("sizes", [[4096] * 4, [4096, 4096, 4096, 1000, 777]])
-def test_gradient_exchange_parity_world2(sizes):
+@pytest.mark.parametrize("world,sizes", [(2, [4096] * 4), (2, [4096, 4096, 4096, 1000, 777]),
+                                         (3, [4096, 4096, 1000, 777, 3000]), (4, [2048] * 8)])
+def test_gradient_exchange_parity(world, sizes):
+    """World 2-4 over gloo: even shards (one reduce_scatter) and uneven ones
+    (one reduce per subgroup to its owner, as C4's 86/87 split at N=8)."""
     import oracle
-    world, seed = 2, 9
+    seed = 9
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
