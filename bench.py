@@ -533,7 +533,7 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
 # (hbm_retain=2). Tier-bound; bounded sample.
 
 
-def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=3, pool=8, ring=4,
+def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=4, pool=8, ring=4,
               lock_shared=True):
     import torch
     dev = torch.cuda.current_device()
