@@ -573,3 +573,45 @@ def test_engine_returns_every_host_block(tf, cuda, lock_dir, tmp_path, hbm, skip
     gc.collect()
     assert tf.host_blocks_live() == base
     assert tf.host_block_free_failures() == 0
+
+
+@pytest.mark.parametrize("hbm", [1, 2])
+def test_tier_read_failure_surfaces_and_engine_stays_consistent(tf, cuda, lock_dir, tmp_path, hbm):
+    """Fault injection (reference scheduler.hpp:689-693): a subgroup file that
+    vanished from its directory tier fails its prefetch; run_update raises the
+    tier's error, the subgroup stays on its tier, no slot is left mid-transfer,
+    and the engine can be closed without leaking a host block."""
+    import gc
+    import os
+    gc.collect()
+    base = tf.host_blocks_live()
+    params = [40_000] * 6
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=4, cache_slots=1, lock_dir=lock_dir,
+                                                      deadlock_timeout_s=10.0),
+                         tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    w.set_fixed_ratio([1.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(5)
+    w.run_backward_sim(0, tf.SyntheticGradSource(5))
+    w.run_update(0)
+    on_dir = [sg for sg in range(len(params)) if w.meta(sg).residency == tf.Residency.on_tier and w.meta(sg).tier == 1]
+    assert on_dir
+    victim = on_dir[0]
+    f = tmp_path / "d" / f"sg_{victim:06d}.bin"
+    os.rename(f, str(f) + ".away")
+    w.run_backward_sim(1, tf.SyntheticGradSource(5))
+    with pytest.raises((tf.PlacementInconsistencyError, tf.IoError)):
+        w.run_update(1)
+    m = w.meta(victim)
+    assert m.residency == tf.Residency.on_tier and m.tier == 1
+    time.sleep(0.5)  # let the device work issued before the failure retire
+    host, per_tier = w.residency_census()
+    assert host + sum(per_tier) <= sum(params)
+    assert all(w.pool_state(s)[0] != tf.SlotState.prefetching for s in range(4))
+    w.close()
+    del w, tiers
+    gc.collect()
+    assert tf.host_blocks_live() == base
