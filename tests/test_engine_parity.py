@@ -615,3 +615,38 @@ def test_tier_read_failure_surfaces_and_engine_stays_consistent(tf, cuda, lock_d
     del w, tiers
     gc.collect()
     assert tf.host_blocks_live() == base
+
+
+def test_tier_write_failure_keeps_state_in_host_slots(tf, cuda, lock_dir, tmp_path):
+    """Fault injection (reference scheduler.hpp:730-733): flushes to a tier
+    whose directory vanished fail; run_update raises IoError and every
+    subgroup that failed to flush is still host-cached in its slot with its
+    updated state, so no state is lost."""
+    import gc
+    import shutil
+    gc.collect()
+    params = [30_000] * 5
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=8, cache_slots=0, lock_dir=lock_dir,
+                                                      deadlock_timeout_s=10.0),
+                         tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 2, 0, 1, 0))
+    w.set_fixed_ratio([1.0, 0.0])  # init: everything on host DRAM
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(8)
+    w.set_fixed_ratio([0.0, 1.0])  # phase 0 flushes everything to the directory tier ...
+    shutil.rmtree(tmp_path / "d")  # ... which is gone
+    (tmp_path / "d").write_text("not a directory")
+    w.run_backward_sim(0, tf.SyntheticGradSource(8))
+    with pytest.raises(tf.IoError):
+        w.run_update(0)
+    time.sleep(0.5)
+    failed = [sg for sg in range(len(params)) if w.meta(sg).residency == tf.Residency.host_cached]
+    assert failed  # their updated state stayed in the pool
+    for sg in failed:
+        n = params[sg]
+        p, m, v, _, _ = oracle.adam_fused(oracle.synthetic_params(n, 8, sg), np.zeros(n, np.float32),
+                                          np.zeros(n, np.float32), oracle.synthetic_grads(n, 8, sg, 0), 0, 0, 1)
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32))
+    w.close()
