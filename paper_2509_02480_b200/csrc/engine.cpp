@@ -1122,6 +1122,12 @@ int OffloadWorker::wait_host_resident(SubgroupId id) {
                 break;
             }
             if (sg.residency == Residency::host_cached) {
+                if (sg.slot < 0 && wb_held_.count(id) != 0 && adopt_wb_held_locked(id) < 0) {
+                    l.unlock();
+                    wait_pool_free();
+                    l.lock();
+                    continue;
+                }
                 ++cache_hits_this_phase_;
                 trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
                 need_grad_fetch = !opt_.skip_gradients && grad_tier_.count(id) != 0;
@@ -1147,6 +1153,8 @@ std::shared_future<IoStats> OffloadWorker::enqueue_flush(SubgroupId id, TierId d
     std::lock_guard<std::mutex> g(mu_);
     Subgroup& sg = subgroups_.at(id);
     if (sg.residency != Residency::host_cached) throw Error("enqueue_flush: subgroup not host-resident");
+    if (sg.slot < 0 && wb_held_.count(id) != 0 && adopt_wb_held_locked(id) < 0)
+        throw Error("enqueue_flush: no host slot free for subgroup " + std::to_string(id));
     if (sg.slot < 0 && !(hbm_cache_mode() && hbm_slot_[index_of_.at(id)] >= 0 && reserve_writeback_slot_locked(id) >= 0))
         throw Error("enqueue_flush: no host slot free for the write-back of subgroup " + std::to_string(id));
     if (!hbm_slot_.empty()) writeback_hbm_copy_locked(index_of_.at(id), sg.slot);
@@ -1181,8 +1189,11 @@ void OffloadWorker::read_current_state(SubgroupId id, float* out) {
         pc = sg.param_count;
         if (sg.residency == Residency::host_cached) {
             const int b = hbm_slot_.empty() ? -1 : hbm_slot_[index_of_.at(id)];
+            const auto held = wb_held_.find(id);
             if (b >= 0)
                 device_state_to_host(hbm_cache_[static_cast<std::size_t>(b)], out, pc);
+            else if (sg.slot < 0 && held != wb_held_.end())
+                std::memcpy(out, wb_blocks_[static_cast<std::size_t>(held->second)].payload(), 12 * pc);
             else
                 std::memcpy(out, pool_->block(sg.slot).payload(), 12 * pc);
             return;
@@ -1228,6 +1239,11 @@ void OffloadWorker::pump_locked() {
     while (frontier_ < order_.size()) {
         const SubgroupId id = order_[frontier_];
         Subgroup& sg = subgroups_.at(id);
+        if (sg.residency == Residency::host_cached && sg.slot < 0 && wb_held_.count(id) != 0) {
+            if (adopt_wb_held_locked(id) < 0) break;  // its slot, in plan order
+            ++frontier_;
+            continue;
+        }
         if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) {
             ++frontier_;
             continue;
@@ -1314,19 +1330,11 @@ std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, Tie
                 pool_->flush_failed(slot);
             } else {
                 // Write-back failed: the state is only in the write-back block.
-                // Adopt it into a free pool slot (block exchange) if one is free.
+                // The subgroup stays host-cached there until a pool slot adopts
+                // it (now if one is free, else in plan order by pump_locked).
                 s.residency = Residency::host_cached;
-                const int ps = pool_->try_reserve(id);
-                if (ps >= 0) {
-                    std::swap(pool_->block(ps), wb_blocks_[static_cast<std::size_t>(wb)]);
-                    pool_->prefetch_done(ps);
-                    s.slot = ps;
-                    wb_free_.push_back(wb);
-                    wb_cv_.notify_all();
-                } else if (!completion_error_) {
-                    completion_error_ = std::make_exception_ptr(IoError(
-                        "write-back of subgroup " + std::to_string(id) + " failed and no pool slot is free to hold it"));
-                }
+                wb_held_[id] = wb;
+                adopt_wb_held_locked(id);
             }
         }
         if (stale) stale->remove_subgroup(id);
@@ -1336,6 +1344,22 @@ std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, Tie
                    .share();
     flush_futures_.emplace_back(id, fut);
     return fut;
+}
+
+// Moves a failed write-back's block into a free pool slot (block exchange).
+// Called with mu_ held; the slot, or -1 if none is free.
+int OffloadWorker::adopt_wb_held_locked(SubgroupId id) {
+    const auto it = wb_held_.find(id);
+    if (it == wb_held_.end()) return subgroups_.at(id).slot;
+    const int ps = pool_->try_reserve(id);
+    if (ps < 0) return -1;
+    std::swap(pool_->block(ps), wb_blocks_[static_cast<std::size_t>(it->second)]);
+    pool_->prefetch_done(ps);
+    subgroups_.at(id).slot = ps;
+    wb_free_.push_back(it->second);
+    wb_held_.erase(it);
+    wb_cv_.notify_all();
+    return ps;
 }
 
 // HBM cache mode write-back thread: pairs each deferred hit (kernel issued,

@@ -393,6 +393,10 @@ private:
     std::condition_variable wb_cv_;   // wb_free_ / wb_pending_ / hbm_free_ changed (with mu_)
     bool wb_stop_ = false;
     int wb_inflight_ = 0;  // deferred write-backs whose HBM buffer is not yet free
+    // A write-back whose flush failed keeps its state in its block until a
+    // pool slot adopts it (in plan order, pump_locked); id -> block.
+    std::unordered_map<SubgroupId, int> wb_held_;
+    int adopt_wb_held_locked(SubgroupId id);
     std::thread wb_thread_;
     float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H
     // baseline flow: pinned D2H staging of fp32 gradients, a few in rotation so

@@ -650,3 +650,51 @@ def test_tier_write_failure_keeps_state_in_host_slots(tf, cuda, lock_dir, tmp_pa
                                           np.zeros(n, np.float32), oracle.synthetic_grads(n, 8, sg, 0), 0, 0, 1)
         assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32))
     w.close()
+
+
+def test_hbm_cache_writeback_failure_recovers(tf, cuda, lock_dir, tmp_path):
+    """HBM cache mode: the write-back lane's flushes fail (tier directory
+    gone); the written-back state survives in the lane's blocks or pool slots,
+    reads back exactly, and once the tier is repaired the next phases run on
+    and end bit-exact with the oracle (no subgroup lost or double-updated)."""
+    import shutil
+    params = [30_000, 31_000, 32_000, 33_000, 34_000, 35_000]
+    seed = 12
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=3, cache_slots=3, lock_dir=lock_dir,
+                                                      deadlock_timeout_s=10.0),
+                         tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 2, 0, 1, 2))
+    w.set_fixed_ratio([1.0, 0.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+
+    def want(sg, steps):
+        n = params[sg]
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(steps):
+            p, m, v, _, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        return np.concatenate([p, m, v]).view(np.uint32)
+
+    w.run_backward_sim(0, tf.SyntheticGradSource(seed))
+    w.run_update(0)  # ascending: 3, 4, 5 retained in HBM
+    w.set_fixed_ratio([0.0, 1.0])
+    shutil.rmtree(tmp_path / "d")
+    (tmp_path / "d").write_text("not a directory")
+    w.run_backward_sim(1, tf.SyntheticGradSource(seed))
+    with pytest.raises(tf.IoError):
+        w.run_update(1)  # descending: hits 5, 4, 3 written back through the lane -> fail
+    time.sleep(0.5)
+    for sg in (3, 4, 5):
+        assert w.meta(sg).residency == tf.Residency.host_cached
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), want(sg, 2))
+    (tmp_path / "d").unlink()
+    (tmp_path / "d").mkdir()
+    w.set_fixed_ratio([1.0, 1.0])
+    for it in (2, 3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        w.run_update(it)
+    for sg in range(len(params)):
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), want(sg, 4)), sg
+    w.close()
