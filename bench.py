@@ -156,6 +156,24 @@ def barrier(world):
         dist.barrier()
 
 
+def allmin(world, x: float) -> float:
+    return -allmax(world, -x)
+
+
+def setup_all_ranks(world, fn):
+    """Runs one rank's setup; every rank learns whether all succeeded before
+    anyone enters the leg's per-phase barriers, so a failure on one rank ends
+    the leg everywhere instead of leaving the others waiting."""
+    err = None
+    try:
+        out = fn()
+    except Exception as exc:  # reported below on every rank
+        out, err = None, exc
+    if allmin(world, 0.0 if err else 1.0) < 1.0:
+        raise RuntimeError(f"setup failed on a rank: {err}" if err else "setup failed on another rank")
+    return out
+
+
 def allmax(world, x: float) -> float:
     if world == 1:
         return x
@@ -470,12 +488,16 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", dram_bw, dram_bw))
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=str(root / "locks"))
-    w = tf.OffloadWorker(rank, [dram, nvme], opt, tf.AdamHyper(), trace,
-                         tf.DeviceOptions(dev, DT, DT, ring, 0, 1, hbm_retain))
-    for k, n in enumerate(sizes):
-        w.add_subgroup(base_id + k, n)
     t0 = time.time()
-    w.init_and_flush_all(seed)
+
+    def setup():
+        w = tf.OffloadWorker(rank, [dram, nvme], opt, tf.AdamHyper(), trace,
+                             tf.DeviceOptions(dev, DT, DT, ring, 0, 1, hbm_retain))
+        for k, n in enumerate(sizes):
+            w.add_subgroup(base_id + k, n)
+        w.init_and_flush_all(seed)
+        return w
+    w = setup_all_ranks(world, setup)
     init_s = time.time() - t0
     log(f"[rank {rank}] e2e init {init_s:.1f}s, nvme probe r={probe.read_bw/1e9:.2f} w={probe.write_bw/1e9:.2f} GB/s,"
         f" pcie h2d={pcie['h2d']/1e9:.1f} d2h={pcie['d2h']/1e9:.1f} GB/s")
@@ -543,6 +565,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     # bounded by the disk the ranks share: at most half the free space
     free = shutil.disk_usage(root).free
     M = max(2, min(len(sizes), 12, int(0.5 * free / world // (12 * max(sizes) + 4096))))
+    M = int(allmin(world, M))  # the same sample on every rank
     sizes = sizes[:M]
     cache = M // 2
     dram_cap = max(1, (M - cache) // 3)  # host DRAM capped: Eq. 1 spills the rest to the directory tiers
@@ -563,10 +586,14 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     tiers = [dram] + dirs
     trace = tf.EventTrace()
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
-    w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2))
-    for k, n in enumerate(sizes):
-        w.add_subgroup(base_id + k, n)
-    w.init_and_flush_all(seed)
+
+    def setup():
+        w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2))
+        for k, n in enumerate(sizes):
+            w.add_subgroup(base_id + k, n)
+        w.init_and_flush_all(seed)
+        return w
+    w = setup_all_ranks(world, setup)
     src = tf.SyntheticGradSource(seed)
     phases = []
     for it in range(warmup + steps):
@@ -749,6 +776,11 @@ def main(argv=None):
     elif not a.skip_e2e:
         try:
             e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots, a.hbm_retain)
+            # every rank streams the same shard shape (MemAvailable is read at slightly different times)
+            n_e = int(allmin(world, len(e_sizes)))
+            pool = int(allmin(world, pool))
+            cache = int(allmin(world, cache)) if cache >= 0 else cache
+            e_sizes = e_sizes[:n_e]
             if len(e_sizes) < len(sizes) or pool != a.pool_slots:
                 log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank, "
                     f"pool {pool}, cache {cache}")
