@@ -7,6 +7,7 @@
 //   16-17               cp.async double buffer
 //   21-23               scalar elements at higher occupancy
 //   32-37               TMA multistage pipeline, every warp computing
+//   38-40               per-warp TMA pipelines (no CTA barrier)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -299,6 +300,121 @@ cudaError_t launch_tma_pipe(const AdamLaunch& a, cudaStream_t stream) {
 }
 
 // ---------------------------------------------------------------------------
+// Per-warp TMA pipelines: every warp owns a ring of S stages of 128 params
+// (one quad per lane; 1.75 KiB) and its own mbarriers. Lane 0 keeps S-1 of
+// the warp's tiles in flight with cp.async.bulk; the warp consumes a stage,
+// __syncwarp, and lane 0 refills that same stage. No CTA-wide barrier: warps
+// never wait for one another, and the bytes in flight per SM (32 warps x
+// (S-1) x 1.75 KiB) do not depend on how long the FP64 chain takes.
+template <int S, bool WD, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    adam_warp_pipe_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                          const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t ntiles, AdamConsts c,
+                          unsigned long long* __restrict__ counters) {
+    constexpr int T = 128;                  // params per warp tile
+    constexpr int kStage = T * 14;          // bytes per stage
+    constexpr int kWarps = kThreads / 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    unsigned char* mine_smem = smem + static_cast<size_t>(warp) * S * kStage;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + static_cast<size_t>(kWarps) * S * kStage) + warp * S;
+    if (lane == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // Warp-global tile index: tile j of this warp is gw + j * (grid warps).
+    const uint64_t gw = static_cast<uint64_t>(blockIdx.x) * kWarps + warp;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kWarps;
+    const uint64_t mine = ntiles > gw ? (ntiles - 1 - gw) / stride + 1 : 0;
+    auto stage_p = [&](int s) { return reinterpret_cast<float*>(mine_smem + s * kStage); };
+    auto issue = [&](uint64_t k) {
+        const int s = static_cast<int>(k % S);
+        const uint64_t off = (gw + k * stride) * T;
+        float* sp = stage_p(s);
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(kStage));
+        bulk_load(sp, p + off, 4u * T, &full[s]);
+        bulk_load(sp + T, m + off, 4u * T, &full[s]);
+        bulk_load(sp + 2 * T, v + off, 4u * T, &full[s]);
+        bulk_load(sp + 3 * T, g + off, 2u * T, &full[s]);
+    };
+    if (lane == 0)
+        for (uint64_t k = 0; k + 1 < static_cast<uint64_t>(S) && k < mine; ++k) issue(k);
+    unsigned nonfinite = 0, overflow = 0;
+    for (uint64_t k = 0; k < mine; ++k) {
+        if (lane == 0 && k + S - 1 < mine) issue(k + S - 1);  // the stage of tile k-1, retired by the __syncwarp
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
+        const uint64_t off = (gw + k * stride) * T;
+        const float* sp = stage_p(s);
+        float4 rp = reinterpret_cast<const float4*>(sp)[lane];
+        float4 rm = reinterpret_cast<const float4*>(sp + T)[lane];
+        float4 rv = reinterpret_cast<const float4*>(sp + 2 * T)[lane];
+        const uint2 graw = reinterpret_cast<const uint2*>(sp + 3 * T)[lane];
+        __syncwarp();  // every lane has its quad in registers: the stage may be refilled
+        U16x4 gh;
+        gh.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
+        gh.y = static_cast<uint16_t>(graw.x >> 16);
+        gh.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
+        gh.w = static_cast<uint16_t>(graw.y >> 16);
+        nonfinite += nonfinite16<kF16>(gh.x) + nonfinite16<kF16>(gh.y) + nonfinite16<kF16>(gh.z) +
+                     nonfinite16<kF16>(gh.w);
+        adam_element<WD, true>(rp.x, rm.x, rv.x, widen16<kF16>(gh.x), c);
+        adam_element<WD, true>(rp.y, rm.y, rv.y, widen16<kF16>(gh.y), c);
+        adam_element<WD, true>(rp.z, rm.z, rv.z, widen16<kF16>(gh.z), c);
+        adam_element<WD, true>(rp.w, rm.w, rv.w, widen16<kF16>(gh.w), c);
+        U16x4 h;
+        h.x = narrow16<kF16>(rp.x);
+        h.y = narrow16<kF16>(rp.y);
+        h.z = narrow16<kF16>(rp.z);
+        h.w = narrow16<kF16>(rp.w);
+        overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
+        __stcs(reinterpret_cast<float4*>(p + off) + lane, rp);
+        __stcs(reinterpret_cast<float4*>(m + off) + lane, rm);
+        __stcs(reinterpret_cast<float4*>(v + off) + lane, rv);
+        store_u16x4(p16 + off + 4 * lane, h);
+    }
+    if (counters != nullptr) {
+        warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+template <int S, int MINB>
+cudaError_t launch_warp_pipe(const AdamLaunch& a, cudaStream_t stream) {
+    constexpr int T = 128;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
+                           reinterpret_cast<uintptr_t>(a.p16)) & 15u) == 0;
+    if (!aligned || a.n_peers > 0 || a.p_out || a.grad_kind != kF16 || a.out_kind != kF16)
+        return cudaErrorInvalidValue;
+    const uint64_t ntiles = a.n / T;
+    constexpr size_t smem = static_cast<size_t>(kThreads / 32) * S * (T * 14 + sizeof(uint64_t));
+    if (ntiles > 0) {
+        auto kern = a.c.lr_wd != 0.0 ? adam_warp_pipe_kernel<S, true, MINB> : adam_warp_pipe_kernel<S, false, MINB>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        const uint64_t warps = (ntiles + 0);  // one warp per tile at most
+        const unsigned grid = static_cast<unsigned>(
+            std::min<uint64_t>((warps + kThreads / 32 - 1) / (kThreads / 32), static_cast<uint64_t>(num_sms()) * MINB));
+        kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, ntiles, a.c,
+                                               a.counters);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    const uint64_t done = ntiles * T;
+    if (done == a.n) return cudaSuccess;
+    AdamLaunch tail = a;
+    tail.p += done;
+    tail.m += done;
+    tail.v += done;
+    tail.g = static_cast<const uint16_t*>(a.g) + done;
+    tail.p16 += done;
+    tail.n = a.n - done;
+    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
+}
+
+// ---------------------------------------------------------------------------
 // cp.async double-buffered variant: each thread copies its NEXT quad of P, m,
 // v, g into its own shared-memory slots with cp.async (LDGSTS, no registers
 // held) before computing the current one, so memory latency overlaps the FP64
@@ -461,6 +577,9 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 35) return launch_tma_pipe<3, 3>(a, stream);
     if constexpr (V == 36) return launch_tma_pipe<3, 4, true>(a, stream);
     if constexpr (V == 37) return launch_tma_pipe<2, 4, true>(a, stream);
+    if constexpr (V == 38) return launch_warp_pipe<3, 4>(a, stream);
+    if constexpr (V == 39) return launch_warp_pipe<2, 4>(a, stream);
+    if constexpr (V == 40) return launch_warp_pipe<4, 3>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -508,10 +627,13 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 35: return launch_variant<35>(a, stream);
         case 36: return launch_variant<36>(a, stream);
         case 37: return launch_variant<37>(a, stream);
+        case 38: return launch_variant<38>(a, stream);
+        case 39: return launch_variant<39>(a, stream);
+        case 40: return launch_variant<40>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 38; }
+int adam_variant_count() { return 41; }
 
 }  // namespace tfb
