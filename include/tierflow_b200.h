@@ -110,6 +110,9 @@ typedef struct tfg_device_options {
                                 as in the reference; 2 (HBM cache): the slot streams again and
                                 C = cache_slots (or pool_slots-3 if < 0), bounded by HBM only */
     int32_t h2d_split;       /* copy mode: concurrent H2D streams per subgroup (0 or 1: one; 2: two) */
+    int32_t hbm_cache_slots; /* hbm_retain 2: HBM buffers for retained subgroups; 0 = all of C. Fewer
+                                than C makes a two-level cache: the rest keep their host slots, and
+                                C = min(cache_slots, hbm_cache_slots + pool_slots - 3) */
 } tfg_device_options;
 
 typedef struct tfg_tier_observation { /* placement.hpp:138-145 */

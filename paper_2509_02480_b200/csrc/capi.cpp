@@ -645,6 +645,8 @@ int tfg_engine_create(int worker_id, tfg_tier* const* tiers, int n_tiers, const 
             d.zero_copy = device->zero_copy;
             d.d2h_split = device->d2h_split;
             d.h2d_split = device->h2d_split > 1 ? 2 : 1;
+            if (device->hbm_cache_slots < 0) throw tfb::ConfigError("hbm_cache_slots must be >= 0");
+            d.hbm_cache_slots = device->hbm_cache_slots;
             d.hbm_retain = device->hbm_retain;
         }
         int ndev = 0;

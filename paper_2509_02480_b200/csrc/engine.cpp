@@ -369,7 +369,9 @@ std::vector<int> OffloadWorker::tier_caps() const {
 int OffloadWorker::retention_capacity() const {
     const int M = static_cast<int>(ids_.size());
     if (dev_.hbm_retain == 2 && dev_.zero_copy == 0 && opt_.skip_gradients && opt_.enable_caching) {
-        const int wanted = opt_.cache_slots < 0 ? opt_.pool_slots - 3 : opt_.cache_slots;
+        int wanted = opt_.cache_slots < 0 ? opt_.pool_slots - 3 : opt_.cache_slots;
+        if (dev_.hbm_cache_slots > 0)  // two-level: the host part keeps three slots streaming
+            wanted = std::min(wanted, dev_.hbm_cache_slots + std::max(0, opt_.pool_slots - 3));
         return std::clamp(wanted, 0, M);
     }
     return opt_.retention_capacity(M);
@@ -424,7 +426,8 @@ void OffloadWorker::setup_device() {
                "cudaMalloc");
     hbm_slot_.assign(ids_.size(), -1);
     if (dev_.hbm_retain != 0 && dev_.zero_copy == 0 && opt_.skip_gradients) {
-        const int cap = retention_capacity();
+        int cap = retention_capacity();
+        if (dev_.hbm_retain == 2 && dev_.hbm_cache_slots > 0) cap = std::min(cap, dev_.hbm_cache_slots);
         hbm_cache_.assign(static_cast<std::size_t>(cap), nullptr);
         hbm_ready_.assign(hbm_cache_.size(), nullptr);
         for (std::size_t b = 0; b < hbm_cache_.size(); ++b) {
@@ -744,6 +747,18 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         std::lock_guard<std::mutex> g(mu_);
         const int cap = retention_capacity();
         dests_ = std::make_unique<DestinationPlan>(order_, cap, placement_bandwidths(), tier_caps());
+        if (hbm_cache_mode()) {
+            // Newly retained subgroups take HBM buffers while there are any:
+            // the free ones plus those the flushed HBM-held hits release.
+            int released = 0, wanted = 0;
+            for (const SubgroupId sid : order_) {
+                const std::size_t k = index_of_.at(sid);
+                const bool keep = dests_->assign_storage_tier(sid).host_retain;
+                if (hbm_slot_[k] >= 0 && !keep) ++released;
+                if (hbm_slot_[k] < 0 && keep) ++wanted;
+            }
+            hbm_budget_ = std::min(wanted, static_cast<int>(hbm_free_.size()) + released);
+        }
         stats.retained = dests_->retained_count();
         stats.flush_allocation = dests_->flush_allocation().counts;
         frontier_ = 0;
@@ -915,13 +930,21 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     if (!hbm_cache_.empty()) {
         std::unique_lock<std::mutex> l(mu_);
         const bool retain = dests_->assign_storage_tier(id).host_retain;
-        // HBM cache mode: a buffer is on its way back from a deferred
-        // write-back; wait for it rather than fall back to the host path.
-        while (retain && hslot < 0 && hbm_free_.empty() && wb_inflight_ > 0) {
-            if (completion_error_) std::rethrow_exception(completion_error_);
-            wb_cv_.wait_for(l, std::chrono::milliseconds(50));
-        }
-        if (retain && hslot < 0 && !hbm_free_.empty()) {
+        if (hbm_cache_mode()) {
+            // HBM cache: a newly retained subgroup within this phase's budget
+            // waits for the buffer a deferred write-back is returning; beyond
+            // the budget (two-level cache) it is retained in its host slot.
+            const bool take = retain && hslot < 0 && hbm_budget_ > 0;
+            while (take && hbm_free_.empty() && wb_inflight_ > 0) {
+                if (completion_error_) std::rethrow_exception(completion_error_);
+                wb_cv_.wait_for(l, std::chrono::milliseconds(50));
+            }
+            if (take && !hbm_free_.empty()) {
+                hslot = hbm_free_.front();
+                hbm_free_.pop_front();
+                --hbm_budget_;
+            }
+        } else if (retain && hslot < 0 && !hbm_free_.empty()) {
             // FIFO: the buffer whose write-back was queued first drains first
             hslot = hbm_free_.front();
             hbm_free_.pop_front();

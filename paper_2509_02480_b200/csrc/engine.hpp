@@ -79,6 +79,9 @@ struct DeviceOptions {
     int zero_copy = 0;       // 1: the kernel reads/writes the pinned slot over PCIe (no ring, no DMA)
     int d2h_split = 1;       // concurrent D2H copy streams per subgroup (1 or 2)
     int h2d_split = 1;       // concurrent H2D copy streams per subgroup (1 or 2)
+    // hbm_retain 2: HBM buffers for retained subgroups (0: all of C). Fewer
+    // than C gives a two-level cache, the rest retained in host slots.
+    int hbm_cache_slots = 0;
     // Copy mode, 16-bit gradient flow: a subgroup the destination plan retains
     // keeps its updated state in HBM until its next update (no D2H now, no H2D
     // then). 1: the host slot stays reserved and is refreshed on demand, C is
@@ -396,6 +399,9 @@ private:
     // A write-back whose flush failed keeps its state in its block until a
     // pool slot adopts it (in plan order, pump_locked); id -> block.
     std::unordered_map<SubgroupId, int> wb_held_;
+    // Two-level cache: HBM buffers this phase's newly retained subgroups may
+    // still take (the rest stay in their host slots). Guarded by mu_.
+    int hbm_budget_ = 0;
     int adopt_wb_held_locked(SubgroupId id);
     std::thread wb_thread_;
     float* grad32_dev_ = nullptr;    // baseline flow: widened gradients before the D2H

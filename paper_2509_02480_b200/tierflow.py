@@ -148,6 +148,9 @@ class DeviceOptions:
     hbm_retain: int = 1
     # concurrent H2D copy streams per subgroup (1 or 2)
     h2d_split: int = 1
+    # hbm_retain 2: HBM buffers for retained subgroups (0: all of C); fewer
+    # gives a two-level cache, the rest retained in host slots
+    hbm_cache_slots: int = 0
 
 
 @dataclass
@@ -552,7 +555,7 @@ class OffloadWorker:
         o, hy = opt.c(), hyper.c()
         d = _lib.DeviceOptionsC(device.device, device.grad_dtype, device.param_dtype, device.device_buffers,
                                 int(device.zero_copy), device.d2h_split, int(device.hbm_retain),
-                                device.h2d_split)
+                                device.h2d_split, device.hbm_cache_slots)
         _lib.call("tfg_engine_create", worker_id, arr, len(self._tiers), C.byref(o), C.byref(hy),
                   trace.handle if trace else None, C.byref(d), C.byref(h))
         self._h = h

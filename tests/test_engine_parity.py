@@ -698,3 +698,46 @@ def test_hbm_cache_writeback_failure_recovers(tf, cuda, lock_dir, tmp_path):
     for sg in range(len(params)):
         assert np.array_equal(w.read_current_state(sg).view(np.uint32), want(sg, 4)), sg
     w.close()
+
+
+def test_two_level_cache_hbm_plus_host_slots(tf, cuda, lock_dir, tmp_path):
+    """DeviceOptions.hbm_cache_slots < C: part of the retention capacity is
+    held in HBM, the rest in host slots (two cache levels). Same hits and bits
+    as the reference's host retention; fewer PCIe bytes than host-only
+    retention, more than an all-HBM cache."""
+    params = [50_000, 52_000, 54_000, 56_000, 58_000, 60_000]
+    seed, C = 19, 4
+    S = sum(params)
+
+    def run(hbm, hbm_slots):
+        tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+                 tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / f"d{hbm}{hbm_slots}"), 2e9, 2e9))]
+        w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=5, cache_slots=C, lock_dir=lock_dir),
+                             tf.AdamHyper(), tf.EventTrace(),
+                             tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm, 1, hbm_slots))
+        w.set_fixed_ratio([1.0, 1.0])
+        for i, n in enumerate(params):
+            w.add_subgroup(i, n)
+        w.init_and_flush_all(seed)
+        hits, pcie = [], []
+        for it in range(4):
+            w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+            st = w.run_update(it)
+            hits.append(st.cache_hits)
+            pcie.append(st.h2d_bytes + st.d2h_bytes)
+        states = [w.read_current_state(sg).view(np.uint32).copy() for sg in range(len(params))]
+        w.close()
+        return hits, pcie, states
+
+    two_hits, two_pcie, two_states = run(2, 2)  # C = min(4, 2 + 5 - 3) = 4: 2 in HBM, 2 in host slots
+    all_hits, all_pcie, _ = run(2, 0)
+    host_hits, host_pcie, _ = run(0, 0)  # reference host retention: C = min(4, 5 - 3) = 2
+    assert two_hits == all_hits == [0, C, C, C]
+    assert host_hits == [0, 2, 2, 2]
+    assert all(p < 2 * 12 * S for p in two_pcie[1:])
+    assert all(a < t for a, t in zip(all_pcie[1:], two_pcie[1:]))
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(4):
+            p, m, v, _, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        assert np.array_equal(two_states[sg], np.concatenate([p, m, v]).view(np.uint32)), sg
