@@ -23,6 +23,7 @@ iopar = int(sys.argv[4]) if len(sys.argv) > 4 else 4
 hbm = int(sys.argv[5]) if len(sys.argv) > 5 else 2
 lock_device = int(sys.argv[6]) if len(sys.argv) > 6 else 0
 dram_cap = int(sys.argv[7]) if len(sys.argv) > 7 else 0  # > 0: a host-DRAM tier capped at this many subgroups
+hbm_slots = int(sys.argv[8]) if len(sys.argv) > 8 else 0  # > 0: two-level cache, this many of C in HBM
 root = ROOT / "gpurun_out" / "spill_trace_tiers"
 shutil.rmtree(root, ignore_errors=True)
 off = 1 if dram_cap > 0 else 0
@@ -40,7 +41,7 @@ for t in tiers:
     print(f"tier {t.id()} probe r={pr.read_bw / 1e9:.2f} w={pr.write_bw / 1e9:.2f}", flush=True)
 trace = tf.EventTrace()
 w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks")),
-                     tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 4, 0, 1, hbm))
+                     tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 4, 0, 1, hbm, 1, hbm_slots))
 for k in range(M):
     w.add_subgroup(k, 100_000_000)
 w.init_and_flush_all(42)
