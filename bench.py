@@ -567,8 +567,11 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     M = max(2, min(len(sizes), 12, int(0.5 * free / world // (12 * max(sizes) + 4096))))
     M = int(allmin(world, M))  # the same sample on every rank
     sizes = sizes[:M]
-    cache = M // 2
-    dram_cap = max(1, (M - cache) // 3)  # host DRAM capped: Eq. 1 spills the rest to the directory tiers
+    # Two-level retention inside the same host budget: M/2 subgroups in HBM
+    # and 2 of the pool's 8 slots retain too (DeviceOptions.hbm_cache_slots).
+    hbm_c = M // 2
+    cache = hbm_c + max(0, min(2, M - hbm_c - 1))
+    dram_cap = max(1, (M - cache) // 2)  # host DRAM capped: Eq. 1 spills the rest to the directory tiers
     block = 4096 * ((32 + 12 * max(sizes) + 4095) // 4096)
     for d in ("nvme", "remote"):
         (root / d).mkdir()
@@ -588,7 +591,8 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
 
     def setup():
-        w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2))
+        w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace,
+                             tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2, 1, hbm_c))
         for k, n in enumerate(sizes):
             w.add_subgroup(base_id + k, n)
         w.init_and_flush_all(seed)
@@ -631,8 +635,8 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     dev_w = max(pr.write_bw for pr in probes)
     serial_s = sum(t["read_bytes"] for t in per_tier) / dev_r + sum(t["write_bytes"] for t in per_tier) / dev_w
     bound_s = serial_s if same_device else parallel_s
-    return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, pool=pool, same_device=same_device,
-                lock_device=lock_dev, dram_cap=dram_cap,
+    return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, hbm_cache=hbm_c, pool=pool,
+                same_device=same_device, lock_device=lock_dev, dram_cap=dram_cap,
                 bound_ms=bound_s * 1e3, independent_bound_ms=parallel_s * 1e3, per_tier=per_tier,
                 hits=statistics.mean(p[1].cache_hits for p in phases),
                 alloc=phases[-1][1].flush_allocation, launches=steps * M)
@@ -813,12 +817,13 @@ def main(argv=None):
                      "independent_tier_bound_ms": round(r["independent_bound_ms"], 1),
                      "tiers_share_one_device": r["same_device"], "device_semaphore": bool(r["lock_device"]),
                      "per_tier": r["per_tier"],
-                     "subgroups_per_rank": r["subgroups"], "hbm_cache_slots": r["cache"], "pool_slots": r["pool"],
+                     "subgroups_per_rank": r["subgroups"], "cache_slots": r["cache"],
+                     "hbm_cache_slots": r["hbm_cache"], "pool_slots": r["pool"],
                      "dram_tier_capacity_subgroups": r["dram_cap"],
                      "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"],
                      "gpu_launches": r["launches"],
                      "path": "C ABI tfg_engine_run_update, tiers [host_dram capped, local_dir O_DIRECT, "
-                             "remote_dir O_DIRECT], retention in HBM (hbm_retain=2)"}
+                             "remote_dir O_DIRECT], retention in HBM + host slots (hbm_retain=2, two-level)"}
         except Exception as exc:
             spill = {"error": f"{type(exc).__name__}: {exc}"}
             log(f"spill leg failed: {exc}")
