@@ -38,6 +38,7 @@ ladder = [
     ("+atomic_rw", True, True, True, False, 16, c_host, 0),
     ("+multi_path (MLP-Offload)", True, True, True, True, 16, c_host, 0),
     ("+HBM cache (B200)", True, True, True, True, 16, c_hbm, 2),
+    ("+two-level HBM + host (B200)", True, True, True, True, 16, c_hbm + c_host, 2),
 ]
 import os
 import subprocess
@@ -78,7 +79,9 @@ for name, caching, skip, atomic, multi, pool, cache, hbm in ladder:
     dram, nvme = t0_, t1_
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, enable_caching=caching, skip_gradients=skip,
                              atomic_rw=atomic, multi_path=multi, lock_dir=str(root / "locks"))
-    w = tf.OffloadWorker(0, [dram, nvme], opt, tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 12, 0, 1, hbm))
+    hbm_slots = c_hbm if name.startswith("+two-level") else 0
+    w = tf.OffloadWorker(0, [dram, nvme], opt, tf.AdamHyper(), tf.EventTrace(),
+                         tf.DeviceOptions(0, 0, 0, 12, 0, 1, hbm, 1, hbm_slots))
     for k, n in enumerate(sizes):
         w.add_subgroup(k, n)
     w.init_and_flush_all(42)
