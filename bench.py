@@ -174,6 +174,17 @@ def setup_all_ranks(world, fn):
     return out
 
 
+def allsum(world, x: float) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
 def allmax(world, x: float) -> float:
     if world == 1:
         return x
@@ -470,7 +481,12 @@ def e2e_shard(sizes, world, pool_slots, cache_slots, hbm_retain=2):
 
 
 def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring,
-            hbm_retain=1):
+            hbm_retain=1, peer=None):
+    """peer: a parallel.PeerGradients holding every rank's contribution to
+    every subgroup (--exchange fused): the engine's owned subgroups are bound
+    to the world's contributions, so each update reduces them over CUDA IPC
+    / NVLink inside the kernel; the contributions are the backward's output,
+    written once before the timed phases."""
     # The bandwidth EMA re-places subgroups off the slow directory tier over the
     # first phases (paper §3.3); time the converged pipeline.
     warmup = max(warmup, 5)
@@ -496,6 +512,8 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
         for k, n in enumerate(sizes):
             w.add_subgroup(base_id + k, n)
         w.init_and_flush_all(seed)
+        if peer is not None:
+            peer.bind(w, [base_id + k for k in range(len(sizes))])
         return w
     w = setup_all_ranks(world, setup)
     init_s = time.time() - t0
@@ -504,7 +522,8 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     src = tf.SyntheticGradSource(seed)
     phases = []
     for it in range(warmup + steps):
-        w.run_backward_sim(it, src, 1)  # the backward's output: device-resident 16-bit gradients
+        if peer is None:
+            w.run_backward_sim(it, src, 1)  # the backward's output: device-resident 16-bit gradients
         barrier(world)
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -642,6 +661,40 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
                 alloc=phases[-1][1].flush_allocation, launches=steps * M)
 
 
+def e2e_exchange(tf, sizes, a, rank, world):
+    """e2e with the fused reduce-scatter (strong scaling over one model): each
+    rank streams the subgroups it owns through the engine, their gradients the
+    in-kernel sum of every rank's contribution."""
+    import torch
+
+    from paper_2509_02480_b200 import parallel
+    begin, count = parallel.shard(len(sizes), world, rank)
+    owned = sizes[begin:begin + count]
+    e_sizes, pool, cache = e2e_shard(owned, world, a.pool_slots, a.cache_slots, a.hbm_retain)
+    n_e = int(allmin(world, len(e_sizes)))
+    pool = int(allmin(world, pool))
+    cache = int(allmin(world, cache)) if cache >= 0 else cache
+    e_sizes = e_sizes[:n_e]
+    with parallel.PeerGradients(sizes, world, rank, device=torch.cuda.current_device(),
+                                dtype="bf16" if DT else "f16") as pg:
+        for sg in range(begin, begin + n_e) if world == 1 else range(len(sizes)):
+            tf.synthetic_grads(pg.local(sg).view(torch.int16), a.seed + 100 * rank, sg, 0, dtype=DT)
+        torch.cuda.synchronize()
+        barrier(world)  # every contribution written before any owner reads it
+        r = e2e_leg(tf, e_sizes, begin, a.steps, a.warmup, a.seed, rank, world, a.tier_root, pool, cache, a.ring,
+                    a.hbm_retain, peer=pg)
+        barrier(world)  # no rank frees its contribution while a peer may still read it
+    e_ms = allmax(world, r["ms"])
+    total = allsum(world, r["params"])
+    return {"value": total / (e_ms / 1e3), "unit": "params/s", "h2d_bytes_per_step": r["h2d"],
+            "d2h_bytes_per_step": r["d2h"], "ms_per_step": e_ms, "pipeline_bound_ms": round(r["bound_ms"], 1),
+            "pipeline_frac": round(r["bound_ms"] / e_ms, 4), "cache_hits_per_phase": r["hits"],
+            "subgroups_per_rank": n_e, "pool_slots": pool, "cache_slots": cache, "gpu_launches": r["launches"],
+            "gradient_sources": world,
+            "path": "C ABI tfg_engine_run_update with bind_grad_sources (fused reduce-scatter over CUDA IPC), "
+                    "tiers [host_dram pinned, local_dir O_DIRECT]"}
+
+
 # ---------------------------------------------------------------------------
 # reference CPU engine (oracle/_ref), bounded sample
 
@@ -775,8 +828,14 @@ def main(argv=None):
                                            if dl.get("copy_sustained_gbs") else None)}
 
     e2e = None
-    if a.exchange != "none":
-        e2e = {"skipped": "the --exchange mode times the device-resident update with the in-phase reduce-scatter"}
+    if a.exchange == "nccl":
+        e2e = {"skipped": "--exchange nccl times the device-resident update only"}
+    elif a.exchange == "fused" and not a.skip_e2e:
+        try:
+            e2e = e2e_exchange(tf, sizes, a, rank, world)
+        except Exception as exc:
+            e2e = {"error": f"{type(exc).__name__}: {exc}"}
+            log(f"e2e leg failed: {exc}")
     elif not a.skip_e2e:
         try:
             e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots, a.hbm_retain)
