@@ -461,8 +461,8 @@ def e2e_shard(sizes, world, pool_slots, cache_slots, hbm_retain=2):
     hbm_cache = hbm_retain == 2 and cache_slots >= 0
     extra = WRITEBACK_BLOCKS if hbm_cache else 0
 
-    def cache_for(n):  # a shrunk shard keeps the requested retained fraction
-        return min(cache_slots, n * cache_slots // len(sizes)) if hbm_cache else 0
+    def cache_for(n):  # a shrunk shard keeps the requested retained fraction, at most 3/7 of it
+        return min(cache_slots, n * cache_slots // len(sizes), 3 * n // 7) if hbm_cache else 0
 
     def need(pool, n):  # retained in HBM: no host block
         return pool + extra + n - cache_for(n)
