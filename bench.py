@@ -607,7 +607,10 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=dram_cap * block))
     tiers = [dram] + dirs
     trace = tf.EventTrace()
-    opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(root / "locks"))
+    # One lock directory for every rank of the node: with lock_device, the
+    # ranks' tiers on one physical disk share one semaphore (the paper's
+    # node-level contention control) even though their paths are partitioned.
+    opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(Path(tier_root) / "spill_locks"))
 
     def setup():
         w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace,
