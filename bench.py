@@ -655,7 +655,11 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     # is charged at that rate.
     dev_r = max(pr.read_bw for pr in probes)
     dev_w = max(pr.write_bw for pr in probes)
-    serial_s = sum(t["read_bytes"] for t in per_tier) / dev_r + sum(t["write_bytes"] for t in per_tier) / dev_w
+    # Every rank's tier roots sit under the one tier_root, i.e. on the same
+    # device: the node's bytes share it.
+    rb_all = allsum(world, sum(t["read_bytes"] for t in per_tier))
+    wb_all = allsum(world, sum(t["write_bytes"] for t in per_tier))
+    serial_s = rb_all / dev_r + wb_all / dev_w
     bound_s = serial_s if same_device else parallel_s
     return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, hbm_cache=hbm_c, pool=pool,
                 same_device=same_device, lock_device=lock_dev, dram_cap=dram_cap,
