@@ -581,11 +581,16 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     root = Path(tier_root) / f"spill_rank{rank}"
     shutil.rmtree(root, ignore_errors=True)
     root.mkdir(parents=True)
-    # bounded by the disk the ranks share: at most half the free space
+    # 12 subgroups per rank, bounded by the disk the ranks share (at most half
+    # its free space): when N ranks' full-size subgroups do not fit, the
+    # subgroups shrink rather than the sample (params/s stays comparable).
     free = shutil.disk_usage(root).free
-    M = max(2, min(len(sizes), 12, int(0.5 * free / world // (12 * max(sizes) + 4096))))
-    M = int(allmin(world, M))  # the same sample on every rank
-    sizes = sizes[:M]
+    M = min(len(sizes), 12)
+    sub = min(max(sizes), int(0.5 * free / world / M // 12) // 4096 * 4096)
+    sub = int(allmin(world, sub))  # the same sample on every rank
+    if sub < 1_000_000:
+        raise RuntimeError(f"not enough free disk for the spill sample ({free / 1e9:.1f} GB)")
+    sizes = [sub] * M
     # Two-level retention inside the same host budget: M/2 subgroups in HBM
     # and 2 of the pool's 8 slots retain too (DeviceOptions.hbm_cache_slots).
     hbm_c = M // 2
@@ -661,7 +666,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     wb_all = allsum(world, sum(t["write_bytes"] for t in per_tier))
     serial_s = rb_all / dev_r + wb_all / dev_w
     bound_s = serial_s if same_device else parallel_s
-    return dict(ms=ms, params=sum(sizes), subgroups=M, cache=cache, hbm_cache=hbm_c, pool=pool,
+    return dict(ms=ms, params=sum(sizes), subgroups=M, subgroup_params=sub, cache=cache, hbm_cache=hbm_c, pool=pool,
                 same_device=same_device, lock_device=lock_dev, dram_cap=dram_cap,
                 bound_ms=bound_s * 1e3, independent_bound_ms=parallel_s * 1e3, per_tier=per_tier,
                 hits=statistics.mean(p[1].cache_hits for p in phases),
@@ -883,7 +888,8 @@ def main(argv=None):
                      "independent_tier_bound_ms": round(r["independent_bound_ms"], 1),
                      "tiers_share_one_device": r["same_device"], "device_semaphore": bool(r["lock_device"]),
                      "per_tier": r["per_tier"],
-                     "subgroups_per_rank": r["subgroups"], "cache_slots": r["cache"],
+                     "subgroups_per_rank": r["subgroups"], "subgroup_params": r["subgroup_params"],
+                     "cache_slots": r["cache"],
                      "hbm_cache_slots": r["hbm_cache"], "pool_slots": r["pool"],
                      "dram_tier_capacity_subgroups": r["dram_cap"],
                      "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"],
