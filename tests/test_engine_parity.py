@@ -741,3 +741,45 @@ def test_two_level_cache_hbm_plus_host_slots(tf, cuda, lock_dir, tmp_path):
         for it in range(4):
             p, m, v, _, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
         assert np.array_equal(two_states[sg], np.concatenate([p, m, v]).view(np.uint32)), sg
+
+
+def test_reference_c1_shape_sampled(tf, cuda, lock_dir, tmp_path):
+    """BASELINE configs[0] shape (1B params as 8 x 125M subgroups, host DRAM +
+    one file tier, 3 Adam iterations, reference pool 5 / C = 2) through the
+    engine. The inputs at 4096 sampled positions per subgroup come from the
+    device generators (bit-exact with the oracle's, test_oracle_golden /
+    test_kernel_parity), their Adam chain from the CPU oracle."""
+    import torch
+    n, M, seed, iters = 125_000_000, 8, 42, 3
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9, io_parallelism=4))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=5, lock_dir=lock_dir), tf.AdamHyper(),
+                         tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 3))
+    w.set_fixed_ratio([1.0, 1.0])
+    for sg in range(M):
+        w.add_subgroup(sg, n)
+    w.init_and_flush_all(seed)
+    hits = []
+    for it in range(iters):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        hits.append(w.run_update(it).cache_hits)
+    assert hits == [0, 2, 2]  # reference survey probe of C1: hits 0/2/2
+    idx = np.random.default_rng(3).integers(0, n, 4096)
+    ti = torch.from_numpy(idx).to(cuda)
+    p_d = torch.empty(n, device=cuda)
+    z = torch.empty(n, device=cuda)
+    g_d = torch.empty(n, dtype=torch.int16, device=cuda)
+    for sg in range(M):
+        tf.synthetic_state(p_d, z, z, seed, sg)
+        p = p_d[ti].cpu().numpy()
+        m = np.zeros(idx.size, np.float32)
+        v = np.zeros(idx.size, np.float32)
+        for it in range(iters):
+            tf.synthetic_grads(g_d, seed, sg, it)
+            g = g_d[ti].cpu().numpy().view(np.uint16)
+            p, m, v, _, _ = oracle.adam_fused(p, m, v, g, 0, 0, it + 1)
+        got = w.read_current_state(sg).view(np.uint32)
+        assert np.array_equal(got[idx], p.view(np.uint32)), sg
+        assert np.array_equal(got[n + idx], m.view(np.uint32)), sg
+        assert np.array_equal(got[2 * n + idx], v.view(np.uint32)), sg
+    w.close()
