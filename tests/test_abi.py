@@ -169,3 +169,15 @@ int main(int argc, char** argv) {
             p, m, v, _, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
         want.append(np.concatenate([p, m, v]).view(np.uint32))
     assert np.array_equal(got, np.concatenate(want))
+
+
+def test_integration_c_example_compiles(tmp_path):
+    """The C caller shown in INTEGRATION.md §3 compiles against the header."""
+    import re
+    text = (ROOT / "INTEGRATION.md").read_text()
+    code = re.search(r"```c\n(.*?)```", text, re.S).group(1).replace('#include "tierflow_b200.h"\n', "")
+    src = tmp_path / "integ.c"
+    src.write_text('#include <stdio.h>\n#include <stdint.h>\n#include "tierflow_b200.h"\n'
+                   "int main(void) {\nint iters = 2;\n" + code + "\nreturn 0;\n}\n")
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"), "-c", str(src),
+                    "-o", str(tmp_path / "integ.o")], check=True)
