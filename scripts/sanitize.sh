@@ -9,6 +9,31 @@ python -m paper_2509_02480_b200.build > gpurun_out/build.log 2>&1 || exit 1
 make -s -C oracle >> gpurun_out/build.log 2>&1
 timeout 900 $CS --tool memcheck --leak-check full --error-exitcode 9 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/san_memcheck_smoke.log 2>&1
 echo "memcheck smoke rc=$?"; tail -3 gpurun_out/san_memcheck_smoke.log
+cat > /tmp/san_engine.py <<'PY'
+# HBM cache mode (write-back lane) and the ZeRO-3 baseline flow (gradient stages), 3 phases each
+import sys, tempfile, os
+sys.path.insert(0, ".")
+from paper_2509_02480_b200 import tierflow as tf
+for hbm, skip in ((2, True), (0, False)):
+    with tempfile.TemporaryDirectory() as d:
+        tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+                 tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, os.path.join(d, "n"), 2e9, 2e9))]
+        w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=4, cache_slots=2, lock_dir=os.path.join(d, "l"),
+                                                          skip_gradients=skip),
+                             tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+        w.set_fixed_ratio([1.0, 1.0])
+        for i in range(5):
+            w.add_subgroup(i, 40_000 + 3 * i)
+        w.init_and_flush_all(1)
+        for it in range(3):
+            w.run_backward_sim(it, tf.SyntheticGradSource(1))
+            w.run_update(it)
+        w.close()
+        del w, tiers
+print("engine modes ok", tf.host_blocks_live(), tf.host_block_free_failures())
+PY
+timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_engine.py > gpurun_out/san_memcheck_engine.log 2>&1
+echo "memcheck engine modes rc=$?"; tail -3 gpurun_out/san_memcheck_engine.log
 cat > /tmp/san_kernels.py <<'PY'
 import sys
 sys.path.insert(0, ".")
