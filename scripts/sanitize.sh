@@ -53,9 +53,9 @@ tf.adam_fused_multi(st[:n], st[n:2*n], st[2*n:], srcs, p16, 2, tf.AdamHyper())
 torch.cuda.synchronize()
 print("kernels ok")
 PY
-timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,1,12,16,32,36 > gpurun_out/san_memcheck_kernels.log 2>&1
+timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,1,12,16,32,36,38 > gpurun_out/san_memcheck_kernels.log 2>&1
 echo "memcheck kernels rc=$?"; tail -3 gpurun_out/san_memcheck_kernels.log
-timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 12,13,16,32,33,36 > gpurun_out/san_racecheck.log 2>&1
+timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 12,13,16,32,33,36,38,39 > gpurun_out/san_racecheck.log 2>&1
 echo "racecheck rc=$?"; tail -3 gpurun_out/san_racecheck.log
-timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 12,16,32,36 > gpurun_out/san_synccheck.log 2>&1
+timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 12,16,32,36,38 > gpurun_out/san_synccheck.log 2>&1
 echo "synccheck rc=$?"; tail -3 gpurun_out/san_synccheck.log
