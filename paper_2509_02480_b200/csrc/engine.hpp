@@ -17,6 +17,13 @@
 // completion thread retires finished subgroups (slot back to cached, lazy
 // flush or retention, frontier pump) exactly where the reference's
 // coordinator would after adam_step returns.
+//
+// Retention can live in HBM (DeviceOptions::hbm_retain): retained subgroups
+// keep their updated state in HBM buffers between phases. In the HBM cache
+// mode (2) their host slots stream again; a retained subgroup the next plan
+// flushes is written back through a small lane of pinned blocks by its own
+// thread and stream, so the misses' H2D starts at phase begin; with
+// hbm_cache_slots < C the cache is two-level (the rest kept in host slots).
 #pragma once
 
 #include <cuda_runtime.h>
