@@ -783,3 +783,57 @@ def test_reference_c1_shape_sampled(tf, cuda, lock_dir, tmp_path):
         assert np.array_equal(got[n + idx], m.view(np.uint32)), sg
         assert np.array_equal(got[2 * n + idx], v.view(np.uint32)), sg
     w.close()
+
+
+@pytest.mark.parametrize("kind,wd", [(0, 0.01), (1, 0.0), (1, 0.05)])
+def test_everything_on_matches_oracle(tf, cuda, lock_dir, tmp_path, kind, wd):
+    """All the B200 extensions at once: bf16 or f16 gradients and working
+    params, AdamW, two-level HBM + host retention, a capacity-capped host-DRAM
+    tier beside two directory tiers on one device semaphore, ragged subgroups,
+    gradient accumulation, a skipped (non-finite) iteration. Bits and hits as
+    the oracle says."""
+    params = [70_001, 65_536, 33_333, 90_000, 12_345, 80_000, 44_444]
+    seed, accum = 27, 2
+    block = 4096 * ((32 + 12 * max(params) + 4095) // 4096)
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=2 * block)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "n"), 3e9, 3e9, io_parallelism=2,
+                                 lock_device=1)),
+             tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(tmp_path / "r"), 1e9, 1e9, lock_device=1))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=5, cache_slots=4, lock_dir=lock_dir),
+                         tf.AdamHyper(weight_decay=wd), tf.EventTrace(),
+                         tf.DeviceOptions(0, kind, kind, 3, 0, 1, 2, 1, 2))
+    w.set_fixed_ratio([5.0, 2.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    applied = []
+    for it in range(5):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed), accum)
+        if it == 2:  # a poisoned gradient: the phase is rejected before any mutation
+            import torch
+            buf = torch.as_tensor(_DevView(w.grad_buffer(3), params[3]), device=cuda)
+            buf[17] = 0x7C00 if kind == 0 else 0x7F80  # +Inf
+            torch.cuda.synchronize()
+            assert not w.gradients_finite()
+            with pytest.raises(tf.GradientOverflowError):
+                w.run_update(it)
+            continue
+        st = w.run_update(it)
+        assert st.flush_allocation[0] <= 2
+        applied.append(it)
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in applied:
+            g = oracle.synthetic_grads(n, seed, sg, it, steps=accum, kind=kind)
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, g, kind, kind, it + 1, weight_decay=wd)
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32)), sg
+        assert np.array_equal(w.read_params16(sg), p16), sg
+    w.close()
+
+
+class _DevView:
+    """__cuda_array_interface__ over an engine-owned 16-bit device buffer."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3,
+                                         "strides": None}
