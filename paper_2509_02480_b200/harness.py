@@ -11,8 +11,9 @@ rebuilt over the C ABI so reference configs and reports carry over.
 
 Config schema = the reference's (config.hpp:150-215: model, tiers[], placement,
 optim, schedule, run, ablation) plus an optional "device" section
-({device, grad_dtype, param_dtype, device_buffers, zero_copy, d2h_split}) and
-the tier kind "host_dram". Semantics follow the reference: ragged last
+({device, grad_dtype, param_dtype, device_buffers, zero_copy, d2h_split,
+hbm_retain, h2d_split, hbm_cache_slots}), the tier kind "host_dram" and the
+per-tier keys lock_device and capacity_gb. Semantics follow the reference: ragged last
 subgroup (config.hpp:77-87), mode-derived ablation flags (config.hpp:91-105),
 lock-dir precedence TIERFLOW_LOCK_DIR > config > tmp (config.hpp:108-112),
 contiguous worker sharding (harness.hpp:118-126), non-finite gradients skip
@@ -58,6 +59,9 @@ class TierConfig:
     probe: bool = False
     probe_mib: float = 8.0
     probe_reps: int = 3
+    # B200 extensions (absent from the reference schema; 0 = reference behaviour)
+    lock_device: int = 0
+    capacity_gb: float = 0.0
 
 
 @dataclass
@@ -170,7 +174,9 @@ class RunConfig:
                                           io_parallelism=int(t.get("io_parallelism", 1)),
                                           persistent=bool(t.get("persistent", kind == "remote_dir")),
                                           probe=bool(t.get("probe", False)), probe_mib=float(t.get("probe_mib", 8.0)),
-                                          probe_reps=int(t.get("probe_reps", 3))))
+                                          probe_reps=int(t.get("probe_reps", 3)),
+                                          lock_device=int(t.get("lock_device", 0)),
+                                          capacity_gb=float(t.get("capacity_gb", 0.0))))
         p = j.get("placement", {})
         c.alpha = float(p.get("alpha", 0.5))
         c.ratio = [float(x) for x in p.get("ratio", [])]
@@ -201,7 +207,9 @@ class RunConfig:
         c.device = tf.DeviceOptions(device=int(d.get("device", 0)), grad_dtype=int(d.get("grad_dtype", tf.F16)),
                                     param_dtype=int(d.get("param_dtype", tf.F16)),
                                     device_buffers=int(d.get("device_buffers", 3)),
-                                    zero_copy=bool(d.get("zero_copy", False)), d2h_split=int(d.get("d2h_split", 1)))
+                                    zero_copy=bool(d.get("zero_copy", False)), d2h_split=int(d.get("d2h_split", 1)),
+                                    hbm_retain=int(d.get("hbm_retain", 1)), h2d_split=int(d.get("h2d_split", 1)),
+                                    hbm_cache_slots=int(d.get("hbm_cache_slots", 0)))
         return c
 
     @staticmethod
@@ -396,7 +404,8 @@ class BenchRunner:
     def _build_tiers(self):
         for i, tc in enumerate(self.cfg.tiers):
             spec = tf.TierSpec(i, KINDS[tc.kind], tc.root or f"{tc.kind}{i}", tc.read_mb_s * 1e6, tc.write_mb_s * 1e6,
-                               tc.io_parallelism, tc.persistent)
+                               tc.io_parallelism, tc.persistent, lock_device=tc.lock_device,
+                               capacity_bytes=int(tc.capacity_gb * 1e9))
             if tc.kind == "host_dram" and spec.read_bw <= 0:
                 spec.read_bw = spec.write_bw = 50e9  # block exchange; the PCIe leg is the transfer cost
             tier = tf.Tier(spec)

@@ -58,6 +58,16 @@ def test_config_parsing_and_validation(H, tmp_path):
             bad.validate()
     with pytest.raises(H.tf.ConfigError):
         H.RunConfig.from_file(tmp_path / "missing.json")
+    # B200 extensions: device section and per-tier keys
+    f.write_text(json.dumps({
+        "model": {"total_params": 1000000, "subgroup_param_count": 300000},
+        "tiers": [{"kind": "host_dram", "capacity_gb": 2.5},
+                  {"kind": "local_dir", "root": "/tmp/tf-y", "lock_device": 1},
+                  {"kind": "remote_dir", "root": "/tmp/tf-z", "lock_device": 1}],
+        "device": {"hbm_retain": 2, "hbm_cache_slots": 3, "h2d_split": 2}}))
+    cfg = H.RunConfig.from_file(f)
+    assert cfg.tiers[0].capacity_gb == 2.5 and cfg.tiers[1].lock_device == cfg.tiers[2].lock_device == 1
+    assert (cfg.device.hbm_retain, cfg.device.hbm_cache_slots, cfg.device.h2d_split) == (2, 3, 2)
     # the reference's own desk configs parse and validate
     for ref in ("desk.json", "local-dirs.json"):
         p = Path("/root/reference/proj/configs") / ref
