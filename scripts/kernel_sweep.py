@@ -12,6 +12,9 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_2509_02480_b200 import tierflow as tf  # noqa: E402
+import bench  # noqa: E402
+
+PEAK = bench.peaks()["hbm_gbs"]  # MEASURED_PEAKS.json when present
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100_000_000
 S = int(sys.argv[2]) if len(sys.argv) > 2 else 8
@@ -65,8 +68,8 @@ for v in range(0, tf.adam_variant_count()):
     stream.synchronize()
     us = a.elapsed_time(b) * 1e3 / (reps * S)
     gbs = 28 * n / (us * 1e-6) / 1e9
-    timing[v] = {"us_per_launch": round(us, 1), "GBs": round(gbs, 1), "frac_of_6422.8": round(gbs / 6422.8, 4)}
-    print(f"variant {v}: {us:8.1f} us/launch  {gbs:7.1f} GB/s  {gbs/6422.8:.3f}", flush=True)
+    timing[v] = {"us_per_launch": round(us, 1), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 4), "peak_GBs": PEAK}
+    print(f"variant {v}: {us:8.1f} us/launch  {gbs:7.1f} GB/s  {gbs/PEAK:.3f}", flush=True)
 # constant-division self-test: bias corrections of the default betas, t = 1..400
 bad = 0
 for t in range(1, 401):
