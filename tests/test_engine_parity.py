@@ -837,3 +837,38 @@ class _DevView:
     def __init__(self, ptr, n):
         self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<i2", "data": (ptr, False), "version": 3,
                                          "strides": None}
+
+
+@pytest.mark.parametrize("hbm", [0, 2])
+def test_tiny_ragged_subgroups_and_narrowing_overflow(tf, cuda, lock_dir, tmp_path, hbm):
+    """Edge cases through the engine: subgroups of 1, 2, 3, 5 and 4099 params
+    (scalar tails only / P % 4 != 0), and a learning rate large enough that
+    the 16-bit working params overflow to Inf: PhaseStats.downscale_overflows
+    equals the oracle's count and the bits still match."""
+    params = [1, 2, 3, 5, 4099, 7]
+    seed, lr = 33, 1.0e5
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=4, cache_slots=2, lock_dir=lock_dir),
+                         tf.AdamHyper(lr=lr), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    w.set_fixed_ratio([1.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    want = {sg: (oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32))
+            for sg, n in enumerate(params)}
+    for it in range(3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        st = w.run_update(it)
+        over = 0
+        for sg, n in enumerate(params):
+            p, m, v = want[sg]
+            p, m, v, p16, o = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1, lr=lr)
+            want[sg] = (p, m, v)
+            over += o
+            if it == 2:
+                assert np.array_equal(w.read_params16(sg), p16), sg
+        assert st.downscale_overflows == over and over > 0
+    for sg, n in enumerate(params):
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate(want[sg]).view(np.uint32)), sg
+    w.close()
