@@ -237,6 +237,32 @@ public:
         check(tfg_engine_wait_host_resident(h_, id, &slot));
         return slot;
     }
+    // The backward's output buffer of a subgroup (16-bit, param_count elements).
+    void* grad_buffer(SubgroupId id) {
+        void* p = nullptr;
+        check(tfg_engine_grad_buffer(h_, id, &p));
+        return p;
+    }
+    void bind_grad_buffer(SubgroupId id, void* device_ptr) { check(tfg_engine_bind_grad_buffer(h_, id, device_ptr)); }
+    // The reduce-scatter fused into the update: every rank's contribution to
+    // this subgroup (e.g. CUDA IPC-mapped peer buffers), summed in rank order.
+    void bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources) {
+        check(tfg_engine_bind_grad_sources(h_, id, sources.data(), static_cast<int>(sources.size())));
+    }
+    // 16-bit working params (the reference's shadow_), device-resident.
+    void* params16_buffer(SubgroupId id) {
+        void* p = nullptr;
+        check(tfg_engine_params16_buffer(h_, id, &p));
+        return p;
+    }
+    std::vector<std::uint16_t> read_params16(SubgroupId id) {
+        std::uint64_t n = 0;
+        for (const auto& [sid, p] : params_)
+            if (sid == id) n = p;
+        std::vector<std::uint16_t> out(n);
+        check(tfg_engine_read_params16(h_, id, out.data()));
+        return out;
+    }
     std::vector<float> read_current_state(SubgroupId id) {
         std::uint64_t n = 0;
         for (const auto& [sid, p] : params_)

@@ -147,6 +147,11 @@ int main(int argc, char** argv) {
         const auto s = w.read_current_state(i);
         std::fwrite(s.data(), sizeof(float), s.size(), f);
     }
+    for (int i = 0; i < 4; ++i) {
+        const auto h = w.read_params16(i);
+        std::fwrite(h.data(), sizeof(std::uint16_t), h.size(), f);
+    }
+    if (w.grad_buffer(0) == nullptr || w.params16_buffer(0) == nullptr) return 6;
     std::fclose(f);
     std::printf("hits %llu\n", hits);
     return 0;
@@ -161,14 +166,19 @@ int main(int argc, char** argv) {
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, (r.returncode, r.stdout, r.stderr)
     assert r.stdout.strip() == "hits 4"  # C = 2 hits in each of the last two phases
-    got = np.fromfile(out_bin, dtype=np.uint32)
-    want = []
+    raw = out_bin.read_bytes()
+    nstate = 4 * 3 * sum(params)
+    got = np.frombuffer(raw[:nstate], dtype=np.uint32)
+    got16 = np.frombuffer(raw[nstate:], dtype=np.uint16)
+    want, want16 = [], []
     for sg, n in enumerate(params):
         p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
         for it in range(iters):
-            p, m, v, _, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
         want.append(np.concatenate([p, m, v]).view(np.uint32))
+        want16.append(p16)
     assert np.array_equal(got, np.concatenate(want))
+    assert np.array_equal(got16, np.concatenate(want16))
 
 
 def test_integration_c_example_compiles(tmp_path):
