@@ -12,9 +12,10 @@ state and fp16 gradients from the reference generators.
 
 Legs of the `ours` line:
   value   device-resident update phase: all 68 subgroups' P/m/v, grads and
-          working params resident in HBM (108 GB), one fused sm_100a kernel
-          per subgroup; CUDA events on the launching stream. Roofline: HBM,
-          28 algorithmic bytes/param.
+          working params resident in HBM (108 GB); as in the engine, a
+          whole-phase non-finite pre-check, then one fused sm_100a kernel per
+          subgroup; CUDA events on the launching stream. Roofline: HBM, 28
+          algorithmic bytes/param for the fused kernel.
   e2e     the same metric through the engine's C ABI with the state on HOST
           tiers (pinned host DRAM + a local O_DIRECT directory tier): prefetch,
           H2D, fused kernel, D2H, flush/retain inside the timed region.
@@ -237,10 +238,22 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
             grads.append(g)
             p16s.append(torch.empty(n, dtype=torch.int16, device=dev))
     counters = torch.zeros(2, dtype=torch.int64, device=dev)
+    sg_counts = torch.zeros(len(sizes), dtype=torch.int64, device=dev)
     hyper = tf.AdamHyper()
     stream.synchronize()
 
     def step(t, events=None):
+        # As the engine's run_update: the whole-phase non-finite pre-check
+        # (every gradient read once, the counts read back on the host) before
+        # any subgroup is mutated, then one fused update per subgroup.
+        with torch.cuda.stream(stream):
+            sg_counts.zero_()
+        for k in range(len(sizes)):
+            tf.count_nonfinite16(grads[k], sg_counts[k:k + 1], DT, stream=stream)
+        with torch.cuda.stream(stream):
+            bad = int(sg_counts.sum().item())  # read back on the launching stream, as the engine does
+        if bad != 0:
+            raise RuntimeError("non-finite gradients in the device leg")
         for k, n in enumerate(sizes):
             st = states[k]
             if events is not None:
@@ -273,7 +286,7 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
         raise RuntimeError("non-finite gradients in the device leg")
     del states, grads, p16s
     torch.cuda.empty_cache()
-    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(sizes), clocks=clk.summary(),
+    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=2 * steps * len(sizes), clocks=clk.summary(),
                 copy_sustained_gbs=sustained_copy_gbs(stream, total_ms))
 
 
