@@ -320,6 +320,12 @@ int tfg_engine_run_backward_sim(tfg_engine* engine, int iteration, uint64_t seed
 int tfg_engine_gradients_finite(tfg_engine* engine, int* out);                              /* :395 */
 int tfg_engine_grad_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);             /* :401 */
 int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_ptr);
+/* The CUDA stream that produces the gradients (backward, reduce-scatter).
+ * run_update and gradients_finite order the engine's streams after the work
+ * queued on it at call time, so no host sync is needed between producing the
+ * gradients and the update. NULL (the default) = the legacy default stream.
+ * (No reference counterpart: the reference's gradients are host memory.) */
+int tfg_engine_set_producer_stream(tfg_engine* engine, void* stream);
 /* Fused data-parallel reduction: the update of `id` consumes the fp32 sum (in
  * order, rounded once to grad_kind) of n (1..8) 16-bit device buffers, e.g.
  * every peer's contribution mapped over NVLink (CUDA IPC). Replaces the

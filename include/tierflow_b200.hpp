@@ -244,6 +244,8 @@ public:
         return p;
     }
     void bind_grad_buffer(SubgroupId id, void* device_ptr) { check(tfg_engine_bind_grad_buffer(h_, id, device_ptr)); }
+    // The stream that produces the gradients; updates are ordered after it.
+    void set_producer_stream(void* cuda_stream) { check(tfg_engine_set_producer_stream(h_, cuda_stream)); }
     // The reduce-scatter fused into the update: every rank's contribution to
     // this subgroup (e.g. CUDA IPC-mapped peer buffers), summed in rank order.
     void bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources) {

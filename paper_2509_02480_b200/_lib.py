@@ -182,6 +182,7 @@ _SIGS = {
     "tfg_engine_gradients_finite": (_i, [_vp, C.POINTER(_i)]),
     "tfg_engine_grad_buffer": (_i, [_vp, C.c_uint32, C.POINTER(_vp)]),
     "tfg_engine_bind_grad_buffer": (_i, [_vp, C.c_uint32, _vp]),
+    "tfg_engine_set_producer_stream": (_i, [_vp, _vp]),
     "tfg_engine_bind_grad_sources": (_i, [_vp, C.c_uint32, C.POINTER(_vp), C.c_int]),
     "tfg_engine_params16_buffer": (_i, [_vp, C.c_uint32, C.POINTER(_vp)]),
     "tfg_engine_run_update": (_i, [_vp, _i, C.POINTER(PhaseStatsC)]),

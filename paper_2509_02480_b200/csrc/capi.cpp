@@ -722,6 +722,13 @@ int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_pt
     });
 }
 
+int tfg_engine_set_producer_stream(tfg_engine* engine, void* stream) {
+    return guarded([&] {
+        need(engine, "engine");
+        engine->w->set_producer_stream(stream ? static_cast<cudaStream_t>(stream) : cudaStreamLegacy);
+    });
+}
+
 int tfg_engine_bind_grad_sources(tfg_engine* engine, uint32_t id, const void* const* device_ptrs, int n) {
     return guarded([&] {
         need(engine, "engine");

@@ -180,7 +180,7 @@ bool HostBufferPool::wait_for_free(std::chrono::milliseconds timeout) {
 TierIoWorker::TierIoWorker(std::shared_ptr<Tier> tier, WorkerId worker, bool use_lock,
                            std::filesystem::path lock_dir, EventTrace* trace)
     : tier_(std::move(tier)), worker_(worker), use_lock_(use_lock), lock_dir_(std::move(lock_dir)), trace_(trace) {
-    thread_ = std::thread([this] { run(); });
+    thread_ = std::thread([this] { serve(); });
 }
 
 TierIoWorker::~TierIoWorker() { shutdown(); }
@@ -188,95 +188,114 @@ TierIoWorker::~TierIoWorker() { shutdown(); }
 std::future<IoStats> TierIoWorker::submit(bool is_prefetch, std::int64_t sg, std::uint64_t bytes_hint,
                                           std::function<IoStats()> transfer, Completion completion) {
     Job job;
-    job.is_prefetch = is_prefetch;
+    job.lane = is_prefetch ? kFetch : kWriteBack;
     job.sg = sg;
     job.bytes_hint = bytes_hint;
     job.transfer = std::move(transfer);
     job.completion = std::move(completion);
-    auto fut = job.promise.get_future();
-    {
-        std::lock_guard<std::mutex> g(mu_);
-        if (stop_) throw Error("tier I/O queue is shut down");
-        (is_prefetch ? prefetch_q_ : flush_q_).push_back(std::move(job));
-    }
-    cv_.notify_one();
-    return fut;
+    std::future<IoStats> result = job.promise.get_future();
+    std::unique_lock<std::mutex> l(mu_);
+    if (closed_) throw Error("tier I/O queue is shut down");
+    lanes_[job.lane].push_back(std::move(job));
+    l.unlock();
+    wake_.notify_one();
+    return result;
+}
+
+// A job that never ran: its owner learns through the completion (state
+// rollback) and the future (the error).
+void TierIoWorker::cancel(Job& job) {
+    if (job.completion) job.completion(false, IoStats{});
+    job.promise.set_exception(std::make_exception_ptr(Error("tier I/O queue shut down, operation cancelled")));
 }
 
 void TierIoWorker::shutdown() {
-    {
-        std::lock_guard<std::mutex> g(mu_);
-        if (stop_) return;
-        stop_ = true;
-    }
-    cv_.notify_all();
+    std::unique_lock<std::mutex> l(mu_);
+    if (closed_) return;
+    closed_ = true;
+    l.unlock();
+    wake_.notify_all();
     if (thread_.joinable()) thread_.join();
-    std::deque<Job> left;
-    {
-        std::lock_guard<std::mutex> g(mu_);
-        left.swap(prefetch_q_);
-        for (auto& j : flush_q_) left.push_back(std::move(j));
-        flush_q_.clear();
-    }
-    for (auto& j : left) {
-        if (j.completion) j.completion(false, IoStats{});
-        j.promise.set_exception(std::make_exception_ptr(Error("tier I/O queue shut down, operation cancelled")));
-    }
-}
-
-void TierIoWorker::run() {
-    for (;;) {
-        Job job;
-        {
-            std::unique_lock<std::mutex> l(mu_);
-            cv_.wait(l, [&] { return stop_ || !prefetch_q_.empty() || !flush_q_.empty(); });
-            if (prefetch_q_.empty() && flush_q_.empty()) {
-                if (stop_) return;
-                continue;
-            }
-            auto& q = prefetch_q_.empty() ? flush_q_ : prefetch_q_;  // prefetches first
-            job = std::move(q.front());
-            q.pop_front();
+    // The thread drains both lanes before it exits; a job that still shows up
+    // here raced the close and is cancelled.
+    for (auto& lane : lanes_) {
+        while (!lane.empty()) {
+            Job j = std::move(lane.front());
+            lane.pop_front();
+            cancel(j);
         }
-        execute(job);
     }
 }
 
-void TierIoWorker::execute(Job& job) {
-    const EventKind start = job.is_prefetch ? EventKind::prefetch_start : EventKind::flush_start;
-    const EventKind end = job.is_prefetch ? EventKind::prefetch_end : EventKind::flush_end;
-    std::optional<TierLockGuard> guard;
-    try {
-        if (use_lock_)
-            guard.emplace(lock_dir_, tier_->id(), worker_, trace_, tier_->spec().lock_width, tier_->spec().lock_device);
-        Event ev;
-        ev.timestamp_ns = now_ns();
-        ev.worker_id = worker_;
-        ev.kind = static_cast<int>(start);
-        ev.subgroup_id = job.sg;
-        ev.tier_id = tier_->id();
-        ev.bytes = job.bytes_hint;
-        const std::int64_t t_start = ev.timestamp_ns;
-        if (trace_) trace_->append(ev);
-        IoStats st = job.transfer();
-        ev.timestamp_ns = now_ns();
-        ev.kind = static_cast<int>(end);
-        ev.bytes = st.bytes;
-        if (trace_) trace_->append(ev);
-        // The traced interval is the duration the metrics use (reference scheduler.hpp:241-243).
-        st.seconds = static_cast<double>(ev.timestamp_ns - t_start) / 1e9;
-        guard.reset();
-        if (job.completion) job.completion(true, st);
-        job.promise.set_value(st);
-    } catch (...) {
-        if (trace_) trace_->record(end, worker_, job.sg, tier_->id(), 0);
-        guard.reset();
+bool TierIoWorker::next_job(Job& out) {
+    std::unique_lock<std::mutex> l(mu_);
+    wake_.wait(l, [&] { return closed_ || !lanes_[kFetch].empty() || !lanes_[kWriteBack].empty(); });
+    if (lanes_[kFetch].empty() && lanes_[kWriteBack].empty()) return false;  // closed and drained
+    auto& lane = lanes_[kFetch].empty() ? lanes_[kWriteBack] : lanes_[kFetch];
+    out = std::move(lane.front());
+    lane.pop_front();
+    return true;
+}
+
+void TierIoWorker::serve() {
+    Job job;
+    while (next_job(job)) {
         try {
-            if (job.completion) job.completion(false, IoStats{});
+            const IoStats st = transfer_traced(job);
+            if (job.completion) job.completion(true, st);
+            job.promise.set_value(st);
         } catch (...) {
+            try {
+                if (job.completion) job.completion(false, IoStats{});
+            } catch (...) {
+            }
+            job.promise.set_exception(std::current_exception());
         }
-        job.promise.set_exception(std::current_exception());
+        job = Job{};
     }
+}
+
+// The transfer under the tier semaphore; its traced interval (lock wait
+// excluded) is the duration the metrics and the EMA use (reference
+// scheduler.hpp:236-243). On failure the end event is still traced, with 0 bytes.
+IoStats TierIoWorker::transfer_traced(Job& job) {
+    const bool fetch = job.lane == kFetch;
+    const TierId tid = tier_->id();
+    std::optional<TierLockGuard> sem;
+    if (use_lock_)
+        sem.emplace(lock_dir_, tid, worker_, trace_, tier_->spec().lock_width, tier_->spec().lock_device);
+    const std::int64_t t0 = now_ns();
+    if (trace_) {
+        Event ev;
+        ev.timestamp_ns = t0;
+        ev.worker_id = worker_;
+        ev.kind = static_cast<int>(fetch ? EventKind::prefetch_start : EventKind::flush_start);
+        ev.subgroup_id = job.sg;
+        ev.tier_id = tid;
+        ev.bytes = job.bytes_hint;
+        trace_->append(ev);
+    }
+    const EventKind end_kind = fetch ? EventKind::prefetch_end : EventKind::flush_end;
+    IoStats st;
+    try {
+        st = job.transfer();
+    } catch (...) {
+        if (trace_) trace_->record(end_kind, worker_, job.sg, tid, 0);
+        throw;
+    }
+    const std::int64_t t1 = now_ns();
+    if (trace_) {
+        Event ev;
+        ev.timestamp_ns = t1;
+        ev.worker_id = worker_;
+        ev.kind = static_cast<int>(end_kind);
+        ev.subgroup_id = job.sg;
+        ev.tier_id = tid;
+        ev.bytes = st.bytes;
+        trace_->append(ev);
+    }
+    st.seconds = static_cast<double>(t1 - t0) / 1e9;
+    return st;  // the semaphore is released here, before the completion runs
 }
 
 // --- OffloadWorker -------------------------------------------------------------
@@ -421,6 +440,7 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaMalloc(&grad_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(grads)");
     cuda_check(cudaMalloc(&p16_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(params16)");
     cuda_check(cudaMemset(grad_arena_, 0, std::max<std::size_t>(arena, 256)), "cudaMemset(grads)");
+    cuda_check(cudaEventCreateWithFlags(&producer_done_, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&counters_), 2 * sizeof(unsigned long long)), "cudaMalloc");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&sg_counts_), ids_.size() * sizeof(unsigned long long)),
                "cudaMalloc");
@@ -500,6 +520,8 @@ void OffloadWorker::release_device() {
     cudaFree(p16_arena_);
     cudaFree(counters_);
     cudaFree(sg_counts_);
+    if (producer_done_) cudaEventDestroy(producer_done_);
+    producer_done_ = nullptr;
     cudaStreamDestroy(s_h2d_);
     cudaStreamDestroy(s_k_);
     cudaStreamDestroy(s_d2h_);
@@ -653,7 +675,7 @@ void OffloadWorker::fetch_grads_for_cached(SubgroupId id) {
             .share();
     const IoStats st = watchdog_wait_value(fut);
     std::lock_guard<std::mutex> g(mu_);
-    record_read_locked(id, gt, st, /*state_fetch=*/false);
+    account_io_locked(id, gt, st, IoDir::read, /*state_fetch=*/false);
 }
 
 void* OffloadWorker::grad_buffer(SubgroupId id) {
@@ -677,6 +699,16 @@ void OffloadWorker::bind_grad_sources(SubgroupId id, const std::vector<const voi
     for (const void* s : sources)
         if (s == nullptr) throw ConfigError("bind_grad_sources: null device pointer");
     grad_sources_.at(index_of_.at(id)) = sources;
+}
+
+void OffloadWorker::set_producer_stream(cudaStream_t s) { producer_ = s; }
+
+// Gradients are read on s_k_ (pre-check, fused kernel): order it after what
+// the producer stream has queued so far, so a caller that filled or bound the
+// buffers asynchronously (a reduce-scatter, a backward) needs no host sync.
+void OffloadWorker::order_after_producer() {
+    cuda_check(cudaEventRecord(producer_done_, producer_), "cudaEventRecord(producer)");
+    cuda_check(cudaStreamWaitEvent(s_k_, producer_done_, 0), "cudaStreamWaitEvent(producer)");
 }
 
 void* OffloadWorker::params16_buffer(SubgroupId id) {
@@ -709,6 +741,7 @@ std::vector<unsigned long long> OffloadWorker::nonfinite_counts() {
 bool OffloadWorker::gradients_finite() {
     if (!device_ready_) throw Error("gradients_finite before init_and_flush_all");
     DeviceGuard dg(dev_.device);
+    order_after_producer();
     for (const auto c : nonfinite_counts())
         if (c != 0) return false;
     return true;
@@ -740,6 +773,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         std::lock_guard<std::mutex> g(mu_);
         order_ = update_order(iteration, ids_, opt_.enable_caching);
     }
+    order_after_producer();
     check_grads_finite_or_throw();
     cuda_check(cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
     std::vector<SubgroupId> order;
@@ -766,6 +800,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         flush_futures_.clear();
         cache_hits_this_phase_ = 0;
         phase_stats_ = &stats;
+        io_index_.clear();
         completion_error_ = nullptr;
         order = order_;
         pump_locked();
@@ -961,11 +996,14 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     }
     float* d = hslot >= 0 ? hbm_cache_[static_cast<std::size_t>(hslot)] : ring_[rb];
     const std::uint64_t ds = seg_stride(pc);
+    // A retention buffer taken now: its previous occupant's write-back D2H
+    // must have drained. Waited before h2d_start is recorded, so every copy
+    // ordered after h2d_start (the second H2D half included) is after it.
+    if (held < 0 && hslot >= 0)
+        cuda_check(cudaStreamWaitEvent(s_h2d_, hbm_ready_[static_cast<std::size_t>(hslot)], 0), "wait");
     cuda_check(cudaEventRecord(e.h2d_start, s_h2d_), "cudaEventRecord");
     std::uint64_t h2d_bytes = 0, d2h_bytes = 0;
     if (held < 0) {
-        if (hslot >= 0)  // the buffer's previous occupant has been written back
-            cuda_check(cudaStreamWaitEvent(s_h2d_, hbm_ready_[static_cast<std::size_t>(hslot)], 0), "wait");
         if (dev_.h2d_split > 1 && ds == pc) {
             // Two concurrent halves on two copy engines: the H2D side of the
             // duplex link arbitration gets a second queue, like d2h_split.
@@ -1013,6 +1051,10 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
         cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
         for (cudaEvent_t ev : {e.k_end, e.d2h_start, e.d2h_end})
             cuda_check(cudaEventRecord(ev, s_k_), "cudaEventRecord");
+        // The ring buffer (and, in the baseline flow, its fp32 gradient
+        // segment) is free once this kernel has read it: the next H2D into
+        // it waits here (there is no D2H to carry the event).
+        if (hslot < 0) cuda_check(cudaEventRecord(ring_ready_[rb], s_k_), "cudaEventRecord");
         auto* ctx = new std::pair<OffloadWorker*, Completion>(this, Completion{id, slot});
         cuda_check(cudaLaunchHostFunc(s_k_, &OffloadWorker::host_done, ctx), "cudaLaunchHostFunc");
         return {h2d_bytes, 12 * pc};
@@ -1023,7 +1065,7 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     if (slot < 0 && held >= 0 && !keep_in_hbm) {  // HBM cache mode: the write-back thread takes it
         {
             std::lock_guard<std::mutex> g(mu_);
-            wb_pending_.push_back(PendingWriteback{id, k, held});
+            wb_pending_.push_back(PendingWriteback{id, k, held, pc});
             ++wb_inflight_;
         }
         wb_cv_.notify_all();
@@ -1132,42 +1174,52 @@ void OffloadWorker::completion_loop() {
     }
 }
 
-int OffloadWorker::wait_host_resident(SubgroupId id) {
-    std::shared_future<IoStats> fut;
-    bool need_grad_fetch = false;
-    {
-        std::unique_lock<std::mutex> l(mu_);
-        for (;;) {
-            Subgroup& sg = subgroups_.at(id);
-            auto it = prefetch_futures_.find(id);
-            if (it != prefetch_futures_.end()) {
-                fut = it->second;
-                break;
-            }
-            if (sg.residency == Residency::host_cached) {
-                if (sg.slot < 0 && wb_held_.count(id) != 0 && adopt_wb_held_locked(id) < 0) {
-                    l.unlock();
-                    wait_pool_free();
-                    l.lock();
-                    continue;
-                }
-                ++cache_hits_this_phase_;
-                trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
-                need_grad_fetch = !opt_.skip_gradients && grad_tier_.count(id) != 0;
-                break;
-            }
-            const int slot = pool_->try_reserve(id);
-            if (slot >= 0) {
-                fut = start_prefetch_locked(id, slot);
-                break;
-            }
-            l.unlock();
-            wait_pool_free();
-            l.lock();
-        }
+// Where subgroup `id` stands on its way into a host slot (mu_ held). A
+// subgroup already fetching this phase is `pending`; one host-resident with no
+// fetch this phase is a cache hit (reference scheduler.hpp:528-533), traced
+// and counted here; one on a tier takes a free slot and its fetch is issued,
+// else it is `blocked` until a slot frees. A state held in the write-back lane
+// after a failed flush first moves into a slot (blocked while none is free).
+OffloadWorker::HostClaim OffloadWorker::claim_host_locked(SubgroupId id) {
+    if (const auto f = prefetch_futures_.find(id); f != prefetch_futures_.end())
+        return {HostClaim::pending, f->second};
+    Subgroup& sg = subgroups_.at(id);
+    if (sg.residency != Residency::host_cached) {
+        const int slot = pool_->try_reserve(id);
+        if (slot < 0) return {HostClaim::blocked, {}};
+        return {HostClaim::pending, start_prefetch_locked(id, slot)};
     }
-    if (fut.valid()) watchdog_wait_value(fut);
-    if (need_grad_fetch) fetch_grads_for_cached(id);
+    if (sg.slot < 0 && wb_held_.count(id) != 0 && adopt_wb_held_locked(id) < 0) return {HostClaim::blocked, {}};
+    ++cache_hits_this_phase_;
+    trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
+    return {HostClaim::hit, {}};
+}
+
+OffloadWorker::HostClaim OffloadWorker::claim_host(SubgroupId id) {
+    std::unique_lock<std::mutex> l(mu_);
+    HostClaim c = claim_host_locked(id);
+    while (c.kind == HostClaim::blocked) {
+        l.unlock();
+        wait_pool_free();
+        l.lock();
+        c = claim_host_locked(id);
+    }
+    return c;
+}
+
+int OffloadWorker::wait_host_resident(SubgroupId id) {
+    HostClaim c = claim_host(id);
+    if (c.kind == HostClaim::pending) {
+        watchdog_wait_value(c.fetch);
+    } else if (!opt_.skip_gradients) {
+        // Baseline flow: a cached subgroup still needs its fp32 gradients.
+        bool stored;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stored = grad_tier_.count(id) != 0;
+        }
+        if (stored) fetch_grads_for_cached(id);
+    }
     std::lock_guard<std::mutex> g(mu_);
     return subgroups_.at(id).slot;
 }
@@ -1185,22 +1237,9 @@ std::shared_future<IoStats> OffloadWorker::enqueue_flush(SubgroupId id, TierId d
 }
 
 std::optional<std::shared_future<IoStats>> OffloadWorker::enqueue_prefetch(SubgroupId id) {
-    std::unique_lock<std::mutex> l(mu_);
-    for (;;) {
-        Subgroup& sg = subgroups_.at(id);
-        auto it = prefetch_futures_.find(id);
-        if (it != prefetch_futures_.end()) return it->second;
-        if (sg.residency == Residency::host_cached) {
-            trace_->record(EventKind::cache_hit, id_, id, kNoTier, 0);
-            ++cache_hits_this_phase_;
-            return std::nullopt;
-        }
-        const int slot = pool_->try_reserve(id);
-        if (slot >= 0) return start_prefetch_locked(id, slot);
-        l.unlock();
-        wait_pool_free();
-        l.lock();
-    }
+    HostClaim c = claim_host(id);
+    if (c.kind == HostClaim::hit) return std::nullopt;
+    return c.fetch;
 }
 
 void OffloadWorker::read_current_state(SubgroupId id, float* out) {
@@ -1238,17 +1277,19 @@ std::uint64_t OffloadWorker::total_params() const {
     return n;
 }
 
+// Params per residency: host-resident (slot, HBM or write-back lane) and per
+// tier; in-flight subgroups are in neither (reference scheduler.hpp:597).
 std::pair<std::uint64_t, std::vector<std::uint64_t>> OffloadWorker::residency_census() {
     std::lock_guard<std::mutex> g(mu_);
-    std::uint64_t host = 0;
-    std::vector<std::uint64_t> per_tier(tiers_.size(), 0);
-    for (const auto& [id, sg] : subgroups_) {
-        if (sg.residency == Residency::host_cached)
-            host += sg.param_count;
-        else if (sg.residency == Residency::on_tier)
-            per_tier[static_cast<std::size_t>(sg.tier)] += sg.param_count;
+    std::pair<std::uint64_t, std::vector<std::uint64_t>> census{0, std::vector<std::uint64_t>(tiers_.size(), 0)};
+    for (const SubgroupId id : ids_) {
+        const Subgroup& sg = subgroups_.at(id);
+        std::uint64_t* bin = sg.residency == Residency::host_cached ? &census.first
+                             : sg.residency == Residency::on_tier  ? &census.second.at(static_cast<std::size_t>(sg.tier))
+                                                                    : nullptr;
+        if (bin) *bin += sg.param_count;
     }
-    return {host, per_tier};
+    return census;
 }
 
 std::vector<SubgroupId> OffloadWorker::current_order() {
@@ -1256,25 +1297,23 @@ std::vector<SubgroupId> OffloadWorker::current_order() {
     return order_;
 }
 
-// Keeps the prefetch frontier as deep as free slots allow (reference
-// scheduler.hpp:645-659). Called with mu_ held.
+// Advances the prefetch frontier through the plan while slots are free
+// (reference scheduler.hpp:645-659). Subgroups already host-resident or
+// already fetching are passed over; a state held in the write-back lane after
+// a failed flush is adopted into a slot at its place in the plan. Called with
+// mu_ held.
 void OffloadWorker::pump_locked() {
-    while (frontier_ < order_.size()) {
+    for (; frontier_ < order_.size(); ++frontier_) {
         const SubgroupId id = order_[frontier_];
-        Subgroup& sg = subgroups_.at(id);
-        if (sg.residency == Residency::host_cached && sg.slot < 0 && wb_held_.count(id) != 0) {
-            if (adopt_wb_held_locked(id) < 0) break;  // its slot, in plan order
-            ++frontier_;
+        const Subgroup& sg = subgroups_.at(id);
+        if (sg.residency == Residency::host_cached) {
+            if (sg.slot < 0 && wb_held_.count(id) != 0 && adopt_wb_held_locked(id) < 0) return;
             continue;
         }
-        if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) {
-            ++frontier_;
-            continue;
-        }
+        if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) continue;
         const int slot = pool_->try_reserve(id);
-        if (slot < 0) break;
+        if (slot < 0) return;  // resumes here when a slot frees
         start_prefetch_locked(id, slot);
-        ++frontier_;
     }
 }
 
@@ -1305,7 +1344,7 @@ std::shared_future<IoStats> OffloadWorker::start_prefetch_locked(SubgroupId id, 
         if (ok) {
             s.finish_prefetch(slot);
             pool_->prefetch_done(slot);
-            record_read_locked(id, origin, st, /*state_fetch=*/true);
+            account_io_locked(id, origin, st, IoDir::read, /*state_fetch=*/true);
         } else {
             s.residency = Residency::on_tier;  // fetch failed: still on its tier
             s.slot = -1;
@@ -1345,7 +1384,7 @@ std::shared_future<IoStats> OffloadWorker::start_flush_locked(SubgroupId id, Tie
                 } else {
                     pool_->flush_done(slot);
                 }
-                record_write_locked(id, dest, st);
+                account_io_locked(id, dest, st, IoDir::write, false);
                 if (origin >= 0 && origin != dest) stale = tiers_[static_cast<std::size_t>(origin)];
                 pump_locked();
             } else if (wb < 0) {
@@ -1405,7 +1444,7 @@ void OffloadWorker::writeback_loop() {
         }
         try {
             const DeviceEvents& e = events_[p.k];
-            const std::uint64_t pc = subgroups_.at(p.id).param_count;
+            const std::uint64_t pc = p.pc;
             cuda_check(cudaStreamWaitEvent(s_d2h2_, e.k_end, 0), "wait");
             cuda_check(cudaEventRecord(e.d2h_start, s_d2h2_), "cudaEventRecord");
             copy_state(hbm_cache_[static_cast<std::size_t>(p.hslot)], wb_blocks_[static_cast<std::size_t>(wb)], pc,
@@ -1432,36 +1471,35 @@ void OffloadWorker::writeback_loop() {
     }
 }
 
-void OffloadWorker::record_read_locked(SubgroupId id, TierId tier, const IoStats& st, bool state_fetch) {
+// One finished transfer into this phase's observations: the tier's totals
+// (the EMA input, reference scheduler.hpp:767-797) and the subgroup's own
+// read/write times (the effective-I/O metric). Outside a phase (op-level
+// calls) nothing is recorded. Called with mu_ held.
+void OffloadWorker::account_io_locked(SubgroupId id, TierId tier, const IoStats& st, IoDir dir, bool state_fetch) {
     if (phase_stats_ == nullptr) return;
-    auto& obs = phase_stats_->tier_obs[static_cast<std::size_t>(tier)];
-    obs.read_transfers += 1;
-    obs.read_bytes += static_cast<double>(st.bytes);
-    obs.read_seconds += st.seconds;
-    auto& io = subgroup_io_entry_locked(id);
-    io.read_seconds += st.seconds;
-    if (state_fetch) io.fetched = true;
-}
-
-void OffloadWorker::record_write_locked(SubgroupId id, TierId tier, const IoStats& st) {
-    if (phase_stats_ == nullptr) return;
-    auto& obs = phase_stats_->tier_obs[static_cast<std::size_t>(tier)];
-    obs.write_transfers += 1;
-    obs.write_bytes += static_cast<double>(st.bytes);
-    obs.write_seconds += st.seconds;
-    auto& io = subgroup_io_entry_locked(id);
-    io.write_seconds += st.seconds;
-    io.flushed = true;
-}
-
-SubgroupIoTimes& OffloadWorker::subgroup_io_entry_locked(SubgroupId id) {
-    for (auto& e : phase_stats_->subgroup_io)
-        if (e.id == id) return e;
-    SubgroupIoTimes e;
-    e.id = id;
-    e.state_bytes = 12 * subgroups_.at(id).param_count;
-    phase_stats_->subgroup_io.push_back(e);
-    return phase_stats_->subgroup_io.back();
+    TierObservation& obs = phase_stats_->tier_obs.at(static_cast<std::size_t>(tier));
+    auto [slot, fresh] = io_index_.try_emplace(id, phase_stats_->subgroup_io.size());
+    if (fresh) {
+        SubgroupIoTimes e;
+        e.id = id;
+        e.state_bytes = 12 * subgroups_.at(id).param_count;
+        phase_stats_->subgroup_io.push_back(e);
+    }
+    SubgroupIoTimes& io = phase_stats_->subgroup_io[slot->second];
+    const double bytes = static_cast<double>(st.bytes);
+    if (dir == IoDir::read) {
+        obs.read_transfers += 1;
+        obs.read_bytes += bytes;
+        obs.read_seconds += st.seconds;
+        io.read_seconds += st.seconds;
+        io.fetched = io.fetched || state_fetch;
+    } else {
+        obs.write_transfers += 1;
+        obs.write_bytes += bytes;
+        obs.write_seconds += st.seconds;
+        io.write_seconds += st.seconds;
+        io.flushed = true;
+    }
 }
 
 void OffloadWorker::wait_pool_free() {

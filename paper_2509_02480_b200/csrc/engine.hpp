@@ -28,6 +28,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <condition_variable>
 #include <deque>
 #include <filesystem>
@@ -206,12 +207,14 @@ private:
 };
 
 // ---------------------------------------------------------------------------
-// One I/O thread per (worker, tier); pending prefetches drain before pending
-// flushes; each job runs under the tier semaphore when atomic_rw is on
-// (reference scheduler.hpp:142-266).
+// One I/O thread per (worker, tier) serving two lanes: a queued fetch always
+// outranks a queued write-back (reference scheduler.hpp:142-266, the
+// prefetch-before-flush rule at :222). Each transfer runs under the tier
+// semaphore when atomic_rw is on, and is traced as one start/end interval.
 class TierIoWorker {
 public:
     using Completion = std::function<void(bool ok, const IoStats&)>;
+    enum Lane : int { kFetch = 0, kWriteBack = 1 };
 
     TierIoWorker(std::shared_ptr<Tier> tier, WorkerId worker, bool use_lock, std::filesystem::path lock_dir,
                  EventTrace* trace);
@@ -223,15 +226,17 @@ public:
 
 private:
     struct Job {
-        bool is_prefetch = false;
+        Lane lane = kFetch;
         std::int64_t sg = -1;
         std::uint64_t bytes_hint = 0;
         std::function<IoStats()> transfer;
         Completion completion;
         std::promise<IoStats> promise;
     };
-    void run();
-    void execute(Job& job);
+    bool next_job(Job& out);  // blocks; false once closed and drained
+    void serve();
+    IoStats transfer_traced(Job& job);
+    static void cancel(Job& job);
 
     std::shared_ptr<Tier> tier_;
     WorkerId worker_;
@@ -239,10 +244,9 @@ private:
     std::filesystem::path lock_dir_;
     EventTrace* trace_;
     std::mutex mu_;
-    std::condition_variable cv_;
-    std::deque<Job> prefetch_q_;
-    std::deque<Job> flush_q_;
-    bool stop_ = false;
+    std::condition_variable wake_;
+    std::array<std::deque<Job>, 2> lanes_;
+    bool closed_ = false;
     std::thread thread_;
 };
 
@@ -278,6 +282,11 @@ public:
     // to the gradient kind, and applies Adam in the same kernel pass.
     void bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources);
     void* params16_buffer(SubgroupId id);
+    // The stream that produces the gradients (the backward / reduce-scatter).
+    // Every run_update and gradients_finite first orders the engine's streams
+    // after the work queued on it so far. Default: the legacy default stream
+    // (also covers torch's default current stream).
+    void set_producer_stream(cudaStream_t s);
 
     PhaseStats run_update(int iteration);
 
@@ -323,15 +332,20 @@ private:
     // slot >= 0: flush from a pool slot; wb >= 0: from a write-back block.
     std::shared_future<IoStats> start_flush_locked(SubgroupId id, TierId dest, int slot, int wb = -1);
     void writeback_loop();
-    void record_read_locked(SubgroupId id, TierId tier, const IoStats& st, bool state_fetch);
-    void record_write_locked(SubgroupId id, TierId tier, const IoStats& st);
+    enum class IoDir { read, write };
+    void account_io_locked(SubgroupId id, TierId tier, const IoStats& st, IoDir dir, bool state_fetch);
+    struct HostClaim {
+        enum Kind { pending, hit, blocked } kind;
+        std::shared_future<IoStats> fetch;  // pending: the fetch to wait on
+    };
+    HostClaim claim_host_locked(SubgroupId id);
+    HostClaim claim_host(SubgroupId id);  // waits out `blocked`
     // ZeRO-3 baseline flow (skip_gradients = false): fp32 gradients through storage.
     void flush_grads_to_storage();
     void fetch_grads_for_cached(SubgroupId id);
     float* grad_annex(const HostBlock& blk) const {
         return reinterpret_cast<float*>(blk.base() + state_block_bytes_);
     }
-    SubgroupIoTimes& subgroup_io_entry_locked(SubgroupId id);
     void wait_pool_free();
 
     void setup_device();
@@ -344,6 +358,7 @@ private:
     void completion_loop();
     static void CUDART_CB host_done(void* arg);
     void check_grads_finite_or_throw();
+    void order_after_producer();
     std::vector<unsigned long long> nonfinite_counts();
 
     WorkerId id_;
@@ -369,6 +384,7 @@ private:
     std::unordered_map<SubgroupId, std::shared_future<IoStats>> prefetch_futures_;
     std::vector<std::pair<SubgroupId, std::shared_future<IoStats>>> flush_futures_;
     PhaseStats* phase_stats_ = nullptr;
+    std::unordered_map<SubgroupId, std::size_t> io_index_;  // id -> phase_stats_->subgroup_io entry
     std::uint64_t cache_hits_this_phase_ = 0;
 
     // Device resources.
@@ -396,6 +412,7 @@ private:
         SubgroupId id;
         std::size_t k;
         int hslot;
+        std::uint64_t pc;  // param count, captured when queued (read off the lock)
     };
     std::vector<HostBlock> wb_blocks_;
     std::deque<int> wb_free_;
@@ -424,6 +441,8 @@ private:
     std::uint64_t ring_stride_ = 0;  // floats per segment (P, m, v each) in a ring buffer
     void* grad_arena_ = nullptr;
     void* p16_arena_ = nullptr;
+    cudaStream_t producer_ = cudaStreamLegacy;  // gradients' producer (set_producer_stream)
+    cudaEvent_t producer_done_ = nullptr;
     unsigned long long* counters_ = nullptr;  // [0] non-finite grads, [1] narrowing overflows
     unsigned long long* sg_counts_ = nullptr; // per-subgroup non-finite counts (pre-check)
     std::unordered_map<SubgroupId, std::size_t> index_of_;

@@ -117,7 +117,7 @@ inline AllocationVector assign_subgroups_capped(int M, const std::vector<double>
         for (std::size_t i = 0; i < N; ++i) {
             if (!(bw[i] > 0.0) || a.counts[i] >= room(i)) continue;
             const double r = (a.counts[i] + 1) / bw[i];
-            if (r < best || (r == best && bw[i] > bw[pick])) {
+            if (pick == N || r < best || (r == best && bw[i] > bw[pick])) {
                 pick = i;
                 best = r;
             }

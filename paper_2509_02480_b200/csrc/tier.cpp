@@ -101,7 +101,7 @@ Tier::Tier(TierSpec spec) : spec_(std::move(spec)) {
                 throw ConfigError("mem_throttled tier needs configured read/write rates");
             mem_read_bw_.store(spec_.read_bw);
             mem_write_bw_.store(spec_.write_bw);
-            bucket_ = std::make_unique<TokenBucket>(1.0);  // tokens are device-seconds
+            pacer_ = std::make_unique<DevicePacer>(1.0);  // costs are device-seconds
             break;
         case TierKind::host_dram:
             break;
@@ -427,7 +427,7 @@ IoStats Tier::mem_write(const std::string& name, SubgroupId id, std::uint64_t pa
     for (std::size_t off = 0; off < bytes; off += chunk) {
         const std::size_t n = std::min(chunk, bytes - off);
         std::memcpy(blob->data() + kHeaderBytes + off, payload + off, n);  // copy first, charge after
-        bucket_->acquire(static_cast<double>(n) / rate);
+        pacer_->book(static_cast<double>(n) / rate);
     }
     return IoStats{bytes, since(t0)};
 }
@@ -450,7 +450,7 @@ IoStats Tier::mem_read(const std::string& name, SubgroupId id, std::uint64_t par
     for (std::size_t off = 0; off < bytes; off += chunk) {
         const std::size_t n = std::min(chunk, bytes - off);
         std::memcpy(payload + off, blob->data() + kHeaderBytes + off, n);
-        bucket_->acquire(static_cast<double>(n) / rate);
+        pacer_->book(static_cast<double>(n) / rate);
     }
     return IoStats{bytes, since(t0)};
 }
@@ -680,10 +680,10 @@ ProbeResult Tier::probe_bandwidth(std::uint64_t probe_bytes, int repetitions) {
         double wsec = 0.0, rsec = 0.0;
         if (spec_.kind == TierKind::mem_throttled) {
             auto t0 = Clock::now();
-            bucket_->acquire(static_cast<double>(probe_bytes) / mem_write_bw_.load());
+            pacer_->book(static_cast<double>(probe_bytes) / mem_write_bw_.load());
             wsec = clamp(since(t0));
             t0 = Clock::now();
-            bucket_->acquire(static_cast<double>(probe_bytes) / mem_read_bw_.load());
+            pacer_->book(static_cast<double>(probe_bytes) / mem_read_bw_.load());
             rsec = clamp(since(t0));
         } else if (spec_.kind == TierKind::host_dram) {
             auto t0 = Clock::now();

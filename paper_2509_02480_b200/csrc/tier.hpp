@@ -5,7 +5,7 @@
 //    header "OPLM" + P||m||v fp32). The engine path reads and writes whole
 //    files with O_DIRECT straight into pinned staging blocks, striped over
 //    io_parallelism threads at 4 KiB-aligned stripes.
-//  * mem_throttled — in-memory blobs paced by a device-time token bucket: the
+//  * mem_throttled — in-memory blobs paced by a device-time pacer (virtual clock): the
 //    deterministic test tier of the reference (tier.hpp:392-448).
 //  * host_dram — pinned host-memory blobs. The engine path exchanges the blob
 //    block with the staging slot (no copy): the DMA engine reads the state
@@ -32,7 +32,7 @@
 
 #include "common.hpp"
 #include "host_block.hpp"
-#include "token_bucket.hpp"
+#include "pacer.hpp"
 
 namespace tfb {
 
@@ -141,7 +141,7 @@ private:
 
     TierSpec spec_;
     // mem_throttled
-    std::unique_ptr<TokenBucket> bucket_;
+    std::unique_ptr<DevicePacer> pacer_;
     std::atomic<double> mem_read_bw_{0.0};
     std::atomic<double> mem_write_bw_{0.0};
     mutable std::mutex mu_;

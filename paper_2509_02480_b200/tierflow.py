@@ -622,6 +622,13 @@ class OffloadWorker:
     def bind_grad_buffer(self, sg: int, device_ptr: int) -> None:
         _lib.call("tfg_engine_bind_grad_buffer", self._h, sg, C.c_void_p(device_ptr))
 
+    def set_producer_stream(self, stream=None) -> None:
+        """The CUDA stream (torch.cuda.Stream, raw handle, or None for the
+        legacy default stream) that produces the gradients: every run_update
+        is ordered after the work queued on it, no host sync needed."""
+        handle = getattr(stream, "cuda_stream", stream) or 0
+        _lib.call("tfg_engine_set_producer_stream", self._h, C.c_void_p(handle))
+
     def bind_grad_sources(self, sg: int, device_ptrs) -> None:
         """Feed subgroup `sg` from the fp32 sum of several 16-bit device
         buffers (in order, rounded once): the fused reduce + update."""

@@ -356,6 +356,36 @@ def test_transfer_modes_bitwise(tf, cuda, lock_dir, tmp_path, zero_copy, split):
     w.close()
 
 
+@pytest.mark.parametrize("zero_copy,skip", [(0, True), (2, True), (2, False), (0, False)])
+def test_ring_reuse_under_slow_kernels(tf, cuda, lock_dir, tmp_path, zero_copy, skip):
+    """Many more streaming subgroups than ring buffers, no retention, and a
+    padded (slow) kernel: an H2D into a ring buffer must wait until the last
+    kernel reading it is done (zero_copy=2 never recorded the
+    buffer's release event). skip=False is the ZeRO-3 baseline flow, whose
+    fp32 gradient segment shares the ring buffer's release."""
+    params = [40_000 + 4 * i for i in range(10)]
+    seed = 31
+    trace = tf.EventTrace()
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9))]
+    opt = tf.ScheduleOptions(pool_slots=8, cache_slots=0, lock_dir=lock_dir, enable_caching=False,
+                             skip_gradients=skip, update_pad_ns=3_000_000)
+    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 2, zero_copy, 1, 0))
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    for it in range(3):
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        st = w.run_update(it)
+        assert st.cache_hits == 0
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(3):
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32)), sg
+        assert np.array_equal(w.read_params16(sg), p16), sg
+    w.close()
+
+
 def _baseline_engine(tf, params, lock_dir, *, baseline, seed=1234, pool_slots=6):
     trace = tf.EventTrace()
     tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.mem_throttled, "m0", 300e6, 300e6)),
@@ -422,8 +452,8 @@ def test_engine_mode_backward_writes_nothing(tf, cuda, lock_dir):
         w.close()
 
 
-@pytest.mark.parametrize("hbm", [0, 1, 2])
-def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
+@pytest.mark.parametrize("hbm,h2d_split", [(0, 1), (1, 1), (2, 1), (1, 2), (2, 2)])
+def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm, h2d_split):
     """Retained subgroups keep their state in HBM between phases: no D2H when
     retained, no H2D at the next update. Same bits and cache hits as the
     host-retention path and the oracle, including re-retention (C > M/2), a
@@ -436,7 +466,7 @@ def test_hbm_retention_bits_and_pcie_bytes(tf, cuda, lock_dir, tmp_path, hbm):
              tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
     opt = (tf.ScheduleOptions(pool_slots=3, cache_slots=C, lock_dir=lock_dir) if hbm == 2 else
            tf.ScheduleOptions(pool_slots=C + 3, lock_dir=lock_dir))
-    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm))
+    w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(0, 0, 0, 2, 0, 1, hbm, h2d_split))
     w.set_fixed_ratio([1.0, 1.0])
     for i, n in enumerate(params):
         w.add_subgroup(i, n)
