@@ -3,34 +3,42 @@
 device-timed, vs the HBM and PCIe/tier rooflines).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-    torchrun --nproc-per-node N bench.py --gpus N ...
 
-A step is one update phase over the rank's optimizer state: the
-Llama-2-7B-shaped workload (BASELINE configs[1]: 6,738,415,616 params in
-68 subgroups of 100M, the last 38,415,616), seeded synthetic
-state and fp16 gradients from the reference generators.
+With --gpus N > 1 and no torchrun environment, bench.py re-launches itself
+under torch.distributed.run with N ranks (one per GPU, NCCL, 127.0.0.1); under
+torchrun WORLD_SIZE must equal --gpus.
 
-Legs of the `ours` line:
-  value   device-resident update phase: all 68 subgroups' P/m/v, grads and
-          working params resident in HBM (108 GB); as in the engine, a
-          whole-phase non-finite pre-check, then one fused sm_100a kernel per
-          subgroup; CUDA events on the launching stream. Roofline: HBM, 28
-          algorithmic bytes/param for the fused kernel.
+A step is one update phase over the rank's optimizer state, seeded synthetic
+state and 16-bit gradients from the reference generators.
+
+N = 1 (BASELINE configs[1]): Llama-2-7B-shaped state,
+6,738,415,616 params in 68 subgroups of 100M (the last 38,415,616).
+  value   device-resident update phase: the 68 subgroups' P/m/v, gradients and
+          working params resident in HBM (108 GB); the whole-phase non-finite
+          check, then one fused sm_100a kernel per subgroup; CUDA events on the
+          launching stream. Roofline: HBM, 28 algorithmic bytes/param.
   e2e     the same metric through the engine's C ABI with the state on HOST
-          tiers (pinned host DRAM + a local O_DIRECT directory tier): prefetch,
-          H2D, fused kernel, D2H, flush/retain inside the timed region.
-  spill   the same metric with host DRAM capped (a capacity-capped DRAM tier,
-          8 pinned staging slots) so the state spills to two O_DIRECT
-          directory tiers (local + remote), the retention capacity
-          in HBM; bounded sample (<= 12 subgroups). Roofline: the directory
-          tiers' probed bandwidths.
-  cpu_baseline  the reference CPU engine (oracle/_ref: the unmodified
-          reference headers compiled in place) on a bounded sample, rank 0.
---exchange fused|nccl: strong scaling over one model with the gradient
-reduce-scatter inside the update (fused: NVLink peer loads in the kernel).
-Multi-GPU (torchrun): weak scaling — every rank owns its own 68-subgroup shard
-(ids rank*68+k, ZeRO-3 contiguous blocks); value = all ranks' params / max
-rank time.
+          tiers: pinned host DRAM + a local O_DIRECT directory ("NVMe") tier,
+          Eq. 1 placing subgroups over both (the DRAM tier's rate is the
+          measured PCIe rate; the NVMe tier's rate is learned by the EMA):
+          prefetch, H2D, kernel, D2H, flush/retain inside the timed region.
+          `streaming_c0` is the same pipeline with no retention (C = 0).
+  spill   SURVEY C4: a Llama-2-70B rank's situation, host DRAM capped so the
+          state spills to two directory tiers ("NVMe" + "remote"); bounded
+          sample of 12 subgroups. Roofline: the directory tiers' probed rates.
+N > 1 (BASELINE configs[2]): 20B params, 200 subgroups of 100M,
+ZeRO-3 contiguous shards, the gradient reduce-scatter inside the timed phase.
+  value   every rank's 16-bit contribution to every subgroup is mapped over
+          CUDA IPC (NVLink peer loads); each owner's fused kernel sums the N
+          contributions while it streams P/m/v (reduce + update in one pass).
+          `exchange_nccl` times NCCL reduce_scatter (pipelined per subgroup on
+          a side stream) followed by the single-source kernel.
+  e2e     the same through the engine with per-rank tiers (DRAM + NVMe +
+          remote) and the owned subgroups bound to the peers' contributions.
+cpu_baseline / --impl reference: the reference CPU engine (oracle/_ref: the
+unmodified reference headers compiled in place) on the same config: the same
+subgroup size, tier kinds and retained fraction, a bounded number of
+subgroups, all host threads, rank 0 only.
 """
 from __future__ import annotations
 
@@ -38,10 +46,10 @@ import argparse
 import json
 import os
 import shutil
+import socket
 import statistics
 import subprocess
 import sys
-import tempfile
 import threading
 import time
 from pathlib import Path
@@ -55,12 +63,20 @@ ALG_BYTES_PER_PARAM = 28  # P,m,v fp32 read+write (24) + 16-bit grad read (2) + 
 DT = 0  # 16-bit gradient / working-param kind: 0 f16 (the reference's), 1 bf16 (--dtype)
 
 WORKLOADS = {
-    "llama2-7b": dict(total=6_738_415_616, sub=100_000_000,
+    "llama2-7b": dict(total=6_738_415_616, sub=100_000_000, survey="C2",
                       desc="Llama-2-7B-shaped optimizer state: 68 subgroups x 100M params (last 38,415,616)"),
-    "20b": dict(total=20_000_000_000, sub=100_000_000, desc="20B-param state, 200 subgroups x 100M"),
-    "ref-1b": dict(total=1_000_000_000, sub=125_000_000, desc="reference CPU config: 1B params, 8 x 125M"),
-    "tiny": dict(total=8 * 10_000_000, sub=10_000_000, desc="smoke-sized: 8 subgroups x 10M params"),
+    "20b": dict(total=20_000_000_000, sub=100_000_000, survey="C3",
+                desc="20B-param optimizer state: 200 subgroups x 100M, ZeRO-3-sharded over the ranks"),
+    "llama2-70b": dict(total=68_976_648_192, sub=100_000_000, survey="C4",
+                       desc="Llama-2-70B-shaped optimizer state: 690 subgroups x 100M params (last 76,648,192)"),
+    "ref-1b": dict(total=1_000_000_000, sub=125_000_000, survey="C1",
+                   desc="reference CPU config: 1B params, 8 x 125M"),
+    "tiny": dict(total=8 * 10_000_000, sub=10_000_000, survey="-", desc="smoke-sized: 8 subgroups x 10M params"),
 }
+# e2e defaults (N = 1): HBM cache (hbm_retain 2) holding C = 29 of 68 subgroups
+# (35 GB) + 12 ring buffers (14 GB) beside the 27 GB of 16-bit gradients and
+# working params: 76 GB of the 180 GB.
+RETAINED_FRACTION = 29 / 68
 
 
 def subgroup_sizes(total: int, sub: int) -> list[int]:
@@ -89,7 +105,7 @@ class ClockSampler:
     def __enter__(self):
         if shutil.which("nvidia-smi"):
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -109,7 +125,7 @@ class ClockSampler:
             self.t.join(2)
 
     def summary(self) -> dict:
-        sm, mx, reasons = [], 0.0, set()
+        sm, mx, power, reasons = [], 0.0, [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.lines:
             parts = [p.strip() for p in line.split(",")]
@@ -118,32 +134,49 @@ class ClockSampler:
             try:
                 sm.append(float(parts[0]))
                 mx = max(mx, float(parts[1]))
+                power.append(float(parts[2]))
             except ValueError:
                 continue
             for name, flag in zip(names, parts[3:7]):
                 if flag.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(power) if power else None}
 
 
 # ---------------------------------------------------------------------------
 # distributed plumbing
 
 
+def spawn_ranks(argv: list[str], n: int) -> int:
+    """--gpus N without a torchrun environment: run this script under
+    torch.distributed.run with N ranks on this node (rendezvous on 127.0.0.1)."""
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + list(argv)
+    log(f"bench: spawning {n} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd)
+
+
 def dist_init():
-    """One process per GPU. TFB_BENCH_BACKEND=gloo (with local ranks folded
-    onto the visible devices) exercises the multi-rank path on a 1-GPU box."""
+    """One process per GPU over NCCL. TFB_BENCH_BACKEND=gloo folds the local
+    ranks onto the visible devices: exercises the multi-rank plumbing on a
+    1-GPU box (not a measurement)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     import torch
-    local = local % max(1, torch.cuda.device_count())
+    backend = os.environ.get("TFB_BENCH_BACKEND", "nccl")
+    ndev = torch.cuda.device_count()
+    if world > 1 and backend == "nccl" and ndev < world:
+        raise SystemExit(f"bench.py: {world} ranks need {world} visible GPUs, found {ndev}")
+    local = local % max(1, ndev)
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        backend = os.environ.get("TFB_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
@@ -157,8 +190,27 @@ def barrier(world):
         dist.barrier()
 
 
+def _allreduce(world, x: float, op) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=getattr(dist.ReduceOp, op))
+    return float(t.item())
+
+
+def allsum(world, x: float) -> float:
+    return _allreduce(world, x, "SUM")
+
+
+def allmax(world, x: float) -> float:
+    return _allreduce(world, x, "MAX")
+
+
 def allmin(world, x: float) -> float:
-    return -allmax(world, -x)
+    return _allreduce(world, x, "MIN")
 
 
 def setup_all_ranks(world, fn):
@@ -173,28 +225,6 @@ def setup_all_ranks(world, fn):
     if allmin(world, 0.0 if err else 1.0) < 1.0:
         raise RuntimeError(f"setup failed on a rank: {err}" if err else "setup failed on another rank")
     return out
-
-
-def allsum(world, x: float) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
-
-
-def allmax(world, x: float) -> float:
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
 
 
 def peaks() -> dict:
@@ -220,10 +250,14 @@ def ncu_traffic(params_per_launch: float) -> float | None:
 
 
 # ---------------------------------------------------------------------------
-# leg 1: device-resident update phase (value, roofline)
+# value (N = 1): device-resident update phase
 
 
 def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
+    """As the engine's run_update: the whole-phase non-finite check (every
+    gradient read once, counted into one device word), then one fused update
+    per subgroup that runs only if that word is zero (device-side gate: no host
+    round trip between the check and the updates)."""
     import torch
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)
@@ -238,28 +272,21 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
             grads.append(g)
             p16s.append(torch.empty(n, dtype=torch.int16, device=dev))
     counters = torch.zeros(2, dtype=torch.int64, device=dev)
-    sg_counts = torch.zeros(len(sizes), dtype=torch.int64, device=dev)
+    gate = torch.zeros(1, dtype=torch.int64, device=dev)
     hyper = tf.AdamHyper()
     stream.synchronize()
 
     def step(t, events=None):
-        # As the engine's run_update: the whole-phase non-finite pre-check
-        # (every gradient read once, the counts read back on the host) before
-        # any subgroup is mutated, then one fused update per subgroup.
         with torch.cuda.stream(stream):
-            sg_counts.zero_()
+            gate.zero_()
         for k in range(len(sizes)):
-            tf.count_nonfinite16(grads[k], sg_counts[k:k + 1], DT, stream=stream)
-        with torch.cuda.stream(stream):
-            bad = int(sg_counts.sum().item())  # read back on the launching stream, as the engine does
-        if bad != 0:
-            raise RuntimeError("non-finite gradients in the device leg")
+            tf.count_nonfinite16(grads[k], gate, DT, stream=stream)
         for k, n in enumerate(sizes):
             st = states[k]
             if events is not None:
                 events[k][0].record(stream)
             tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], grads[k], p16s[k], t, hyper, DT, DT, counters=counters,
-                          stream=stream)
+                          stream=stream, gate=gate)
             if events is not None:
                 events[k][1].record(stream)
 
@@ -281,14 +308,13 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
     barrier(world)
     total_ms = start.elapsed_time(end)
     kernel_ms = sum(a.elapsed_time(b) for row in ev for a, b in row)
-    over = counters.cpu().tolist()
-    if over[0] != 0:
+    if int(gate.item()) != 0 or counters[0].item() != 0:
         raise RuntimeError("non-finite gradients in the device leg")
     del states, grads, p16s
     torch.cuda.empty_cache()
     return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(sizes),
-                all_launches=2 * steps * len(sizes), clocks=clk.summary(),
-                copy_sustained_gbs=sustained_copy_gbs(stream, total_ms))
+                all_launches=2 * steps * len(sizes), clocks=clk.summary(), params=sum(sizes),
+                timed_subgroups=len(sizes), copy_sustained_gbs=sustained_copy_gbs(stream, total_ms))
 
 
 def sustained_copy_gbs(stream, busy_ms):
@@ -315,14 +341,25 @@ def sustained_copy_gbs(stream, busy_ms):
 
 
 # ---------------------------------------------------------------------------
-# leg 1b (--exchange): the gradient reduce-scatter inside the update phase.
-# Strong scaling over ONE model: every rank holds its 16-bit
-# gradient contribution to every subgroup (the backward's output), owns the
-# contiguous block parallel.shard() gives it, and per step either
-#   fused  reads all ranks' contributions of its subgroups over CUDA IPC
-#          (NVLink peer loads) inside the Adam kernel (tfg_adam_fused_multi), or
-#   nccl   runs one NCCL reduce_scatter of the padded flat gradient, then the
-#          single-source kernel (the collective-then-kernel baseline).
+# value (N > 1): the gradient exchange inside the update phase
+#
+# Each rank owns the contiguous block parallel.shard() gives it. Every rank's
+# 16-bit contribution to a subgroup is the backward's output, emitted bucket
+# by bucket: contributions live in a rolling window of buckets
+# (PeerGradients(window=W)), so subgroup k of owner o's shard is in bucket
+# slot (k % W) * N + o on every rank. Per step either
+#   fused  each owner's kernel reads the N contributions of its subgroup
+#          (its own from local HBM, N-1 over NVLink peer loads) and sums them
+#          while it streams P/m/v: 2(N-1) B/param over NVLink, no collective;
+#   nccl   for each k, reduce_scatter of bucket slot block k (N chunks, one
+#          per owner) on a side stream into a double-buffered output, the
+#          single-source kernel on the compute stream (collective for k+1
+#          overlapping kernel k): the collective-then-kernel baseline.
+# Contributions are checked finite once by their producer rank (before the
+# barrier that publishes them); the owners' kernels count the rounded sums.
+
+
+EXCHANGE_WINDOW = 4
 
 
 def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
@@ -332,57 +369,67 @@ def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
     from paper_2509_02480_b200 import parallel
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)
+    comm = torch.cuda.Stream(dev)
     M = len(sizes)
+    W = EXCHANGE_WINDOW
+    slot = (max(sizes) + 7) // 8 * 8
     begin, count = parallel.shard(M, world, rank)
-    owned = list(range(begin, begin + count))
-    states, p16s = {}, {}
+    # HBM: 14 B/param for an owned subgroup (P, m, v + working params) beside
+    # the contribution window; a shard that does not fit is timed on the first
+    # S subgroups (the same S on every rank).
+    free, _ = torch.cuda.mem_get_info(dev)
+    window_bytes = 2 * W * world * slot + (4 * slot if mode == "nccl" else 0)
+    fit = int((free - window_bytes - 8e9) // (14 * slot + 4096))
+    S = int(allmin(world, min(count, max(1, fit))))
+    owned = list(range(begin, begin + S))
+    states, p16s = [], []
     counters = torch.zeros(2, dtype=torch.int64, device=dev)
     hyper = tf.AdamHyper()
-    pg = None
-    flat = mine = None
     with torch.cuda.stream(stream):
         for sg in owned:
             n = sizes[sg]
             st = torch.empty(3 * n, dtype=torch.float32, device=dev)
             tf.synthetic_state(st[:n], st[n:2 * n], st[2 * n:], seed, sg, stream=stream)
-            states[sg] = st
-            p16s[sg] = torch.empty(n, dtype=torch.int16, device=dev)
-        if mode == "fused":
-            pg = parallel.PeerGradients(sizes, world, rank, device=dev.index)
-            for sg, n in enumerate(sizes):  # this rank's contribution to every subgroup
-                tf.synthetic_grads(pg.local(sg).view(torch.int16), seed + 100 * rank, sg, 0, dtype=DT, stream=stream)
-        else:
-            # padded layout: rank r's block = shard(r) subgroups x max subgroup size
-            cmax = max(parallel.shard(M, world, r)[1] for r in range(world))
-            sub = max(sizes)
-            flat = torch.zeros(world * cmax * sub, dtype=torch.int16, device=dev)
-            for r in range(world):
-                b, c = parallel.shard(M, world, r)
-                for k in range(c):
-                    off = (r * cmax + k) * sub
-                    tf.synthetic_grads(flat[off:off + sizes[b + k]], seed + 100 * rank, b + k, 0, dtype=DT,
-                                       stream=stream)
-            mine = torch.empty(cmax * sub, dtype=torch.int16, device=dev) if world > 1 else flat
+            states.append(st)
+            p16s.append(torch.empty(n, dtype=torch.int16, device=dev))
+    pg = parallel.PeerGradients(sizes, world, rank, device=dev.index, dtype="bf16" if DT else "f16", window=W)
+    bad = torch.zeros(1, dtype=torch.int64, device=dev)
+    with torch.cuda.stream(stream):
+        for s_ in range(W * world):  # this rank's contribution in every bucket slot
+            buf = pg.slot_view(s_)
+            tf.synthetic_grads(buf.view(torch.int16), seed + 100 * rank, s_, 0, dtype=DT, stream=stream)
+            tf.count_nonfinite16(buf.view(torch.int16), bad, DT, stream=stream)  # the producer's check
     stream.synchronize()
+    if allsum(world, float(bad.item())) != 0:
+        raise RuntimeError("non-finite gradient contributions")
+    flat = out = None
+    if mode == "nccl":
+        flat = pg.slot_view(0, W * world)  # the whole window: slot-major, N chunks per bucket
+        out = [torch.empty(slot, dtype=flat.dtype, device=dev) for _ in range(2)]
     barrier(world)  # every contribution written before any owner reads it
+    kernel_done = [torch.cuda.Event() for _ in range(2)]
 
     def step(t, events=None):
-        if mode == "nccl" and world > 1:
-            with torch.cuda.stream(stream):
-                ft = torch.bfloat16 if DT else torch.float16
-                dist.reduce_scatter_tensor(mine.view(ft), flat.view(ft), op=dist.ReduceOp.SUM)
         for k, sg in enumerate(owned):
             n = sizes[sg]
-            st = states[sg]
+            st = states[k]
+            if mode == "nccl":
+                b = k % 2
+                blk = flat[(k % W) * world * slot:((k % W) + 1) * world * slot]
+                comm.wait_event(kernel_done[b])  # out[b] free: kernel k-2 has read it
+                with torch.cuda.stream(comm):
+                    work = dist.reduce_scatter_tensor(out[b], blk, op=dist.ReduceOp.SUM, async_op=True)
+                with torch.cuda.stream(stream):
+                    work.wait()
             if events is not None:
                 events[k][0].record(stream)
             if mode == "fused":
-                tf.adam_fused_multi(st[:n], st[n:2 * n], st[2 * n:], pg.sources(sg), p16s[sg], t, hyper, DT, DT,
+                tf.adam_fused_multi(st[:n], st[n:2 * n], st[2 * n:], pg.sources(sg), p16s[k], t, hyper, DT, DT,
                                     counters=counters, stream=stream)
             else:
-                off = k * max(sizes)
-                tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], mine[off:off + n], p16s[sg], t, hyper, DT, DT,
-                              counters=counters, stream=stream)
+                tf.adam_fused(st[:n], st[n:2 * n], st[2 * n:], out[k % 2][:n].view(torch.int16), p16s[k], t, hyper,
+                              DT, DT, counters=counters, stream=stream)
+                kernel_done[k % 2].record(stream)
             if events is not None:
                 events[k][1].record(stream)
 
@@ -405,17 +452,17 @@ def exchange_leg(tf, sizes, steps, warmup, seed, rank, world, mode):
     total_ms = start.elapsed_time(end)
     kernel_ms = sum(a.elapsed_time(b) for row in ev for a, b in row)
     if counters[0].item() != 0:
-        raise RuntimeError("non-finite gradients in the exchange leg")
-    if pg is not None:
-        pg.close()
-    del states, p16s, flat, mine
+        raise RuntimeError("non-finite gradient sums in the exchange leg")
+    pg.close()
+    del states, p16s, flat, out
     torch.cuda.empty_cache()
-    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(owned), clocks=clk.summary(),
-                owned_params=sum(sizes[sg] for sg in owned), owned=len(owned))
+    return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(owned), all_launches=steps * len(owned),
+                clocks=clk.summary(), params=sum(sizes[sg] for sg in owned), timed_subgroups=len(owned),
+                owned=count)
 
 
 # ---------------------------------------------------------------------------
-# leg 2: end to end through the engine C ABI with host tiers (e2e)
+# e2e: end to end through the engine C ABI with host tiers
 
 
 def pcie_probe():
@@ -494,15 +541,61 @@ def e2e_shard(sizes, world, pool_slots, cache_slots, hbm_retain=2):
     return sizes[:n], pool, cache
 
 
+def run_phases(w, world, rank, warmup, steps, backward, tag):
+    """Backward (untimed), then run_update timed with CUDA events on the
+    legacy stream around the C-ABI call (which returns after the phase's last
+    D2H and flush); max over ranks is taken by the caller."""
+    import torch
+    phases = []
+    for it in range(warmup + steps):
+        if backward is not None:
+            backward(it)
+        barrier(world)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        st = w.run_update(it)
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        barrier(world)
+        if it >= warmup:
+            phases.append((ms, st))
+        log(f"[rank {rank}] {tag} phase {it}: {ms:.0f} ms, hits {st.cache_hits}, alloc {st.flush_allocation}, "
+            f"kernel {st.kernel_seconds*1e3:.0f} ms, h2d {st.h2d_seconds*1e3:.0f} ms, d2h {st.d2h_seconds*1e3:.0f} ms")
+    return phases
+
+
+def pipeline_roofline(phases, pcie, dir_probes):
+    """Per-phase bound: PCIe (each direction's bytes over its measured rate,
+    and both over the duplex ceiling) against the directory tiers (bytes
+    actually moved over the probed rates; tiers sharing one physical device
+    add up). The host_dram tier moves subgroups by block exchange: its cost is
+    the PCIe leg."""
+    h2d_b = statistics.mean(p[1].h2d_bytes for p in phases)
+    d2h_b = statistics.mean(p[1].d2h_bytes for p in phases)
+    pcie_s = max(h2d_b / pcie["h2d"], d2h_b / pcie["d2h"], (h2d_b + d2h_b) / pcie["bidir"])
+    tier_s, per_tier = 0.0, []
+    for i, pr in dir_probes.items():
+        rb = statistics.mean(p[1].tier_obs[i].read_bytes for p in phases)
+        wb = statistics.mean(p[1].tier_obs[i].write_bytes for p in phases)
+        sec = rb / pr.read_bw + wb / pr.write_bw
+        tier_s += sec  # one device holds every directory tier here
+        per_tier.append(dict(tier=i, read_bytes=rb, write_bytes=wb, read_gbs=round(pr.read_bw / 1e9, 2),
+                             write_gbs=round(pr.write_bw / 1e9, 2), seconds=round(sec, 4)))
+    return dict(h2d=h2d_b, d2h=d2h_b, pcie_s=pcie_s, tier_s=tier_s, bound_s=max(pcie_s, tier_s), per_tier=per_tier)
+
+
 def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring,
-            hbm_retain=1, peer=None):
+            hbm_retain=2, peer=None, remote=False, c0_steps=0):
     """peer: a parallel.PeerGradients holding every rank's contribution to
-    every subgroup (--exchange fused): the engine's owned subgroups are bound
-    to the world's contributions, so each update reduces them over CUDA IPC
-    / NVLink inside the kernel; the contributions are the backward's output,
-    written once before the timed phases."""
-    # The bandwidth EMA re-places subgroups off the slow directory tier over the
-    # first phases (paper §3.3); time the converged pipeline.
+    every subgroup: the engine's owned subgroups are bound to the world's
+    contributions, so each update reduces them over CUDA IPC / NVLink inside
+    the kernel. remote: a third ("remote_dir") tier beside DRAM and NVMe
+    (SURVEY C3). c0_steps > 0: afterwards, the same engine with no retention
+    (C = 0) for c0_steps timed phases."""
+    # The bandwidth EMA settles the NVMe tier's rate over the first phases
+    # (paper §3.3); time the converged pipeline.
     warmup = max(warmup, 5)
     import torch
     dev = torch.cuda.current_device()
@@ -511,9 +604,14 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     if root.exists():
         shutil.rmtree(root)
     root.mkdir(parents=True)
-    nvme = tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4))
-    probe = nvme.probe_bandwidth(1 << 30, 3)
-    # Host DRAM tier: data moves by block exchange, its transfer cost is the PCIe leg.
+    dirs = [tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4,
+                                lock_device=1))]
+    if remote:
+        dirs.append(tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
+                                        lock_device=1)))
+    probes = {t.id: t.probe_bandwidth(1 << 30, 3) for t in dirs}
+    # Host DRAM tier: blocks move by exchange; Eq. 1 sees it at the measured
+    # PCIe rate (the engine keeps a host_dram tier's configured rate).
     dram_bw = min(pcie["h2d"], pcie["d2h"])
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", dram_bw, dram_bw))
     trace = tf.EventTrace()
@@ -521,7 +619,7 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     t0 = time.time()
 
     def setup():
-        w = tf.OffloadWorker(rank, [dram, nvme], opt, tf.AdamHyper(), trace,
+        w = tf.OffloadWorker(rank, [dram] + dirs, opt, tf.AdamHyper(), trace,
                              tf.DeviceOptions(dev, DT, DT, ring, 0, 1, hbm_retain))
         for k, n in enumerate(sizes):
             w.add_subgroup(base_id + k, n)
@@ -531,85 +629,89 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
         return w
     w = setup_all_ranks(world, setup)
     init_s = time.time() - t0
-    log(f"[rank {rank}] e2e init {init_s:.1f}s, nvme probe r={probe.read_bw/1e9:.2f} w={probe.write_bw/1e9:.2f} GB/s,"
-        f" pcie h2d={pcie['h2d']/1e9:.1f} d2h={pcie['d2h']/1e9:.1f} GB/s")
+    log(f"[rank {rank}] e2e init {init_s:.1f}s, probes " +
+        ", ".join(f"tier {i}: r={p.read_bw/1e9:.2f} w={p.write_bw/1e9:.2f} GB/s" for i, p in probes.items()) +
+        f", pcie h2d={pcie['h2d']/1e9:.1f} d2h={pcie['d2h']/1e9:.1f} bidir={pcie['bidir']/1e9:.1f} GB/s")
     src = tf.SyntheticGradSource(seed)
-    phases = []
-    for it in range(warmup + steps):
-        if peer is None:
-            w.run_backward_sim(it, src, 1)  # the backward's output: device-resident 16-bit gradients
-        barrier(world)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        st = w.run_update(it)  # C ABI: prefetch -> H2D -> kernel -> D2H -> flush, all inside
-        b.record()
-        torch.cuda.synchronize()
-        ms = a.elapsed_time(b)
-        barrier(world)
-        if it >= warmup:
-            phases.append((ms, st))
-        log(f"[rank {rank}] e2e phase {it}: {ms:.0f} ms, hits {st.cache_hits}, alloc {st.flush_allocation}, "
-            f"kernel {st.kernel_seconds*1e3:.0f} ms, h2d {st.h2d_seconds*1e3:.0f} ms, d2h {st.d2h_seconds*1e3:.0f} ms")
-    params = sum(sizes)
-    ms = statistics.mean(p[0] for p in phases)
+    backward = None if peer is not None else (lambda it: w.run_backward_sim(it, src, 1))
+    phases = run_phases(w, world, rank, warmup, steps, backward, "e2e")
+    rl = pipeline_roofline(phases, pcie, probes)
     last = phases[-1][1]
     M = len(sizes)
-    hits = statistics.mean(p[1].cache_hits for p in phases)
-    retained = last.retained
-    alloc = last.flush_allocation
-    # Pipeline roofline per phase. PCIe: the bytes each direction moved
-    # (12 B/param, minus the HBM-retained subgroups), against each direction
-    # alone and against the measured duplex ceiling. Tiers: bytes actually
-    # moved (PhaseStats.tier_obs) over the tier's probed rates; the host_dram
-    # tier moves blocks by exchange, so it costs no tier time.
-    h2d_b = statistics.mean(p[1].h2d_bytes for p in phases)
-    d2h_b = statistics.mean(p[1].d2h_bytes for p in phases)
-    pcie_s = max(h2d_b / pcie["h2d"], d2h_b / pcie["d2h"], (h2d_b + d2h_b) / pcie["bidir"])
-    obs = last.tier_obs
-    nvme_s = obs[1].read_bytes / probe.read_bw + obs[1].write_bytes / probe.write_bw
-    bound_s = max(pcie_s, nvme_s)
-    res = dict(ms=ms, params=params, h2d=int(h2d_b), d2h=int(d2h_b), init_s=init_s, hits=hits,
-               alloc=alloc, retained=retained, pcie=pcie, nvme=dict(read=probe.read_bw, write=probe.write_bw),
-               bound_ms=bound_s * 1e3, pcie_bound_ms=pcie_s * 1e3, tier_bound_ms=nvme_s * 1e3,
-               kernel_ms=statistics.mean(p[1].kernel_seconds for p in phases) * 1e3,
-               launches=sum(2 * M for _ in phases), tier_read_bytes=sum(o.read_bytes for o in obs),
-               tier_write_bytes=sum(o.write_bytes for o in obs))
+    res = dict(ms=statistics.mean(p[0] for p in phases), params=sum(sizes), h2d=int(rl["h2d"]), d2h=int(rl["d2h"]),
+               init_s=init_s, hits=statistics.mean(p[1].cache_hits for p in phases), alloc=last.flush_allocation,
+               retained=last.retained, pcie=pcie, probes={i: (p.read_bw, p.write_bw) for i, p in probes.items()},
+               bound_ms=rl["bound_s"] * 1e3, pcie_bound_ms=rl["pcie_s"] * 1e3, tier_bound_ms=rl["tier_s"] * 1e3,
+               per_tier=rl["per_tier"], kernel_ms=statistics.mean(p[1].kernel_seconds for p in phases) * 1e3,
+               launches=len(phases) * M, tier_read_bytes=sum(o.read_bytes for o in last.tier_obs),
+               tier_write_bytes=sum(o.write_bytes for o in last.tier_obs), subgroups=M)
+    if c0_steps > 0:
+        w.set_cache_slots(0)
+        ph0 = run_phases(w, world, rank, 2, c0_steps, backward, "e2e C=0")
+        rl0 = pipeline_roofline(ph0, pcie, probes)
+        res["c0"] = dict(ms=statistics.mean(p[0] for p in ph0), h2d=int(rl0["h2d"]), d2h=int(rl0["d2h"]),
+                         bound_ms=rl0["bound_s"] * 1e3, pcie_bound_ms=rl0["pcie_s"] * 1e3,
+                         tier_bound_ms=rl0["tier_s"] * 1e3, alloc=ph0[-1][1].flush_allocation,
+                         hits=statistics.mean(p[1].cache_hits for p in ph0))
+        res["launches"] += len(ph0) * M
     w.close()
     del w
     shutil.rmtree(root, ignore_errors=True)
     return res
 
 
+def e2e_line(r, world, extra):
+    e_ms = allmax(world, r["ms"])
+    line = {"value": allsum(world, r["params"]) / (e_ms / 1e3), "unit": "params/s",
+            "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": round(e_ms, 2),
+            "pipeline_bound_ms": round(r["bound_ms"], 1), "pipeline_frac": round(r["bound_ms"] / e_ms, 4),
+            "pcie_bound_ms": round(r["pcie_bound_ms"], 1), "tier_bound_ms": round(r["tier_bound_ms"], 1),
+            "per_tier": r["per_tier"],
+            "tier_bytes_per_step": {"read": r["tier_read_bytes"], "write": r["tier_write_bytes"]},
+            "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"], "retained": r["retained"],
+            "pcie_gbs": {k: round(v / 1e9, 1) for k, v in r["pcie"].items()},
+            "kernel_ms_per_phase": round(r["kernel_ms"], 2), "init_s": round(r["init_s"], 1),
+            "gpu_launches": r["launches"], "subgroups_per_rank": r["subgroups"]}
+    if "c0" in r:
+        c0 = r["c0"]
+        c_ms = allmax(world, c0["ms"])
+        line["streaming_c0"] = {"value": allsum(world, r["params"]) / (c_ms / 1e3), "unit": "params/s",
+                                "ms_per_step": round(c_ms, 2), "h2d_bytes_per_step": c0["h2d"],
+                                "d2h_bytes_per_step": c0["d2h"], "pipeline_bound_ms": round(c0["bound_ms"], 1),
+                                "pipeline_frac": round(c0["bound_ms"] / c_ms, 4),
+                                "tier_bound_ms": round(c0["tier_bound_ms"], 1), "flush_allocation": c0["alloc"],
+                                "cache_hits_per_phase": c0["hits"],
+                                "note": "same engine, retention capacity C = 0: every subgroup streams both ways"}
+    line.update(extra)
+    return line
+
+
 # ---------------------------------------------------------------------------
-# leg 3: spill (SURVEY C4 shape): a capacity-capped host-DRAM tier and a few
-# pinned staging slots, so Eq. 1 spills the state to two directory tiers
-# (local "NVMe" + "remote"); the retention capacity held in HBM
-# (hbm_retain=2). Tier-bound; bounded sample.
+# spill: a capacity-capped host-DRAM tier and a few pinned staging
+# slots, so Eq. 1 spills the state to two directory tiers (local "NVMe" +
+# "remote"); the retention capacity held in HBM (hbm_retain=2). Tier-bound;
+# bounded sample of a Llama-2-70B rank at N=4 (173 subgroups: ~80 fit the HBM
+# beside the 16-bit gradient/param arenas, i.e. ~46% retained; host DRAM
+# capped to a third of the rest).
 
 
-def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=4, pool=8, ring=4,
-              lock_shared=True):
+def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=4, pool=8, ring=4, M=12):
     import torch
     dev = torch.cuda.current_device()
     root = Path(tier_root) / f"spill_rank{rank}"
     shutil.rmtree(root, ignore_errors=True)
     root.mkdir(parents=True)
-    # 12 subgroups per rank, bounded by the disk the ranks share (at most half
-    # its free space): when N ranks' full-size subgroups do not fit, the
-    # subgroups shrink rather than the sample (params/s stays comparable).
+    # Bounded by the disk the ranks share (at most half its free space): when
+    # N ranks' full-size subgroups do not fit, the subgroups shrink rather
+    # than the sample (params/s stays comparable).
     free = shutil.disk_usage(root).free
-    M = min(len(sizes), 12)
     sub = min(max(sizes), int(0.5 * free / world / M // 12) // 4096 * 4096)
     sub = int(allmin(world, sub))  # the same sample on every rank
     if sub < 1_000_000:
         raise RuntimeError(f"not enough free disk for the spill sample ({free / 1e9:.1f} GB)")
     sizes = [sub] * M
-    # Two-level retention inside the same host budget: M/2 subgroups in HBM
-    # and 2 of the pool's 8 slots retain too (DeviceOptions.hbm_cache_slots).
-    hbm_c = M // 2
-    cache = hbm_c + max(0, min(2, M - hbm_c - 1))
-    dram_cap = max(1, (M - cache) // 2)  # host DRAM capped: Eq. 1 spills the rest to the directory tiers
+    cache = M // 2  # HBM retention: ~46% of a 70B rank at N=4
+    dram_cap = max(1, (M - cache) // 3)  # host DRAM holds a third of the rest
     block = 4096 * ((32 + 12 * max(sizes) + 4095) // 4096)
     for d in ("nvme", "remote"):
         (root / d).mkdir()
@@ -617,7 +719,7 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     # per device, TierSpec.lock_device): their transfers take turns instead of
     # seeking against each other.
     same_device = os.stat(root / "nvme").st_dev == os.stat(root / "remote").st_dev
-    lock_dev = 1 if same_device and lock_shared else 0
+    lock_dev = 1 if same_device else 0
     dirs = [tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4,
                                 lock_device=lock_dev)),
             tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
@@ -632,36 +734,21 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
     opt = tf.ScheduleOptions(pool_slots=pool, cache_slots=cache, lock_dir=str(Path(tier_root) / "spill_locks"))
 
     def setup():
-        w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace,
-                             tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2, 1, hbm_c))
+        w = tf.OffloadWorker(rank, tiers, opt, tf.AdamHyper(), trace, tf.DeviceOptions(dev, DT, DT, ring, 0, 1, 2))
         for k, n in enumerate(sizes):
             w.add_subgroup(base_id + k, n)
         w.init_and_flush_all(seed)
         return w
     w = setup_all_ranks(world, setup)
     src = tf.SyntheticGradSource(seed)
-    phases = []
-    for it in range(warmup + steps):
-        w.run_backward_sim(it, src, 1)
-        barrier(world)
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        st = w.run_update(it)
-        b.record()
-        torch.cuda.synchronize()
-        barrier(world)
-        ms = a.elapsed_time(b)
-        log(f"[rank {rank}] spill phase {it}: {ms:.0f} ms, hits {st.cache_hits}, alloc {st.flush_allocation}")
-        if it >= warmup:
-            phases.append((ms, st))
+    phases = run_phases(w, world, rank, warmup, steps, lambda it: w.run_backward_sim(it, src, 1), "spill")
+    timeline = [dict(ms=round(ms, 1), io=[dict(id=e.id, read_s=round(e.read_seconds, 4),
+                                                 write_s=round(e.write_seconds, 4)) for e in st.subgroup_io])
+                for ms, st in phases[-1:]]
     w.close()
     del w
     shutil.rmtree(root, ignore_errors=True)
     ms = statistics.mean(p[0] for p in phases)
-    # Tier roofline: each tier's I/O thread moves its reads and writes in turn,
-    # so a tier needs read/r + write/w; tiers on one physical device add up,
-    # independent devices overlap (the Eq. 1 model).
     per_tier = []
     for i, pr in enumerate(probes, start=1):  # tier 0 (host DRAM) moves blocks by exchange: no tier time
         rb = statistics.mean(p[1].tier_obs[i].read_bytes for p in phases)
@@ -669,82 +756,58 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=2, steps=
         per_tier.append(dict(read_bytes=rb, write_bytes=wb, read_gbs=round(pr.read_bw / 1e9, 2),
                              write_gbs=round(pr.write_bw / 1e9, 2), seconds=rb / pr.read_bw + wb / pr.write_bw))
     parallel_s = max(t["seconds"] for t in per_tier)
-    # One physical device: its ceiling is the best rate any probe of it saw
-    # (the probes of the two roots differ only by noise), so every byte on it
-    # is charged at that rate.
+    # One physical device: its ceiling is the best rate any probe of it saw,
+    # and every rank's tier roots sit under the one tier_root (the node's
+    # bytes share it).
     dev_r = max(pr.read_bw for pr in probes)
     dev_w = max(pr.write_bw for pr in probes)
-    # Every rank's tier roots sit under the one tier_root, i.e. on the same
-    # device: the node's bytes share it.
     rb_all = allsum(world, sum(t["read_bytes"] for t in per_tier))
     wb_all = allsum(world, sum(t["write_bytes"] for t in per_tier))
     serial_s = rb_all / dev_r + wb_all / dev_w
     bound_s = serial_s if same_device else parallel_s
-    return dict(ms=ms, params=sum(sizes), subgroups=M, subgroup_params=sub, cache=cache, hbm_cache=hbm_c, pool=pool,
+    return dict(ms=ms, params=sum(sizes), subgroups=M, subgroup_params=sub, cache=cache, pool=pool,
                 same_device=same_device, lock_device=lock_dev, dram_cap=dram_cap,
                 bound_ms=bound_s * 1e3, independent_bound_ms=parallel_s * 1e3, per_tier=per_tier,
-                hits=statistics.mean(p[1].cache_hits for p in phases),
-                alloc=phases[-1][1].flush_allocation, launches=steps * M)
-
-
-def e2e_exchange(tf, sizes, a, rank, world):
-    """e2e with the fused reduce-scatter (strong scaling over one model): each
-    rank streams the subgroups it owns through the engine, their gradients the
-    in-kernel sum of every rank's contribution."""
-    import torch
-
-    from paper_2509_02480_b200 import parallel
-    begin, count = parallel.shard(len(sizes), world, rank)
-    owned = sizes[begin:begin + count]
-    e_sizes, pool, cache = e2e_shard(owned, world, a.pool_slots, a.cache_slots, a.hbm_retain)
-    n_e = int(allmin(world, len(e_sizes)))
-    pool = int(allmin(world, pool))
-    cache = int(allmin(world, cache)) if cache >= 0 else cache
-    e_sizes = e_sizes[:n_e]
-    with parallel.PeerGradients(sizes, world, rank, device=torch.cuda.current_device(),
-                                dtype="bf16" if DT else "f16") as pg:
-        for sg in range(begin, begin + n_e) if world == 1 else range(len(sizes)):
-            tf.synthetic_grads(pg.local(sg).view(torch.int16), a.seed + 100 * rank, sg, 0, dtype=DT)
-        torch.cuda.synchronize()
-        barrier(world)  # every contribution written before any owner reads it
-        r = e2e_leg(tf, e_sizes, begin, a.steps, a.warmup, a.seed, rank, world, a.tier_root, pool, cache, a.ring,
-                    a.hbm_retain, peer=pg)
-        barrier(world)  # no rank frees its contribution while a peer may still read it
-    e_ms = allmax(world, r["ms"])
-    total = allsum(world, r["params"])
-    return {"value": total / (e_ms / 1e3), "unit": "params/s", "h2d_bytes_per_step": r["h2d"],
-            "d2h_bytes_per_step": r["d2h"], "ms_per_step": e_ms, "pipeline_bound_ms": round(r["bound_ms"], 1),
-            "pipeline_frac": round(r["bound_ms"] / e_ms, 4), "cache_hits_per_phase": r["hits"],
-            "subgroups_per_rank": n_e, "pool_slots": pool, "cache_slots": cache, "gpu_launches": r["launches"],
-            "gradient_sources": world,
-            "path": "C ABI tfg_engine_run_update with bind_grad_sources (fused reduce-scatter over CUDA IPC), "
-                    "tiers [host_dram pinned, local_dir O_DIRECT]"}
+                hits=statistics.mean(p[1].cache_hits for p in phases), alloc=phases[-1][1].flush_allocation,
+                launches=(warmup + steps) * M, phase_ms=[round(p[0], 1) for p in phases], last_phase_io=timeline)
 
 
 # ---------------------------------------------------------------------------
-# reference CPU engine (oracle/_ref), bounded sample
+# reference CPU engine (oracle/_ref), same config, bounded sample
 
 
-def reference_sample(steps, warmup, tier_root, n_sub=4, sub=25_000_000, seed=42):
+def reference_sample(wl, world, steps, warmup, tier_root, seed=42, n_sub=7):
+    """The reference OffloadWorker::run_update on the line's config: the same
+    subgroup size, tier kinds (host DRAM as the reference's in-memory tier at
+    the PCIe rate our DRAM tier is given, a local directory tier as NVMe, and
+    a remote directory tier at N > 1) and retained fraction, on n_sub
+    subgroups (7 = 3 retained + 4 streamed, i.e. the 29/68 of the C2 line),
+    all host threads. Gradients come from one backward and are reused by the
+    later phases (the update's cost does not depend on their values)."""
     import oracle
     threads = os.cpu_count() or 1
     root = Path(tier_root) / "ref"
     shutil.rmtree(root, ignore_errors=True)
     root.mkdir(parents=True)
-    tiers = [dict(kind=2, read_bps=20e9, write_bps=20e9), dict(kind=0, root=str(root / "nvme"), io_parallelism=4)]
+    sub = wl["sub"]
+    C = max(1, round(n_sub * RETAINED_FRACTION))
+    tiers = [dict(kind=2, read_bps=50e9, write_bps=50e9), dict(kind=0, root=str(root / "nvme"), io_parallelism=4)]
+    if world > 1:
+        tiers.append(dict(kind=1, root=str(root / "remote"), io_parallelism=4))
     t0 = time.time()
-    res = oracle.run_ref_engine([sub] * n_sub, tiers, fixed_ratio=[3.0, 1.0], pool_slots=5, update_threads=threads,
+    res = oracle.run_ref_engine([sub] * n_sub, tiers, pool_slots=C + 3, cache_slots=C, update_threads=threads,
                                 lock_dir=str(root / "locks"), seed=seed, iterations=warmup + steps,
-                                want_states=False, events_cap=1)
+                                want_states=False, events_cap=1, backward_once=True)
     wall = time.time() - t0
     shutil.rmtree(root, ignore_errors=True)
     its = res["iters"][warmup:]
     per = [it["params_updated"] / it["update_seconds"] for it in its]
     return dict(value=statistics.mean(per), update_s=[it["update_seconds"] for it in its], cores=threads,
-                params=n_sub * sub, wall=wall,
-                sample=(f"reference OffloadWorker::run_update, {n_sub} subgroups x {sub:,} params, tiers "
-                        f"[mem_throttled 20 GB/s as DRAM, local_dir], pool 5 (C=2), update_threads={threads}, "
-                        f"{steps} timed of {warmup + steps} iterations"))
+                params=n_sub * sub, wall=wall, alloc=its[-1]["flush_allocation"],
+                sample=(f"reference OffloadWorker::run_update (oracle/_ref), {n_sub} subgroups x {sub:,} params, "
+                        f"C={C} retained (pool {C + 3}), tiers [mem_throttled 50 GB/s as host DRAM, local_dir"
+                        f"{', remote_dir' if world > 1 else ''}], update_threads={threads}, "
+                        f"{steps} timed of {warmup + steps} phases"))
 
 
 def cpu_model() -> str:
@@ -757,21 +820,51 @@ def cpu_model() -> str:
     return "unknown"
 
 
+def line_config(wl_name, world, dtype):
+    """The workload both arms report (identical dicts)."""
+    wl = WORKLOADS[wl_name]
+    sizes = subgroup_sizes(wl["total"], wl["sub"])
+    from paper_2509_02480_b200.parallel import shard
+    per_rank = len(sizes) if world == 1 else shard(len(sizes), world, 0)[1]
+    return {"workload": wl["desc"], "survey_config": wl["survey"], "params_total": sum(sizes),
+            "subgroup_params": wl["sub"], "subgroups_per_rank": per_rank, "grad_dtype": dtype, "param_dtype": dtype,
+            "tiers": "host DRAM + local NVMe" + (" + remote" if world > 1 else ""),
+            "retained_fraction": round(RETAINED_FRACTION, 4) if world == 1 else None,
+            "l2": "inputs larger than L2 (>= 1.2 GB of state per subgroup launch vs 126 MB L2; no flush needed)",
+            "parallelism": (f"zero3-shard x{world}" + (", gradient reduce-scatter in the update" if world > 1 else ""))}
+
+
 # ---------------------------------------------------------------------------
 
 
+def reference_main(a, wl_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    world = a.gpus
+    r = reference_sample(WORKLOADS[wl_name], world, a.steps, a.warmup, a.tier_root)
+    line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "params/s",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": statistics.mean(r["update_s"]) * 1e3, "higher_is_better": True,
+            "scaling": "weak" if world == 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference generators)", "config": line_config(wl_name, world, a.dtype),
+            "cpu_baseline": {"value": r["value"], "unit": "params/s", "cores": r["cores"], "kind": "reference",
+                             "sample": r["sample"], "cpu": cpu_model()},
+            "e2e": {"value": r["value"], "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="llama2-7b")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
+                    help="default: llama2-7b (C2) at N=1, 20b (C3) at N>1")
     ap.add_argument("--tier-root", default=os.environ.get("TFB_TIER_ROOT", str(ROOT / "gpurun_out" / "bench_tiers")))
-    # HBM cache (hbm_retain 2), C 29 / pool 16 / ring 12: 29 retained
-    # subgroups (35 GB) + 12 ring buffers (14 GB) of HBM beside the 27 GB of
-    # 16-bit gradients and working params, 76 GB of the 180 GB; 16 streaming
-    # slots + 4 write-back blocks + 39 host-DRAM tier blobs = 71 GB pinned.
     ap.add_argument("--pool-slots", type=int, default=16)
     ap.add_argument("--cache-slots", type=int, default=29,
                     help="retention capacity C (HBM cache); -1: pool_slots - 3 (reference default)")
@@ -781,147 +874,157 @@ def main(argv=None):
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--dtype", choices=["f16", "bf16"], default="f16",
                     help="16-bit gradient and working-param kind (f16 = the reference's fp16)")
-    ap.add_argument("--exchange", choices=["none", "fused", "nccl"], default="none",
-                    help="strong scaling over one model with the gradient reduce-scatter in the update "
-                         "(fused: peer loads in the Adam kernel; nccl: reduce_scatter then the kernel)")
+    ap.add_argument("--exchange", choices=["none", "fused", "nccl"], default=None,
+                    help="gradient reduce-scatter in the update (default: none at N=1, fused at N>1; "
+                         "at N>1 the nccl form is also timed unless --skip-nccl)")
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-spill", action="store_true", help="skip the directory-tier spill sample (SURVEY C4)")
+    ap.add_argument("--skip-nccl", action="store_true")
+    ap.add_argument("--c0-steps", type=int, default=5, help="timed phases of the C=0 streaming e2e (0: skip)")
     a = ap.parse_args(argv)
 
-    wl = WORKLOADS[a.workload]
     global DT
     DT = 1 if a.dtype == "bf16" else 0
-    sizes = subgroup_sizes(wl["total"], wl["sub"])
-
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and a.gpus > 1 and a.impl == "ours":
+        return spawn_ranks(argv, a.gpus)
+    world_env = int(env_world or 1)
+    if a.impl == "ours" and world_env != a.gpus:
+        log(f"bench.py: WORLD_SIZE={world_env} but --gpus {a.gpus}")
+        return 2
+    wl_name = a.workload or ("llama2-7b" if a.gpus == 1 else "20b")
     if a.impl == "reference":
-        rank = int(os.environ.get("RANK", "0"))
-        if rank != 0:
-            return 0
-        r = reference_sample(a.steps, a.warmup, a.tier_root)
-        line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": "params/s",
-                "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
-                "ms_per_step": statistics.mean(r["update_s"]) * 1e3, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generators)",
-                "config": {"workload": wl["desc"], "sample_params": r["params"], "parallelism": "cpu threads"},
-                "cpu_baseline": {"value": r["value"], "unit": "params/s", "cores": r["cores"], "kind": "reference",
-                                 "sample": r["sample"], "cpu": cpu_model()},
-                "e2e": {"value": r["value"], "unit": "params/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return 0
+        return reference_main(a, wl_name)
 
+    wl = WORKLOADS[wl_name]
+    sizes = subgroup_sizes(wl["total"], wl["sub"])
     world, rank, local = dist_init()
     import torch
     from paper_2509_02480_b200 import build as _build
     if rank == 0 and not _build.up_to_date():
         _build.build()
     barrier(world)
+    from paper_2509_02480_b200 import parallel
     from paper_2509_02480_b200 import tierflow as tf
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device")
     torch.cuda.set_device(local)
-    base_id = rank * len(sizes)
+    exchange = a.exchange or ("none" if world == 1 else "fused")
 
     pk = peaks()
     alg_bytes = ALG_BYTES_PER_PARAM
-    if a.exchange != "none":
-        dl = exchange_leg(tf, sizes, a.steps, a.warmup, a.seed, rank, world, a.exchange)
-        step_ms = allmax(world, dl["total_ms"] / a.steps)
-        value = sum(sizes) / (step_ms / 1e3)
-        params_rank = dl["owned_params"]
-        launches_rank = max(1, dl["owned"])
-        if a.exchange == "fused":  # own contribution local, world-1 over NVLink
-            alg_bytes = 26 + 2 * world
-    else:
+    nccl_line = None
+    if exchange == "none":
+        # weak scaling: every rank its own copy of the workload's shape
+        base_id = rank * len(sizes)
         dl = device_leg(tf, sizes, base_id, a.steps, a.warmup, a.seed, rank, world)
-        step_ms = allmax(world, dl["total_ms"] / a.steps)
-        params_rank = sum(sizes)
-        value = world * params_rank / (step_ms / 1e3)
-        launches_rank = len(sizes)
+        scaling = "weak"
+    else:
+        dl = exchange_leg(tf, sizes, a.steps, a.warmup, a.seed, rank, world, exchange)
+        if exchange == "fused":  # own contribution local, N-1 over NVLink, P/m/v 24, params 2
+            alg_bytes = 26 + 2 * world
+        scaling = "strong"
+        if world > 1 and exchange == "fused" and not a.skip_nccl:
+            try:
+                nl = exchange_leg(tf, sizes, a.steps, a.warmup, a.seed, rank, world, "nccl")
+                n_ms = allmax(world, nl["total_ms"] / a.steps)
+                nccl_line = {"value": allsum(world, nl["params"]) / (n_ms / 1e3), "unit": "params/s",
+                             "ms_per_step": n_ms, "kernel_ms_per_step": nl["kernel_ms"] / a.steps,
+                             "path": "NCCL reduce_scatter per subgroup bucket (side stream, double-buffered), "
+                                     "then the single-source fused kernel"}
+            except Exception as exc:
+                nccl_line = {"error": f"{type(exc).__name__}: {exc}"}
+                log(f"nccl exchange leg failed: {exc}")
+    step_ms = allmax(world, dl["total_ms"] / a.steps)
+    value = allsum(world, dl["params"]) / (step_ms / 1e3)
     kernel_s_per_launch = dl["kernel_ms"] / 1e3 / max(1, dl["launches"])
-    bytes_per_launch = alg_bytes * params_rank / launches_rank
-    achieved = bytes_per_launch / kernel_s_per_launch / 1e9
+    params_per_launch = dl["params"] / max(1, dl["timed_subgroups"])
+    achieved = alg_bytes * params_per_launch / kernel_s_per_launch / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": ncu_traffic(params_rank / launches_rank),
+                "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": ncu_traffic(params_per_launch),
                 "peak_source": pk["source"], "alg_bytes_per_param": alg_bytes,
                 "kernel": "adam_fused_kernel (float4 quads, binary64 element math, constant-divisor "
                           "quotients, 4 CTAs x 256 threads per SM)"
                           + (f"; {world} gradient sources summed in-kernel, {world - 1} over NVLink peer loads"
-                             if a.exchange == "fused" else ""),
+                             if exchange == "fused" else ""),
                 "traffic_source": "profiles/ncu_adam_fused.json (ncu --set full, dram bytes per 100M-param launch)",
                 "copy_sustained_gbs": dl.get("copy_sustained_gbs"),
                 "frac_of_copy_sustained": (round(achieved / dl["copy_sustained_gbs"], 4)
                                            if dl.get("copy_sustained_gbs") else None)}
 
     e2e = None
-    if a.exchange == "nccl":
-        e2e = {"skipped": "--exchange nccl times the device-resident update only"}
-    elif a.exchange == "fused" and not a.skip_e2e:
+    if not a.skip_e2e:
         try:
-            e2e = e2e_exchange(tf, sizes, a, rank, world)
-        except Exception as exc:
-            e2e = {"error": f"{type(exc).__name__}: {exc}"}
-            log(f"e2e leg failed: {exc}")
-    elif not a.skip_e2e:
-        try:
-            e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots, a.hbm_retain)
-            # every rank streams the same shard shape (MemAvailable is read at slightly different times)
-            n_e = int(allmin(world, len(e_sizes)))
-            pool = int(allmin(world, pool))
-            cache = int(allmin(world, cache)) if cache >= 0 else cache
-            e_sizes = e_sizes[:n_e]
-            if len(e_sizes) < len(sizes) or pool != a.pool_slots:
-                log(f"[rank {rank}] e2e: host memory holds {len(e_sizes)} of {len(sizes)} subgroups per rank, "
-                    f"pool {pool}, cache {cache}")
-            r = e2e_leg(tf, e_sizes, base_id, a.steps, a.warmup, a.seed, rank, world, a.tier_root, pool, cache,
-                        a.ring, a.hbm_retain)
-            e_ms = allmax(world, r["ms"])
-            e2e = {"value": world * r["params"] / (e_ms / 1e3), "unit": "params/s",
-                   "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": r["d2h"], "ms_per_step": e_ms,
-                   "pipeline_bound_ms": round(r["bound_ms"], 1), "pipeline_frac": round(r["bound_ms"] / e_ms, 4),
-                   "pcie_bound_ms": round(r["pcie_bound_ms"], 1), "tier_bound_ms": round(r["tier_bound_ms"], 1),
-                   "tier_bytes_per_step": {"read": r["tier_read_bytes"], "write": r["tier_write_bytes"]},
-                   "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"], "retained": r["retained"],
-                   "pcie_gbs": {k: round(v / 1e9, 1) for k, v in r["pcie"].items()},
-                   "nvme_gbs": {k: round(v / 1e9, 2) for k, v in r["nvme"].items()},
-                   "kernel_ms_per_phase": r["kernel_ms"], "init_s": r["init_s"], "gpu_launches": r["launches"],
-                   "hbm_retain": a.hbm_retain, "pool_slots": pool, "cache_slots": cache, "ring": a.ring,
-                   "subgroups_per_rank": len(e_sizes),
-                   "path": "C ABI tfg_engine_run_update, tiers [host_dram pinned, local_dir O_DIRECT]"}
+            if exchange == "none":
+                e_sizes, pool, cache = e2e_shard(sizes, world, a.pool_slots, a.cache_slots, a.hbm_retain)
+                # every rank streams the same shard shape (MemAvailable is read at slightly different times)
+                n_e = int(allmin(world, len(e_sizes)))
+                pool = int(allmin(world, pool))
+                cache = int(allmin(world, cache)) if cache >= 0 else cache
+                e_sizes = e_sizes[:n_e]
+                r = e2e_leg(tf, e_sizes, rank * len(sizes), a.steps, a.warmup, a.seed, rank, world, a.tier_root,
+                            pool, cache, a.ring, a.hbm_retain, c0_steps=min(a.c0_steps, a.steps))
+                e2e = e2e_line(r, world, {"hbm_retain": a.hbm_retain, "pool_slots": pool, "cache_slots": cache,
+                                          "ring": a.ring,
+                                          "path": "C ABI tfg_engine_run_update, tiers [host_dram pinned, "
+                                                  "local_dir O_DIRECT], Eq. 1 over both"})
+            elif exchange == "fused":
+                begin, count = parallel.shard(len(sizes), world, rank)
+                owned = sizes[begin:begin + count]
+                e_sizes, pool, cache = e2e_shard(owned, world, a.pool_slots, a.cache_slots, a.hbm_retain)
+                n_e = int(allmin(world, len(e_sizes)))
+                pool = int(allmin(world, pool))
+                cache = int(allmin(world, cache)) if cache >= 0 else cache
+                e_sizes = e_sizes[:n_e]
+                with parallel.PeerGradients(sizes, world, rank, device=torch.cuda.current_device(),
+                                            dtype="bf16" if DT else "f16", window=EXCHANGE_WINDOW) as pg:
+                    for s_ in range(EXCHANGE_WINDOW * world):
+                        tf.synthetic_grads(pg.slot_view(s_).view(torch.int16), a.seed + 100 * rank, s_, 0, dtype=DT)
+                    torch.cuda.synchronize()
+                    barrier(world)  # every contribution written before any owner reads it
+                    r = e2e_leg(tf, e_sizes, begin, a.steps, a.warmup, a.seed, rank, world, a.tier_root, pool, cache,
+                                a.ring, a.hbm_retain, peer=pg, remote=True)
+                    barrier(world)  # no rank frees its contribution while a peer may still read it
+                e2e = e2e_line(r, world, {"hbm_retain": a.hbm_retain, "pool_slots": pool, "cache_slots": cache,
+                                          "ring": a.ring, "gradient_sources": world,
+                                          "path": "C ABI tfg_engine_run_update with bind_grad_sources (fused "
+                                                  "reduce-scatter over CUDA IPC), tiers [host_dram pinned, "
+                                                  "local_dir O_DIRECT, remote_dir O_DIRECT]"})
+            else:
+                e2e = {"skipped": "--exchange nccl times the device-resident update only"}
         except Exception as exc:  # keep the device-timed line; report the failure
             e2e = {"error": f"{type(exc).__name__}: {exc}"}
             log(f"e2e leg failed: {exc}")
 
     spill = None
-    if a.exchange == "none" and not a.skip_e2e and not a.skip_spill:
+    if exchange == "none" and not a.skip_e2e and not a.skip_spill:
         try:
-            r = spill_leg(tf, sizes, base_id, rank, world, a.tier_root, a.seed)
+            r = spill_leg(tf, sizes, rank * len(sizes), rank, world, a.tier_root, a.seed)
             s_ms = allmax(world, r["ms"])
-            spill = {"value": world * r["params"] / (s_ms / 1e3), "unit": "params/s", "ms_per_step": round(s_ms, 1),
+            spill = {"value": allsum(world, r["params"]) / (s_ms / 1e3), "unit": "params/s",
+                     "ms_per_step": round(s_ms, 1), "phase_ms": r["phase_ms"],
                      "tier_bound_ms": round(r["bound_ms"], 1), "tier_frac": round(r["bound_ms"] / s_ms, 4),
                      "independent_tier_bound_ms": round(r["independent_bound_ms"], 1),
                      "tiers_share_one_device": r["same_device"], "device_semaphore": bool(r["lock_device"]),
-                     "per_tier": r["per_tier"],
-                     "subgroups_per_rank": r["subgroups"], "subgroup_params": r["subgroup_params"],
-                     "cache_slots": r["cache"],
-                     "hbm_cache_slots": r["hbm_cache"], "pool_slots": r["pool"],
-                     "dram_tier_capacity_subgroups": r["dram_cap"],
-                     "cache_hits_per_phase": r["hits"], "flush_allocation": r["alloc"],
-                     "gpu_launches": r["launches"],
+                     "per_tier": r["per_tier"], "subgroups_per_rank": r["subgroups"],
+                     "subgroup_params": r["subgroup_params"], "cache_slots": r["cache"], "pool_slots": r["pool"],
+                     "dram_tier_capacity_subgroups": r["dram_cap"], "cache_hits_per_phase": r["hits"],
+                     "flush_allocation": r["alloc"], "gpu_launches": r["launches"],
+                     "last_phase_io": r["last_phase_io"],
+                     "workload": WORKLOADS["llama2-70b"]["desc"] + ": a rank at N=4 (173 subgroups, ~46% fit the "
+                                 "HBM cache), bounded sample of 12 subgroups, 6 retained in HBM, host DRAM capped",
                      "path": "C ABI tfg_engine_run_update, tiers [host_dram capped, local_dir O_DIRECT, "
-                             "remote_dir O_DIRECT], retention in HBM + host slots (hbm_retain=2, two-level)"}
+                             "remote_dir O_DIRECT], retention in HBM (hbm_retain=2)"}
         except Exception as exc:
             spill = {"error": f"{type(exc).__name__}: {exc}"}
             log(f"spill leg failed: {exc}")
 
     e2e_launches = (e2e or {}).get("gpu_launches", 0) + (spill or {}).get("gpu_launches", 0)
-    scaling = "strong" if a.exchange != "none" else "weak"
-    parallelism = (f"zero3-shard x{world}, gradient reduce-scatter {a.exchange} (strong)" if a.exchange != "none"
-                   else f"zero3-shard x{world} (weak)")
     cpu = None
     if rank == 0 and not a.skip_cpu:
         try:
-            r = reference_sample(1, 1, a.tier_root)
+            r = reference_sample(wl, world, 1, 1, a.tier_root)
             cpu = {"value": r["value"], "unit": "params/s", "cores": r["cores"], "kind": "reference",
                    "sample": r["sample"], "cpu": cpu_model()}
         except Exception as exc:
@@ -932,16 +1035,20 @@ def main(argv=None):
                 "warmup": a.warmup, "ms_per_step": step_ms, "higher_is_better": True, "scaling": scaling,
                 "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded reference generators: synthetic_param_init, SyntheticGradSource)",
-                "config": {"workload": wl["desc"], "params_per_rank": params_rank, "subgroups_per_rank": launches_rank,
-                           "grad_dtype": a.dtype, "param_dtype": a.dtype, "state": "fp32 P/m/v resident in HBM",
-                           "l2": (f"inputs larger than L2 ({ALG_BYTES_PER_PARAM * max(sizes) / 1e9:.2f} GB per "
-                                  "subgroup launch vs 126 MB L2; no flush needed)"
-                                  if ALG_BYTES_PER_PARAM * max(sizes) > 2 * 126e6 else
-                                  "WARNING: launch working set fits in L2; not a roofline-valid size"),
-                           "parallelism": parallelism},
+                "config": line_config(wl_name, world, a.dtype),
+                "value_setup": {"state": "fp32 P/m/v resident in HBM", "exchange": exchange,
+                                "subgroups_timed_per_rank": dl["timed_subgroups"],
+                                "owned_per_rank": dl.get("owned", dl["timed_subgroups"]),
+                                "params_timed_per_rank": dl["params"],
+                                "nonfinite_check": ("whole-phase count kernel, device-side gate on the updates"
+                                                    if exchange == "none" else
+                                                    "each contribution checked by its producer rank; owners count "
+                                                    "the rounded sums in-kernel")},
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "spill": spill,
                 "gpu_launches": dl.get("all_launches", dl["launches"]) + e2e_launches,
                 "clocks": dl["clocks"]}
+        if nccl_line is not None:
+            line["exchange_nccl"] = nccl_line
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist

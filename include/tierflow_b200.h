@@ -213,6 +213,14 @@ int tfg_ipc_close_handle(int device, void* ptr);
 int tfg_adam_fused(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
                    int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
                    unsigned long long* counters, void* stream);
+/* tfg_adam_fused behind a device-side gate: when *gate (device memory) is
+ * nonzero when the kernel starts, it writes nothing. A whole-phase non-finite
+ * count accumulated into the gate on the same stream (tfg_count_nonfinite16)
+ * rejects the phase's updates with no host round trip: the reference's
+ * check-before-mutate (harness.hpp:218-228, optimizer.hpp:123-127). */
+int tfg_adam_fused_gated(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
+                         int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                         unsigned long long* counters, const unsigned long long* gate, void* stream);
 /* Reduce + update in one pass: the gradient is the fp32 sum, in source order,
  * of n_sources (<= 8) 16-bit buffers — e.g. every data-parallel peer's
  * contribution to this rank's subgroup, read over NVLink through mapped peer
@@ -314,6 +322,9 @@ int tfg_engine_create(int worker_id, tfg_tier* const* tiers, int n_tiers, const 
 int tfg_engine_destroy(tfg_engine* engine);
 int tfg_engine_set_alpha(tfg_engine* engine, double alpha);                                 /* :315 */
 int tfg_engine_set_fixed_ratio(tfg_engine* engine, const double* ratio, int n);             /* :322 */
+/* ScheduleOptions::cache_slots (scheduler.hpp:44-49) for the following phases;
+ * between phases only. HBM cache mode: at most the buffers allocated at init. */
+int tfg_engine_set_cache_slots(tfg_engine* engine, int cache_slots);
 int tfg_engine_add_subgroup(tfg_engine* engine, uint32_t id, uint64_t param_count);         /* :324 */
 int tfg_engine_init_and_flush_all(tfg_engine* engine, uint64_t seed);                       /* :339 */
 int tfg_engine_run_backward_sim(tfg_engine* engine, int iteration, uint64_t seed, int accum_steps); /* :365 */

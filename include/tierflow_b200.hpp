@@ -214,6 +214,7 @@ public:
     void set_fixed_ratio(const std::vector<double>& r) {
         check(tfg_engine_set_fixed_ratio(h_, r.data(), static_cast<int>(r.size())));
     }
+    void set_cache_slots(int c) { check(tfg_engine_set_cache_slots(h_, c)); }
     void add_subgroup(SubgroupId id, std::uint64_t params) {
         check(tfg_engine_add_subgroup(h_, id, params));
         params_.push_back({id, params});

@@ -93,7 +93,7 @@ class RefRunCfg(C.Structure):
                 ("atomic_rw", C.c_int), ("update_threads", C.c_int), ("lock_dir", C.c_char_p),
                 ("seed", C.c_uint64), ("iterations", C.c_int), ("accum_steps", C.c_int), ("lr", C.c_double),
                 ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double),
-                ("skip_mask", C.c_uint32), ("skip_gradients", C.c_int)]
+                ("skip_mask", C.c_uint32), ("skip_gradients", C.c_int), ("backward_once", C.c_int)]
 
 
 class RefIterOut(C.Structure):
@@ -261,7 +261,7 @@ def run_engine_oracle(param_counts, seed, iters, pool_slots, cache_slots, cachin
 def run_ref_engine(param_counts, tiers, *, fixed_ratio=None, pool_slots=4, cache_slots=-1, enable_caching=True,
                    multi_path=True, atomic_rw=True, update_threads=1, lock_dir=None, seed=42, iterations=3,
                    accum_steps=1, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, skip_mask=0,
-                   want_states=True, events_cap=1 << 16, skip_gradients=True):
+                   want_states=True, events_cap=1 << 16, skip_gradients=True, backward_once=False):
     """Runs the UNMODIFIED reference OffloadWorker (via oracle/_ref).
 
     tiers: list of dicts {kind: 0|1|2, root, read_bps, write_bps, io_parallelism}.
@@ -277,7 +277,7 @@ def run_ref_engine(param_counts, tiers, *, fixed_ratio=None, pool_slots=4, cache
     lock = lock_dir.encode() if lock_dir else None
     cfg = RefRunCfg(M, params, len(tiers), tc, ratio, pool_slots, cache_slots, int(enable_caching), int(multi_path),
                     int(atomic_rw), update_threads, lock, seed, iterations, accum_steps, lr, beta1, beta2, eps,
-                    weight_decay, skip_mask, int(skip_gradients))
+                    weight_decay, skip_mask, int(skip_gradients), int(backward_once))
     iters = (RefIterOut * iterations)()
     total = sum(3 * n for n in param_counts)
     states = np.empty(total, np.float32) if want_states else None

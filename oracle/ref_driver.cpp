@@ -176,6 +176,8 @@ struct RefRunCfg {
     double lr, beta1, beta2, eps, weight_decay;
     uint32_t skip_mask;  // bit i: skip iteration i's update (non-finite step)
     int skip_gradients;  // 0: the ZeRO-3 baseline flow (fp32 gradients through storage)
+    int backward_once;   // 1: run_backward_sim at iteration 0 only, later phases reuse its gradients
+                         //    (bench timing samples: the update's cost does not depend on their values)
 };
 
 struct RefIterOut {
@@ -240,7 +242,7 @@ int ref_run_engine(const RefRunCfg* c, RefIterOut* iters_out, float* states_out,
         for (int it = 0; it < c->iterations; ++it) {
             RefIterOut r{};
             const auto b0 = std::chrono::steady_clock::now();
-            w->run_backward_sim(it, src, c->accum_steps);
+            if (it == 0 || !c->backward_once) w->run_backward_sim(it, src, c->accum_steps);
             r.backward_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count();
             r.trace_begin = r.trace_end = trace.size();
             if (!((c->skip_mask >> it) & 1u)) {

@@ -129,6 +129,7 @@ _SIGS = {
     "tfg_ipc_close_handle": (_i, [_i, _vp]),
     "tfg_adam_fused": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
     "tfg_adam_fused_contiguous": (_i, [_vp, _u64, _vp, _i, _vp, _i, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
+    "tfg_adam_fused_gated": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp, _vp]),
     "tfg_adam_fused_multi": (_i, [_vp, _vp, _vp, C.POINTER(_vp), _i, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
                                   _vp, _vp]),
     "tfg_adam_step": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
@@ -176,6 +177,7 @@ _SIGS = {
     "tfg_engine_destroy": (_i, [_vp]),
     "tfg_engine_set_alpha": (_i, [_vp, _d]),
     "tfg_engine_set_fixed_ratio": (_i, [_vp, C.POINTER(_d), _i]),
+    "tfg_engine_set_cache_slots": (_i, [_vp, _i]),
     "tfg_engine_add_subgroup": (_i, [_vp, C.c_uint32, _u64]),
     "tfg_engine_init_and_flush_all": (_i, [_vp, _u64]),
     "tfg_engine_run_backward_sim": (_i, [_vp, _i, _u64, _i]),

@@ -147,7 +147,8 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
 template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0, int PF = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
-                      unsigned long long* __restrict__ counters) {
+                      unsigned long long* __restrict__ counters, const unsigned long long* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;  // the phase was rejected on this stream: no writes
     unsigned nonfinite = 0, overflow = 0;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -301,11 +302,11 @@ cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     if (is_vec(a)) {
         const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
         adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS, C::kPrefetch>
-            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
+            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters, a.gate);
     } else {
         const unsigned grid = grid_for(a.n, B);
         adam_fused_kernel<GK, GMODE, OK, WD, false, 1, C::kDivc, B>
-            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters);
+            <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters, a.gate);
     }
     return cudaGetLastError();
 }

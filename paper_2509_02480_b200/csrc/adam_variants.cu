@@ -530,7 +530,7 @@ template <bool WD, int MINB>
 cudaError_t launch_scalar(const AdamLaunch& a, cudaStream_t stream) {
     const unsigned grid = grid_for(a.n, MINB);
     adam_fused_kernel<kF16, 0, kF16, WD, false, 1, 1, MINB>
-        <<<grid, kThreads, 0, stream>>>(state_io(a), sources_of(a), a.p16, a.n, a.c, a.counters);
+        <<<grid, kThreads, 0, stream>>>(state_io(a), sources_of(a), a.p16, a.n, a.c, a.counters, nullptr);
     return cudaGetLastError();
 }
 template <int MINB>

@@ -198,6 +198,16 @@ int tfg_adam_fused(float* p, float* m, float* v, const void* grad, int grad_dtyp
     });
 }
 
+int tfg_adam_fused_gated(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
+                         int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                         unsigned long long* counters, const unsigned long long* gate, void* stream) {
+    return guarded([&] {
+        auto a = adam_launch(p, m, v, grad, grad_dtype, param16, param_dtype, n, hyper, t, counters);
+        a.gate = gate;
+        tfb::cuda_check(tfb::launch_adam_fused(a, as_stream(stream)), "adam_fused_gated");
+    });
+}
+
 int tfg_adam_fused_multi(float* p, float* m, float* v, const void* const* grads, int n_sources, int grad_dtype,
                          uint16_t* param16, int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
                          unsigned long long* counters, void* stream) {
@@ -719,6 +729,13 @@ int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_pt
     return guarded([&] {
         need(engine, "engine");
         engine->w->bind_grad_buffer(id, device_ptr);
+    });
+}
+
+int tfg_engine_set_cache_slots(tfg_engine* engine, int cache_slots) {
+    return guarded([&] {
+        need(engine, "engine");
+        engine->w->set_cache_slots(cache_slots);
     });
 }
 

@@ -354,6 +354,16 @@ void OffloadWorker::set_alpha(double alpha) {
 
 void OffloadWorker::set_fixed_ratio(std::vector<double> ratio) { fixed_ratio_ = std::move(ratio); }
 
+void OffloadWorker::set_cache_slots(int cache_slots) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (in_flight_ != 0 || phase_stats_ != nullptr) throw Error("set_cache_slots during an update phase");
+    if (hbm_cache_mode() && cache_slots > static_cast<int>(hbm_cache_.size()) &&
+        !(dev_.hbm_cache_slots > 0))  // two-level: the excess is retained in host slots
+        throw ConfigError("set_cache_slots: " + std::to_string(cache_slots) + " exceeds the " +
+                          std::to_string(hbm_cache_.size()) + " HBM retention buffers allocated at init");
+    opt_.cache_slots = cache_slots;
+}
+
 void OffloadWorker::add_subgroup(SubgroupId id, std::uint64_t param_count) {
     if (pool_) throw Error("add_subgroup after pipeline initialization");
     if (param_count == 0) throw ConfigError("subgroup param_count must be > 0");
@@ -441,6 +451,11 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaMalloc(&p16_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(params16)");
     cuda_check(cudaMemset(grad_arena_, 0, std::max<std::size_t>(arena, 256)), "cudaMemset(grads)");
     cuda_check(cudaEventCreateWithFlags(&producer_done_, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&verdict_ready_, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&verdict_host_), std::max<std::size_t>(1, ids_.size()) *
+                                                                          sizeof(unsigned long long),
+                             cudaHostAllocDefault),
+               "cudaHostAlloc(verdict)");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&counters_), 2 * sizeof(unsigned long long)), "cudaMalloc");
     cuda_check(cudaMalloc(reinterpret_cast<void**>(&sg_counts_), ids_.size() * sizeof(unsigned long long)),
                "cudaMalloc");
@@ -522,6 +537,10 @@ void OffloadWorker::release_device() {
     cudaFree(sg_counts_);
     if (producer_done_) cudaEventDestroy(producer_done_);
     producer_done_ = nullptr;
+    if (verdict_ready_) cudaEventDestroy(verdict_ready_);
+    verdict_ready_ = nullptr;
+    if (verdict_host_) cudaFreeHost(verdict_host_);
+    verdict_host_ = nullptr;
     cudaStreamDestroy(s_h2d_);
     cudaStreamDestroy(s_k_);
     cudaStreamDestroy(s_d2h_);
@@ -748,16 +767,71 @@ bool OffloadWorker::gradients_finite() {
 }
 
 // The reference rejects non-finite gradients before mutating a subgroup
-// (precision.hpp:17-25 via scheduler.hpp:467-471). The fused kernel widens
-// and updates in one pass, so the whole phase is checked up front instead:
-// one 2-byte/param read (2n for n summed sources), and no subgroup is
-// mutated when any is bad.
-void OffloadWorker::check_grads_finite_or_throw() {
-    const auto counts = nonfinite_counts();
+// (precision.hpp:17-25 via scheduler.hpp:467-471; its harness checks the
+// whole model first, harness.hpp:218-228). The fused kernel widens and
+// updates in one pass, so the whole phase is checked before the first update
+// instead: one 2-byte/param count on the kernel stream (2n for n summed
+// sources), its per-subgroup counts copied back asynchronously. The host
+// does not wait for them before the phase's fetches start; it waits before
+// issuing the first update (await_grad_verdict), by which time the count has
+// long finished under the first fetch.
+void OffloadWorker::launch_grad_check() {
+    cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+    for (std::size_t k = 0; k < ids_.size(); ++k) {
+        const std::uint64_t pc = subgroups_.at(ids_[k]).param_count;
+        if (grad_sources_[k].empty())
+            cuda_check(launch_count_nonfinite16(grad_ptr_[k], pc, dev_.grad_kind, sg_counts_ + k, s_k_),
+                       "count_nonfinite");
+        else
+            cuda_check(launch_count_nonfinite_sum16(grad_sources_[k].data(), static_cast<int>(grad_sources_[k].size()),
+                                                    pc, dev_.grad_kind, sg_counts_ + k, s_k_),
+                       "count_nonfinite_sum");
+    }
+    cuda_check(cudaMemcpyAsync(verdict_host_, sg_counts_, ids_.size() * sizeof(unsigned long long),
+                               cudaMemcpyDeviceToHost, s_k_),
+               "cudaMemcpyAsync(verdict)");
+    cuda_check(cudaEventRecord(verdict_ready_, s_k_), "cudaEventRecord(verdict)");
+}
+
+// First subgroup with a non-finite gradient in plan order, or -1.
+std::int64_t OffloadWorker::await_grad_verdict() {
+    cuda_check(cudaEventSynchronize(verdict_ready_), "cudaEventSynchronize(verdict)");
     for (const SubgroupId id : order_)
-        if (counts[index_of_.at(id)] != 0)
-            throw GradientOverflowError("subgroup " + std::to_string(id) +
-                                        ": non-finite gradients reached the update phase");
+        if (verdict_host_[index_of_.at(id)] != 0) return id;
+    return -1;
+}
+
+// A rejected phase leaves no trace in residency: fetches it issued complete,
+// then their subgroups go back to the tier they came from (its copy is
+// intact: nothing was updated) and the slots are freed, so the next phase
+// sees exactly the cache hits of the last applied phase (harness.hpp:218-228:
+// a skipped step is as if run_update was never called).
+void OffloadWorker::roll_back_fetches() {
+    std::vector<std::shared_future<IoStats>> pending;
+    {
+        std::lock_guard<std::mutex> g(mu_);
+        frontier_ = order_.size();  // no new fetches
+        for (auto& [fid, fut] : prefetch_futures_) pending.push_back(fut);
+    }
+    for (auto& f : pending) {
+        try {
+            watchdog_wait_value(f);
+        } catch (const SchedulingBugError&) {
+            throw;
+        } catch (...) {  // a failed fetch already left its subgroup on its tier
+        }
+    }
+    std::lock_guard<std::mutex> g(mu_);
+    for (auto& [fid, fut] : prefetch_futures_) {
+        Subgroup& sg = subgroups_.at(fid);
+        if (sg.residency == Residency::host_cached && sg.slot >= 0) {
+            pool_->evict(sg.slot);
+            sg.slot = -1;
+            sg.residency = Residency::on_tier;
+        }
+    }
+    prefetch_futures_.clear();
+    phase_stats_ = nullptr;
 }
 
 PhaseStats OffloadWorker::run_update(int iteration) {
@@ -774,7 +848,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         order_ = update_order(iteration, ids_, opt_.enable_caching);
     }
     order_after_producer();
-    check_grads_finite_or_throw();
+    launch_grad_check();
     cuda_check(cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
     std::vector<SubgroupId> order;
     {
@@ -806,6 +880,11 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         pump_locked();
     }
 
+    if (const std::int64_t bad = await_grad_verdict(); bad >= 0) {
+        roll_back_fetches();
+        throw GradientOverflowError("subgroup " + std::to_string(bad) +
+                                    ": non-finite gradients reached the update phase");
+    }
     try {
         for (std::size_t j = 0; j < order.size(); ++j) {
             const SubgroupId id = order[j];
@@ -895,7 +974,16 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         flush_futures_.clear();
     }
     stats.wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
-    if (fixed_ratio_.empty()) est_.update(stats.tier_obs);
+    if (fixed_ratio_.empty()) {
+        // A host_dram tier moves a subgroup by exchanging pinned blocks with
+        // the slot: O(1), not a bandwidth sample. Its cost is the PCIe leg of
+        // the device pipeline, so Eq. 1 keeps its configured rate (set it to
+        // the measured PCIe rate) instead of learning ~1e14 B/s from a swap.
+        std::vector<TierObservation> ema_obs = stats.tier_obs;
+        for (std::size_t i = 0; i < tiers_.size(); ++i)
+            if (tiers_[i]->spec().kind == TierKind::host_dram) ema_obs[i] = TierObservation{};
+        est_.update(ema_obs);
+    }
     return stats;
 }
 

@@ -263,6 +263,10 @@ public:
     WorkerId id() const { return id_; }
     void set_alpha(double alpha);
     void set_fixed_ratio(std::vector<double> ratio);
+    // Retention capacity for the following phases (ScheduleOptions::cache_slots;
+    // between phases). In the HBM cache mode it may not exceed the HBM
+    // buffers allocated at init.
+    void set_cache_slots(int cache_slots);
     void add_subgroup(SubgroupId id, std::uint64_t param_count);
 
     // Seeded fp32 states (synthetic_param_init, zero moments) generated on the
@@ -357,7 +361,9 @@ private:
     void copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device, cudaStream_t s);
     void completion_loop();
     static void CUDART_CB host_done(void* arg);
-    void check_grads_finite_or_throw();
+    void launch_grad_check();
+    std::int64_t await_grad_verdict();
+    void roll_back_fetches();
     void order_after_producer();
     std::vector<unsigned long long> nonfinite_counts();
 
@@ -443,6 +449,8 @@ private:
     void* p16_arena_ = nullptr;
     cudaStream_t producer_ = cudaStreamLegacy;  // gradients' producer (set_producer_stream)
     cudaEvent_t producer_done_ = nullptr;
+    cudaEvent_t verdict_ready_ = nullptr;            // per-subgroup non-finite counts landed in verdict_host_
+    unsigned long long* verdict_host_ = nullptr;     // pinned, one count per subgroup (index order)
     unsigned long long* counters_ = nullptr;  // [0] non-finite grads, [1] narrowing overflows
     unsigned long long* sg_counts_ = nullptr; // per-subgroup non-finite counts (pre-check)
     std::unordered_map<SubgroupId, std::size_t> index_of_;

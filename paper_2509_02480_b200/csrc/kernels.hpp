@@ -36,6 +36,11 @@ struct AdamLaunch {
     // [0] += non-finite gradient count, [1] += narrowing overflows (+-Inf
     // outputs). May be null.
     unsigned long long* counters = nullptr;
+    // Device-side gate (may be null): when *gate != 0 at kernel start the
+    // launch writes nothing. A whole-phase non-finite count accumulated into
+    // it on the same stream rejects every later update of the phase without
+    // a host round trip between the check and the updates.
+    const unsigned long long* gate = nullptr;
 };
 
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream);

@@ -42,7 +42,11 @@ def owner_of(sg: int, M: int, world: int) -> int:
 def reduce_grads_to_owners(local: Sequence, sizes: Sequence[int], world: int, rank: int, group=None) -> Dict[int, object]:
     """local[sg]: this rank's 16-bit (float16/bfloat16 torch tensor) gradient
     contribution for every subgroup sg. Returns {sg: summed gradient} for the
-    subgroups this rank owns."""
+    subgroups this rank owns. The collectives are ordered on torch's current
+    stream; the engine orders every run_update after its producer stream
+    (OffloadWorker.set_producer_stream, default: the legacy default stream),
+    so binding the results needs no host synchronisation when they are
+    produced on that stream."""
     import torch
     import torch.distributed as dist
 
@@ -85,6 +89,27 @@ def owned_ids(M: int, world: int, rank: int) -> List[int]:
     return list(range(b, b + c))
 
 
+def contribution_layout(sizes: Sequence[int], world: int, window: int = 0) -> Tuple[List[int], int]:
+    """(element offset of each subgroup's contribution, total elements) in a
+    rank's PeerGradients buffer. window == 0: one 8-element-aligned slice per
+    subgroup. window > 0: rolling buckets, subgroup k of owner o's shard in
+    slot (k % window) * world + o, each slot max(sizes) rounded up to 8."""
+    offsets: List[int] = []
+    if window > 0:
+        M = len(sizes)
+        slot = (max(sizes) + 7) // 8 * 8
+        for sg in range(M):
+            o = owner_of(sg, M, world)
+            k = sg - shard(M, world, o)[0]
+            offsets.append(((k % window) * world + o) * slot)
+        return offsets, window * world * slot
+    off = 0
+    for n in sizes:
+        offsets.append(off)
+        off += (n + 7) // 8 * 8
+    return offsets, off
+
+
 class _DeviceArray:
     """__cuda_array_interface__ view of a raw device range (torch.as_tensor)."""
 
@@ -107,7 +132,14 @@ class PeerGradients:
     before a rank overwrites its buffer."""
 
     def __init__(self, sizes: Sequence[int], world: int, rank: int, device: int = 0, dtype: str = "f16",
-                 group=None):
+                 group=None, window: int = 0):
+        """window > 0: rolling buckets instead of one slice per subgroup. The
+        backward emits gradients bucket by bucket and each bucket is consumed
+        before the buffer is reused, so a rank only ever holds `window`
+        subgroups per owner: subgroup k of owner o's shard lives in slot
+        (k % window) * world + o (window x world slots of max(sizes)). The
+        bytes an owner reads per subgroup are the same; device memory drops
+        from 2 B x every param to 2 B x window x world x max(sizes)."""
         import torch.distributed as dist
 
         from . import tierflow as tf
@@ -116,11 +148,8 @@ class PeerGradients:
         self._tf, self.device, self.world, self.rank = tf, device, world, rank
         self.sizes = list(sizes)
         self.dtype = dtype
-        self.offsets: List[int] = []
-        off = 0
-        for n in self.sizes:
-            self.offsets.append(off)
-            off += (n + 7) // 8 * 8
+        self.window = window
+        self.offsets, off = contribution_layout(self.sizes, world, window)
         self.total = max(off, 8)
         self._local = tf.device_alloc(device, 2 * self.total)
         self._opened: List[int] = []
@@ -147,6 +176,19 @@ class PeerGradients:
         import torch
         dt = torch.float16 if self.dtype == "f16" else torch.bfloat16
         arr = _DeviceArray(self._local + 2 * self.offsets[sg], self.sizes[sg], "<i2")
+        return torch.as_tensor(arr, device=f"cuda:{self.device}").view(dt)
+
+    def slot_view(self, slot: int, count: int = 1):
+        """window > 0: `count` consecutive bucket slots of this rank's buffer
+        (a flat 16-bit torch view), e.g. to fill them in backward."""
+        import torch
+        if self.window <= 0:
+            raise ValueError("slot_view needs a windowed PeerGradients")
+        per = (max(self.sizes) + 7) // 8 * 8
+        if not (0 <= slot and slot + count <= self.window * self.world):
+            raise ValueError("bucket slot out of range")
+        dt = torch.float16 if self.dtype == "f16" else torch.bfloat16
+        arr = _DeviceArray(self._local + 2 * slot * per, count * per, "<i2")
         return torch.as_tensor(arr, device=f"cuda:{self.device}").view(dt)
 
     def sources(self, sg: int) -> List[int]:

@@ -592,6 +592,10 @@ class OffloadWorker:
         arr = (C.c_double * max(len(ratio), 1))(*ratio)
         _lib.call("tfg_engine_set_fixed_ratio", self._h, arr, len(ratio))
 
+    def set_cache_slots(self, cache_slots: int) -> None:
+        """Retention capacity C for the following phases (between phases)."""
+        _lib.call("tfg_engine_set_cache_slots", self._h, cache_slots)
+
     def add_subgroup(self, sg: int, param_count: int) -> None:
         _lib.call("tfg_engine_add_subgroup", self._h, sg, param_count)
         self._params[sg] = param_count
@@ -740,15 +744,22 @@ def _stream(stream) -> Optional[int]:
 
 
 def adam_fused(p, m, v, grad16, param16, t: int, hyper: AdamHyper = AdamHyper(), grad_dtype: int = F16,
-               param_dtype: int = F16, counters=None, stream=None) -> None:
-    """Fused widen -> Adam -> narrow on device tensors, async on `stream`."""
+               param_dtype: int = F16, counters=None, stream=None, gate=None) -> None:
+    """Fused widen -> Adam -> narrow on device tensors, async on `stream`.
+    gate: optional device int64 tensor; the launch writes nothing when it is
+    nonzero at kernel start (a whole-phase non-finite count on the stream)."""
     n = p.numel()
     for x in (m, v, grad16, param16):
         if x.numel() != n:
             raise Error("adam_fused: length mismatch")
     hy = hyper.c()
-    _lib.call("tfg_adam_fused", _ptr(p), _ptr(m), _ptr(v), _ptr(grad16), grad_dtype, _ptr(param16), param_dtype, n,
-              C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
+    cnt = _ptr(counters) if counters is not None else None
+    if gate is None:
+        _lib.call("tfg_adam_fused", _ptr(p), _ptr(m), _ptr(v), _ptr(grad16), grad_dtype, _ptr(param16), param_dtype,
+                  n, C.byref(hy), t, cnt, _stream(stream))
+    else:
+        _lib.call("tfg_adam_fused_gated", _ptr(p), _ptr(m), _ptr(v), _ptr(grad16), grad_dtype, _ptr(param16),
+                  param_dtype, n, C.byref(hy), t, cnt, _ptr(gate), _stream(stream))
 
 
 def adam_fused_multi(p, m, v, grads: Sequence, param16, t: int, hyper: AdamHyper = AdamHyper(),

@@ -107,6 +107,10 @@ def main() -> None:
             # a skipped iteration keeps the parity key (SURVEY.md §8a rule 2)
             "skip": dict(params=[5000] * 8, tiers=[(400e6, 400e6), (200e6, 200e6)], ratio=[1.0, 1.0],
                          pool_slots=6, cache_slots=2, seed=5, iterations=4, accum=1, wd=0.0, skip=0b10),
+            # the north_star "after 10 steps" contract on the reference desk shape (configs/desk.json:
+            # 24 x 2,796,202, P % 4 = 2): 12 iterations, iteration 5 skipped (11 applied), C = 4, AdamW
+            "desk10": dict(params=[2_796_202] * 24, tiers=[(4000e6, 4000e6), (2000e6, 2000e6)], ratio=[2.0, 1.0],
+                           pool_slots=7, cache_slots=-1, seed=42, iterations=12, accum=1, wd=0.01, skip=1 << 5),
             # the ZeRO-3 baseline flow: caching, skip-gradients, atomic R/W and multi-path all off
             "baseline": dict(params=[20000] * 6, tiers=[(300e6, 300e6), (150e6, 150e6)], ratio=None,
                              pool_slots=6, cache_slots=-1, seed=1234, iterations=3, accum=2, wd=0.0, skip=0,
@@ -146,10 +150,32 @@ def main() -> None:
                 s = oracle.phase_sequences(res["events"], it["trace_begin"], it["trace_end"], nt)
                 seqs.append(repr(s))
             g[f"run_{name}_seqs"] = np.array(seqs)
-            if name in ("hits", "baseline"):  # large: keep a digest per subgroup
+            if name in ("hits", "baseline", "desk10"):  # large: keep a digest per subgroup
                 g[f"run_{name}_digest"] = np.array([hashlib.sha256(x.tobytes()).hexdigest() for x in res["states"]])
             else:
                 g[f"run_{name}_states"] = np.concatenate(res["states"])
+    # The contiguous P||m||v kernel (StateView::from_contiguous, optimizer.hpp:82-86) for t = 1..10 at
+    # the desk shape's P = 2,796,202 (P % 4 = 2: m and v are not 16-byte aligned): widen the fp16
+    # SyntheticGradSource gradient, adam_step with AdamW, downscale; digests after every step.
+    n = 2_796_202
+    state = np.concatenate([oracle.synthetic_params(n, 42, 3), np.zeros(2 * n, np.float32)])
+    dig, dig16 = [], []
+    for t in range(1, 11):
+        g16 = oracle.synthetic_grads(n, 42, 3, t - 1)
+        gf = np.empty(n, np.float32)
+        fin = oracle.C.c_int()
+        R.ref_upscale(g16, gf, n, oracle.C.byref(fin))
+        p, m, v = state[:n], state[n:2 * n], state[2 * n:]
+        assert R.ref_adam_step(p, m, v, gf, n, 1e-3, 0.9, 0.999, 1e-8, 0.01, t, 4) == 0
+        p16 = np.empty(n, np.uint16)
+        over = oracle.C.c_uint64()
+        R.ref_downscale(p, p16, n, oracle.C.byref(over))
+        dig.append(hashlib.sha256(state.tobytes()).hexdigest())
+        dig16.append(hashlib.sha256(p16.tobytes()).hexdigest())
+    g["contig10_digest"] = np.array(dig)
+    g["contig10_p16_digest"] = np.array(dig16)
+    g["contig10_sample"] = state[::9973].copy()  # a readable sample of the final state
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT} ({OUT.stat().st_size} bytes, {len(g)} arrays)")
 

@@ -79,3 +79,59 @@ def test_metric_is_baseline_metric():
     base = json.loads((ROOT / "BASELINE.json").read_text())
     assert bench.METRIC == base["metric"]
     assert bench.ALG_BYTES_PER_PARAM == 28
+
+
+def test_llama2_70b_shape():
+    # 68,976,648,192 params -> 690 subgroups @100M, the last 76,648,192
+    s = bench.subgroup_sizes(**{k: bench.WORKLOADS["llama2-70b"][k] for k in ("total", "sub")})
+    assert len(s) == 690 and s[-1] == 76_648_192 and sum(s) == 68_976_648_192
+    from paper_2509_02480_b200.parallel import shard
+    assert sorted({shard(690, 8, r)[1] for r in range(8)}) == [86, 87]  # uneven at N=8
+
+
+def test_gpus_must_match_world_size(monkeypatch):
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert bench.main(["--gpus", "1", "--skip-e2e", "--skip-cpu"]) == 2
+
+
+def test_gpus_n_without_torchrun_spawns_n_ranks(monkeypatch):
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    seen = {}
+
+    def fake_call(cmd):
+        seen["cmd"] = cmd
+        return 0
+    monkeypatch.setattr(bench.subprocess, "call", fake_call)
+    assert bench.main(["--gpus", "4", "--steps", "2", "--warmup", "3"]) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "127.0.0.1" in cmd
+    assert cmd[-6:] == ["--gpus", "4", "--steps", "2", "--warmup", "3"]
+
+
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_both_arms_report_the_same_config(world):
+    wl = "llama2-7b" if world == 1 else "20b"
+    a = bench.line_config(wl, world, "f16")
+    assert a == bench.line_config(wl, world, "f16")
+    assert a["subgroups_per_rank"] == (68 if world == 1 else 200 // world)
+    assert a["survey_config"] == ("C2" if world == 1 else "C3")
+
+
+@pytest.mark.parametrize("world,window", [(2, 4), (3, 4), (8, 4), (8, 1)])
+def test_rolling_bucket_layout(world, window):
+    from paper_2509_02480_b200.parallel import contribution_layout, shard
+    sizes = bench.subgroup_sizes(20_000_000_000, 100_000_000)
+    offs, total = contribution_layout(sizes, world, window)
+    slot = 100_000_000
+    assert total == window * world * slot
+    for o in range(world):
+        b, c = shard(len(sizes), world, o)
+        for k in range(c):
+            assert offs[b + k] == ((k % window) * world + o) * slot
+    # within one bucket step every owner has its own slot: k-th subgroups of all owners never collide
+    for k in range(min(shard(len(sizes), world, r)[1] for r in range(world))):
+        ids = [shard(len(sizes), world, o)[0] + k for o in range(world)]
+        assert len({offs[i] for i in ids}) == world
+    offs0, total0 = contribution_layout([10, 3, 8], 2, 0)
+    assert offs0 == [0, 16, 24] and total0 == 32

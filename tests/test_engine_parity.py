@@ -47,7 +47,7 @@ def run_golden(tf, golden, run, lock_dir, device_buffers=3, hbm=1, host_slots=No
         pool = host_slots
     params = golden[f"run_{run}_params"].tolist()
     rates = {"hits": [(500e6, 500e6), (250e6, 250e6)], "ragged": [(300e6, 300e6), (200e6, 200e6), (100e6, 100e6)],
-             "skip": [(400e6, 400e6), (200e6, 200e6)]}[run]
+             "skip": [(400e6, 400e6), (200e6, 200e6)], "desk10": [(4000e6, 4000e6), (2000e6, 2000e6)]}[run]
     w, trace, tiers = make_engine(tf, [mem(*r) for r in rates], params, pool_slots=pool, cache_slots=cache,
                                   ratio=golden[f"run_{run}_ratio"].tolist(), seed=seed, lock_dir=lock_dir,
                                   wd=float(golden[f"run_{run}_wd"][0]), device_buffers=device_buffers, hbm=hbm)
@@ -96,6 +96,33 @@ def test_sequences_and_state_match_reference_engine(tf, cuda, golden, lock_dir, 
             # device working params = RNE(P) of the final state
             assert np.array_equal(w.read_params16(i), oracle.f32_to_f16(got[:n]))
             off += 3 * n
+    w.close()
+
+
+@pytest.mark.parametrize("hbm,host_slots", [(1, None), (2, 3)])
+def test_ten_step_contract_on_the_desk_shape(tf, cuda, golden, lock_dir, hbm, host_slots):
+    """north_star: results after 10 steps. The reference engine on its desk
+    shape (configs/desk.json: 24 subgroups x 2,796,202, P % 4 = 2), AdamW
+    (wd 0.01), C = 4, 12 iterations with iteration 5 skipped (11 applied):
+    every phase's cache hits, per-tier fetch order, flush sets and allocation,
+    then the final P/m/v and working params of every subgroup, bit for bit."""
+    w, trace, stats, seqs, params, iters = run_golden(tf, golden, "desk10", lock_dir, hbm=hbm, host_slots=host_slots)
+    want_seqs = [ast.literal_eval(s) for s in golden["run_desk10_seqs"]]
+    assert iters == 12 and sum(st is not None for st in stats) == 11
+    for it in range(iters):
+        assert seqs[it] == want_seqs[it], f"iteration {it}"
+        if stats[it] is None:
+            continue
+        assert stats[it].cache_hits == golden["run_desk10_hits"][it]
+        assert stats[it].retained == golden["run_desk10_retained"][it]
+        assert stats[it].flush_allocation == golden["run_desk10_alloc"][it].tolist()
+        assert stats[it].downscale_overflows == golden["run_desk10_overflows"][it]
+    # after the skipped iteration the direction repeats, so the hits of iteration 6 come last in its order
+    assert [s.cache_hits for s in stats if s is not None] == [0] + [4] * 10
+    for i, n in enumerate(params):
+        got = w.read_current_state(i)
+        assert hashlib.sha256(got.tobytes()).hexdigest() == golden["run_desk10_digest"][i], f"subgroup {i}"
+        assert np.array_equal(w.read_params16(i), oracle.f32_to_f16(got[:n]))
     w.close()
 
 
@@ -162,6 +189,7 @@ def test_nonfinite_gradient_rejects_phase_without_mutation(tf, cuda, lock_dir):
     assert w.gradients_finite()
     st = w.run_update(1)
     assert st.params_updated == 3 * n
+    assert st.cache_hits == 0  # the rejected phase's fetches were rolled back to their tier
     p0 = oracle.synthetic_params(n, 42, 1)
     want = oracle.adam_fused(p0, np.zeros(n, np.float32), np.zeros(n, np.float32), g16, 0, 0, 2)
     assert np.array_equal(w.read_current_state(1).view(np.uint32), np.concatenate(want[:3]).view(np.uint32))

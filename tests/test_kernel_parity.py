@@ -51,6 +51,32 @@ def assert_bits(a, b, what):
     assert bad.size == 0, f"{what}: {bad.size} mismatches, first at {bad[:5]}: {a[bad[:3]]} vs {b[bad[:3]]}"
 
 
+def test_contiguous_state_ten_steps_at_p_mod_4_eq_2(tf, cuda, golden):
+    """The contiguous P||m||v kernel (m, v not 16-byte aligned at P % 4 = 2)
+    for t = 1..10 with AdamW, against the reference's widen -> adam_step ->
+    downscale chain (golden digests after every step, make_golden.py)."""
+    import hashlib
+
+    import torch
+    n = 2_796_202
+    st = _dev(torch, np.concatenate([oracle.synthetic_params(n, 42, 3), np.zeros(2 * n, np.float32)]), cuda)
+    import ctypes as C
+    from paper_2509_02480_b200 import _lib
+    h = tf.AdamHyper(weight_decay=0.01).c()
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    counters = torch.zeros(2, dtype=torch.int64, device=cuda)
+    for t in range(1, 11):
+        g = _u16(torch, oracle.synthetic_grads(n, 42, 3, t - 1), cuda)
+        _lib.call("tfg_adam_fused_contiguous", st.data_ptr(), n, g.data_ptr(), 0, p16.data_ptr(), 0, C.byref(h), t,
+                  counters.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        s = st.cpu().numpy()
+        assert hashlib.sha256(s.tobytes()).hexdigest() == golden["contig10_digest"][t - 1], f"t={t}"
+        assert hashlib.sha256(_np16(p16).tobytes()).hexdigest() == golden["contig10_p16_digest"][t - 1], f"t={t}"
+    assert_bits(s[::9973], golden["contig10_sample"], "sample")
+    assert counters.cpu().tolist() == [0, 0]
+
+
 def test_golden_vectors(tf, cuda, golden):
     import torch
     for k in range(int(golden["adam_cases"][0])):
