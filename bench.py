@@ -609,7 +609,7 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     if remote:
         dirs.append(tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
                                         lock_device=1)))
-    probes = {t.id: t.probe_bandwidth(1 << 30, 3) for t in dirs}
+    probes = {t.id(): t.probe_bandwidth(1 << 30, 3) for t in dirs}
     # Host DRAM tier: blocks move by exchange; Eq. 1 sees it at the measured
     # PCIe rate (the engine keeps a host_dram tier's configured rate).
     dram_bw = min(pcie["h2d"], pcie["d2h"])
@@ -635,6 +635,12 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     src = tf.SyntheticGradSource(seed)
     backward = None if peer is not None else (lambda it: w.run_backward_sim(it, src, 1))
     phases = run_phases(w, world, rank, warmup, steps, backward, "e2e")
+    if os.environ.get("TFB_TIMELINE"):  # diagnostics: the last phase's per-subgroup timeline
+        st = phases[-1][1]
+        Path(os.environ["TFB_TIMELINE"]).write_text(json.dumps(dict(
+            ms=phases[-1][0], alloc=st.flush_allocation, timeline=w.last_timeline(),
+            io=[dict(id=e.id, read_s=e.read_seconds, write_s=e.write_seconds, fetched=e.fetched, flushed=e.flushed)
+                for e in st.subgroup_io])))
     rl = pipeline_roofline(phases, pcie, probes)
     last = phases[-1][1]
     M = len(sizes)

@@ -354,11 +354,54 @@ int tfg_engine_enqueue_flush(tfg_engine* engine, uint32_t id, int dest, uint64_t
 int tfg_engine_wait_ticket(tfg_engine* engine, uint64_t ticket, uint64_t* bytes_out, double* seconds_out);
 int tfg_engine_read_state(tfg_engine* engine, uint32_t id, float* out_3n);                  /* :611 */
 int tfg_engine_read_params16(tfg_engine* engine, uint32_t id, uint16_t* out_n);
+int tfg_engine_read_grads16(tfg_engine* engine, uint32_t id, uint16_t* out_n);              /* grad_buffer(id).values(), :401 */
 int tfg_engine_meta(tfg_engine* engine, uint32_t id, tfg_subgroup_meta* out);               /* :587 */
 int tfg_engine_residency_census(tfg_engine* engine, uint64_t* host_params, uint64_t* per_tier, int n_tiers); /* :597 */
 int tfg_engine_current_order(tfg_engine* engine, uint32_t* out, int max_n, int* n_out);     /* :582 */
 int tfg_engine_estimates(tfg_engine* engine, double* read_bw, double* write_bw, int n_tiers); /* :583 */
 int tfg_engine_pool_state(tfg_engine* engine, int slot, int* state_out, uint32_t* owner_out);
+
+/* ---- host-side reference API --------------------------------------------
+ * The reference's own C++ calls on host spans, served by the B200 objects and
+ * sm_100a kernels (host arrays staged through HBM: H2D, one kernel, D2H).
+ * include/tierflow_compat/ builds the reference's header API on these, so the
+ * reference's scheduler / optimizer suites compile against this library with
+ * only the include path changed (tests/dropin/). */
+int tfg_now_ns(int64_t* out);                                                                /* common.hpp:21-26 */
+int tfg_upscale16_host(const uint16_t* src, float* dst, uint64_t n, int dtype, int* all_finite); /* precision.hpp:17 */
+int tfg_downscale16_host(const float* src, uint16_t* dst, uint64_t n, int dtype, uint64_t* overflows); /* precision.hpp:29 */
+/* adam_step(StateView, span<const float> g, hyper, t), optimizer.hpp:116-157: TFG_ERROR for t < 1,
+ * TFG_CONFIG_ERROR for bad hyperparameters, TFG_GRADIENT_OVERFLOW (arrays untouched) on a
+ * non-finite gradient. */
+int tfg_adam_step_host(float* p, float* m, float* v, const float* g, uint64_t n, const tfg_adam_hyper* hyper,
+                       uint64_t t);
+
+/* HostBufferPool, pool.hpp:35-161: slots of 3*max_params fp32 state plus a max_params fp32 gradient
+ * annex; the slot state machine of the engine (free -> prefetching -> cached -> updating -> cached
+ * -> flushing -> free); illegal transitions fail with TFG_ERROR. */
+typedef struct tfg_pool tfg_pool;
+enum {
+    TFG_POOL_PREFETCH_DONE = 0,
+    TFG_POOL_BEGIN_UPDATE = 1,
+    TFG_POOL_END_UPDATE = 2,
+    TFG_POOL_BEGIN_FLUSH = 3,
+    TFG_POOL_FLUSH_DONE = 4,
+    TFG_POOL_EVICT = 5
+};
+int tfg_pool_create(int slots, uint64_t max_params, tfg_pool** out);                        /* pool.hpp:37-45 */
+int tfg_pool_destroy(tfg_pool* pool);
+int tfg_pool_slot_count(tfg_pool* pool, int* out);
+int tfg_pool_try_reserve(tfg_pool* pool, uint32_t owner, int* slot_out);                    /* pool.hpp:52-62 */
+int tfg_pool_find_cached(tfg_pool* pool, uint32_t owner, int* slot_out);
+int tfg_pool_transition(tfg_pool* pool, int slot, int op);                                   /* pool.hpp:72-85 */
+int tfg_pool_query(tfg_pool* pool, int slot, int* state_out, uint32_t* owner_out);         /* state: tfg SlotState order */
+/* which 0: the slot's P||m||v (3*params floats), 1: its fp32 gradient annex (params floats);
+ * TFG_ERROR when params exceeds the slot capacity (pool.hpp:123-131). */
+int tfg_pool_span(tfg_pool* pool, int slot, uint64_t params, int which, float** ptr_out, uint64_t* len_out);
+
+/* Subgroup residency transitions, optimizer.hpp:47-72 (TFG_ERROR on an illegal one). */
+enum { TFG_SG_BEGIN_FLUSH = 0, TFG_SG_FINISH_FLUSH = 1, TFG_SG_BEGIN_PREFETCH = 2, TFG_SG_FINISH_PREFETCH = 3 };
+int tfg_subgroup_step(tfg_subgroup_meta* sg, int op, int arg);
 
 #ifdef __cplusplus
 }

@@ -196,6 +196,20 @@ _SIGS = {
     "tfg_engine_wait_ticket": (_i, [_vp, _u64, C.POINTER(_u64), C.POINTER(_d)]),
     "tfg_engine_read_state": (_i, [_vp, C.c_uint32, _vp]),
     "tfg_engine_read_params16": (_i, [_vp, C.c_uint32, _vp]),
+    "tfg_engine_read_grads16": (_i, [_vp, C.c_uint32, _vp]),
+    "tfg_now_ns": (_i, [C.POINTER(C.c_int64)]),
+    "tfg_upscale16_host": (_i, [_vp, _vp, _u64, _i, C.POINTER(_i)]),
+    "tfg_downscale16_host": (_i, [_vp, _vp, _u64, _i, C.POINTER(_u64)]),
+    "tfg_adam_step_host": (_i, [_vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64]),
+    "tfg_pool_create": (_i, [_i, _u64, C.POINTER(_vp)]),
+    "tfg_pool_destroy": (_i, [_vp]),
+    "tfg_pool_slot_count": (_i, [_vp, C.POINTER(_i)]),
+    "tfg_pool_try_reserve": (_i, [_vp, C.c_uint32, C.POINTER(_i)]),
+    "tfg_pool_find_cached": (_i, [_vp, C.c_uint32, C.POINTER(_i)]),
+    "tfg_pool_transition": (_i, [_vp, _i, _i]),
+    "tfg_pool_query": (_i, [_vp, _i, C.POINTER(_i), C.POINTER(C.c_uint32)]),
+    "tfg_pool_span": (_i, [_vp, _i, _u64, _i, C.POINTER(_vp), C.POINTER(_u64)]),
+    "tfg_subgroup_step": (_i, [C.POINTER(SubgroupMetaC), _i, _i]),
     "tfg_engine_meta": (_i, [_vp, C.c_uint32, C.POINTER(SubgroupMetaC)]),
     "tfg_engine_residency_census": (_i, [_vp, C.POINTER(_u64), C.POINTER(_u64), _i]),
     "tfg_engine_current_order": (_i, [_vp, C.POINTER(C.c_uint32), _i, C.POINTER(_i)]),

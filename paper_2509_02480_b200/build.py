@@ -27,7 +27,7 @@ NVCC = str(CUDA_HOME / "bin" / "nvcc")
 GENCODE = "-gencode=arch=compute_100a,code=sm_100a"
 
 CU_SOURCES = ["kernels.cu", "adam_kernel.cu", "adam_variants.cu"]
-CXX_SOURCES = ["tier.cpp", "engine.cpp", "capi.cpp"]
+CXX_SOURCES = ["tier.cpp", "engine.cpp", "capi.cpp", "capi_host.cpp"]
 
 
 def _sources() -> list[Path]:

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <string>
 
+#include "capi_internal.hpp"
 #include "engine.hpp"
 #include "kernels.hpp"
 #include "placement.hpp"
@@ -37,6 +38,12 @@ struct tfg_engine {
 namespace {
 
 thread_local std::string g_last_error;
+
+}  // namespace
+
+void tfb::set_last_error(const std::string& msg) { g_last_error = msg; }
+
+namespace {
 
 template <class F>
 int guarded(F&& f) {
@@ -887,6 +894,17 @@ int tfg_engine_read_params16(tfg_engine* engine, uint32_t id, uint16_t* out_n) {
         tfb::cuda_check(cudaSetDevice(engine->w->device_options().device), "cudaSetDevice");
         tfb::cuda_check(cudaMemcpy(out_n, engine->w->params16_buffer(id), 2 * meta.param_count, cudaMemcpyDeviceToHost),
                         "cudaMemcpy(params16)");
+    });
+}
+
+int tfg_engine_read_grads16(tfg_engine* engine, uint32_t id, uint16_t* out_n) {
+    return guarded([&] {
+        need(engine, "engine");
+        need(out_n, "out");
+        const auto meta = engine->w->meta(id);
+        tfb::cuda_check(cudaSetDevice(engine->w->device_options().device), "cudaSetDevice");
+        tfb::cuda_check(cudaMemcpy(out_n, engine->w->grad_buffer(id), 2 * meta.param_count, cudaMemcpyDeviceToHost),
+                        "cudaMemcpy(grads16)");
     });
 }
 

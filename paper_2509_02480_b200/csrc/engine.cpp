@@ -802,10 +802,11 @@ std::int64_t OffloadWorker::await_grad_verdict() {
 }
 
 // A rejected phase leaves no trace in residency: fetches it issued complete,
-// then their subgroups go back to the tier they came from (its copy is
-// intact: nothing was updated) and the slots are freed, so the next phase
-// sees exactly the cache hits of the last applied phase (harness.hpp:218-228:
-// a skipped step is as if run_update was never called).
+// then their subgroups go back to the tier they came from and the slots are
+// freed, so the next phase sees exactly the cache hits of the last applied
+// phase (harness.hpp:218-228: a skipped step is as if run_update was never
+// called). Nothing was updated, so a directory tier's file is still current;
+// a host_dram tier handed its block to the slot, so the block goes back.
 void OffloadWorker::roll_back_fetches() {
     std::vector<std::shared_future<IoStats>> pending;
     {
@@ -825,6 +826,8 @@ void OffloadWorker::roll_back_fetches() {
     for (auto& [fid, fut] : prefetch_futures_) {
         Subgroup& sg = subgroups_.at(fid);
         if (sg.residency == Residency::host_cached && sg.slot >= 0) {
+            Tier& origin = *tiers_.at(static_cast<std::size_t>(sg.tier));
+            if (!origin.has_subgroup(fid)) origin.write_from(fid, sg.param_count, pool_->block(sg.slot));
             pool_->evict(sg.slot);
             sg.slot = -1;
             sg.residency = Residency::on_tier;
