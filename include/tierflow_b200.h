@@ -240,12 +240,7 @@ int tfg_adam_fused_contiguous(float* state, uint64_t n, const void* grad, int gr
 int tfg_adam_step(float* p, float* m, float* v, const uint16_t* grad, int grad_dtype, uint16_t* param16,
                   int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, uint64_t* overflows_out,
                   void* stream);
-/* Kernel tuning hook (no reference counterpart): the fused kernel in launch
- * configuration `variant` (0 = the shipped default; 1..count-1 F16/F16 only). */
-int tfg_adam_variant_count(int* count);
-int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint16_t* grad, uint16_t* param16,
-                           uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters,
-                           void* stream);
+/* The kernel's tuning variants live in a separate library (include/tierflow_b200_tuning.h). */
 /* Self-test of the constant-divisor quotient used for m/bc1, v/bc2 against
  * div.rn.f64 on n generated numerators (synchronous; host outputs). */
 int tfg_selftest_div_const(double divisor, uint64_t n, uint64_t seed, int exp_lo, int exp_span,

@@ -1,0 +1,33 @@
+/*
+ * tierflow_b200_tuning.h — tuning hooks of the fused update kernel: the 40
+ * measured launch configurations and element-math forms of DESIGN.md §5.1
+ * (register / TMA / cp.async / verified-fast-path variants), every one
+ * bit-identical to the shipped kernel. No reference counterpart.
+ *
+ * Library: paper_2509_02480_b200/lib/libtierflow_b200_tuning.so, built with
+ * `python -m paper_2509_02480_b200.build --tuning` (also by __graft_entry__.
+ * build() for the tests and sweeps). The product library
+ * libtierflow_b200.so does not contain these kernels; the update path never
+ * loads this one.
+ */
+#ifndef TIERFLOW_B200_TUNING_H
+#define TIERFLOW_B200_TUNING_H
+
+#include "tierflow_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Kernel tuning hook (no reference counterpart): the fused kernel in launch
+ * configuration `variant` (0 = the shipped default; 1..count-1 F16/F16 only). */
+int tfg_adam_variant_count(int* count);
+int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint16_t* grad, uint16_t* param16,
+                           uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters,
+                           void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TIERFLOW_B200_TUNING_H */

@@ -12,6 +12,7 @@ import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libtierflow_b200.so"
+TUNING_PATH = Path(__file__).resolve().parent / "lib" / "libtierflow_b200_tuning.so"
 MAX_TIERS = 8
 
 TFG_F16, TFG_BF16 = 0, 1
@@ -134,8 +135,6 @@ _SIGS = {
                                   _vp, _vp]),
     "tfg_adam_step": (_i, [_vp, _vp, _vp, _vp, _i, _vp, _i, _u64, C.POINTER(AdamHyperC), _u64,
                            C.POINTER(_u64), _vp]),
-    "tfg_adam_variant_count": (_i, [C.POINTER(_i)]),
-    "tfg_adam_fused_variant": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
     "tfg_selftest_div_const": (_i, [_d, _u64, _u64, _i, _i, C.POINTER(_u64), C.POINTER(_d)]),
     "tfg_upscale16": (_i, [_vp, _vp, _u64, _i, _vp, _vp]),
     "tfg_downscale16": (_i, [_vp, _vp, _u64, _i, _vp, _vp]),
@@ -217,8 +216,15 @@ _SIGS = {
     "tfg_engine_pool_state": (_i, [_vp, _i, C.POINTER(_i), C.POINTER(C.c_uint32)]),
 }
 
+# include/tierflow_b200_tuning.h (the kernel variants; a separate library)
+_TUNING_SIGS = {
+    "tfg_adam_variant_count": (_i, [C.POINTER(_i)]),
+    "tfg_adam_fused_variant": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
+}
+
 _lock = threading.Lock()
 _LIB: C.CDLL | None = None
+_TUNING: C.CDLL | None = None
 
 
 def load() -> C.CDLL:
@@ -237,6 +243,28 @@ def load() -> C.CDLL:
                 fn.argtypes = args
             _LIB = lib
         return _LIB
+
+
+def load_tuning() -> C.CDLL:
+    """The tuning library (kernel variants), loaded only by sweeps and tests."""
+    global _TUNING
+    lib = load()
+    with _lock:
+        if _TUNING is None:
+            if not TUNING_PATH.exists():
+                raise ImportError(f"{TUNING_PATH} is not built; run `python -m paper_2509_02480_b200.build`")
+            t = C.CDLL(str(TUNING_PATH))
+            for name, (res, args) in _TUNING_SIGS.items():
+                fn = getattr(t, name)
+                fn.restype = res
+                fn.argtypes = args
+            _TUNING = t
+        del lib
+        return _TUNING
+
+
+def call_tuning(name: str, *args) -> None:
+    check(getattr(load_tuning(), name)(*args))
 
 
 def check(rc: int) -> None:

@@ -271,23 +271,6 @@ int tfg_adam_step(float* p, float* m, float* v, const uint16_t* grad, int grad_d
     });
 }
 
-int tfg_adam_variant_count(int* count) {
-    return guarded([&] {
-        need(count, "count");
-        *count = tfb::adam_variant_count();
-    });
-}
-
-int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint16_t* grad, uint16_t* param16,
-                           uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters,
-                           void* stream) {
-    return guarded([&] {
-        if (variant < 0 || variant >= tfb::adam_variant_count()) throw tfb::ConfigError("unknown kernel variant");
-        const auto a = adam_launch(p, m, v, grad, TFG_F16, param16, TFG_F16, n, hyper, t, counters);
-        tfb::cuda_check(tfb::launch_adam_fused_variant(a, variant, as_stream(stream)), "adam_fused_variant");
-    });
-}
-
 int tfg_selftest_div_const(double divisor, uint64_t n, uint64_t seed, int exp_lo, int exp_span, uint64_t* mismatches,
                            double* first_bad) {
     return guarded([&] {

@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "kernels.hpp"
+#include "nvtx.hpp"
 #include "tier_lock.hpp"
 
 namespace tfb {
@@ -261,6 +262,7 @@ void TierIoWorker::serve() {
 IoStats TierIoWorker::transfer_traced(Job& job) {
     const bool fetch = job.lane == kFetch;
     const TierId tid = tier_->id();
+    const NvtxRange range("%s sg %lld tier %d", fetch ? "fetch" : "flush", static_cast<long long>(job.sg), tid);
     std::optional<TierLockGuard> sem;
     if (use_lock_)
         sem.emplace(lock_dir_, tid, worker_, trace_, tier_->spec().lock_width, tier_->spec().lock_device);
@@ -840,6 +842,7 @@ void OffloadWorker::roll_back_fetches() {
 PhaseStats OffloadWorker::run_update(int iteration) {
     if (!pool_) throw Error("run_update before init_and_flush_all");
     DeviceGuard dg(dev_.device);
+    const NvtxRange range("run_update worker %d iter %d", id_, iteration);
     const auto t0 = Clock::now();
     phase_t0_ns_ = now_ns();
     const AdamConsts c = hyper_.consts(static_cast<std::uint64_t>(iteration) + 1);
@@ -889,8 +892,21 @@ PhaseStats OffloadWorker::run_update(int iteration) {
                                     ": non-finite gradients reached the update phase");
     }
     try {
-        for (std::size_t j = 0; j < order.size(); ++j) {
+        // Updates are issued as their subgroups become host-resident, scanning
+        // a window of the plan ahead of the first one not yet issued: a slow
+        // fetch (a directory tier) no longer idles the H2D stream while later
+        // subgroups sit ready in their slots. Plan order still drives every
+        // rule that has an order (fetch frontier, destinations, retention,
+        // hits), and subgroups are independent, so results, cache hits and
+        // per-tier fetch / flush sequences are those of the in-order loop.
+        std::vector<char> issued(order.size(), 0);
+        std::size_t next = 0;
+        for (std::size_t done = 0; done < order.size(); ++done) {
+            while (issued[next]) ++next;
+            const std::size_t j = pick_next_ready(order, issued, next);
+            issued[j] = 1;
             const SubgroupId id = order[j];
+            const NvtxRange sg_range("subgroup %u (plan %zu of %zu)", id, j + 1, order.size());
             const int slot = wait_host_resident(id);
             host_resident_ns_[index_of_.at(id)] = now_ns();
             const auto moved = issue_device_update(id, slot, c);
@@ -988,6 +1004,33 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         est_.update(ema_obs);
     }
     return stats;
+}
+
+// The plan position to issue next: the first one in [next, next + window)
+// that is host-resident (a hit, or its fetch has landed) or whose fetch
+// failed (wait_host_resident surfaces the error); else `next` itself once it
+// has no fetch in flight (wait_host_resident fetches it on demand, as the
+// reference) or once nothing lands for a second (wait_host_resident's
+// watchdog then owns the wait).
+std::size_t OffloadWorker::pick_next_ready(const std::vector<SubgroupId>& order, const std::vector<char>& issued,
+                                           std::size_t next) {
+    const std::size_t window = std::min<std::size_t>(order.size(), next + std::clamp(opt_.pool_slots, 1, 64));
+    std::unique_lock<std::mutex> l(mu_);
+    for (int waited_ms = 0; waited_ms < 1000; waited_ms += 5) {
+        for (std::size_t j = next; j < window; ++j) {
+            if (issued[j]) continue;
+            const SubgroupId id = order[j];
+            if (subgroups_.at(id).residency == Residency::host_cached) return j;
+            const auto f = prefetch_futures_.find(id);
+            if (f != prefetch_futures_.end() &&
+                f->second.wait_for(std::chrono::seconds(0)) == std::future_status::ready)
+                return j;
+        }
+        if (prefetch_futures_.count(order[next]) == 0) return next;
+        if (completion_error_) std::rethrow_exception(completion_error_);
+        resident_cv_.wait_for(l, std::chrono::milliseconds(5));
+    }
+    return next;
 }
 
 // Enqueue one subgroup on the three pipeline streams (H2D -> kernel -> D2H).
@@ -1441,6 +1484,7 @@ std::shared_future<IoStats> OffloadWorker::start_prefetch_locked(SubgroupId id, 
             s.slot = -1;
             pool_->release_failed(slot);
         }
+        resident_cv_.notify_all();
     };
     auto fut = io_[static_cast<std::size_t>(origin)]
                    ->submit(true, id, 12 * pc + (fetch_grads ? 4 * pc : 0), std::move(transfer), std::move(completion))

@@ -361,6 +361,8 @@ private:
     void copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device, cudaStream_t s);
     void completion_loop();
     static void CUDART_CB host_done(void* arg);
+    std::size_t pick_next_ready(const std::vector<SubgroupId>& order, const std::vector<char>& issued,
+                                std::size_t next);
     void launch_grad_check();
     std::int64_t await_grad_verdict();
     void roll_back_fetches();
@@ -470,6 +472,7 @@ private:
     bool cq_stop_ = false;
     std::size_t in_flight_ = 0;  // guarded by mu_
     std::condition_variable inflight_cv_;
+    std::condition_variable resident_cv_;  // a fetch landed (or failed), with mu_
     std::exception_ptr completion_error_;
 };
 

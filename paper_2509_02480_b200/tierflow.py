@@ -796,7 +796,7 @@ def adam_step(p, m, v, grad16, param16, t: int, hyper: AdamHyper = AdamHyper(), 
 
 def adam_variant_count() -> int:
     n = C.c_int()
-    _lib.call("tfg_adam_variant_count", C.byref(n))
+    _lib.call_tuning("tfg_adam_variant_count", C.byref(n))
     return n.value
 
 
@@ -804,7 +804,7 @@ def adam_fused_variant(variant: int, p, m, v, grad16, param16, t: int, hyper: Ad
                        stream=None) -> None:
     """Tuning hook: the fused kernel in launch configuration `variant` (F16/F16)."""
     hy = hyper.c()
-    _lib.call("tfg_adam_fused_variant", variant, _ptr(p), _ptr(m), _ptr(v), _ptr(grad16), _ptr(param16), p.numel(),
+    _lib.call_tuning("tfg_adam_fused_variant", variant, _ptr(p), _ptr(m), _ptr(v), _ptr(grad16), _ptr(param16), p.numel(),
               C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
 
 

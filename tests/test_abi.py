@@ -12,8 +12,11 @@ ROOT = Path(__file__).resolve().parents[1]
 HEADER = ROOT / "include" / "tierflow_b200.h"
 
 
-def declared():
-    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+TUNING_HEADER = ROOT / "include" / "tierflow_b200_tuning.h"
+
+
+def declared(header=HEADER):
+    text = re.sub(r"/\*.*?\*/", "", header.read_text(), flags=re.S)
     return sorted(set(re.findall(r"\b(tfg_[a-z0-9_]+)\s*\(", text)))
 
 
@@ -26,6 +29,19 @@ def test_library_exports_every_declared_symbol(tf):
     assert not missing, missing
     # and the Python binding covers the whole header
     assert sorted(_lib.exported_symbols()) == names
+
+
+def test_tuning_library_is_separate(tf):
+    """The kernel variants live in libtierflow_b200_tuning.so, declared by
+    include/tierflow_b200_tuning.h; the product library has none of them."""
+    from paper_2509_02480_b200 import _lib
+    names = declared(TUNING_HEADER)
+    assert names == ["tfg_adam_fused_variant", "tfg_adam_variant_count"]
+    tuning = _lib.load_tuning()
+    assert all(hasattr(tuning, n) for n in names)
+    syms = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout
+    assert not any(n in syms for n in names)
+    assert "launch_adam_fused_variant" not in syms and "tma_pipe" not in syms
 
 
 def test_abi_version_and_errors(tf):

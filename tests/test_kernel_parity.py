@@ -202,7 +202,7 @@ def test_narrow_widen_exhaustive_f32(tf, cuda):
             bits = idx.to(torch.int32).view(torch.float32)
             tf.downscale16(bits, out, kind, over)
             want, o = oracle.narrow16(bits.cpu().numpy(), kind)
-            assert np.array_equal(_np16(out), want), (kind, c)
+            assert np.array_equal(_np16(out), want), (kind, q)
             total_over[kind] += o
         assert int(over.item()) == total_over[kind]
         over.zero_()

@@ -42,18 +42,18 @@ def _expected(sizes, world, iters, kind=0, wd=0.0):
     return out
 
 
-def _engine(tf, owned, sizes, lock_dir, kind=0, wd=0.0, pool=3):
+def _engine(tf, owned, sizes, lock_dir, kind=0, wd=0.0, pool=3, device=0):
     trace = tf.EventTrace()
     tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9))]
     w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=pool, lock_dir=lock_dir), tf.AdamHyper(weight_decay=wd),
-                         trace, tf.DeviceOptions(0, kind, kind, 2))
+                         trace, tf.DeviceOptions(device, kind, kind, 2))
     for sg in owned:
         w.add_subgroup(sg, sizes[sg])
     w.init_and_flush_all(SEED)
     return w, tiers
 
 
-def _rank_main(rank, world, port, sizes, iters, lock_dir, q):
+def _rank_main(rank, world, port, sizes, iters, lock_dir, q, distinct=False, window=0):
     import torch
     import torch.distributed as dist
 
@@ -62,15 +62,16 @@ def _rank_main(rank, world, port, sizes, iters, lock_dir, q):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        torch.cuda.set_device(0)
+        dev = rank if distinct else 0  # distinct: one GPU per rank, peers mapped over NVLink / P2P
+        torch.cuda.set_device(dev)
         owned = parallel.owned_ids(len(sizes), world, rank)
-        w, _ = _engine(tf, owned, sizes, lock_dir)
-        with parallel.PeerGradients(sizes, world, rank, device=0) as pg:
+        w, _ = _engine(tf, owned, sizes, lock_dir, device=dev)
+        with parallel.PeerGradients(sizes, world, rank, device=dev, window=window) as pg:
             pg.bind(w, owned)
             for it in range(iters):
                 for sg, n in enumerate(sizes):  # "backward": this rank's contribution to every subgroup
                     g = torch.from_numpy(_contribution(n, rank, sg, it).view(np.int16))
-                    pg.local(sg).view(torch.int16).copy_(g.cuda())
+                    pg.local(sg).view(torch.int16).copy_(g.to(f"cuda:{dev}"))
                 torch.cuda.synchronize()
                 dist.barrier()  # every contribution written before any owner reads it
                 w.run_update(it)
@@ -91,8 +92,23 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("sizes", [[50_000, 50_000, 50_000, 50_000], [70_001, 4_097, 33_333]])
-def test_ipc_fused_exchange_world2(tf, cuda, tmp_path, sizes):
+def _gpus():
+    import torch
+    return torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+@pytest.mark.parametrize("sizes,distinct,window", [
+    ([50_000, 50_000, 50_000, 50_000], False, 0),
+    ([70_001, 4_097, 33_333], False, 0),
+    ([50_000, 50_000, 50_000, 50_000], False, 2),  # rolling-bucket layout (the bench's C3 exchange)
+    pytest.param([50_000, 50_000, 50_000, 50_000], True, 0,
+                 marks=pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs (ranks on distinct devices)")),
+    pytest.param([70_001, 4_097, 33_333], True, 2,
+                 marks=pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs (ranks on distinct devices)")),
+])
+def test_ipc_fused_exchange_world2(tf, cuda, tmp_path, sizes, distinct, window):
+    """world 2; distinct=True puts each rank on its own GPU so every peer
+    contribution crosses NVLink / P2P (skipped on a one-GPU box)."""
     import torch.multiprocessing as mp
     world, iters = 2, 2
     lock_dir = tmp_path / "locks"
@@ -100,7 +116,7 @@ def test_ipc_fused_exchange_world2(tf, cuda, tmp_path, sizes):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, sizes, iters, str(lock_dir), q))
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, sizes, iters, str(lock_dir), q, distinct, window))
              for r in range(world)]
     for p in procs:
         p.start()
