@@ -261,6 +261,12 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
     import torch
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.Stream(dev)
+    # 16 B/param resident (P, m, v, gradient, working params); a shard larger
+    # than HBM (the 70B shape on one GPU) is timed on the subgroups that fit.
+    free, _ = torch.cuda.mem_get_info(dev)
+    fit = int((free - 8e9) // (16 * max(sizes) + 8192))
+    owned = len(sizes)
+    sizes = sizes[:int(allmin(world, max(1, min(len(sizes), fit))))]
     states, grads, p16s = [], [], []
     with torch.cuda.stream(stream):
         for k, n in enumerate(sizes):
@@ -314,7 +320,7 @@ def device_leg(tf, sizes, base_id, steps, warmup, seed, rank, world):
     torch.cuda.empty_cache()
     return dict(total_ms=total_ms, kernel_ms=kernel_ms, launches=steps * len(sizes),
                 all_launches=2 * steps * len(sizes), clocks=clk.summary(), params=sum(sizes),
-                timed_subgroups=len(sizes), copy_sustained_gbs=sustained_copy_gbs(stream, total_ms))
+                timed_subgroups=len(sizes), owned=owned, copy_sustained_gbs=sustained_copy_gbs(stream, total_ms))
 
 
 def sustained_copy_gbs(stream, busy_ms):
@@ -554,6 +560,7 @@ def run_phases(w, world, rank, warmup, steps, backward, tag):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
+        census = w.residency_census() if os.environ.get("TFB_TIMELINE_DIR") else None
         st = w.run_update(it)
         b.record()
         torch.cuda.synchronize()
@@ -561,6 +568,14 @@ def run_phases(w, world, rank, warmup, steps, backward, tag):
         barrier(world)
         if it >= warmup:
             phases.append((ms, st))
+        if census is not None:  # diagnostics: every phase's per-subgroup timeline
+            d = Path(os.environ["TFB_TIMELINE_DIR"])
+            d.mkdir(parents=True, exist_ok=True)
+            (d / f"{tag.replace(' ', '_').replace('=', '')}_r{rank}_p{it}.json").write_text(json.dumps(dict(
+                ms=ms, hits=st.cache_hits, alloc=st.flush_allocation, census_before=census,
+                timeline=w.last_timeline(),
+                io=[dict(id=e.id, read_s=e.read_seconds, write_s=e.write_seconds, fetched=e.fetched,
+                         flushed=e.flushed) for e in st.subgroup_io])))
         log(f"[rank {rank}] {tag} phase {it}: {ms:.0f} ms, hits {st.cache_hits}, alloc {st.flush_allocation}, "
             f"kernel {st.kernel_seconds*1e3:.0f} ms, h2d {st.h2d_seconds*1e3:.0f} ms, d2h {st.d2h_seconds*1e3:.0f} ms")
     return phases
