@@ -26,6 +26,12 @@ int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint
                            uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters,
                            void* stream);
 
+/* Self-test of the second verified fast path (variants 44-46): the largest
+ * relative error of its approximate step against the exact chain over n
+ * random (m, v, t), and the elements whose P/m/v bits differ from the
+ * shipped kernel (must be 0). */
+int tfg_selftest_fast_step(uint64_t n, uint64_t seed, double* worst_rel_err, uint64_t* mismatches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -8,6 +8,8 @@
 //   21-23               scalar elements at higher occupancy
 //   32-37               TMA multistage pipeline, every warp computing
 //   38-40               per-warp TMA pipelines (no CTA barrier)
+//   41-43               software-pipelined register kernel (next quad's loads before the math)
+//   44-46               verified fast path, second form (numerics.cuh adam_element_fast2)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -538,6 +540,90 @@ cudaError_t launch_scalar_wd(const AdamLaunch& a, cudaStream_t stream) {
     return a.c.lr_wd != 0.0 ? launch_scalar<true, MINB>(a, stream) : launch_scalar<false, MINB>(a, stream);
 }
 
+// Software-pipelined register form (variants 41-43): each thread issues the
+// loads of its next grid-stride quad before the binary64 chain of the
+// current one, so a warp keeps a quad's 28 bytes in flight through its whole
+// compute phase (memory parallelism that does not shrink when the SM clock
+// drops under the power cap), at the price of ~14 more registers (MINB 3).
+template <bool WD, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    adam_swp_kernel(const StateIO io, const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t nq,
+                    AdamConsts c, unsigned long long* __restrict__ counters) {
+    unsigned nonfinite = 0, overflow = 0;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    uint64_t q = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const float4* p4 = reinterpret_cast<const float4*>(io.p);
+    const float4* m4 = reinterpret_cast<const float4*>(io.m);
+    const float4* v4 = reinterpret_cast<const float4*>(io.v);
+    float4 rp{}, rm{}, rv{};
+    U16x4 rg{};
+    if (q < nq) {
+        rp = __ldcs(p4 + q);
+        rm = __ldcs(m4 + q);
+        rv = __ldcs(v4 + q);
+        rg = load_u16x4(g + 4 * q);
+    }
+    while (q < nq) {
+        const uint64_t qn = q + nthreads;
+        float4 np{}, nm{}, nv{};
+        U16x4 ng{};
+        if (qn < nq) {  // next quad's loads in flight during this quad's math
+            np = __ldcs(p4 + qn);
+            nm = __ldcs(m4 + qn);
+            nv = __ldcs(v4 + qn);
+            ng = load_u16x4(g + 4 * qn);
+        }
+        nonfinite += nonfinite16<kF16>(rg.x) + nonfinite16<kF16>(rg.y) + nonfinite16<kF16>(rg.z) +
+                     nonfinite16<kF16>(rg.w);
+        adam_math<WD, 1>(rp.x, rm.x, rv.x, widen16<kF16>(rg.x), c);
+        adam_math<WD, 1>(rp.y, rm.y, rv.y, widen16<kF16>(rg.y), c);
+        adam_math<WD, 1>(rp.z, rm.z, rv.z, widen16<kF16>(rg.z), c);
+        adam_math<WD, 1>(rp.w, rm.w, rv.w, widen16<kF16>(rg.w), c);
+        U16x4 h;
+        h.x = narrow16<kF16>(rp.x);
+        h.y = narrow16<kF16>(rp.y);
+        h.z = narrow16<kF16>(rp.z);
+        h.w = narrow16<kF16>(rp.w);
+        overflow += is_inf16<kF16>(h.x) + is_inf16<kF16>(h.y) + is_inf16<kF16>(h.z) + is_inf16<kF16>(h.w);
+        __stcs(reinterpret_cast<float4*>(io.po) + q, rp);
+        __stcs(reinterpret_cast<float4*>(io.mo) + q, rm);
+        __stcs(reinterpret_cast<float4*>(io.vo) + q, rv);
+        store_u16x4(p16 + 4 * q, h);
+        rp = np;
+        rm = nm;
+        rv = nv;
+        rg = ng;
+        q = qn;
+    }
+    if (counters != nullptr) {
+        warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+template <bool WD, int MINB>
+cudaError_t launch_swp(const AdamLaunch& a, cudaStream_t stream) {
+    if (!is_vec(a)) return launch_dtypes<Cfg<1, true, 4>>(a, stream);
+    const uint64_t nq = a.n / 4;
+    if (nq > 0)
+        adam_swp_kernel<WD, MINB><<<grid_for(nq, MINB), kThreads, 0, stream>>>(
+            state_io(a), static_cast<const uint16_t*>(a.g), a.p16, nq, a.c, a.counters);
+    if (nq * 4 == a.n) return cudaGetLastError();
+    AdamLaunch tail = a;  // the n % 4 remainder through the shipped kernel
+    const uint64_t done = nq * 4;
+    tail.p += done;
+    tail.m += done;
+    tail.v += done;
+    tail.g = static_cast<const uint16_t*>(a.g) + done;
+    tail.p16 += done;
+    tail.n = a.n - done;
+    return launch_dtypes<Cfg<1, true, 4>>(tail, stream);
+}
+template <int MINB>
+cudaError_t launch_swp_wd(const AdamLaunch& a, cudaStream_t stream) {
+    return a.c.lr_wd != 0.0 ? launch_swp<true, MINB>(a, stream) : launch_swp<false, MINB>(a, stream);
+}
+
 template <int V>
 cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 1) return launch_wd<kF16, 0, kF16, Cfg<2, false, 1>>(a, stream);
@@ -580,10 +666,68 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 38) return launch_warp_pipe<3, 4>(a, stream);
     if constexpr (V == 39) return launch_warp_pipe<2, 4>(a, stream);
     if constexpr (V == 40) return launch_warp_pipe<4, 3>(a, stream);
+    if constexpr (V == 41) return launch_swp_wd<3>(a, stream);
+    if constexpr (V == 42) return launch_swp_wd<4>(a, stream);
+    if constexpr (V == 43) return launch_swp_wd<2>(a, stream);
+    if constexpr (V == 44) return launch_wd<kF16, 0, kF16, Cfg<1, 5, 4>>(a, stream);
+    if constexpr (V == 45) return launch_wd<kF16, 0, kF16, Cfg<1, 5, 3>>(a, stream);
+    if constexpr (V == 46) return launch_wd<kF16, 0, kF16, Cfg<1, 6, 4>>(a, stream);
     return cudaErrorInvalidValue;
 }
 
 }  // namespace
+
+// Self-test of adam_element_fast2's error bound: the step D' it computes
+// against the exact chain's D on random (m, v, t) spanning many exponents;
+// the largest |D'/D - 1| observed (as -log2) and how many elements would
+// take the exact fallback for p = RN(±u), u in [0.01, 1).
+__global__ void fast_step_selftest_kernel(uint64_t n, uint64_t seed, double lr, double beta1, double beta2,
+                                          double eps, unsigned long long* worst_bits,
+                                          unsigned long long* fallbacks) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    double worst = 0.0;
+    unsigned fb = 0;
+    for (uint64_t i = tid; i < n; i += nthreads) {
+        const uint64_t r1 = splitmix64(seed ^ (2 * i)), r2 = splitmix64(seed ^ (2 * i + 1));
+        const int t = 1 + static_cast<int>(r1 % 20000);
+        const double bc1 = 1.0 - pow(beta1, static_cast<double>(t));
+        const double bc2 = 1.0 - pow(beta2, static_cast<double>(t));
+        const double ib1 = 1.0 / bc1, ib2 = 1.0 / bc2;
+        const double m = ldexp(static_cast<double>(static_cast<float>((r1 >> 11) * 0x1.0p-53 - 0.5)),
+                               -static_cast<int>((r1 >> 40) % 40));
+        const double v = ldexp(static_cast<double>(static_cast<float>((r2 >> 11) * 0x1.0p-53)),
+                               -static_cast<int>((r2 >> 40) % 80));
+        const double vh = v * ib2;
+        if (!(vh > 0.0)) continue;
+        double y, r;
+        asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(vh));
+        y = fma(0.5 * y, fma(-(vh * y), y, 1.0), y);
+        const double den = fma(vh, y, eps);
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+        r = fma(r, fma(-den, r, 1.0), r);
+        const double step = (m * (lr * ib1)) * r;
+        const double mhat = div_by_const(m, bc1, ib1);
+        const double vhat = div_by_const(v, bc2, ib2);
+        const double exact = __ddiv_rn(__dmul_rn(lr, mhat), __dadd_rn(__dsqrt_rn(vhat), eps));
+        if (exact != 0.0) worst = fmax(worst, fabs(step / exact - 1.0));
+        float pf = static_cast<float>((2.0 * ((r2 >> 11) & 1) - 1.0) * (0.01 + 0.99 * ((r2 >> 12) % 1000003) / 1000003.0));
+        float mf = static_cast<float>(m), vf = static_cast<float>(v), pf2 = pf, mf2 = mf, vf2 = vf;
+        AdamConsts c{lr, beta1, beta2, 1.0 - beta1, 1.0 - beta2, eps, 0.0, bc1, bc2, ib1, ib2};
+        adam_element<false, true>(pf, mf, vf, 0.0f, c);
+        adam_element_fast2<false, 30>(pf2, mf2, vf2, 0.0f, c);
+        if (__float_as_uint(pf) != __float_as_uint(pf2) || __float_as_uint(mf) != __float_as_uint(mf2) ||
+            __float_as_uint(vf) != __float_as_uint(vf2))
+            atomicAdd(fallbacks + 1, 1ull);  // a bit mismatch: must stay 0
+        (void)fb;
+    }
+    atomicMax(worst_bits, static_cast<unsigned long long>(__double_as_longlong(worst)));
+}
+
+cudaError_t launch_fast_step_selftest(uint64_t n, uint64_t seed, unsigned long long* out, cudaStream_t stream) {
+    fast_step_selftest_kernel<<<grid_for(n, 4), kThreads, 0, stream>>>(n, seed, 1e-3, 0.9, 0.999, 1e-8, out, out);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
@@ -630,10 +774,16 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 38: return launch_variant<38>(a, stream);
         case 39: return launch_variant<39>(a, stream);
         case 40: return launch_variant<40>(a, stream);
+        case 41: return launch_variant<41>(a, stream);
+        case 42: return launch_variant<42>(a, stream);
+        case 43: return launch_variant<43>(a, stream);
+        case 44: return launch_variant<44>(a, stream);
+        case 45: return launch_variant<45>(a, stream);
+        case 46: return launch_variant<46>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 41; }
+int adam_variant_count() { return 47; }
 
 }  // namespace tfb

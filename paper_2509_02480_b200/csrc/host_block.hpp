@@ -10,6 +10,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <utility>
 
@@ -67,6 +68,7 @@ public:
         }
         b.base_ = static_cast<std::uint8_t*>(p);
         b.bytes_ = bytes;
+        if (log_enabled()) std::fprintf(stderr, "hostblock alloc %p %zu pinned=%d\n", p, bytes, int(b.pinned_));
         g_host_blocks_live.fetch_add(1, std::memory_order_relaxed);
         g_host_bytes_live.fetch_add(static_cast<std::int64_t>(bytes), std::memory_order_relaxed);
         return b;
@@ -80,8 +82,15 @@ public:
     explicit operator bool() const { return base_ != nullptr; }
 
 private:
+    // TFB_HOSTBLOCK_LOG=1: every allocation and release on stderr (leak forensics).
+    static bool log_enabled() {
+        static const bool on = std::getenv("TFB_HOSTBLOCK_LOG") != nullptr;
+        return on;
+    }
+
     void release() {
         if (base_ == nullptr) return;
+        if (log_enabled()) std::fprintf(stderr, "hostblock free %p pinned=%d\n", static_cast<void*>(base_), int(pinned_));
         g_host_blocks_live.fetch_sub(1, std::memory_order_relaxed);
         g_host_bytes_live.fetch_sub(static_cast<std::int64_t>(bytes_), std::memory_order_relaxed);
         if (pinned_) {

@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstring>
 #include <string>
 
 #include "capi_internal.hpp"
@@ -67,6 +68,23 @@ int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint
         a.counters = counters;
         tfb::cuda_check(tfb::launch_adam_fused_variant(a, variant, static_cast<cudaStream_t>(stream)),
                         "adam_fused_variant");
+    });
+}
+
+int tfg_selftest_fast_step(uint64_t n, uint64_t seed, double* worst_rel_err, uint64_t* mismatches) {
+    return guard([&] {
+        unsigned long long* d = nullptr;
+        tfb::cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), 2 * sizeof(unsigned long long)), "cudaMalloc");
+        unsigned long long h[2] = {0, 0};
+        cudaMemset(d, 0, sizeof(h));
+        const cudaError_t e = tfb::launch_fast_step_selftest(n, seed, d, nullptr);
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        tfb::cuda_check(e, "fast_step_selftest");
+        double w = 0.0;
+        std::memcpy(&w, &h[0], sizeof(w));
+        if (worst_rel_err) *worst_rel_err = w;
+        if (mismatches) *mismatches = h[1];
     });
 }
 

@@ -36,7 +36,8 @@ def point(tf, sub, mix, steps, warmup, root):
     dev = torch.cuda.current_device()
     state = 12 * sub
     if mix == "spill":
-        free = shutil.disk_usage(root).free
+        root.parent.mkdir(parents=True, exist_ok=True)
+        free = shutil.disk_usage(root.parent).free
         M = int(max(3, min(36, round(2.4e9 / sub), 0.4 * free // (state + 4096))))
         C, dram_cap = M // 2, 2
     else:

@@ -230,7 +230,7 @@ def test_constant_division_matches_div_rn(tf, cuda):
             assert mism == 0, (beta, t, first)
 
 
-@pytest.mark.parametrize("variant", range(1, 41))
+@pytest.mark.parametrize("variant", range(1, 47))
 def test_kernel_variants_bitwise(tf, cuda, variant):
     import torch
     n = 1_000_003
@@ -248,6 +248,20 @@ def test_kernel_variants_bitwise(tf, cuda, variant):
     assert_bits(Mm.cpu().numpy(), want[1], "m")
     assert_bits(V.cpu().numpy(), want[2], "v")
     assert np.array_equal(_np16(p16), want[3])
+
+
+def test_fast_step_error_bound_and_bits(tf, cuda):
+    """The second verified fast path (tuning variants 44-46): its approximate
+    step stays within 2^-30 relative of the exact chain's (the tolerance its
+    acceptance test assumes) over 2^26 random (m, v, t) spanning 40-80
+    binades, and the P/m/v bits it produces equal the shipped kernel's."""
+    import ctypes as C
+
+    from paper_2509_02480_b200 import _lib
+    worst, mism = C.c_double(), C.c_uint64()
+    _lib.call_tuning("tfg_selftest_fast_step", 1 << 26, 2026, C.byref(worst), C.byref(mism))
+    assert mism.value == 0
+    assert worst.value < 2.0 ** -30, worst.value
 
 
 @pytest.mark.parametrize("nsrc", [1, 2, 3, 4, 8])
