@@ -31,6 +31,9 @@ int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint
  * random (m, v, t), and the elements whose P/m/v bits differ from the
  * shipped kernel (must be 0). */
 int tfg_selftest_fast_step(uint64_t n, uint64_t seed, double* worst_rel_err, uint64_t* mismatches);
+/* Self-test of variant 47's in-range sqrt / division against the library's
+ * __dsqrt_rn / __ddiv_rn on n random operand pairs: mismatches (must be 0). */
+int tfg_selftest_fast_rn(uint64_t n, uint64_t seed, uint64_t* mismatches);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@
 //   38-40               per-warp TMA pipelines (no CTA barrier)
 //   41-43               software-pipelined register kernel (next quad's loads before the math)
 //   44-46               verified fast path, second form (numerics.cuh adam_element_fast2)
+//   47                  in-range correctly rounded sqrt / division without the special-operand checks
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -624,6 +625,48 @@ cudaError_t launch_swp_wd(const AdamLaunch& a, cudaStream_t stream) {
     return a.c.lr_wd != 0.0 ? launch_swp<true, MINB>(a, stream) : launch_swp<false, MINB>(a, stream);
 }
 
+// The operand domain of adam_element_rn (numerics.cuh): lr in [2^-600, 2^600],
+// eps in [2^-600, 2^96], lr / eps <= 2^600, bias corrections in [2^-64, 1].
+bool fast_rn_domain(const AdamConsts& c) {
+    auto in = [](double x, double lo, double hi) { return x >= lo && x <= hi; };
+    return in(c.lr, 0x1p-600, 0x1p600) && in(c.eps, 0x1p-600, 0x1p96) && c.lr / c.eps <= 0x1p600 &&
+           in(c.bc1, 0x1p-64, 1.0) && in(c.bc2, 0x1p-64, 1.0);
+}
+
+// Self-test of sqrt_rn_in_range / div_rn_in_range against __dsqrt_rn /
+// __ddiv_rn: random significands (plus all-ones / power-of-two / exact
+// multiples) over the domain's exponent ranges; counts mismatches.
+__global__ void fast_rn_selftest_kernel(uint64_t n, uint64_t seed, unsigned long long* bad) {
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    unsigned nb = 0;
+    for (uint64_t i = tid; i < n; i += nthreads) {
+        const uint64_t r1 = splitmix64(seed ^ (3 * i)), r2 = splitmix64(seed ^ (3 * i + 1)),
+                       r3 = splitmix64(seed ^ (3 * i + 2));
+        auto mant = [](uint64_t r) {
+            uint64_t m = r & 0xFFFFFFFFFFFFFULL;
+            const int sel = static_cast<int>((r >> 52) & 7u);
+            if (sel == 0) m |= 0xFFFFFFFFFF000ULL;
+            if (sel == 1) m &= 0x0000000000FFFULL;
+            return m;
+        };
+        // sqrt: x in [2^-1000, 2^960)
+        const int ex = -1000 + static_cast<int>(r1 >> 53) % 1960;
+        const double x = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(ex + 1023) << 52) | mant(r1)));
+        nb += __double_as_longlong(sqrt_rn_in_range(x)) != __double_as_longlong(__dsqrt_rn(x));
+        // division: b in [2^-600, 2^160), a / b in [2^-846, 2^792)
+        const int eb = -600 + static_cast<int>((r2 >> 53) % 760);
+        const int eq = -846 + static_cast<int>((r3 >> 53) % 1638);
+        const double b = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(eb + 1023) << 52) | mant(r2)));
+        double a = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(eb + eq + 1023) << 52) | mant(r3)));
+        if ((r3 & 15) == 0) a = __dmul_rn(b, static_cast<double>(static_cast<int>((r3 >> 4) & 0xFFFF) + 1));
+        if (r3 >> 63) a = -a;
+        nb += __double_as_longlong(div_rn_in_range(a, b)) != __double_as_longlong(__ddiv_rn(a, b));
+    }
+    warp_count_add(bad, nb);
+}
+
+
 template <int V>
 cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 1) return launch_wd<kF16, 0, kF16, Cfg<2, false, 1>>(a, stream);
@@ -672,6 +715,9 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 44) return launch_wd<kF16, 0, kF16, Cfg<1, 5, 4>>(a, stream);
     if constexpr (V == 45) return launch_wd<kF16, 0, kF16, Cfg<1, 5, 3>>(a, stream);
     if constexpr (V == 46) return launch_wd<kF16, 0, kF16, Cfg<1, 6, 4>>(a, stream);
+    if constexpr (V == 47)
+        return fast_rn_domain(a.c) ? launch_wd<kF16, 0, kF16, Cfg<1, 7, 4>>(a, stream)
+                                   : launch_dtypes<Cfg<1, true, 4>>(a, stream);
     return cudaErrorInvalidValue;
 }
 
@@ -722,6 +768,11 @@ __global__ void fast_step_selftest_kernel(uint64_t n, uint64_t seed, double lr, 
         (void)fb;
     }
     atomicMax(worst_bits, static_cast<unsigned long long>(__double_as_longlong(worst)));
+}
+
+cudaError_t launch_fast_rn_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t stream) {
+    fast_rn_selftest_kernel<<<grid_for(n, 4), kThreads, 0, stream>>>(n, seed, bad);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_fast_step_selftest(uint64_t n, uint64_t seed, unsigned long long* out, cudaStream_t stream) {
@@ -780,10 +831,11 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 44: return launch_variant<44>(a, stream);
         case 45: return launch_variant<45>(a, stream);
         case 46: return launch_variant<46>(a, stream);
+        case 47: return launch_variant<47>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 47; }
+int adam_variant_count() { return 48; }
 
 }  // namespace tfb

@@ -49,6 +49,8 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
 int adam_variant_count();
 // Self-test of the second verified fast path: out[0] = largest |D'/D - 1| (double bits), out[1] += bit mismatches.
 cudaError_t launch_fast_step_selftest(uint64_t n, uint64_t seed, unsigned long long* out, cudaStream_t stream);
+// Self-test of the in-range sqrt / division (variant 47) against __dsqrt_rn / __ddiv_rn: *bad += mismatches.
+cudaError_t launch_fast_rn_selftest(uint64_t n, uint64_t seed, unsigned long long* bad, cudaStream_t stream);
 // Self-test: div_by_const(a, b, y) vs div.rn.f64 on generated numerators.
 cudaError_t launch_divtest(double b, double y, uint64_t n, uint64_t seed, int exp_lo, int exp_span,
                            unsigned long long* mismatches, double* first_bad, cudaStream_t stream);

@@ -88,4 +88,18 @@ int tfg_selftest_fast_step(uint64_t n, uint64_t seed, double* worst_rel_err, uin
     });
 }
 
+int tfg_selftest_fast_rn(uint64_t n, uint64_t seed, uint64_t* mismatches) {
+    return guard([&] {
+        unsigned long long* d = nullptr;
+        tfb::cuda_check(cudaMalloc(reinterpret_cast<void**>(&d), sizeof(unsigned long long)), "cudaMalloc");
+        unsigned long long h = 0;
+        cudaMemset(d, 0, sizeof(h));
+        const cudaError_t e = tfb::launch_fast_rn_selftest(n, seed, d, nullptr);
+        cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        cudaFree(d);
+        tfb::cuda_check(e, "fast_rn_selftest");
+        if (mismatches) *mismatches = h;
+    });
+}
+
 }  // extern "C"

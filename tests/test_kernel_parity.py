@@ -230,7 +230,7 @@ def test_constant_division_matches_div_rn(tf, cuda):
             assert mism == 0, (beta, t, first)
 
 
-@pytest.mark.parametrize("variant", range(1, 47))
+@pytest.mark.parametrize("variant", range(1, 48))
 def test_kernel_variants_bitwise(tf, cuda, variant):
     import torch
     n = 1_000_003
@@ -262,6 +262,19 @@ def test_fast_step_error_bound_and_bits(tf, cuda):
     _lib.call_tuning("tfg_selftest_fast_step", 1 << 26, 2026, C.byref(worst), C.byref(mism))
     assert mism.value == 0
     assert worst.value < 2.0 ** -30, worst.value
+
+
+def test_in_range_sqrt_and_division_are_correctly_rounded(tf, cuda):
+    """Variant 47's sqrt / division without the special-operand checks equal
+    __dsqrt_rn / __ddiv_rn bit for bit on 2^28 random operand pairs over the
+    exponent ranges the Adam chain keeps them in (fast_rn_domain)."""
+    import ctypes as C
+
+    from paper_2509_02480_b200 import _lib
+    bad = C.c_uint64()
+    for seed in (1, 2, 3, 4):
+        _lib.call_tuning("tfg_selftest_fast_rn", 1 << 26, seed, C.byref(bad))
+        assert bad.value == 0, seed
 
 
 @pytest.mark.parametrize("nsrc", [1, 2, 3, 4, 8])
