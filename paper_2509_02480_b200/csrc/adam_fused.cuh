@@ -141,6 +141,33 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// State-stream load / store forms (PF < 0, tuning variants 48-50): -1 keeps
+// evict-first and asks L2 for 256-byte fetches (ld.global.cs.L2::256B), -2
+// the same without evict-first (L1::no_allocate), -3 plain cached accesses.
+// Otherwise evict-first __ldcs / __stcs (the shipped form).
+template <int PF>
+__device__ __forceinline__ float4 ld_state(const float4* p) {
+    float4 r;
+    if constexpr (PF == -1) {
+        asm volatile("ld.global.cs.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    } else if constexpr (PF == -2) {
+        asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+    } else if constexpr (PF == -3) {
+        r = *p;
+    } else {
+        r = __ldcs(p);
+    }
+    return r;
+}
+
+template <int PF>
+__device__ __forceinline__ void st_state(float4* p, float4 v) {
+    if constexpr (PF == -3) *p = v;
+    else __stcs(p, v);
+}
+
 // PF > 0: one thread per CTA asks the TMA unit to pull the CTA's chunk PF
 // grid-stride iterations ahead into L2 (cp.async.bulk.prefetch), so more bytes
 // are in flight than the registers of 32 warps per SM can hold.
@@ -184,9 +211,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
             for (int u = 0; u < UNROLL; ++u) {  // all loads first: UNROLL quads in flight
                 const uint64_t q = base + static_cast<uint64_t>(u) * nthreads;
                 if (q < nq) {
-                    rp[u] = __ldcs(p4 + q);
-                    rm[u] = __ldcs(m4 + q);
-                    rv[u] = __ldcs(v4 + q);
+                    rp[u] = ld_state<PF>(p4 + q);
+                    rm[u] = ld_state<PF>(m4 + q);
+                    rv[u] = ld_state<PF>(v4 + q);
                     rg[u].load(gs, q, nonfinite);
                 }
             }
@@ -220,9 +247,9 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     h.z = narrow16<OK>(rp[u].z);
                     h.w = narrow16<OK>(rp[u].w);
                     overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
-                    __stcs(po4 + q, rp[u]);
-                    __stcs(mo4 + q, rm[u]);
-                    __stcs(vo4 + q, rv[u]);
+                    st_state<PF>(po4 + q, rp[u]);
+                    st_state<PF>(mo4 + q, rm[u]);
+                    st_state<PF>(vo4 + q, rv[u]);
                     store_u16x4(p16 + 4 * q, h);
                 }
             }

@@ -11,6 +11,7 @@
 //   41-43               software-pipelined register kernel (next quad's loads before the math)
 //   44-46               verified fast path, second form (numerics.cuh adam_element_fast2)
 //   47                  in-range correctly rounded sqrt / division without the special-operand checks
+//   48-50               state-stream cache hints: L2::256B fetches (evict-first or not), plain cached
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -650,13 +651,14 @@ __global__ void fast_rn_selftest_kernel(uint64_t n, uint64_t seed, unsigned long
             if (sel == 1) m &= 0x0000000000FFFULL;
             return m;
         };
-        // sqrt: x in [2^-1000, 2^960)
-        const int ex = -1000 + static_cast<int>(r1 >> 53) % 1960;
+        // sqrt: x in [2^-960, 2^960) (the Adam chain's v/bc2 lies in [2^-149, 2^192])
+        const int ex = -960 + static_cast<int>((r1 >> 53) % 1920);
         const double x = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(ex + 1023) << 52) | mant(r1)));
         nb += __double_as_longlong(sqrt_rn_in_range(x)) != __double_as_longlong(__dsqrt_rn(x));
-        // division: b in [2^-600, 2^160), a / b in [2^-846, 2^792)
+        // division: b in [2^-600, 2^160), a in [2^-960, 2^1000), a / b in [2^-846, 2^792)
         const int eb = -600 + static_cast<int>((r2 >> 53) % 760);
-        const int eq = -846 + static_cast<int>((r3 >> 53) % 1638);
+        const int lo = max(-846, -960 - eb), hi = min(792, 1000 - eb);
+        const int eq = lo + static_cast<int>((r3 >> 53) % static_cast<uint64_t>(hi - lo));
         const double b = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(eb + 1023) << 52) | mant(r2)));
         double a = __longlong_as_double(static_cast<long long>((static_cast<uint64_t>(eb + eq + 1023) << 52) | mant(r3)));
         if ((r3 & 15) == 0) a = __dmul_rn(b, static_cast<double>(static_cast<int>((r3 >> 4) & 0xFFFF) + 1));
@@ -715,6 +717,9 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 44) return launch_wd<kF16, 0, kF16, Cfg<1, 5, 4>>(a, stream);
     if constexpr (V == 45) return launch_wd<kF16, 0, kF16, Cfg<1, 5, 3>>(a, stream);
     if constexpr (V == 46) return launch_wd<kF16, 0, kF16, Cfg<1, 6, 4>>(a, stream);
+    if constexpr (V == 48) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, -1>>(a, stream);
+    if constexpr (V == 49) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, -2>>(a, stream);
+    if constexpr (V == 50) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, -3>>(a, stream);
     if constexpr (V == 47)
         return fast_rn_domain(a.c) ? launch_wd<kF16, 0, kF16, Cfg<1, 7, 4>>(a, stream)
                                    : launch_dtypes<Cfg<1, true, 4>>(a, stream);
@@ -832,10 +837,13 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 45: return launch_variant<45>(a, stream);
         case 46: return launch_variant<46>(a, stream);
         case 47: return launch_variant<47>(a, stream);
+        case 48: return launch_variant<48>(a, stream);
+        case 49: return launch_variant<49>(a, stream);
+        case 50: return launch_variant<50>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 48; }
+int adam_variant_count() { return 51; }
 
 }  // namespace tfb
