@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define TFG_ABI_VERSION 2
+#define TFG_ABI_VERSION 3
 #define TFG_MAX_TIERS 8
 
 typedef enum tfg_status {
@@ -113,6 +113,11 @@ typedef struct tfg_device_options {
     int32_t hbm_cache_slots; /* hbm_retain 2: HBM buffers for retained subgroups; 0 = all of C. Fewer
                                 than C makes a two-level cache: the rest keep their host slots, and
                                 C = min(cache_slots, hbm_cache_slots + pool_slots - 3) */
+    int32_t host_grads;      /* (ABI 3) 1: the 16-bit gradients and working params live in pinned host
+                                memory per subgroup and stream with the state (2 B/param more each
+                                way) instead of 4 B/param of HBM for the whole shard; grad_buffer /
+                                params16_buffer / bind_grad_buffer then take host pointers. Copy
+                                pipeline and 16-bit gradient flow only */
 } tfg_device_options;
 
 typedef struct tfg_tier_observation { /* placement.hpp:138-145 */

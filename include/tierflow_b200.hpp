@@ -187,6 +187,7 @@ struct DeviceOptions {
     int hbm_retain = 1;  // 0 off, 1 host slot kept, 2 HBM cache (see tfg_device_options)
     int h2d_split = 1;
     int hbm_cache_slots = 0;  // hbm_retain 2: HBM part of C (0: all)
+    bool host_grads = false;  // 16-bit gradients / working params in pinned host memory (ABI 3)
 };
 
 using PhaseStats = tfg_phase_stats;
@@ -203,7 +204,7 @@ public:
                                 o.update_pad_ns};
         tfg_adam_hyper ah{h.lr, h.beta1, h.beta2, h.eps, h.weight_decay};
         tfg_device_options dv{d.device, d.grad_dtype, d.param_dtype, d.device_buffers, d.zero_copy ? 1 : 0,
-                              d.d2h_split, d.hbm_retain, d.h2d_split, d.hbm_cache_slots};
+                              d.d2h_split, d.hbm_retain, d.h2d_split, d.hbm_cache_slots, d.host_grads ? 1 : 0};
         check(tfg_engine_create(id, th.data(), static_cast<int>(th.size()), &so, &ah, trace.handle(), &dv, &h_));
     }
     ~OffloadWorker() { tfg_engine_destroy(h_); }

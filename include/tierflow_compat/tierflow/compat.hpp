@@ -577,7 +577,7 @@ public:
                                 opt_.atomic_rw, opt_.multi_path, lock.c_str(), opt_.update_threads,
                                 opt_.deadlock_timeout_s, opt_.update_pad_ns};
         const tfg_adam_hyper ah = hyper.c();
-        tfg_device_options dv{0, TFG_F16, TFG_F16, 3, 0, 1, 1, 1, 0};
+        tfg_device_options dv{0, TFG_F16, TFG_F16, 3, 0, 1, 1, 1, 0, 0};
         detail::check(tfg_engine_create(id, th.data(), static_cast<int>(th.size()), &so, &ah, trace.handle(), &dv, &h_));
     }
     ~OffloadWorker() { tfg_engine_destroy(h_); }

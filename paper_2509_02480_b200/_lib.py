@@ -77,7 +77,8 @@ class ScheduleOptionsC(C.Structure):
 class DeviceOptionsC(C.Structure):
     _fields_ = [("device", C.c_int32), ("grad_dtype", C.c_int32), ("param_dtype", C.c_int32),
                 ("device_buffers", C.c_int32), ("zero_copy", C.c_int32), ("d2h_split", C.c_int32),
-                ("hbm_retain", C.c_int32), ("h2d_split", C.c_int32), ("hbm_cache_slots", C.c_int32)]
+                ("hbm_retain", C.c_int32), ("h2d_split", C.c_int32), ("hbm_cache_slots", C.c_int32),
+                ("host_grads", C.c_int32)]
 
 
 class TierObservationC(C.Structure):

@@ -648,6 +648,7 @@ int tfg_engine_create(int worker_id, tfg_tier* const* tiers, int n_tiers, const 
             if (device->hbm_cache_slots < 0) throw tfb::ConfigError("hbm_cache_slots must be >= 0");
             d.hbm_cache_slots = device->hbm_cache_slots;
             d.hbm_retain = device->hbm_retain;
+            d.host_grads = device->host_grads != 0;
         }
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= d.device || d.device < 0) {
@@ -875,7 +876,7 @@ int tfg_engine_read_params16(tfg_engine* engine, uint32_t id, uint16_t* out_n) {
         need(out_n, "out");
         const auto meta = engine->w->meta(id);
         tfb::cuda_check(cudaSetDevice(engine->w->device_options().device), "cudaSetDevice");
-        tfb::cuda_check(cudaMemcpy(out_n, engine->w->params16_buffer(id), 2 * meta.param_count, cudaMemcpyDeviceToHost),
+        tfb::cuda_check(cudaMemcpy(out_n, engine->w->params16_buffer(id), 2 * meta.param_count, cudaMemcpyDefault),
                         "cudaMemcpy(params16)");
     });
 }
@@ -886,7 +887,7 @@ int tfg_engine_read_grads16(tfg_engine* engine, uint32_t id, uint16_t* out_n) {
         need(out_n, "out");
         const auto meta = engine->w->meta(id);
         tfb::cuda_check(cudaSetDevice(engine->w->device_options().device), "cudaSetDevice");
-        tfb::cuda_check(cudaMemcpy(out_n, engine->w->grad_buffer(id), 2 * meta.param_count, cudaMemcpyDeviceToHost),
+        tfb::cuda_check(cudaMemcpy(out_n, engine->w->grad_buffer(id), 2 * meta.param_count, cudaMemcpyDefault),
                         "cudaMemcpy(grads16)");
     });
 }

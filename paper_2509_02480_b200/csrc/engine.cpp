@@ -312,6 +312,8 @@ OffloadWorker::OffloadWorker(WorkerId id, std::vector<std::shared_ptr<Tier>> tie
     if (dev_.device_buffers < 1) throw ConfigError("device_buffers must be >= 1");
     if (dev_.grad_kind != kF16 && dev_.grad_kind != kBF16) throw ConfigError("unknown gradient dtype");
     if (dev_.out_kind != kF16 && dev_.out_kind != kBF16) throw ConfigError("unknown working-param dtype");
+    if (dev_.host_grads && (dev_.zero_copy != 0 || !opt_.skip_gradients))
+        throw ConfigError("host_grads needs the copy pipeline (zero_copy 0) and the 16-bit gradient flow");
     if (opt_.lock_dir.empty()) opt_.lock_dir = (std::filesystem::temp_directory_path() / "tierflow-locks").string();
     std::vector<double> rbw, wbw;
     for (const auto& t : tiers_) {
@@ -449,9 +451,27 @@ void OffloadWorker::setup_device() {
         offs.push_back(arena);
         arena += round_up(2 * subgroups_.at(id).param_count, 256);
     }
-    cuda_check(cudaMalloc(&grad_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(grads)");
-    cuda_check(cudaMalloc(&p16_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(params16)");
-    cuda_check(cudaMemset(grad_arena_, 0, std::max<std::size_t>(arena, 256)), "cudaMemset(grads)");
+    if (dev_.host_grads) {
+        for (const SubgroupId id : ids_) {
+            const std::size_t bytes = 2 * static_cast<std::size_t>(subgroups_.at(id).param_count);
+            grads_host_.push_back(HostBlock::allocate(bytes, true));
+            std::memset(grads_host_.back().base(), 0, bytes);
+            p16_host_.push_back(HostBlock::allocate(bytes, true));
+        }
+        aux_.assign(ring_.size(), nullptr);
+        aux_ready_.assign(ring_.size(), nullptr);
+        for (std::size_t b = 0; b < aux_.size(); ++b) {
+            cuda_check(cudaMalloc(reinterpret_cast<void**>(&aux_[b]), 4 * ring_stride_), "cudaMalloc(staging)");
+            cuda_check(cudaEventCreateWithFlags(&aux_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
+        }
+        aux_next_ = 0;
+        grads_verified_.assign(ids_.size(), 1);  // zero gradients: finite
+        verified_counts_.assign(ids_.size(), 0);
+    } else {
+        cuda_check(cudaMalloc(&grad_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(grads)");
+        cuda_check(cudaMalloc(&p16_arena_, std::max<std::size_t>(arena, 256)), "cudaMalloc(params16)");
+        cuda_check(cudaMemset(grad_arena_, 0, std::max<std::size_t>(arena, 256)), "cudaMemset(grads)");
+    }
     cuda_check(cudaEventCreateWithFlags(&producer_done_, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaEventCreateWithFlags(&verdict_ready_, cudaEventDisableTiming), "cudaEventCreate");
     cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&verdict_host_), std::max<std::size_t>(1, ids_.size()) *
@@ -489,8 +509,13 @@ void OffloadWorker::setup_device() {
     host_retired_ns_.assign(ids_.size(), 0);
     for (std::size_t k = 0; k < ids_.size(); ++k) {
         index_of_[ids_[k]] = k;
-        grad_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(grad_arena_) + offs[k]));
-        p16_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(p16_arena_) + offs[k]));
+        if (dev_.host_grads) {
+            grad_ptr_.push_back(reinterpret_cast<std::uint16_t*>(grads_host_[k].base()));
+            p16_ptr_.push_back(reinterpret_cast<std::uint16_t*>(p16_host_[k].base()));
+        } else {
+            grad_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(grad_arena_) + offs[k]));
+            p16_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(p16_arena_) + offs[k]));
+        }
         DeviceEvents& e = events_[k];
         for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_start, &e.d2h_end})
             cuda_check(cudaEventCreate(ev), "cudaEventCreate");
@@ -535,6 +560,13 @@ void OffloadWorker::release_device() {
     grad_stage_free_.clear();
     cudaFree(grad_arena_);
     cudaFree(p16_arena_);
+    for (std::uint16_t* a : aux_) cudaFree(a);
+    aux_.clear();
+    for (cudaEvent_t ev : aux_ready_)
+        if (ev) cudaEventDestroy(ev);
+    aux_ready_.clear();
+    grads_host_.clear();
+    p16_host_.clear();
     cudaFree(counters_);
     cudaFree(sg_counts_);
     if (producer_done_) cudaEventDestroy(producer_done_);
@@ -609,6 +641,29 @@ void OffloadWorker::run_backward_sim(int iteration, std::uint64_t seed, int accu
     if (accum_steps < 1) throw ConfigError("grad_accum_steps must be >= 1");
     if (!device_ready_) throw Error("run_backward_sim before init_and_flush_all");
     DeviceGuard dg(dev_.device);
+    if (dev_.host_grads) {
+        // Generated (and counted) on the device in a staging buffer, then
+        // copied to the subgroup's pinned host block: the gradients a
+        // ZeRO-Offload backward leaves in host memory.
+        cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+        for (std::size_t k = 0; k < ids_.size(); ++k) {
+            const SubgroupId id = ids_[k];
+            const std::uint64_t pc = subgroups_.at(id).param_count;
+            std::uint16_t* g = aux_[0];
+            for (int step = 0; step < accum_steps; ++step)
+                cuda_check(launch_synthetic_grads(g, pc, dev_.grad_kind, grad_prefix(seed, id, iteration, step),
+                                                  step > 0, s_k_),
+                           "synthetic_grads");
+            cuda_check(launch_count_nonfinite16(g, pc, dev_.grad_kind, sg_counts_ + k, s_k_), "count_nonfinite");
+            cuda_check(cudaMemcpyAsync(grad_ptr_[k], g, 2 * pc, cudaMemcpyDeviceToHost, s_k_), "cudaMemcpyAsync(grads)");
+        }
+        cuda_check(cudaMemcpyAsync(verified_counts_.data(), sg_counts_, ids_.size() * sizeof(unsigned long long),
+                                   cudaMemcpyDeviceToHost, s_k_),
+                   "cudaMemcpyAsync(counts)");
+        cuda_check(cudaStreamSynchronize(s_k_), "cudaStreamSynchronize");
+        std::fill(grads_verified_.begin(), grads_verified_.end(), 1);
+        return;
+    }
     for (std::size_t k = 0; k < ids_.size(); ++k) {
         const SubgroupId id = ids_[k];
         const std::uint64_t pc = subgroups_.at(id).param_count;
@@ -701,15 +756,18 @@ void OffloadWorker::fetch_grads_for_cached(SubgroupId id) {
 
 void* OffloadWorker::grad_buffer(SubgroupId id) {
     if (!device_ready_) throw Error("grad_buffer before init_and_flush_all");
-    return grad_ptr_.at(index_of_.at(id));
+    const std::size_t k = index_of_.at(id);
+    if (dev_.host_grads) grads_verified_.at(k) = 0;  // the caller may write it now
+    return grad_ptr_.at(k);
 }
 
 void OffloadWorker::bind_grad_buffer(SubgroupId id, void* device_ptr) {
     if (!device_ready_) throw Error("bind_grad_buffer before init_and_flush_all");
     if (device_ptr == nullptr) throw ConfigError("bind_grad_buffer: null device pointer");
     const std::size_t k = index_of_.at(id);
-    grad_ptr_.at(k) = static_cast<std::uint16_t*>(device_ptr);
+    grad_ptr_.at(k) = static_cast<std::uint16_t*>(device_ptr);  // host_grads: a pinned host pointer
     grad_sources_.at(k).clear();
+    if (dev_.host_grads) grads_verified_.at(k) = 0;
 }
 
 void OffloadWorker::bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources) {
@@ -717,6 +775,7 @@ void OffloadWorker::bind_grad_sources(SubgroupId id, const std::vector<const voi
     if (sources.empty() || sources.size() > static_cast<std::size_t>(kMaxGradSources))
         throw ConfigError("bind_grad_sources: 1.." + std::to_string(kMaxGradSources) + " sources");
     if (!opt_.skip_gradients) throw ConfigError("bind_grad_sources: not available in the baseline gradient flow");
+    if (dev_.host_grads) throw ConfigError("bind_grad_sources: the sources are device buffers (host_grads is on)");
     for (const void* s : sources)
         if (s == nullptr) throw ConfigError("bind_grad_sources: null device pointer");
     grad_sources_.at(index_of_.at(id)) = sources;
@@ -739,18 +798,43 @@ void* OffloadWorker::params16_buffer(SubgroupId id) {
 
 // Non-finite gradient count per subgroup (index order): of the bound buffer,
 // or of the rounded fp32 sum for a subgroup fed by several sources.
-std::vector<unsigned long long> OffloadWorker::nonfinite_counts() {
-    cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
-    for (std::size_t k = 0; k < ids_.size(); ++k) {
+// Per-subgroup non-finite gradient counts into sg_counts_, async on s_k_:
+// a device buffer in place, several sources as their rounded fp32 sum. With
+// host_grads, a block its producer (run_backward_sim) counted as it wrote it
+// keeps that count; any other is staged through the staging ring and counted
+// (2 B/param over PCIe).
+void OffloadWorker::count_grads_async() {
+    const std::size_t M = ids_.size();
+    if (dev_.host_grads) {
+        for (std::size_t k = 0; k < M; ++k) verdict_host_[k] = grads_verified_[k] ? verified_counts_[k] : 0;
+        cuda_check(cudaMemcpyAsync(sg_counts_, verdict_host_, M * sizeof(unsigned long long), cudaMemcpyHostToDevice,
+                                   s_k_),
+                   "cudaMemcpyAsync(counts)");
+        cuda_check(cudaStreamWaitEvent(s_k_, aux_ready_[0], 0), "wait");
+    } else {
+        cuda_check(cudaMemsetAsync(sg_counts_, 0, M * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+    }
+    for (std::size_t k = 0; k < M; ++k) {
         const std::uint64_t pc = subgroups_.at(ids_[k]).param_count;
-        if (grad_sources_[k].empty())
-            cuda_check(launch_count_nonfinite16(grad_ptr_[k], pc, dev_.grad_kind, sg_counts_ + k, s_k_),
-                       "count_nonfinite");
-        else
+        if (!grad_sources_[k].empty()) {
             cuda_check(launch_count_nonfinite_sum16(grad_sources_[k].data(), static_cast<int>(grad_sources_[k].size()),
                                                     pc, dev_.grad_kind, sg_counts_ + k, s_k_),
                        "count_nonfinite_sum");
+        } else if (dev_.host_grads) {
+            if (grads_verified_[k]) continue;
+            cuda_check(cudaMemcpyAsync(aux_[0], grad_ptr_[k], 2 * pc, cudaMemcpyHostToDevice, s_k_),
+                       "cudaMemcpyAsync(grads)");
+            cuda_check(launch_count_nonfinite16(aux_[0], pc, dev_.grad_kind, sg_counts_ + k, s_k_), "count_nonfinite");
+        } else {
+            cuda_check(launch_count_nonfinite16(grad_ptr_[k], pc, dev_.grad_kind, sg_counts_ + k, s_k_),
+                       "count_nonfinite");
+        }
     }
+    if (dev_.host_grads) cuda_check(cudaEventRecord(aux_ready_[0], s_k_), "cudaEventRecord");
+}
+
+std::vector<unsigned long long> OffloadWorker::nonfinite_counts() {
+    count_grads_async();
     std::vector<unsigned long long> counts(ids_.size());
     cuda_check(cudaMemcpyAsync(counts.data(), sg_counts_, counts.size() * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s_k_),
@@ -778,17 +862,7 @@ bool OffloadWorker::gradients_finite() {
 // issuing the first update (await_grad_verdict), by which time the count has
 // long finished under the first fetch.
 void OffloadWorker::launch_grad_check() {
-    cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
-    for (std::size_t k = 0; k < ids_.size(); ++k) {
-        const std::uint64_t pc = subgroups_.at(ids_[k]).param_count;
-        if (grad_sources_[k].empty())
-            cuda_check(launch_count_nonfinite16(grad_ptr_[k], pc, dev_.grad_kind, sg_counts_ + k, s_k_),
-                       "count_nonfinite");
-        else
-            cuda_check(launch_count_nonfinite_sum16(grad_sources_[k].data(), static_cast<int>(grad_sources_[k].size()),
-                                                    pc, dev_.grad_kind, sg_counts_ + k, s_k_),
-                       "count_nonfinite_sum");
-    }
+    count_grads_async();
     cuda_check(cudaMemcpyAsync(verdict_host_, sg_counts_, ids_.size() * sizeof(unsigned long long),
                                cudaMemcpyDeviceToHost, s_k_),
                "cudaMemcpyAsync(verdict)");
@@ -1164,6 +1238,18 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
         a.g = dg;
         a.grad_kind = kF32;
     }
+    std::size_t xb = 0;  // host_grads: the staging buffer of this update
+    if (dev_.host_grads) {
+        // The 16-bit gradient comes over with the state; the working params
+        // go back after the kernel (below), through one staging buffer.
+        xb = aux_next_++ % aux_.size();
+        cuda_check(cudaStreamWaitEvent(s_h2d_, aux_ready_[xb], 0), "wait");
+        cuda_check(cudaMemcpyAsync(aux_[xb], grad_ptr_[k], 2 * pc, cudaMemcpyHostToDevice, s_h2d_),
+                   "cudaMemcpyAsync(grads16)");
+        h2d_bytes += 2 * pc;
+        a.g = aux_[xb];
+        a.p16 = aux_[xb] + ring_stride_;
+    }
     cuda_check(cudaEventRecord(e.h2d_done, s_h2d_), "cudaEventRecord");
 
     cuda_check(cudaStreamWaitEvent(s_k_, e.h2d_done, 0), "wait");
@@ -1195,6 +1281,13 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     }
     cuda_check(launch_adam_fused(a, s_k_), "adam_fused");
     cuda_check(cudaEventRecord(e.k_end, s_k_), "cudaEventRecord");
+    if (dev_.host_grads) {  // working params to their host block; the staging buffer is free after
+        cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
+        cuda_check(cudaMemcpyAsync(p16_ptr_[k], aux_[xb] + ring_stride_, 2 * pc, cudaMemcpyDeviceToHost, s_d2h_),
+                   "cudaMemcpyAsync(params16)");
+        cuda_check(cudaEventRecord(aux_ready_[xb], s_d2h_), "cudaEventRecord");
+        d2h_bytes += 2 * pc;
+    }
 
     if (slot < 0 && held >= 0 && !keep_in_hbm) {  // HBM cache mode: the write-back thread takes it
         {
@@ -1203,7 +1296,7 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
             ++wb_inflight_;
         }
         wb_cv_.notify_all();
-        return {h2d_bytes, 12 * pc};
+        return {h2d_bytes, d2h_bytes + 12 * pc};
     }
     cuda_check(cudaStreamWaitEvent(s_d2h_, e.k_end, 0), "wait");
     cuda_check(cudaEventRecord(e.d2h_start, s_d2h_), "cudaEventRecord");

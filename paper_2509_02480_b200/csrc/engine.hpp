@@ -99,6 +99,11 @@ struct DeviceOptions {
     // pool_slots - 3); all pool slots stream. A retained subgroup the next
     // plan flushes takes a slot for its write-back in plan order.
     int hbm_retain = 1;
+    // Host-resident 16-bit gradients and working params: pinned host blocks
+    // per subgroup streamed with the state (2 B/param more each way through a
+    // small device staging ring) instead of 4 B/param of HBM arenas for the
+    // whole shard, so a rank's shard is bounded by host memory, not HBM.
+    bool host_grads = false;
 };
 
 // HBM cache mode: pinned blocks in the write-back lane.
@@ -363,6 +368,7 @@ private:
     static void CUDART_CB host_done(void* arg);
     std::size_t pick_next_ready(const std::vector<SubgroupId>& order, const std::vector<char>& issued,
                                 std::size_t next);
+    void count_grads_async();
     void launch_grad_check();
     std::int64_t await_grad_verdict();
     void roll_back_fetches();
@@ -449,6 +455,21 @@ private:
     std::uint64_t ring_stride_ = 0;  // floats per segment (P, m, v each) in a ring buffer
     void* grad_arena_ = nullptr;
     void* p16_arena_ = nullptr;
+    // host_grads: per-subgroup pinned 16-bit gradient / working-param blocks,
+    // and a device staging ring (gradient segment + params16 segment per
+    // buffer) each update passes through; a buffer is free again once its
+    // params16 D2H drained (aux_ready_).
+    std::vector<HostBlock> grads_host_;
+    std::vector<HostBlock> p16_host_;
+    std::vector<std::uint16_t*> aux_;
+    std::vector<cudaEvent_t> aux_ready_;
+    std::size_t aux_next_ = 0;
+    // Subgroups whose host gradients were produced by run_backward_sim (and
+    // counted on the device as they were generated): their non-finite counts
+    // need no second pass over PCIe. Cleared when the caller may write them.
+    std::vector<char> grads_verified_;
+    std::vector<unsigned long long> verified_counts_;
+
     cudaStream_t producer_ = cudaStreamLegacy;  // gradients' producer (set_producer_stream)
     cudaEvent_t producer_done_ = nullptr;
     cudaEvent_t verdict_ready_ = nullptr;            // per-subgroup non-finite counts landed in verdict_host_

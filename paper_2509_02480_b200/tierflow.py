@@ -151,6 +151,8 @@ class DeviceOptions:
     # hbm_retain 2: HBM buffers for retained subgroups (0: all of C); fewer
     # gives a two-level cache, the rest retained in host slots
     hbm_cache_slots: int = 0
+    # 16-bit gradients / working params in pinned host memory, streamed with the state
+    host_grads: bool = False
 
 
 @dataclass
@@ -555,7 +557,7 @@ class OffloadWorker:
         o, hy = opt.c(), hyper.c()
         d = _lib.DeviceOptionsC(device.device, device.grad_dtype, device.param_dtype, device.device_buffers,
                                 int(device.zero_copy), device.d2h_split, int(device.hbm_retain),
-                                device.h2d_split, device.hbm_cache_slots)
+                                device.h2d_split, device.hbm_cache_slots, int(device.host_grads))
         _lib.call("tfg_engine_create", worker_id, arr, len(self._tiers), C.byref(o), C.byref(hy),
                   trace.handle if trace else None, C.byref(d), C.byref(h))
         self._h = h

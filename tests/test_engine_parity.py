@@ -19,14 +19,14 @@ pytestmark = pytest.mark.gpu
 
 def make_engine(tf, tiers_cfg, params, *, pool_slots=4, cache_slots=-1, ratio=None, seed=42, lock_dir="",
                 wd=0.0, device_buffers=3, grad_dtype=0, param_dtype=0, deadlock=30.0, pad_ns=0, caching=True,
-                multi_path=True, hbm=1, lock_device=0):
+                multi_path=True, hbm=1, lock_device=0, host_grads=False):
     trace = tf.EventTrace()
     tiers = [tf.Tier(tf.TierSpec(i, *cfg, lock_device=lock_device)) for i, cfg in enumerate(tiers_cfg)]
     opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=lock_dir,
                              deadlock_timeout_s=deadlock, update_pad_ns=pad_ns, enable_caching=caching,
                              multi_path=multi_path)
     w = tf.OffloadWorker(0, tiers, opt, tf.AdamHyper(weight_decay=wd), trace,
-                         tf.DeviceOptions(0, grad_dtype, param_dtype, device_buffers, 0, 1, hbm))
+                         tf.DeviceOptions(0, grad_dtype, param_dtype, device_buffers, 0, 1, hbm, host_grads=host_grads))
     if ratio is not None:
         w.set_fixed_ratio(ratio)
     for i, n in enumerate(params):
@@ -39,7 +39,7 @@ def mem(rate_r, rate_w):
     return (2, "mem", rate_r, rate_w)
 
 
-def run_golden(tf, golden, run, lock_dir, device_buffers=3, hbm=1, host_slots=None):
+def run_golden(tf, golden, run, lock_dir, device_buffers=3, hbm=1, host_slots=None, host_grads=False):
     cfg = golden[f"run_{run}_config"]
     M, nt, pool, cache, seed, iters, accum, skip = (int(x) for x in cfg)
     if hbm == 2:  # HBM cache: the reference's C on HBM, `host_slots` pool slots all streaming
@@ -50,7 +50,8 @@ def run_golden(tf, golden, run, lock_dir, device_buffers=3, hbm=1, host_slots=No
              "skip": [(400e6, 400e6), (200e6, 200e6)], "desk10": [(4000e6, 4000e6), (2000e6, 2000e6)]}[run]
     w, trace, tiers = make_engine(tf, [mem(*r) for r in rates], params, pool_slots=pool, cache_slots=cache,
                                   ratio=golden[f"run_{run}_ratio"].tolist(), seed=seed, lock_dir=lock_dir,
-                                  wd=float(golden[f"run_{run}_wd"][0]), device_buffers=device_buffers, hbm=hbm)
+                                  wd=float(golden[f"run_{run}_wd"][0]), device_buffers=device_buffers, hbm=hbm,
+                                  host_grads=host_grads)
     stats, seqs = [], []
     for it in range(iters):
         w.run_backward_sim(it, tf.SyntheticGradSource(seed), accum)
@@ -99,14 +100,15 @@ def test_sequences_and_state_match_reference_engine(tf, cuda, golden, lock_dir, 
     w.close()
 
 
-@pytest.mark.parametrize("hbm,host_slots", [(1, None), (2, 3)])
-def test_ten_step_contract_on_the_desk_shape(tf, cuda, golden, lock_dir, hbm, host_slots):
+@pytest.mark.parametrize("hbm,host_slots,host_grads", [(1, None, False), (2, 3, False), (2, 3, True)])
+def test_ten_step_contract_on_the_desk_shape(tf, cuda, golden, lock_dir, hbm, host_slots, host_grads):
     """north_star: results after 10 steps. The reference engine on its desk
     shape (configs/desk.json: 24 subgroups x 2,796,202, P % 4 = 2), AdamW
     (wd 0.01), C = 4, 12 iterations with iteration 5 skipped (11 applied):
     every phase's cache hits, per-tier fetch order, flush sets and allocation,
     then the final P/m/v and working params of every subgroup, bit for bit."""
-    w, trace, stats, seqs, params, iters = run_golden(tf, golden, "desk10", lock_dir, hbm=hbm, host_slots=host_slots)
+    w, trace, stats, seqs, params, iters = run_golden(tf, golden, "desk10", lock_dir, hbm=hbm, host_slots=host_slots,
+                                                      host_grads=host_grads)
     want_seqs = [ast.literal_eval(s) for s in golden["run_desk10_seqs"]]
     assert iters == 12 and sum(st is not None for st in stats) == 11
     for it in range(iters):
@@ -123,6 +125,61 @@ def test_ten_step_contract_on_the_desk_shape(tf, cuda, golden, lock_dir, hbm, ho
         got = w.read_current_state(i)
         assert hashlib.sha256(got.tobytes()).hexdigest() == golden["run_desk10_digest"][i], f"subgroup {i}"
         assert np.array_equal(w.read_params16(i), oracle.f32_to_f16(got[:n]))
+    w.close()
+
+
+@pytest.mark.parametrize("run,hbm,host_slots", [("ragged", 1, None), ("skip", 2, 4), ("hits", 2, 3)])
+def test_host_resident_grads_match_reference_engine(tf, cuda, golden, lock_dir, run, hbm, host_slots):
+    """DeviceOptions.host_grads: the 16-bit gradients and working params live
+    in pinned host blocks and stream with the state (no HBM arenas for the
+    shard). Same sequences and bits as the reference; the PCIe byte count
+    carries the 2 B/param each way; the working params read back from host."""
+    w, trace, stats, seqs, params, iters = run_golden(tf, golden, run, lock_dir, hbm=hbm, host_slots=host_slots,
+                                                      host_grads=True)
+    want_seqs = [ast.literal_eval(s) for s in golden[f"run_{run}_seqs"]]
+    S = sum(params)
+    for it in range(iters):
+        assert seqs[it] == want_seqs[it], f"iteration {it}"
+        if stats[it] is None:
+            continue
+        assert stats[it].cache_hits == golden[f"run_{run}_hits"][it]
+        assert stats[it].flush_allocation == golden[f"run_{run}_alloc"][it].tolist()
+        assert stats[it].h2d_bytes >= 2 * S and stats[it].d2h_bytes >= 2 * S
+    for i, n in enumerate(params):
+        got = w.read_current_state(i)
+        if run == "hits":
+            assert hashlib.sha256(got.tobytes()).hexdigest() == golden["run_hits_digest"][i]
+        else:
+            off = sum(3 * m for m in params[:i])
+            assert np.array_equal(got.view(np.uint32), golden[f"run_{run}_states"][off:off + 3 * n].view(np.uint32))
+        assert np.array_equal(w.read_params16(i), oracle.f32_to_f16(got[:n]))
+    w.close()
+
+
+def test_host_resident_grads_reject_a_nonfinite_phase(tf, cuda, lock_dir):
+    """A gradient the caller writes into the host block (grad_buffer returns a
+    pinned host pointer with host_grads): not counted by a producer, so the
+    phase check stages it to the device; a poisoned one rejects the phase."""
+    import ctypes
+    n = 10_000
+    w, trace, _ = make_engine(tf, [mem(800e6, 800e6)], [n] * 3, pool_slots=3, lock_dir=lock_dir, host_grads=True)
+    w.run_backward_sim(0, tf.SyntheticGradSource(29))
+    before = [w.read_current_state(i) for i in range(3)]
+    host = np.ctypeslib.as_array((ctypes.c_uint16 * n).from_address(w.grad_buffer(1)))
+    keep = host[77]
+    host[77] = 0x7C00
+    assert not w.gradients_finite()
+    with pytest.raises(tf.GradientOverflowError):
+        w.run_update(0)
+    for i in range(3):
+        assert np.array_equal(w.read_current_state(i), before[i])
+    host[77] = keep
+    st = w.run_update(1)
+    assert st.cache_hits == 0 and st.params_updated == 3 * n
+    p0 = oracle.synthetic_params(n, 42, 1)
+    want = oracle.adam_fused(p0, np.zeros(n, np.float32), np.zeros(n, np.float32),
+                             oracle.synthetic_grads(n, 29, 1, 0), 0, 0, 2)
+    assert np.array_equal(w.read_current_state(1).view(np.uint32), np.concatenate(want[:3]).view(np.uint32))
     w.close()
 
 
@@ -929,4 +986,40 @@ def test_tiny_ragged_subgroups_and_narrowing_overflow(tf, cuda, lock_dir, tmp_pa
         assert st.downscale_overflows == over and over > 0
     for sg, n in enumerate(params):
         assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate(want[sg]).view(np.uint32)), sg
+    w.close()
+
+
+@pytest.mark.parametrize("fixed", [True, False])
+def test_cache_slots_lowered_to_zero_between_phases(tf, cuda, lock_dir, tmp_path, fixed):
+    """set_cache_slots(0) after HBM-cache phases (the bench's streaming_c0):
+    the retained subgroups are written back in the next phase, after which
+    every phase has no cache hits and nothing stays host-resident; bits stay
+    the oracle's."""
+    params = [60_000 + 8 * i for i in range(14)]
+    seed, C = 19, 6
+    tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
+             tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(tmp_path / "d"), 2e9, 2e9))]
+    w = tf.OffloadWorker(0, tiers, tf.ScheduleOptions(pool_slots=5, cache_slots=C, lock_dir=lock_dir),
+                         tf.AdamHyper(), tf.EventTrace(), tf.DeviceOptions(0, 0, 0, 3, 0, 1, 2))
+    if fixed:
+        w.set_fixed_ratio([3.0, 1.0])
+    for i, n in enumerate(params):
+        w.add_subgroup(i, n)
+    w.init_and_flush_all(seed)
+    hits = []
+    for it in range(8):
+        if it == 3:
+            w.set_cache_slots(0)
+        w.run_backward_sim(it, tf.SyntheticGradSource(seed))
+        st = w.run_update(it)
+        hits.append(st.cache_hits)
+        host, _ = w.residency_census()
+        if it >= 3:
+            assert st.retained == 0 and host == 0, (it, st.retained, host)
+    assert hits[:4] == [0, C, C, C] and hits[4:] == [0, 0, 0, 0], hits
+    for sg, n in enumerate(params):
+        p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
+        for it in range(8):
+            p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
+        assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32)), sg
     w.close()
