@@ -1045,7 +1045,7 @@ def main(argv=None):
     cpu = None
     if rank == 0 and not a.skip_cpu:
         try:
-            r = reference_sample(wl, world, 1, 1, a.tier_root)
+            r = reference_sample(wl, world, 2, 1, a.tier_root)  # 2 timed phases (~11 s of CPU work)
             cpu = {"value": r["value"], "unit": "params/s", "cores": r["cores"], "kind": "reference",
                    "sample": r["sample"], "cpu": cpu_model()}
         except Exception as exc:
