@@ -602,7 +602,7 @@ def pipeline_roofline(phases, pcie, dir_probes):
 
 
 def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, pool_slots, cache_slots, ring,
-            hbm_retain=2, peer=None, remote=False, c0_steps=0):
+            hbm_retain=2, peer=None, remote=False, c0_steps=0, host_grads=False):
     """peer: a parallel.PeerGradients holding every rank's contribution to
     every subgroup: the engine's owned subgroups are bound to the world's
     contributions, so each update reduces them over CUDA IPC / NVLink inside
@@ -630,12 +630,16 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     dram_bw = min(pcie["h2d"], pcie["d2h"])
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", dram_bw, dram_bw))
     trace = tf.EventTrace()
-    opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots, lock_dir=str(root / "locks"))
+    # One lock directory for the node: the ranks' directory tiers on one
+    # physical disk (lock_device 1) share one semaphore, the paper's
+    # node-level contention control, although their paths are per rank.
+    opt = tf.ScheduleOptions(pool_slots=pool_slots, cache_slots=cache_slots,
+                             lock_dir=str(Path(tier_root) / "e2e_locks"))
     t0 = time.time()
 
     def setup():
         w = tf.OffloadWorker(rank, [dram] + dirs, opt, tf.AdamHyper(), trace,
-                             tf.DeviceOptions(dev, DT, DT, ring, 0, 1, hbm_retain))
+                             tf.DeviceOptions(dev, DT, DT, ring, 0, 1, hbm_retain, host_grads=host_grads))
         for k, n in enumerate(sizes):
             w.add_subgroup(base_id + k, n)
         w.init_and_flush_all(seed)
@@ -903,6 +907,8 @@ def main(argv=None):
     ap.add_argument("--skip-spill", action="store_true", help="skip the directory-tier spill sample (SURVEY C4)")
     ap.add_argument("--skip-nccl", action="store_true")
     ap.add_argument("--c0-steps", type=int, default=5, help="timed phases of the C=0 streaming e2e (0: skip)")
+    ap.add_argument("--host-grads", action="store_true",
+                    help="e2e: 16-bit gradients and working params in pinned host memory, streamed with the state")
     a = ap.parse_args(argv)
 
     global DT
@@ -985,7 +991,8 @@ def main(argv=None):
                 cache = int(allmin(world, cache)) if cache >= 0 else cache
                 e_sizes = e_sizes[:n_e]
                 r = e2e_leg(tf, e_sizes, rank * len(sizes), a.steps, a.warmup, a.seed, rank, world, a.tier_root,
-                            pool, cache, a.ring, a.hbm_retain, c0_steps=min(a.c0_steps, a.steps))
+                            pool, cache, a.ring, a.hbm_retain, c0_steps=min(a.c0_steps, a.steps),
+                            host_grads=a.host_grads)
                 e2e = e2e_line(r, world, {"hbm_retain": a.hbm_retain, "pool_slots": pool, "cache_slots": cache,
                                           "ring": a.ring,
                                           "path": "C ABI tfg_engine_run_update, tiers [host_dram pinned, "

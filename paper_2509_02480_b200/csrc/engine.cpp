@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.hpp"
@@ -1065,6 +1067,21 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         stats.cache_hits = cache_hits_this_phase_;
         prefetch_futures_.clear();
         flush_futures_.clear();
+    }
+    if (std::getenv("TFB_DEBUG_RESIDENCY") != nullptr) {  // forensics: host-resident beyond the retained set
+        std::lock_guard<std::mutex> g(mu_);
+        int host = 0;
+        for (const SubgroupId sid : ids_) host += subgroups_.at(sid).residency == Residency::host_cached;
+        if (host != stats.retained) {
+            std::fprintf(stderr, "residency: %d host-resident after the phase, %d retained;", host, stats.retained);
+            for (const SubgroupId sid : ids_) {
+                const Subgroup& sg = subgroups_.at(sid);
+                if (sg.residency == Residency::host_cached && !dests_->assign_storage_tier(sid).host_retain)
+                    std::fprintf(stderr, " %u(slot %d hbm %d wb %d)", sid, sg.slot, hbm_slot_[index_of_.at(sid)],
+                                 static_cast<int>(wb_held_.count(sid)));
+            }
+            std::fprintf(stderr, "\n");
+        }
     }
     stats.wall_seconds = std::chrono::duration<double>(Clock::now() - t0).count();
     if (fixed_ratio_.empty()) {
