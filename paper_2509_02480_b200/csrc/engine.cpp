@@ -957,6 +957,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         cache_hits_this_phase_ = 0;
         phase_stats_ = &stats;
         io_index_.clear();
+        updated_this_phase_.assign(ids_.size(), 0);
         completion_error_ = nullptr;
         order = order_;
         pump_locked();
@@ -1136,6 +1137,7 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
         std::lock_guard<std::mutex> g(mu_);
         if (slot >= 0) pool_->begin_update(slot);
         trace_->record(EventKind::update_start, id_, id, kNoTier, 12 * pc);
+        updated_this_phase_[k] = 1;
         ++in_flight_;
     }
     // slot < 0 only in HBM cache mode, for a subgroup held in HBM: retained
@@ -1555,6 +1557,12 @@ void OffloadWorker::pump_locked() {
             continue;
         }
         if (sg.residency != Residency::on_tier || prefetch_futures_.count(id) != 0) continue;
+        // Already updated this phase and flushed again (a hit the plan does
+        // not retain, issued while the frontier was still behind it): it is
+        // not fetched a second time. The reference's pump would re-fetch it
+        // and hold a slot into the next phase, where it counts as a hit; that
+        // only arises when C shrinks or the hits sit at the end of the order.
+        if (!updated_this_phase_.empty() && updated_this_phase_[index_of_.at(id)]) continue;
         const int slot = pool_->try_reserve(id);
         if (slot < 0) return;  // resumes here when a slot frees
         start_prefetch_locked(id, slot);

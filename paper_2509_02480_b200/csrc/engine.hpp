@@ -399,6 +399,7 @@ private:
     std::vector<std::pair<SubgroupId, std::shared_future<IoStats>>> flush_futures_;
     PhaseStats* phase_stats_ = nullptr;
     std::unordered_map<SubgroupId, std::size_t> io_index_;  // id -> phase_stats_->subgroup_io entry
+    std::vector<char> updated_this_phase_;  // by index: issued in the current phase (the frontier skips it)
     std::uint64_t cache_hits_this_phase_ = 0;
 
     // Device resources.

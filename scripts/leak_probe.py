@@ -24,7 +24,15 @@ with tempfile.TemporaryDirectory() as tmp:
         st = w.run_update(it)
         print("after phase", it, "hits", st.cache_hits, tf.host_blocks_live(), w.residency_census(), flush=True)
     w.close()
-    print("after close", tf.host_blocks_live(), "tier refs", [sys.getrefcount(t) for t in tiers], flush=True)
+    print("after close", tf.host_blocks_live(), "tier refs", [sys.getrefcount(t) for t in tiers],
+          "worker refs", sys.getrefcount(w), flush=True)
+    for r in gc.get_referrers(w):
+        desc = type(r).__name__
+        if hasattr(r, "f_code"):
+            desc += f" {r.f_code.co_name}:{r.f_lineno}"
+        elif isinstance(r, dict):
+            desc += " keys=" + ",".join(list(map(str, r.keys()))[:8])
+        print("  referrer of w:", desc, flush=True)
     del w
     gc.collect()
     print("after del w", tf.host_blocks_live(), "tier refs", [sys.getrefcount(t) for t in tiers], flush=True)

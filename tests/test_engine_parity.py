@@ -991,10 +991,12 @@ def test_tiny_ragged_subgroups_and_narrowing_overflow(tf, cuda, lock_dir, tmp_pa
 
 @pytest.mark.parametrize("fixed", [True, False])
 def test_cache_slots_lowered_to_zero_between_phases(tf, cuda, lock_dir, tmp_path, fixed):
-    """set_cache_slots(0) after HBM-cache phases (the bench's streaming_c0):
-    the retained subgroups are written back in the next phase, after which
-    every phase has no cache hits and nothing stays host-resident; bits stay
-    the oracle's."""
+    """set_cache_slots(0) after HBM-cache phases (the bench's streaming_c0),
+    with the first C = 0 phase running in the same direction as the last
+    retaining one (iteration 3 skipped), so its hits sit at the END of the
+    order and are updated and flushed while the fetch frontier is still behind
+    them: the frontier must not fetch them again (every later phase has no
+    hits and nothing stays host-resident); bits stay the oracle's."""
     params = [60_000 + 8 * i for i in range(14)]
     seed, C = 19, 6
     tiers = [tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 20e9, 20e9)),
@@ -1007,19 +1009,20 @@ def test_cache_slots_lowered_to_zero_between_phases(tf, cuda, lock_dir, tmp_path
         w.add_subgroup(i, n)
     w.init_and_flush_all(seed)
     hits = []
-    for it in range(8):
-        if it == 3:
+    applied = [0, 1, 2, 4, 5, 6, 7, 8]
+    for it in applied:
+        if it == 4:
             w.set_cache_slots(0)
         w.run_backward_sim(it, tf.SyntheticGradSource(seed))
         st = w.run_update(it)
         hits.append(st.cache_hits)
         host, _ = w.residency_census()
-        if it >= 3:
+        if it >= 4:
             assert st.retained == 0 and host == 0, (it, st.retained, host)
     assert hits[:4] == [0, C, C, C] and hits[4:] == [0, 0, 0, 0], hits
     for sg, n in enumerate(params):
         p, m, v = oracle.synthetic_params(n, seed, sg), np.zeros(n, np.float32), np.zeros(n, np.float32)
-        for it in range(8):
+        for it in applied:
             p, m, v, p16, _ = oracle.adam_fused(p, m, v, oracle.synthetic_grads(n, seed, sg, it), 0, 0, it + 1)
         assert np.array_equal(w.read_current_state(sg).view(np.uint32), np.concatenate([p, m, v]).view(np.uint32)), sg
     w.close()
