@@ -419,10 +419,15 @@ class Tier:
         self._h = h
         self._spec = spec
 
-    def __del__(self):
+    def close(self) -> None:
+        """Drops this handle's reference to the native tier (an engine built on
+        it keeps its own); the tier's blobs are freed with the last one."""
         if getattr(self, "_h", None) and _lib is not None:  # not during interpreter teardown
             _lib.load().tfg_tier_destroy(self._h)
             self._h = None
+
+    def __del__(self):
+        self.close()
 
     @property
     def handle(self):

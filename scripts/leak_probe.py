@@ -36,6 +36,9 @@ with tempfile.TemporaryDirectory() as tmp:
     del w
     gc.collect()
     print("after del w", tf.host_blocks_live(), "tier refs", [sys.getrefcount(t) for t in tiers], flush=True)
+    for t in tiers:
+        t.close()
+    print("after tier close", tf.host_blocks_live(), flush=True)
     print("referrers of dram tier:", [type(r).__name__ for r in gc.get_referrers(tiers[0])], flush=True)
     del tiers, trace
     gc.collect()
