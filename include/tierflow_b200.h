@@ -337,11 +337,16 @@ int tfg_engine_bind_grad_buffer(tfg_engine* engine, uint32_t id, void* device_pt
  * gradients and the update. NULL (the default) = the legacy default stream.
  * (No reference counterpart: the reference's gradients are host memory.) */
 int tfg_engine_set_producer_stream(tfg_engine* engine, void* stream);
-/* Fused data-parallel reduction: the update of `id` consumes the fp32 sum (in
- * order, rounded once to grad_kind) of n (1..8) 16-bit device buffers, e.g.
- * every peer's contribution mapped over NVLink (CUDA IPC). Replaces the
+/* Data-parallel reduction in the engine: the update of `id` consumes the fp32
+ * sum (in order, rounded once to grad_kind) of n (1..8) 16-bit device
+ * buffers, e.g. every peer's contribution mapped over NVLink (CUDA IPC). Each
+ * phase's gradient check reads every source once, writes the rounded sum to
+ * the subgroup's own buffer and counts non-finite results (a sum that
+ * overflows rejects the phase before any state moves); the update reads the
+ * reduced buffer: 2(N-1) B/param over NVLink. Replaces the
  * reduce_grads_to_owners step in front of run_update.
- * TFG_ERR_CONFIG in the baseline gradient flow (skip_gradients = 0). */
+ * TFG_ERR_CONFIG in the baseline gradient flow (skip_gradients = 0) and with
+ * host_grads. */
 int tfg_engine_bind_grad_sources(tfg_engine* engine, uint32_t id, const void* const* device_ptrs, int n);
 int tfg_engine_params16_buffer(tfg_engine* engine, uint32_t id, void** device_ptr);         /* shadow_, :861 */
 int tfg_engine_run_update(tfg_engine* engine, int iteration, tfg_phase_stats* stats);      /* :405 */

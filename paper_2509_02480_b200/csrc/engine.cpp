@@ -505,6 +505,7 @@ void OffloadWorker::setup_device() {
     }
     grad_ptr_.clear();
     p16_ptr_.clear();
+    arena_grad_.clear();
     events_.assign(ids_.size(), DeviceEvents{});
     grad_sources_.assign(ids_.size(), {});
     host_resident_ns_.assign(ids_.size(), 0);
@@ -518,6 +519,7 @@ void OffloadWorker::setup_device() {
             grad_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(grad_arena_) + offs[k]));
             p16_ptr_.push_back(reinterpret_cast<std::uint16_t*>(static_cast<char*>(p16_arena_) + offs[k]));
         }
+        arena_grad_.push_back(grad_ptr_.back());
         DeviceEvents& e = events_[k];
         for (cudaEvent_t* ev : {&e.h2d_start, &e.h2d_done, &e.k_start, &e.k_end, &e.d2h_start, &e.d2h_end})
             cuda_check(cudaEventCreate(ev), "cudaEventCreate");
@@ -648,6 +650,7 @@ void OffloadWorker::run_backward_sim(int iteration, std::uint64_t seed, int accu
         // copied to the subgroup's pinned host block: the gradients a
         // ZeRO-Offload backward leaves in host memory.
         cuda_check(cudaMemsetAsync(sg_counts_, 0, ids_.size() * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
+        cuda_check(cudaStreamWaitEvent(s_k_, aux_ready_[0], 0), "wait");  // staging buffer 0 is free
         for (std::size_t k = 0; k < ids_.size(); ++k) {
             const SubgroupId id = ids_[k];
             const std::uint64_t pc = subgroups_.at(id).param_count;
@@ -819,9 +822,14 @@ void OffloadWorker::count_grads_async() {
     for (std::size_t k = 0; k < M; ++k) {
         const std::uint64_t pc = subgroups_.at(ids_[k]).param_count;
         if (!grad_sources_[k].empty()) {
-            cuda_check(launch_count_nonfinite_sum16(grad_sources_[k].data(), static_cast<int>(grad_sources_[k].size()),
-                                                    pc, dev_.grad_kind, sg_counts_ + k, s_k_),
-                       "count_nonfinite_sum");
+            // The contributions are reduced here, once (2(N-1) B/param over
+            // NVLink for N peers), into the subgroup's own gradient buffer,
+            // which the update then reads: the check sees exactly the rounded
+            // sum the update uses, and a sum that overflows the 16-bit range
+            // rejects the phase before any state moves.
+            cuda_check(launch_reduce_sum16(grad_sources_[k].data(), static_cast<int>(grad_sources_[k].size()), pc,
+                                           dev_.grad_kind, arena_grad_[k], sg_counts_ + k, s_k_),
+                       "reduce_sum16");
         } else if (dev_.host_grads) {
             if (grads_verified_[k]) continue;
             cuda_check(cudaMemcpyAsync(aux_[0], grad_ptr_[k], 2 * pc, cudaMemcpyHostToDevice, s_k_),
@@ -1020,6 +1028,10 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             pending = flush_futures_;
         }
         for (auto& [fid, fut] : pending) watchdog_wait_value(fut);
+        // host_grads: the working params' D2H of a subgroup whose state went
+        // back through the write-back lane may still be in flight; the host
+        // blocks are the caller's once run_update returns.
+        if (dev_.host_grads) cuda_check(cudaStreamSynchronize(s_d2h_), "cudaStreamSynchronize");
     } catch (...) {
         std::lock_guard<std::mutex> g(mu_);
         phase_stats_ = nullptr;
@@ -1146,11 +1158,8 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     static HostBlock no_block;
     const HostBlock& blk = slot >= 0 ? pool_->block(slot) : no_block;
     AdamLaunch a;
-    a.g = grad_ptr_[k];
-    if (!grad_sources_[k].empty()) {  // reduce + update in one pass over the peers' contributions
-        for (std::size_t i = 0; i < grad_sources_[k].size(); ++i) a.peers[i] = grad_sources_[k][i];
-        a.n_peers = static_cast<int>(grad_sources_[k].size());
-    }
+    // Bound sources were reduced into the subgroup's own buffer at the phase check.
+    a.g = grad_sources_[k].empty() ? grad_ptr_[k] : arena_grad_[k];
     a.p16 = p16_ptr_[k];
     a.n = pc;
     a.grad_kind = dev_.grad_kind;

@@ -287,8 +287,9 @@ public:
     void* grad_buffer(SubgroupId id);
     void bind_grad_buffer(SubgroupId id, void* device_ptr);
     // Several gradient sources (e.g. every data-parallel peer's contribution,
-    // mapped over NVLink): the update sums them in fp32 in order, rounds once
-    // to the gradient kind, and applies Adam in the same kernel pass.
+    // mapped over NVLink): each phase's gradient check sums them in fp32 in
+    // order, rounds once to the gradient kind into the subgroup's own buffer
+    // (one read of every source), and the update reads that buffer.
     void bind_grad_sources(SubgroupId id, const std::vector<const void*>& sources);
     void* params16_buffer(SubgroupId id);
     // The stream that produces the gradients (the backward / reduce-scatter).
@@ -479,6 +480,7 @@ private:
     unsigned long long* sg_counts_ = nullptr; // per-subgroup non-finite counts (pre-check)
     std::unordered_map<SubgroupId, std::size_t> index_of_;
     std::vector<std::uint16_t*> grad_ptr_;
+    std::vector<std::uint16_t*> arena_grad_;  // the engine's own gradient buffer per subgroup (bound sources reduce here)
     std::vector<std::vector<const void*>> grad_sources_;  // non-empty: fused multi-source reduction
     std::vector<std::uint16_t*> p16_ptr_;
     std::vector<DeviceEvents> events_;

@@ -195,12 +195,55 @@ struct SumSources {
     int n;
 };
 
-// Non-finite count of the reduced gradient the fused multi-source update
-// will see: the fp32 sum of the sources in order, rounded once to K. An
-// overflow created by the sum itself is caught here, before any state moves.
+// The reduction of several 16-bit sources (a data-parallel gradient's
+// contributions, peers' through NVLink-mapped pointers): the fp32 sum in
+// source order, rounded once to K — exactly what the fused multi-source
+// update computes in-kernel — written to dst (may be null: count only) with
+// the non-finite count of the rounded values. Quads of 8-byte loads from every
+// source issued before the sum; NS sources fixed at compile time.
+template <int K, int NS>
+__global__ void __launch_bounds__(kThreads)
+    reduce_sum16_kernel(SumSources s, uint64_t n, uint16_t* __restrict__ dst, unsigned long long* __restrict__ out) {
+    unsigned bad = 0;
+    const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t nq = n / 4;
+    for (uint64_t q = tid; q < nq; q += nthreads) {
+        U16x4 x[NS];
+#pragma unroll
+        for (int k = 0; k < NS; ++k) x[k] = load_u16x4(s.src[k] + 4 * q);
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int k = 0; k < NS; ++k) {
+            acc.x = __fadd_rn(acc.x, widen16<K>(x[k].x));
+            acc.y = __fadd_rn(acc.y, widen16<K>(x[k].y));
+            acc.z = __fadd_rn(acc.z, widen16<K>(x[k].z));
+            acc.w = __fadd_rn(acc.w, widen16<K>(x[k].w));
+        }
+        U16x4 h;
+        h.x = narrow16<K>(acc.x);
+        h.y = narrow16<K>(acc.y);
+        h.z = narrow16<K>(acc.z);
+        h.w = narrow16<K>(acc.w);
+        bad += nonfinite16<K>(h.x) + nonfinite16<K>(h.y) + nonfinite16<K>(h.z) + nonfinite16<K>(h.w);
+        if (dst != nullptr) store_u16x4(dst + 4 * q, h);
+    }
+    for (uint64_t i = nq * 4 + tid; i < n; i += nthreads) {  // n % 4 tail
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < NS; ++k) acc = __fadd_rn(acc, widen16<K>(s.src[k][i]));
+        const uint16_t h = narrow16<K>(acc);
+        bad += nonfinite16<K>(h);
+        if (dst != nullptr) dst[i] = h;
+    }
+    warp_count_add(out, bad);
+}
+
+// Scalar form for sources or destinations not 8-byte aligned.
 template <int K>
 __global__ void __launch_bounds__(kThreads)
-    count_nonfinite_sum_kernel(SumSources s, uint64_t n, unsigned long long* __restrict__ out) {
+    reduce_sum16_scalar_kernel(SumSources s, uint64_t n, uint16_t* __restrict__ dst,
+                               unsigned long long* __restrict__ out) {
     unsigned bad = 0;
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
@@ -209,25 +252,61 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
         for (int k = 0; k < kMaxGradSources; ++k)
             if (k < s.n) acc = __fadd_rn(acc, widen16<K>(__ldcs(s.src[k] + i)));
-        bad += nonfinite16<K>(narrow16<K>(acc));
+        const uint16_t h = narrow16<K>(acc);
+        bad += nonfinite16<K>(h);
+        if (dst != nullptr) dst[i] = h;
     }
     warp_count_add(out, bad);
 }
 
+template <int K, int NS>
+void launch_reduce_ns(const SumSources& s, uint64_t n, uint16_t* dst, unsigned long long* out, cudaStream_t st) {
+    reduce_sum16_kernel<K, NS><<<grid_for((n + 3) / 4, 8), kThreads, 0, st>>>(s, n, dst, out);
+}
+
+template <int K>
+void launch_reduce(const SumSources& s, uint64_t n, uint16_t* dst, unsigned long long* out, cudaStream_t st,
+                   bool vec) {
+    if (!vec) {
+        reduce_sum16_scalar_kernel<K><<<grid_for(n, 8), kThreads, 0, st>>>(s, n, dst, out);
+        return;
+    }
+    switch (s.n) {
+        case 1: return launch_reduce_ns<K, 1>(s, n, dst, out, st);
+        case 2: return launch_reduce_ns<K, 2>(s, n, dst, out, st);
+        case 3: return launch_reduce_ns<K, 3>(s, n, dst, out, st);
+        case 4: return launch_reduce_ns<K, 4>(s, n, dst, out, st);
+        case 5: return launch_reduce_ns<K, 5>(s, n, dst, out, st);
+        case 6: return launch_reduce_ns<K, 6>(s, n, dst, out, st);
+        case 7: return launch_reduce_ns<K, 7>(s, n, dst, out, st);
+        default: return launch_reduce_ns<K, 8>(s, n, dst, out, st);
+    }
+}
+
 }  // namespace
 
-cudaError_t launch_count_nonfinite_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind,
-                                         unsigned long long* out, cudaStream_t stream) {
+cudaError_t launch_reduce_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind, uint16_t* dst,
+                                unsigned long long* out, cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     if (nsrc < 1 || nsrc > kMaxGradSources) return cudaErrorInvalidValue;
     SumSources s{};
-    for (int k = 0; k < nsrc; ++k) s.src[k] = static_cast<const uint16_t*>(srcs[k]);
+    uintptr_t align = reinterpret_cast<uintptr_t>(dst);
+    for (int k = 0; k < nsrc; ++k) {
+        s.src[k] = static_cast<const uint16_t*>(srcs[k]);
+        align |= reinterpret_cast<uintptr_t>(srcs[k]);
+    }
     s.n = nsrc;
+    const bool vec = (align & 7u) == 0;
     if (kind == kF16)
-        count_nonfinite_sum_kernel<kF16><<<grid_for(n, 8), kThreads, 0, stream>>>(s, n, out);
+        launch_reduce<kF16>(s, n, dst, out, stream, vec);
     else
-        count_nonfinite_sum_kernel<kBF16><<<grid_for(n, 8), kThreads, 0, stream>>>(s, n, out);
+        launch_reduce<kBF16>(s, n, dst, out, stream, vec);
     return cudaGetLastError();
+}
+
+cudaError_t launch_count_nonfinite_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind,
+                                         unsigned long long* out, cudaStream_t stream) {
+    return launch_reduce_sum16(srcs, nsrc, n, kind, nullptr, out, stream);
 }
 
 }  // namespace tfb

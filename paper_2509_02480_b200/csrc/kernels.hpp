@@ -67,6 +67,11 @@ cudaError_t launch_count_nonfinite16(const uint16_t* src, uint64_t n, int kind,
                                      unsigned long long* out, cudaStream_t stream);
 // Non-finite count of the fp32 sum (in order, rounded once to kind) of nsrc
 // 16-bit sources: the pre-check of the fused multi-source update.
+// The fp32 sum (in order, rounded once to kind) of nsrc 16-bit sources into
+// dst (null: count only), *out += non-finite results: the engine's reduction
+// of bound gradient sources at the phase check.
+cudaError_t launch_reduce_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind, uint16_t* dst,
+                                unsigned long long* out, cudaStream_t stream);
 cudaError_t launch_count_nonfinite_sum16(const void* const* srcs, int nsrc, uint64_t n, int kind,
                                          unsigned long long* out, cudaStream_t stream);
 
