@@ -291,6 +291,8 @@ int tfg_trace_destroy(tfg_trace* trace);
 int tfg_trace_size(tfg_trace* trace, uint64_t* size_out);
 int tfg_trace_copy(tfg_trace* trace, uint64_t begin, tfg_event* out, uint64_t max_n, uint64_t* n_out);
 int tfg_trace_record(tfg_trace* trace, int kind, int worker, int64_t subgroup, int tier, uint64_t bytes);
+int tfg_trace_record_at(tfg_trace* trace, int64_t timestamp_ns, int kind, int worker, int64_t subgroup, int tier,
+                        uint64_t bytes);                      /* EventTrace::append, trace.hpp:79 */
 int tfg_trace_write(tfg_trace* trace, const char* path);     /* .jsonl or CSV, trace.hpp:119-134 */
 int tfg_trace_clear(tfg_trace* trace);
 
@@ -312,6 +314,30 @@ int tfg_tier_probe(tfg_tier* tier, uint64_t probe_bytes, int repetitions, double
 int tfg_tier_available_bytes(tfg_tier* tier, uint64_t* out);                                 /* tier.hpp:244 */
 
 /* TierLockGuard, tier_lock.hpp:36-106: acquire returns an opaque token. */
+/* TokenBucket (token_bucket.hpp:23-70): byte-rate pacing, served by the
+   library's device pacer (a virtual-clock schedule with the bucket's 1 ms
+   burst). TFG_CONFIG_ERROR for a rate <= 0. */
+typedef struct tfg_pacer tfg_pacer;
+int tfg_pacer_create(double bytes_per_second, tfg_pacer** out);
+int tfg_pacer_destroy(tfg_pacer* pacer);
+int tfg_pacer_set_rate(tfg_pacer* pacer, double bytes_per_second);
+int tfg_pacer_rate(tfg_pacer* pacer, double* out);
+int tfg_pacer_acquire(tfg_pacer* pacer, double bytes);          /* blocks until the bytes are due */
+/* v1 subgroup file header (tier.hpp:92-134): encode the 32 bytes from the
+   fields, decode them back, validate against an expected id and size
+   (TFG_FORMAT_ERROR with the reference's messages). */
+typedef struct tfg_file_header {
+    uint32_t magic;
+    uint16_t version;
+    uint16_t element_kind;
+    uint32_t subgroup_id;
+    uint64_t param_count;
+} tfg_file_header;
+int tfg_file_header_encode(const tfg_file_header* h, uint8_t out[32]);
+int tfg_file_header_decode(const uint8_t in[32], tfg_file_header* out);
+int tfg_file_header_validate(const tfg_file_header* h, uint32_t expected_id, uint64_t expected_params);
+/* subgroup_file_name (tier.hpp:136-140) into out (>= 32 bytes). */
+int tfg_subgroup_file_name(uint32_t id, char* out, uint64_t out_len);
 int tfg_tier_lock_acquire(const char* lock_dir, int tier, int worker, tfg_trace* trace, int width, void** token);
 int tfg_tier_lock_release(void* token);
 
@@ -375,6 +401,10 @@ int tfg_engine_pool_state(tfg_engine* engine, int slot, int* state_out, uint32_t
 int tfg_now_ns(int64_t* out);                                                                /* common.hpp:21-26 */
 int tfg_upscale16_host(const uint16_t* src, float* dst, uint64_t n, int dtype, int* all_finite); /* precision.hpp:17 */
 int tfg_downscale16_host(const float* src, uint16_t* dst, uint64_t n, int dtype, uint64_t* overflows); /* precision.hpp:29 */
+/* GradBufferF16::accumulate (precision.hpp:66-75) on host arrays: acc[i] =
+   narrow(widen(acc[i]) + widen(grads[i])) in fp32, staged through HBM (the
+   reduce kernel with two sources). */
+int tfg_accumulate16_host(uint16_t* acc, const uint16_t* grads, uint64_t n, int dtype);
 /* adam_step(StateView, span<const float> g, hyper, t), optimizer.hpp:116-157: TFG_ERROR for t < 1,
  * TFG_CONFIG_ERROR for bad hyperparameters, TFG_GRADIENT_OVERFLOW (arrays untouched) on a
  * non-finite gradient. */

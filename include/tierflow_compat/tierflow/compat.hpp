@@ -23,16 +23,20 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cstdint>
 #include <filesystem>
 #include <future>
+#include <istream>
 #include <map>
 #include <memory>
 #include <optional>
 #include <span>
+#include <sstream>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -134,21 +138,41 @@ inline bool all_finite(std::span<const f16> values) {
     return std::all_of(values.begin(), values.end(), [](f16 v) { return f16_is_finite(v); });
 }
 
-// Host view of a subgroup's 16-bit gradient (the engine keeps it in HBM).
+// Host 16-bit gradient buffer (precision.hpp:44-82). Standalone it is the
+// reference's accumulation buffer, the fp32 add-and-round done by the
+// library's reduce kernel; OffloadWorker::grad_buffer returns one as a host
+// snapshot of the engine's HBM gradient.
 class GradBufferF16 {
 public:
     GradBufferF16() = default;
     GradBufferF16(SubgroupId id, std::size_t length) : id_(id), values_(length) {}
     SubgroupId id() const { return id_; }
     std::size_t size() const { return values_.size(); }
+    int accumulation_steps() const { return steps_; }
     std::span<const f16> values() const { return values_; }
     std::span<f16> mutable_values() { return values_; }
     bool finite() const { return all_finite(values_); }
+
+    void reset() {
+        std::fill(values_.begin(), values_.end(), f16{});
+        steps_ = 0;
+    }
+    void accumulate(std::span<const f16> grads) {
+        if (grads.size() != values_.size()) throw Error("grad accumulate: length mismatch");
+        if (steps_ == 0)
+            std::copy(grads.begin(), grads.end(), values_.begin());
+        else
+            detail::check(tfg_accumulate16_host(reinterpret_cast<std::uint16_t*>(values_.data()),
+                                                reinterpret_cast<const std::uint16_t*>(grads.data()), values_.size(),
+                                                TFG_F16));
+        ++steps_;
+    }
 
 private:
     friend class OffloadWorker;
     SubgroupId id_ = 0;
     std::vector<f16> values_;
+    int steps_ = 0;
 };
 
 // --- optimizer.hpp ----------------------------------------------------------------
@@ -247,6 +271,89 @@ struct TierObservation {
     double write_seconds = 0.0;
 };
 
+// Per-tier bandwidth EMA (placement.hpp:102-162); init validates alpha and
+// update_bandwidth_estimates runs in the library.
+struct BandwidthEstimate {
+    struct PerTier {
+        double read_bw = 0.0;
+        double write_bw = 0.0;
+        std::uint64_t sample_count = 0;
+    };
+    std::vector<PerTier> tiers;
+    double alpha = 0.5;
+
+    static BandwidthEstimate init(std::span<const double> read_bw, std::span<const double> write_bw, double alpha) {
+        detail::check(tfg_update_bandwidth_estimates(nullptr, nullptr, nullptr, 0, alpha, nullptr, 0));
+        if (read_bw.size() != write_bw.size()) throw ConfigError("bandwidth estimate: tier count mismatch");
+        BandwidthEstimate est;
+        est.alpha = alpha;
+        for (std::size_t i = 0; i < read_bw.size(); ++i) est.tiers.push_back(PerTier{read_bw[i], write_bw[i], 0});
+        return est;
+    }
+    double effective(std::size_t i) const { return std::min(tiers.at(i).read_bw, tiers.at(i).write_bw); }
+    std::vector<double> effective_all() const {
+        std::vector<double> out;
+        for (std::size_t i = 0; i < tiers.size(); ++i) out.push_back(effective(i));
+        return out;
+    }
+};
+
+inline void update_bandwidth_estimates(BandwidthEstimate& est, std::span<const TierObservation> observed) {
+    const std::size_t n = est.tiers.size();
+    std::vector<double> r(n), w(n);
+    std::vector<std::uint64_t> c(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        r[i] = est.tiers[i].read_bw;
+        w[i] = est.tiers[i].write_bw;
+        c[i] = est.tiers[i].sample_count;
+    }
+    std::vector<tfg_tier_observation> obs;
+    for (const TierObservation& o : observed)
+        obs.push_back(tfg_tier_observation{o.read_transfers, o.read_bytes, o.read_seconds, o.write_transfers,
+                                           o.write_bytes, o.write_seconds});
+    detail::check(tfg_update_bandwidth_estimates(r.data(), w.data(), c.data(), static_cast<int>(n), est.alpha,
+                                                 obs.data(), static_cast<int>(obs.size())));
+    for (std::size_t i = 0; i < n; ++i) est.tiers[i] = BandwidthEstimate::PerTier{r[i], w[i], c[i]};
+}
+
+struct CachePlan {
+    int capacity = 0;
+};
+
+struct TierAssignment {
+    bool host_retain = false;
+    TierId tier = kNoTier;
+};
+
+// Flush destinations of one phase (placement.hpp:173-225), computed by the
+// library (the engine's own plan).
+class DestinationPlan {
+public:
+    DestinationPlan(std::span<const SubgroupId> order, CachePlan cache, std::span<const double> bandwidths) {
+        const int M = static_cast<int>(order.size());
+        const int T = static_cast<int>(bandwidths.size());
+        std::vector<int> retain(order.size()), tier(order.size());
+        alloc_.counts.assign(bandwidths.size(), 0);
+        detail::check(tfg_destination_plan(order.data(), M, cache.capacity, bandwidths.data(), T, retain.data(),
+                                           tier.data(), alloc_.counts.data()));
+        retained_ = std::clamp(cache.capacity, 0, M);
+        alloc_.total = M - retained_;
+        for (std::size_t k = 0; k < order.size(); ++k) map_[order[k]] = TierAssignment{retain[k] != 0, tier[k]};
+    }
+    TierAssignment assign_storage_tier(SubgroupId sg) const {
+        const auto it = map_.find(sg);
+        if (it == map_.end()) throw Error("destination plan: unknown subgroup " + std::to_string(sg));
+        return it->second;
+    }
+    const AllocationVector& flush_allocation() const { return alloc_; }
+    int retained_count() const { return retained_; }
+
+private:
+    std::map<SubgroupId, TierAssignment> map_;
+    AllocationVector alloc_;
+    int retained_ = 0;
+};
+
 // --- trace.hpp ----------------------------------------------------------------------
 
 enum class EventKind : int {
@@ -264,6 +371,26 @@ enum class EventKind : int {
     grad_upscale_end,
     cache_hit,
 };
+
+// Kind names of the trace schema (trace.hpp:31-62); the library writes the
+// same names (tfg_trace_write).
+inline const char* event_kind_name(EventKind k) {
+    static constexpr const char* names[] = {"prefetch_start", "prefetch_end", "update_start", "update_end",
+                                            "flush_start",    "flush_end",    "lock_acquire", "lock_release",
+                                            "h2d_start",      "h2d_end",      "grad_upscale_start",
+                                            "grad_upscale_end", "cache_hit"};
+    const int i = static_cast<int>(k);
+    return i >= 0 && i <= static_cast<int>(EventKind::cache_hit) ? names[i] : "unknown";
+}
+
+inline bool event_kind_from_name(std::string_view name, EventKind& out) {
+    for (int i = 0; i <= static_cast<int>(EventKind::cache_hit); ++i)
+        if (name == event_kind_name(static_cast<EventKind>(i))) {
+            out = static_cast<EventKind>(i);
+            return true;
+        }
+    return false;
+}
 
 struct Event {
     std::int64_t timestamp_ns = 0;
@@ -304,8 +431,54 @@ public:
         return out;
     }
     std::vector<Event> snapshot() const { return snapshot_from(0); }
+    void append(Event e) {
+        detail::check(tfg_trace_record_at(h_, e.timestamp_ns, static_cast<int>(e.kind), e.worker_id, e.subgroup_id,
+                                          e.tier_id, e.bytes));
+    }
+    std::uint64_t progress_count() const { return size(); }
+    void clear() { detail::check(tfg_trace_clear(h_)); }
     void write_csv(const std::filesystem::path& p) const { detail::check(tfg_trace_write(h_, p.c_str())); }
     tfg_trace* handle() const { return h_; }
+
+    // The trace file schema (trace.hpp:116-161): CSV with this header, or
+    // one JSON object per line.
+    static constexpr const char* kCsvHeader = "timestamp_ns,worker_id,kind,subgroup_id,tier_id,bytes";
+
+    static void write_csv(std::ostream& os, const std::vector<Event>& events) {
+        os << kCsvHeader << '\n';
+        for (const Event& e : events)
+            os << e.timestamp_ns << ',' << e.worker_id << ',' << event_kind_name(e.kind) << ',' << e.subgroup_id
+               << ',' << e.tier_id << ',' << e.bytes << '\n';
+    }
+    static void write_jsonl(std::ostream& os, const std::vector<Event>& events) {
+        for (const Event& e : events)
+            os << "{\"timestamp_ns\":" << e.timestamp_ns << ",\"worker_id\":" << e.worker_id << ",\"kind\":\""
+               << event_kind_name(e.kind) << "\",\"subgroup_id\":" << e.subgroup_id << ",\"tier_id\":" << e.tier_id
+               << ",\"bytes\":" << e.bytes << "}\n";
+    }
+    static std::vector<Event> read_csv(std::istream& is) {
+        std::vector<Event> out;
+        std::string line;
+        for (bool first = true; std::getline(is, line);) {
+            if (line.empty()) continue;
+            const bool header = first && line.rfind("timestamp_ns", 0) == 0;
+            first = false;
+            if (header) continue;
+            std::vector<std::string> f;
+            std::stringstream ss(line);
+            for (std::string x; std::getline(ss, x, ',');) f.push_back(x);
+            if (f.size() != 6) throw FormatError("trace line has " + std::to_string(f.size()) + " fields: " + line);
+            Event e;
+            e.timestamp_ns = std::stoll(f[0]);
+            e.worker_id = std::stoi(f[1]);
+            if (!event_kind_from_name(f[2], e.kind)) throw FormatError("unknown trace event kind: " + f[2]);
+            e.subgroup_id = std::stoll(f[3]);
+            e.tier_id = std::stoi(f[4]);
+            e.bytes = std::stoull(f[5]);
+            out.push_back(e);
+        }
+        return out;
+    }
 
 private:
     tfg_trace* h_ = nullptr;
@@ -316,6 +489,52 @@ private:
 // host_dram is the B200 engine's pinned-host tier (no reference counterpart).
 enum class TierKind { local_dir = TFG_LOCAL_DIR, remote_dir = TFG_REMOTE_DIR, mem_throttled = TFG_MEM_THROTTLED,
                       host_dram = TFG_HOST_DRAM };
+
+// v1 subgroup file header (tier.hpp:92-134), encoded and checked by the
+// library's tier code.
+struct SubgroupFileHeader {
+    static constexpr std::uint32_t kMagic = 0x4D4C504F;
+    static constexpr std::uint16_t kVersion = 1;
+    static constexpr std::uint16_t kElementF32 = 0;
+    static constexpr std::size_t kSize = 32;
+
+    std::uint32_t magic = kMagic;
+    std::uint16_t version = kVersion;
+    std::uint16_t element_kind = kElementF32;
+    std::uint32_t subgroup_id = 0;
+    std::uint64_t param_count = 0;
+
+    std::array<std::uint8_t, kSize> encode() const {
+        std::array<std::uint8_t, kSize> buf{};
+        const tfg_file_header h = c();
+        detail::check(tfg_file_header_encode(&h, buf.data()));
+        return buf;
+    }
+    static SubgroupFileHeader decode(const std::uint8_t* buf) {
+        tfg_file_header h{};
+        detail::check(tfg_file_header_decode(buf, &h));
+        SubgroupFileHeader out;
+        out.magic = h.magic;
+        out.version = h.version;
+        out.element_kind = h.element_kind;
+        out.subgroup_id = h.subgroup_id;
+        out.param_count = h.param_count;
+        return out;
+    }
+    void validate(std::uint32_t expected_id, std::uint64_t expected_params) const {
+        const tfg_file_header h = c();
+        detail::check(tfg_file_header_validate(&h, expected_id, expected_params));
+    }
+
+private:
+    tfg_file_header c() const { return tfg_file_header{magic, version, element_kind, subgroup_id, param_count}; }
+};
+
+inline std::string subgroup_file_name(SubgroupId id) {
+    char buf[64];
+    detail::check(tfg_subgroup_file_name(id, buf, sizeof(buf)));
+    return buf;
+}
 
 struct TierSpec {
     TierId tier_id = 0;
@@ -592,7 +811,9 @@ public:
     void add_subgroup(SubgroupId id, std::uint64_t param_count) {
         detail::check(tfg_engine_add_subgroup(h_, id, param_count));
         params_[id] = param_count;
+        ids_.push_back(id);
     }
+    const std::vector<SubgroupId>& subgroup_ids() const { return ids_; }
     void init_and_flush_all(std::uint64_t seed) { detail::check(tfg_engine_init_and_flush_all(h_, seed)); }
     void run_backward_sim(int iteration, const SyntheticGradSource& src, int accum_steps) {
         detail::check(tfg_engine_run_backward_sim(h_, iteration, src.seed, accum_steps));
@@ -695,6 +916,7 @@ private:
     ScheduleOptions opt_;
     tfg_engine* h_ = nullptr;
     std::map<SubgroupId, std::uint64_t> params_;
+    std::vector<SubgroupId> ids_;
     std::map<SubgroupId, GradBufferF16> grads_;
 };
 

@@ -156,6 +156,7 @@ _SIGS = {
     "tfg_trace_size": (_i, [_vp, C.POINTER(_u64)]),
     "tfg_trace_copy": (_i, [_vp, _u64, C.POINTER(EventC), _u64, C.POINTER(_u64)]),
     "tfg_trace_record": (_i, [_vp, _i, _i, C.c_int64, _i, _u64]),
+    "tfg_trace_record_at": (_i, [_vp, C.c_int64, _i, _i, C.c_int64, _i, _u64]),
     "tfg_trace_write": (_i, [_vp, C.c_char_p]),
     "tfg_trace_clear": (_i, [_vp]),
     "tfg_tier_create": (_i, [C.POINTER(TierSpecC), C.POINTER(_vp)]),
@@ -170,6 +171,15 @@ _SIGS = {
     "tfg_tier_remove_subgroup": (_i, [_vp, C.c_uint32]),
     "tfg_tier_probe": (_i, [_vp, _u64, _i, C.POINTER(_d), C.POINTER(_d), C.POINTER(_i)]),
     "tfg_tier_available_bytes": (_i, [_vp, C.POINTER(_u64)]),
+    "tfg_pacer_create": (_i, [C.c_double, C.POINTER(_vp)]),
+    "tfg_pacer_destroy": (_i, [_vp]),
+    "tfg_pacer_set_rate": (_i, [_vp, C.c_double]),
+    "tfg_pacer_rate": (_i, [_vp, C.POINTER(C.c_double)]),
+    "tfg_pacer_acquire": (_i, [_vp, C.c_double]),
+    "tfg_file_header_encode": (_i, [_vp, _vp]),
+    "tfg_file_header_decode": (_i, [_vp, _vp]),
+    "tfg_file_header_validate": (_i, [_vp, C.c_uint32, _u64]),
+    "tfg_subgroup_file_name": (_i, [C.c_uint32, C.c_char_p, _u64]),
     "tfg_tier_lock_acquire": (_i, [C.c_char_p, _i, _i, _vp, _i, C.POINTER(_vp)]),
     "tfg_tier_lock_release": (_i, [_vp]),
     "tfg_engine_create": (_i, [_i, C.POINTER(_vp), _i, C.POINTER(ScheduleOptionsC), C.POINTER(AdamHyperC), _vp,
@@ -200,6 +210,7 @@ _SIGS = {
     "tfg_now_ns": (_i, [C.POINTER(C.c_int64)]),
     "tfg_upscale16_host": (_i, [_vp, _vp, _u64, _i, C.POINTER(_i)]),
     "tfg_downscale16_host": (_i, [_vp, _vp, _u64, _i, C.POINTER(_u64)]),
+    "tfg_accumulate16_host": (_i, [_vp, _vp, _u64, _i]),
     "tfg_adam_step_host": (_i, [_vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64]),
     "tfg_pool_create": (_i, [_i, _u64, C.POINTER(_vp)]),
     "tfg_pool_destroy": (_i, [_vp]),

@@ -39,7 +39,7 @@ struct GradSources {
 // In-order fp32 sum of one quad over the sources, rounded once to GK.
 template <int GK, int NS>
 __device__ __forceinline__ U16x4 sum_quad16(const GradSources& gs, uint64_t q) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 acc = make_float4(-0.f, -0.f, -0.f, -0.f);  // -0 + x == x for every x: the sum starts at source 0
     auto add = [&](const U16x4& x) {
         acc.x = __fadd_rn(acc.x, widen16<GK>(x.x));
         acc.y = __fadd_rn(acc.y, widen16<GK>(x.y));
@@ -105,7 +105,7 @@ __device__ __forceinline__ float load_grad1(const GradSources& gs, uint64_t i, u
         if constexpr (GMODE == 0) {
             h = __ldcs(reinterpret_cast<const uint16_t*>(gs.src[0]) + i);
         } else {
-            float acc = 0.f;
+            float acc = -0.f;
 #pragma unroll
             for (int s = 0; s < kMaxGradSources; ++s)
                 if (s < gs.n) acc = __fadd_rn(acc, widen16<GK>(__ldcs(reinterpret_cast<const uint16_t*>(gs.src[s]) + i)));

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -13,6 +14,7 @@
 #include <string>
 
 #include "capi_internal.hpp"
+#include "pacer.hpp"
 #include "engine.hpp"
 #include "kernels.hpp"
 #include "placement.hpp"
@@ -461,6 +463,102 @@ int tfg_trace_record(tfg_trace* trace, int kind, int worker, int64_t subgroup, i
     return guarded([&] {
         need(trace, "trace");
         trace->t->record(static_cast<tfb::EventKind>(kind), worker, subgroup, tier, bytes);
+    });
+}
+
+struct tfg_pacer {
+    tfb::DevicePacer pacer{1.0};  // books device-seconds: bytes / rate
+    std::atomic<double> rate{0.0};
+};
+
+int tfg_pacer_create(double bytes_per_second, tfg_pacer** out) {
+    return guarded([&] {
+        need(out, "out");
+        if (!(bytes_per_second > 0.0)) throw tfb::ConfigError("token bucket rate must be > 0");
+        auto p = std::make_unique<tfg_pacer>();
+        p->rate = bytes_per_second;
+        *out = p.release();
+    });
+}
+
+int tfg_pacer_destroy(tfg_pacer* pacer) {
+    delete pacer;
+    return TFG_OK;
+}
+
+int tfg_pacer_set_rate(tfg_pacer* pacer, double bytes_per_second) {
+    return guarded([&] {
+        need(pacer, "pacer");
+        if (!(bytes_per_second > 0.0)) throw tfb::ConfigError("token bucket rate must be > 0");
+        pacer->rate = bytes_per_second;
+    });
+}
+
+int tfg_pacer_rate(tfg_pacer* pacer, double* out) {
+    return guarded([&] {
+        need(pacer, "pacer");
+        need(out, "out");
+        *out = pacer->rate.load();
+    });
+}
+
+int tfg_pacer_acquire(tfg_pacer* pacer, double bytes) {
+    return guarded([&] {
+        need(pacer, "pacer");
+        pacer->pacer.book(bytes / pacer->rate.load());
+    });
+}
+
+int tfg_file_header_encode(const tfg_file_header* h, uint8_t out[32]) {
+    return guarded([&] {
+        need(h, "header");
+        need(out, "out");
+        tfb::SubgroupFileHeader f;
+        f.magic = h->magic;
+        f.version = h->version;
+        f.element_kind = h->element_kind;
+        f.subgroup_id = h->subgroup_id;
+        f.param_count = h->param_count;
+        f.encode(out);
+    });
+}
+
+int tfg_file_header_decode(const uint8_t in[32], tfg_file_header* out) {
+    return guarded([&] {
+        need(in, "in");
+        need(out, "out");
+        const auto f = tfb::SubgroupFileHeader::decode(in);
+        *out = tfg_file_header{f.magic, f.version, f.element_kind, f.subgroup_id, f.param_count};
+    });
+}
+
+int tfg_file_header_validate(const tfg_file_header* h, uint32_t expected_id, uint64_t expected_params) {
+    return guarded([&] {
+        need(h, "header");
+        tfb::SubgroupFileHeader f;
+        f.magic = h->magic;
+        f.version = h->version;
+        f.element_kind = h->element_kind;
+        f.subgroup_id = h->subgroup_id;
+        f.param_count = h->param_count;
+        f.validate(expected_id, expected_params);
+    });
+}
+
+int tfg_subgroup_file_name(uint32_t id, char* out, uint64_t out_len) {
+    return guarded([&] {
+        need(out, "out");
+        const std::string name = tfb::subgroup_file_name(id);
+        if (out_len < name.size() + 1) throw tfb::ConfigError("subgroup_file_name: buffer too small");
+        std::memcpy(out, name.c_str(), name.size() + 1);
+    });
+}
+
+int tfg_trace_record_at(tfg_trace* trace, int64_t timestamp_ns, int kind, int worker, int64_t subgroup, int tier,
+                        uint64_t bytes) {
+    return guarded([&] {
+        need(trace, "trace");
+        trace->t->append(tfb::Event{timestamp_ns, worker, kind, subgroup, tier, 0, bytes});
     });
 }
 

@@ -117,6 +117,22 @@ int tfg_downscale16_host(const float* src, uint16_t* dst, uint64_t n, int dtype,
     });
 }
 
+int tfg_accumulate16_host(uint16_t* acc, const uint16_t* grads, uint64_t n, int dtype) {
+    return guard([&] {
+        if (dtype != TFG_F16 && dtype != TFG_BF16) throw tfb::ConfigError("unknown 16-bit dtype");
+        if (n == 0) return;
+        need(acc, "acc");
+        need(grads, "grads");
+        DevBuf da(2 * n), dg(2 * n), dout(2 * n);
+        h2d(da.p, acc, 2 * n);
+        h2d(dg.p, grads, 2 * n);
+        const void* srcs[2] = {da.p, dg.p};
+        tfb::cuda_check(tfb::launch_reduce_sum16(srcs, 2, n, dtype, dout.as<uint16_t>(), nullptr, nullptr),
+                        "accumulate16");
+        d2h(acc, dout.p, 2 * n);
+    });
+}
+
 int tfg_adam_step_host(float* p, float* m, float* v, const float* g, uint64_t n, const tfg_adam_hyper* hyper,
                        uint64_t t) {
     return guard([&] {

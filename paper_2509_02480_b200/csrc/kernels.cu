@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads)
         U16x4 x[NS];
 #pragma unroll
         for (int k = 0; k < NS; ++k) x[k] = load_u16x4(s.src[k] + 4 * q);
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 acc = make_float4(-0.f, -0.f, -0.f, -0.f);  // -0 + x == x for every x: the sum starts at source 0
 #pragma unroll
         for (int k = 0; k < NS; ++k) {
             acc.x = __fadd_rn(acc.x, widen16<K>(x[k].x));
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kThreads)
         if (dst != nullptr) store_u16x4(dst + 4 * q, h);
     }
     for (uint64_t i = nq * 4 + tid; i < n; i += nthreads) {  // n % 4 tail
-        float acc = 0.f;
+        float acc = -0.f;
 #pragma unroll
         for (int k = 0; k < NS; ++k) acc = __fadd_rn(acc, widen16<K>(s.src[k][i]));
         const uint16_t h = narrow16<K>(acc);
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kThreads)
     const uint64_t tid = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const uint64_t nthreads = static_cast<uint64_t>(gridDim.x) * blockDim.x;
     for (uint64_t i = tid; i < n; i += nthreads) {
-        float acc = 0.f;
+        float acc = -0.f;
 #pragma unroll
         for (int k = 0; k < kMaxGradSources; ++k)
             if (k < s.n) acc = __fadd_rn(acc, widen16<K>(__ldcs(s.src[k] + i)));

@@ -286,7 +286,9 @@ def test_fused_reduce_update_matches_oracle(tf, cuda, nsrc, kind):
     n = 300_001
     rng = np.random.default_rng(nsrc * 10 + kind)
     srcs = [oracle.synthetic_grads(n, 77, s, 2, kind=kind) for s in range(nsrc)]
-    acc = np.zeros(n, np.float32)
+    for s in srcs:  # negative zeros in every source sum to -0 (the sum starts at source 0)
+        s[:64] = 0x8000
+    acc = np.full(n, -0.0, np.float32)
     for s in srcs:
         acc = (acc + oracle.widen16(s, kind)).astype(np.float32)
     g16, _ = oracle.narrow16(acc, kind)

@@ -33,7 +33,7 @@ def _expected(sizes, world, iters, kind=0, wd=0.0):
         v = np.zeros(n, np.float32)
         p16 = None
         for it in range(iters):
-            acc = np.zeros(n, np.float32)
+            acc = np.full(n, -0.0, np.float32)  # the in-order sum starts at source 0
             for r in range(world):
                 acc = (acc + oracle.widen16(_contribution(n, r, sg, it, kind), kind)).astype(np.float32)
             g16, _ = oracle.narrow16(acc, kind)
