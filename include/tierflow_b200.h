@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define TFG_ABI_VERSION 3
+#define TFG_ABI_VERSION 4
 #define TFG_MAX_TIERS 8
 
 typedef enum tfg_status {
@@ -386,6 +386,9 @@ int tfg_engine_wait_ticket(tfg_engine* engine, uint64_t ticket, uint64_t* bytes_
 int tfg_engine_read_state(tfg_engine* engine, uint32_t id, float* out_3n);                  /* :611 */
 int tfg_engine_read_params16(tfg_engine* engine, uint32_t id, uint16_t* out_n);
 int tfg_engine_read_grads16(tfg_engine* engine, uint32_t id, uint16_t* out_n);              /* grad_buffer(id).values(), :401 */
+/* Writes a host array back into the subgroup's 16-bit gradient buffer (a
+   caller that edited grad_buffer(id).mutable_values(), :401). */
+int tfg_engine_write_grads16(tfg_engine* engine, uint32_t id, const uint16_t* in_n);
 int tfg_engine_meta(tfg_engine* engine, uint32_t id, tfg_subgroup_meta* out);               /* :587 */
 int tfg_engine_residency_census(tfg_engine* engine, uint64_t* host_params, uint64_t* per_tier, int n_tiers); /* :597 */
 int tfg_engine_current_order(tfg_engine* engine, uint32_t* out, int max_n, int* n_out);     /* :582 */
@@ -401,6 +404,10 @@ int tfg_engine_pool_state(tfg_engine* engine, int slot, int* state_out, uint32_t
 int tfg_now_ns(int64_t* out);                                                                /* common.hpp:21-26 */
 int tfg_upscale16_host(const uint16_t* src, float* dst, uint64_t n, int dtype, int* all_finite); /* precision.hpp:17 */
 int tfg_downscale16_host(const float* src, uint16_t* dst, uint64_t n, int dtype, uint64_t* overflows); /* precision.hpp:29 */
+/* One-value f16_to_f32 / f32_to_f16 (fp16.hpp:21-88), bf16 alike: the
+   kernels' codec run on the host (a scalar is not worth a device trip). */
+int tfg_f16_to_f32(uint16_t h, int dtype, float* out);
+int tfg_f32_to_f16(float x, int dtype, uint16_t* out);
 /* GradBufferF16::accumulate (precision.hpp:66-75) on host arrays: acc[i] =
    narrow(widen(acc[i]) + widen(grads[i])) in fp32, staged through HBM (the
    reduce kernel with two sources). */

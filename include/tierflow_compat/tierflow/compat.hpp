@@ -16,8 +16,10 @@
 // Differences a caller can observe, all by design of the B200 engine:
 //  * adam_step's `threads` argument is accepted and ignored (the step runs on
 //    the GPU); the numeric results are bit-identical to the reference.
-//  * OffloadWorker::grad_buffer(id) returns a host snapshot of the device
-//    gradient buffer, refreshed on every call (the gradients live in HBM).
+//  * OffloadWorker::grad_buffer(id) returns a host view of the device
+//    gradient buffer, read on every call (the gradients live in HBM); edits
+//    through it are written back before the next gradients_finite() or
+//    run_update().
 //  * enqueue_prefetch / enqueue_flush futures are deferred waits on engine
 //    tickets: the transfer is queued at the call, get() waits for it.
 #pragma once
@@ -124,13 +126,13 @@ inline std::size_t downscale_f32_to_f16(std::span<const float> src, std::span<f1
 
 inline float f16_to_f32(f16 h) {
     float out = 0.0f;
-    upscale_f16_to_f32(std::span<const f16>(&h, 1), std::span<float>(&out, 1));
+    detail::check(tfg_f16_to_f32(h.bits, TFG_F16, &out));
     return out;
 }
 
 inline f16 f32_to_f16(float x) {
     f16 out;
-    downscale_f32_to_f16(std::span<const float>(&x, 1), std::span<f16>(&out, 1));
+    detail::check(tfg_f32_to_f16(x, TFG_F16, &out.bits));
     return out;
 }
 
@@ -816,23 +818,30 @@ public:
     const std::vector<SubgroupId>& subgroup_ids() const { return ids_; }
     void init_and_flush_all(std::uint64_t seed) { detail::check(tfg_engine_init_and_flush_all(h_, seed)); }
     void run_backward_sim(int iteration, const SyntheticGradSource& src, int accum_steps) {
+        lent_.clear();  // the backward rewrites the device gradients: earlier host views are stale
         detail::check(tfg_engine_run_backward_sim(h_, iteration, src.seed, accum_steps));
     }
     bool gradients_finite() {
+        write_back_lent();
         int out = 0;
         detail::check(tfg_engine_gradients_finite(h_, &out));
         return out != 0;
     }
-    // Host snapshot of the subgroup's device gradient buffer, refreshed here.
+    // Host view of the subgroup's HBM gradient buffer, read here. Edits made
+    // through mutable_values() reach the engine before the next
+    // gradients_finite() or run_update() (the reference hands out the live
+    // host buffer).
     GradBufferF16& grad_buffer(SubgroupId id) {
         GradBufferF16& b = grads_[id];
         b.id_ = id;
         b.values_.resize(params_.at(id));
         detail::check(tfg_engine_read_grads16(h_, id, reinterpret_cast<std::uint16_t*>(b.values_.data())));
+        if (std::find(lent_.begin(), lent_.end(), id) == lent_.end()) lent_.push_back(id);
         return b;
     }
 
     PhaseStats run_update(int iteration) {
+        write_back_lent();
         tfg_phase_stats st{};
         detail::check(tfg_engine_run_update(h_, iteration, &st));
         PhaseStats out;
@@ -902,6 +911,11 @@ public:
     const ScheduleOptions& options() const { return opt_; }
 
 private:
+    void write_back_lent() {
+        for (const SubgroupId id : lent_)
+            detail::check(tfg_engine_write_grads16(h_, id, reinterpret_cast<const std::uint16_t*>(grads_[id].values_.data())));
+        lent_.clear();
+    }
     std::shared_future<IoStats> ticket_future(std::uint64_t ticket) {
         tfg_engine* h = h_;
         return std::async(std::launch::deferred, [h, ticket] {
@@ -918,6 +932,7 @@ private:
     std::map<SubgroupId, std::uint64_t> params_;
     std::vector<SubgroupId> ids_;
     std::map<SubgroupId, GradBufferF16> grads_;
+    std::vector<SubgroupId> lent_;  // grad_buffer views handed out since the last backward
 };
 
 }  // namespace tierflow

@@ -207,10 +207,13 @@ _SIGS = {
     "tfg_engine_read_state": (_i, [_vp, C.c_uint32, _vp]),
     "tfg_engine_read_params16": (_i, [_vp, C.c_uint32, _vp]),
     "tfg_engine_read_grads16": (_i, [_vp, C.c_uint32, _vp]),
+    "tfg_engine_write_grads16": (_i, [_vp, C.c_uint32, _vp]),
     "tfg_now_ns": (_i, [C.POINTER(C.c_int64)]),
     "tfg_upscale16_host": (_i, [_vp, _vp, _u64, _i, C.POINTER(_i)]),
     "tfg_downscale16_host": (_i, [_vp, _vp, _u64, _i, C.POINTER(_u64)]),
     "tfg_accumulate16_host": (_i, [_vp, _vp, _u64, _i]),
+    "tfg_f16_to_f32": (_i, [C.c_uint16, _i, C.POINTER(C.c_float)]),
+    "tfg_f32_to_f16": (_i, [C.c_float, _i, C.POINTER(C.c_uint16)]),
     "tfg_adam_step_host": (_i, [_vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64]),
     "tfg_pool_create": (_i, [_i, _u64, C.POINTER(_vp)]),
     "tfg_pool_destroy": (_i, [_vp]),

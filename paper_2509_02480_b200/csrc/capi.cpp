@@ -990,6 +990,17 @@ int tfg_engine_read_grads16(tfg_engine* engine, uint32_t id, uint16_t* out_n) {
     });
 }
 
+int tfg_engine_write_grads16(tfg_engine* engine, uint32_t id, const uint16_t* in_n) {
+    return guarded([&] {
+        need(engine, "engine");
+        need(in_n, "in");
+        const auto meta = engine->w->meta(id);
+        tfb::cuda_check(cudaSetDevice(engine->w->device_options().device), "cudaSetDevice");
+        tfb::cuda_check(cudaMemcpy(engine->w->grad_buffer(id), in_n, 2 * meta.param_count, cudaMemcpyDefault),
+                        "cudaMemcpy(grads16)");
+    });
+}
+
 int tfg_engine_meta(tfg_engine* engine, uint32_t id, tfg_subgroup_meta* out) {
     return guarded([&] {
         need(engine, "engine");

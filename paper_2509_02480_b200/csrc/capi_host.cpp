@@ -117,6 +117,22 @@ int tfg_downscale16_host(const float* src, uint16_t* dst, uint64_t n, int dtype,
     });
 }
 
+int tfg_f16_to_f32(uint16_t h, int dtype, float* out) {
+    return guard([&] {
+        if (dtype != TFG_F16 && dtype != TFG_BF16) throw tfb::ConfigError("unknown 16-bit dtype");
+        need(out, "out");
+        *out = tfb::widen16_scalar(h, dtype);
+    });
+}
+
+int tfg_f32_to_f16(float x, int dtype, uint16_t* out) {
+    return guard([&] {
+        if (dtype != TFG_F16 && dtype != TFG_BF16) throw tfb::ConfigError("unknown 16-bit dtype");
+        need(out, "out");
+        *out = tfb::narrow16_scalar(x, dtype);
+    });
+}
+
 int tfg_accumulate16_host(uint16_t* acc, const uint16_t* grads, uint64_t n, int dtype) {
     return guard([&] {
         if (dtype != TFG_F16 && dtype != TFG_BF16) throw tfb::ConfigError("unknown 16-bit dtype");

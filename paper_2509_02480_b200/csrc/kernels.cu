@@ -133,6 +133,10 @@ __global__ void spin_kernel(uint64_t ns) {
 
 }  // namespace
 
+// Scalar codecs on the host, the kernels' own __host__ __device__ code.
+float widen16_scalar(uint16_t h, int kind) { return kind == kF16 ? widen16<kF16>(h) : widen16<kBF16>(h); }
+uint16_t narrow16_scalar(float f, int kind) { return kind == kF16 ? narrow16<kF16>(f) : narrow16<kBF16>(f); }
+
 cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t stream) {
     if (ns == 0) return cudaSuccess;
     spin_kernel<<<1, 1, 0, stream>>>(ns);

@@ -63,6 +63,9 @@ cudaError_t launch_widen16(const uint16_t* src, float* dst, uint64_t n, int kind
 cudaError_t launch_narrow16(const float* src, uint16_t* dst, uint64_t n, int kind,
                             unsigned long long* overflow_out, cudaStream_t stream);
 cudaError_t launch_spin_ns(uint64_t ns, cudaStream_t stream);
+// One-value conversions on the host (the kernels' codec, numerics.cuh).
+float widen16_scalar(uint16_t h, int kind);
+uint16_t narrow16_scalar(float f, int kind);
 cudaError_t launch_count_nonfinite16(const uint16_t* src, uint64_t n, int kind,
                                      unsigned long long* out, cudaStream_t stream);
 // Non-finite count of the fp32 sum (in order, rounded once to kind) of nsrc

@@ -47,7 +47,7 @@ def test_tuning_library_is_separate(tf):
 
 def test_abi_version_and_errors(tf):
     from paper_2509_02480_b200 import _lib
-    assert _lib.load().tfg_abi_version() == 3
+    assert _lib.load().tfg_abi_version() == 4
     with pytest.raises(tf.ConfigError):
         tf.assign_subgroups(0, [1.0])
     with pytest.raises(tf.ConfigError):
@@ -208,3 +208,46 @@ def test_integration_c_example_compiles(tmp_path):
                    "int main(void) {\nint iters = 2;\n" + code + "\nreturn 0;\n}\n")
     subprocess.run(["gcc", "-std=c11", "-Wall", "-Werror", "-I", str(ROOT / "include"), "-c", str(src),
                     "-o", str(tmp_path / "integ.o")], check=True)
+
+
+def test_scalar_codec_matches_oracle(tf):
+    """tfg_f16_to_f32 / tfg_f32_to_f16 (the one-value conversions the
+    reference's fp16.hpp offers, run on the host with the kernels' codec):
+    every 16-bit pattern widened, and 2^17 float patterns (every exponent,
+    NaN payloads, subnormals, the overflow boundary) narrowed, f16 and bf16,
+    bit-equal to the oracle."""
+    import numpy as np
+    import oracle
+    from paper_2509_02480_b200 import _lib
+    lib = _lib.load()
+    rng = np.random.default_rng(7)
+    floats = np.concatenate([rng.integers(0, 2**32, 2**17, dtype=np.uint64).astype(np.uint32),
+                             np.array([0, 0x80000000, 0x7F800000, 0xFF800000, 0x7FC00001, 0xFFBFFFFF,
+                                       0x477FEFFF, 0x477FF000, 0x33000000, 0x33000001, 0x387FC000],
+                                      np.uint32)]).view(np.float32)
+    for kind in (0, 1):
+        want_w = oracle.widen16(np.arange(65536, dtype=np.uint32).astype(np.uint16), kind)
+        out = C.c_uint32()  # raw bits: a Python float would quiet signalling NaNs
+        out_f = C.cast(C.pointer(out), C.POINTER(C.c_float))
+        got_w = np.empty(65536, np.uint32)
+        for h in range(65536):
+            assert lib.tfg_f16_to_f32(h, kind, out_f) == 0
+            got_w[h] = out.value
+        assert np.array_equal(got_w, want_w.view(np.uint32))
+        want_n, _ = oracle.narrow16(floats, kind)
+        h16 = C.c_uint16()
+        got_n = np.empty(len(floats), np.uint16)
+        for i, f in enumerate(floats.tolist()):
+            if f != f:  # NaN: a Python float round trip may quiet it; check those by bits below
+                continue
+            assert lib.tfg_f32_to_f16(f, kind, C.byref(h16)) == 0
+            got_n[i] = h16.value
+        nan = np.isnan(floats)
+        got_n[nan] = want_n[nan]
+        assert np.array_equal(got_n, want_n)
+        # NaN inputs by bits (the argument goes by value as a float: pass it through a c_float built from bits)
+        for bits in floats.view(np.uint32)[nan][:2000].tolist():
+            f = C.c_float.from_buffer_copy(np.uint32(bits).tobytes())
+            assert lib.tfg_f32_to_f16(f, kind, C.byref(h16)) == 0
+            want, _ = oracle.narrow16(np.array([bits], np.uint32).view(np.float32), kind)
+            assert h16.value == int(want[0]), hex(bits)
