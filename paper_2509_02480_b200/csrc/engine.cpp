@@ -1110,15 +1110,18 @@ PhaseStats OffloadWorker::run_update(int iteration) {
     return stats;
 }
 
-// The plan position to issue next: the first one in [next, next + window)
-// that is host-resident (a hit, or its fetch has landed) or whose fetch
-// failed (wait_host_resident surfaces the error); else `next` itself once it
-// has no fetch in flight (wait_host_resident fetches it on demand, as the
-// reference) or once nothing lands for a second (wait_host_resident's
-// watchdog then owns the wait).
+// The plan position to issue next: the first one from `next` on that is
+// host-resident (a hit, or its fetch has landed) or whose fetch failed
+// (wait_host_resident surfaces the error); else `next` itself once it has no
+// fetch in flight (wait_host_resident fetches it on demand, as the reference)
+// or once nothing lands for a second (wait_host_resident's watchdog then owns
+// the wait). The scan is not limited to pool_slots positions: while a slow
+// directory fetch holds `next`, the slots of the subgroups issued past it
+// turn over and the frontier refills them further down the plan; those must
+// stay issuable, or the H2D stream idles until the slow fetch lands.
 std::size_t OffloadWorker::pick_next_ready(const std::vector<SubgroupId>& order, const std::vector<char>& issued,
                                            std::size_t next) {
-    const std::size_t window = std::min<std::size_t>(order.size(), next + std::clamp(opt_.pool_slots, 1, 64));
+    const std::size_t window = order.size();
     std::unique_lock<std::mutex> l(mu_);
     for (int waited_ms = 0; waited_ms < 1000; waited_ms += 5) {
         for (std::size_t j = next; j < window; ++j) {

@@ -55,10 +55,17 @@ for it in range(5):
     t0 = ev[0].timestamp_ns
     open_ = {}
     iv = []
+    locks = []
     for e in ev:
         key = (e.subgroup_id, e.tier_id)
         if e.kind in (tf.EventKind.prefetch_start, tf.EventKind.flush_start):
             open_[(key, e.kind)] = e.timestamp_ns
+        elif e.kind == tf.EventKind.lock_acquire:
+            open_[(("L", e.tier_id, e.worker_id), e.kind)] = e.timestamp_ns
+        elif e.kind == tf.EventKind.lock_release:
+            s = open_.pop((("L", e.tier_id, e.worker_id), tf.EventKind.lock_acquire), None)
+            if s is not None:
+                locks.append(("L", -1, e.tier_id, (s - t0) / 1e6, (e.timestamp_ns - t0) / 1e6))
         elif e.kind in (tf.EventKind.prefetch_end, tf.EventKind.flush_end):
             k0 = tf.EventKind.prefetch_start if e.kind == tf.EventKind.prefetch_end else tf.EventKind.flush_start
             s = open_.pop((key, k0), None)
@@ -79,7 +86,7 @@ for it in range(5):
     if cur:
         busy += cur[1] - cur[0]
     print(f"phase {it}: {st.wall_seconds * 1e3:.0f} ms, io busy(union) {busy:.0f} ms, hits {st.cache_hits}", flush=True)
-    for x in iv:
+    for x in sorted(iv + locks, key=lambda x: x[3]):
         print(f"   {x[0]} sg{x[1]:3d} tier{x[2]} {x[3]:8.0f} -> {x[4]:8.0f} ({x[4] - x[3]:6.0f} ms)")
     out.append(dict(phase=it, wall_ms=st.wall_seconds * 1e3, busy_ms=busy, intervals=iv))
 w.close()
