@@ -673,6 +673,12 @@ def e2e_leg(tf, sizes, base_id, steps, warmup, seed, rank, world, tier_root, poo
     if c0_steps > 0:
         w.set_cache_slots(0)
         ph0 = run_phases(w, world, rank, 2, c0_steps, backward, "e2e C=0")
+        if os.environ.get("TFB_TIMELINE_C0"):  # diagnostics: the last C = 0 phase's timeline
+            st = ph0[-1][1]
+            Path(os.environ["TFB_TIMELINE_C0"]).write_text(json.dumps(dict(
+                ms=ph0[-1][0], alloc=st.flush_allocation, timeline=w.last_timeline(),
+                io=[dict(id=e.id, read_s=e.read_seconds, write_s=e.write_seconds, fetched=e.fetched,
+                         flushed=e.flushed) for e in st.subgroup_io])))
         rl0 = pipeline_roofline(ph0, pcie, probes)
         res["c0"] = dict(ms=statistics.mean(p[0] for p in ph0), h2d=int(rl0["h2d"]), d2h=int(rl0["d2h"]),
                          bound_ms=rl0["bound_s"] * 1e3, pcie_bound_ms=rl0["pcie_s"] * 1e3,
