@@ -10,9 +10,13 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "capi_internal.hpp"
 #include "engine.hpp"
@@ -44,27 +48,123 @@ void need(const void* p, const char* what) {
     if (p == nullptr) throw tfb::ConfigError(std::string(what) + " must not be NULL");
 }
 
-// Device scratch for one host call, freed on every path.
-struct DevBuf {
-    void* p = nullptr;
-    explicit DevBuf(std::size_t bytes) {
-        if (bytes) tfb::cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(host-call scratch)");
+// Staging for the host-span calls. The caller's arrays are pageable
+// (std::vector in the reference's API), so every copy goes through two
+// pinned chunks: chunk i+1 is memcpy'd on the CPU while chunk i is on the
+// link. Device scratch is kept across calls (a cudaMalloc/cudaFree pair per
+// call costs more than the copies at the reference suites' sizes); a call
+// larger than kKeepBytes gets its own scratch, freed on return. One stage
+// per device, calls on it serialised.
+class HostStage {
+   public:
+    static constexpr std::size_t kChunk = std::size_t{8} << 20;
+    static constexpr std::size_t kKeepBytes = std::size_t{1} << 30;
+    static constexpr int kScratch = 5;  // 4 data arrays + the counters
+
+    static HostStage& get() {
+        int dev = 0;
+        tfb::cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+        static std::mutex map_mu;
+        static std::map<int, std::unique_ptr<HostStage>> stages;
+        std::lock_guard<std::mutex> g(map_mu);
+        auto& s = stages[dev];
+        if (!s) s.reset(new HostStage());
+        return *s;
     }
-    ~DevBuf() {
-        if (p) cudaFree(p);
+
+    std::mutex mu;  // held for the whole host call
+    cudaStream_t stream = nullptr;
+
+    // Device scratch i of at least `bytes` (valid until the call returns).
+    void* scratch(int i, std::size_t bytes) {
+        if (bytes == 0) return nullptr;
+        if (bytes > kKeepBytes) {
+            void* p = nullptr;
+            tfb::cuda_check(cudaMalloc(&p, bytes), "cudaMalloc(host-call scratch)");
+            oversize_.push_back(p);
+            return p;
+        }
+        if (cap_[i] < bytes) {
+            if (dev_[i]) tfb::cuda_check(cudaFree(dev_[i]), "cudaFree");
+            dev_[i] = nullptr;
+            cap_[i] = 0;
+            tfb::cuda_check(cudaMalloc(&dev_[i], bytes), "cudaMalloc(host-call scratch)");
+            cap_[i] = bytes;
+        }
+        return dev_[i];
     }
-    DevBuf(const DevBuf&) = delete;
-    DevBuf& operator=(const DevBuf&) = delete;
-    template <class T>
-    T* as() const { return static_cast<T*>(p); }
+
+    // Frees this call's oversize scratch (after the stream has drained).
+    void end_call() {
+        for (void* p : oversize_) cudaFree(p);
+        oversize_.clear();
+    }
+
+    void h2d(void* d, const void* h, std::size_t bytes) {
+        auto* dst = static_cast<char*>(d);
+        auto* src = static_cast<const char*>(h);
+        for (std::size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+            const std::size_t n = std::min(kChunk, bytes - off);
+            const int b = static_cast<int>(i & 1);
+            tfb::cuda_check(cudaEventSynchronize(done_[b]), "cudaEventSynchronize");  // its last DMA has read it
+            std::memcpy(pin_[b], src + off, n);
+            tfb::cuda_check(cudaMemcpyAsync(dst + off, pin_[b], n, cudaMemcpyHostToDevice, stream), "cudaMemcpyAsync");
+            tfb::cuda_check(cudaEventRecord(done_[b], stream), "cudaEventRecord");
+        }
+    }
+
+    // Copies after the work queued on `stream`; returns with the host array written.
+    void d2h(void* h, const void* d, std::size_t bytes) {
+        auto* dst = static_cast<char*>(h);
+        auto* src = static_cast<const char*>(d);
+        const std::size_t chunks = (bytes + kChunk - 1) / kChunk;
+        auto issue = [&](std::size_t i) {
+            const std::size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+            const int b = static_cast<int>(i & 1);
+            tfb::cuda_check(cudaMemcpyAsync(pin_[b], src + off, n, cudaMemcpyDeviceToHost, stream), "cudaMemcpyAsync");
+            tfb::cuda_check(cudaEventRecord(done_[b], stream), "cudaEventRecord");
+        };
+        if (chunks > 0) issue(0);
+        for (std::size_t i = 0; i < chunks; ++i) {
+            const int b = static_cast<int>(i & 1);
+            tfb::cuda_check(cudaEventSynchronize(done_[b]), "cudaEventSynchronize");
+            if (i + 1 < chunks) issue(i + 1);  // into the other chunk while this one is copied out
+            const std::size_t off = i * kChunk;
+            std::memcpy(dst + off, pin_[b], std::min(kChunk, bytes - off));
+        }
+    }
+
+    void sync() { tfb::cuda_check(cudaStreamSynchronize(stream), "cudaStreamSynchronize"); }
+
+   private:
+    HostStage() {
+        tfb::cuda_check(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        for (int b = 0; b < 2; ++b) {
+            tfb::cuda_check(cudaHostAlloc(&pin_[b], kChunk, cudaHostAllocPortable), "cudaHostAlloc(staging)");
+            tfb::cuda_check(cudaEventCreateWithFlags(&done_[b], cudaEventDisableTiming), "cudaEventCreate");
+            tfb::cuda_check(cudaEventRecord(done_[b], stream), "cudaEventRecord");
+        }
+    }
+    // Never destroyed: process-lifetime resources, released with the context.
+    void* pin_[2] = {nullptr, nullptr};
+    cudaEvent_t done_[2] = {nullptr, nullptr};
+    void* dev_[kScratch] = {};
+    std::size_t cap_[kScratch] = {};
+    std::vector<void*> oversize_;
 };
 
-void h2d(void* d, const void* h, std::size_t bytes) {
-    if (bytes) tfb::cuda_check(cudaMemcpy(d, h, bytes, cudaMemcpyHostToDevice), "cudaMemcpy(H2D)");
-}
-void d2h(void* h, const void* d, std::size_t bytes) {
-    if (bytes) tfb::cuda_check(cudaMemcpy(h, d, bytes, cudaMemcpyDeviceToHost), "cudaMemcpy(D2H)");
-}
+// One host call on the stage: serialised, drained and oversize scratch freed on every path.
+struct StagedCall {
+    HostStage& st;
+    std::lock_guard<std::mutex> lock;
+    StagedCall() : st(HostStage::get()), lock(st.mu) {}
+    ~StagedCall() {
+        cudaStreamSynchronize(st.stream);
+        st.end_call();
+    }
+    template <class T>
+    T* scratch(int i, std::size_t bytes) { return static_cast<T*>(st.scratch(i, bytes)); }
+};
 
 }  // namespace
 
@@ -84,15 +184,16 @@ int tfg_upscale16_host(const uint16_t* src, float* dst, uint64_t n, int dtype, i
             need(src, "src");
             need(dst, "dst");
         }
-        DevBuf ds(2 * n), dd(4 * n), dc(sizeof(unsigned long long));
-        tfb::cuda_check(cudaMemset(dc.p, 0, sizeof(unsigned long long)), "cudaMemset");
-        h2d(ds.p, src, 2 * n);
-        tfb::cuda_check(tfb::launch_widen16(ds.as<uint16_t>(), dd.as<float>(), n, dtype, dc.as<unsigned long long>(),
-                                            nullptr),
-                        "upscale16");
+        StagedCall c;
+        auto* ds = c.scratch<uint16_t>(0, 2 * n);
+        auto* dd = c.scratch<float>(1, 4 * n);
+        auto* dc = c.scratch<unsigned long long>(4, sizeof(unsigned long long));
+        tfb::cuda_check(cudaMemsetAsync(dc, 0, sizeof(unsigned long long), c.st.stream), "cudaMemsetAsync");
+        c.st.h2d(ds, src, 2 * n);
+        tfb::cuda_check(tfb::launch_widen16(ds, dd, n, dtype, dc, c.st.stream), "upscale16");
         unsigned long long bad = 0;
-        d2h(dst, dd.p, 4 * n);
-        d2h(&bad, dc.p, sizeof(bad));
+        c.st.d2h(dst, dd, 4 * n);
+        c.st.d2h(&bad, dc, sizeof(bad));
         if (all_finite) *all_finite = bad == 0;
     });
 }
@@ -104,15 +205,16 @@ int tfg_downscale16_host(const float* src, uint16_t* dst, uint64_t n, int dtype,
             need(src, "src");
             need(dst, "dst");
         }
-        DevBuf ds(4 * n), dd(2 * n), dc(sizeof(unsigned long long));
-        tfb::cuda_check(cudaMemset(dc.p, 0, sizeof(unsigned long long)), "cudaMemset");
-        h2d(ds.p, src, 4 * n);
-        tfb::cuda_check(tfb::launch_narrow16(ds.as<float>(), dd.as<uint16_t>(), n, dtype, dc.as<unsigned long long>(),
-                                             nullptr),
-                        "downscale16");
+        StagedCall c;
+        auto* ds = c.scratch<float>(0, 4 * n);
+        auto* dd = c.scratch<uint16_t>(1, 2 * n);
+        auto* dc = c.scratch<unsigned long long>(4, sizeof(unsigned long long));
+        tfb::cuda_check(cudaMemsetAsync(dc, 0, sizeof(unsigned long long), c.st.stream), "cudaMemsetAsync");
+        c.st.h2d(ds, src, 4 * n);
+        tfb::cuda_check(tfb::launch_narrow16(ds, dd, n, dtype, dc, c.st.stream), "downscale16");
         unsigned long long over = 0;
-        d2h(dst, dd.p, 2 * n);
-        d2h(&over, dc.p, sizeof(over));
+        c.st.d2h(dst, dd, 2 * n);
+        c.st.d2h(&over, dc, sizeof(over));
         if (overflows) *overflows = over;
     });
 }
@@ -139,13 +241,15 @@ int tfg_accumulate16_host(uint16_t* acc, const uint16_t* grads, uint64_t n, int 
         if (n == 0) return;
         need(acc, "acc");
         need(grads, "grads");
-        DevBuf da(2 * n), dg(2 * n), dout(2 * n);
-        h2d(da.p, acc, 2 * n);
-        h2d(dg.p, grads, 2 * n);
-        const void* srcs[2] = {da.p, dg.p};
-        tfb::cuda_check(tfb::launch_reduce_sum16(srcs, 2, n, dtype, dout.as<uint16_t>(), nullptr, nullptr),
-                        "accumulate16");
-        d2h(acc, dout.p, 2 * n);
+        StagedCall c;
+        auto* da = c.scratch<uint16_t>(0, 2 * n);
+        auto* dg = c.scratch<uint16_t>(1, 2 * n);
+        auto* dout = c.scratch<uint16_t>(2, 2 * n);
+        c.st.h2d(da, acc, 2 * n);
+        c.st.h2d(dg, grads, 2 * n);
+        const void* srcs[2] = {da, dg};
+        tfb::cuda_check(tfb::launch_reduce_sum16(srcs, 2, n, dtype, dout, nullptr, c.st.stream), "accumulate16");
+        c.st.d2h(acc, dout, 2 * n);
     });
 }
 
@@ -166,32 +270,35 @@ int tfg_adam_step_host(float* p, float* m, float* v, const float* g, uint64_t n,
         need(m, "m");
         need(v, "v");
         need(g, "g");
-        DevBuf st(12 * n), dg(4 * n), d16(2 * n), dc(2 * sizeof(unsigned long long));
-        float* dp = st.as<float>();
-        h2d(dp, p, 4 * n);
-        h2d(dp + n, m, 4 * n);
-        h2d(dp + 2 * n, v, 4 * n);
-        h2d(dg.p, g, 4 * n);
-        tfb::cuda_check(cudaMemset(dc.p, 0, 2 * sizeof(unsigned long long)), "cudaMemset");
+        StagedCall c;
+        float* dp = c.scratch<float>(0, 12 * n);
+        auto* dg = c.scratch<float>(1, 4 * n);
+        auto* d16 = c.scratch<uint16_t>(2, 2 * n);
+        auto* dc = c.scratch<unsigned long long>(4, 2 * sizeof(unsigned long long));
+        c.st.h2d(dp, p, 4 * n);
+        c.st.h2d(dp + n, m, 4 * n);
+        c.st.h2d(dp + 2 * n, v, 4 * n);
+        c.st.h2d(dg, g, 4 * n);
+        tfb::cuda_check(cudaMemsetAsync(dc, 0, 2 * sizeof(unsigned long long), c.st.stream), "cudaMemsetAsync");
         a.p = dp;
         a.m = dp + n;
         a.v = dp + 2 * n;
-        a.g = dg.p;
+        a.g = dg;
         a.grad_kind = TFG_F32;
-        a.p16 = d16.as<uint16_t>();
+        a.p16 = d16;
         a.out_kind = TFG_F16;
         a.n = n;
-        a.counters = dc.as<unsigned long long>();
-        tfb::cuda_check(tfb::launch_adam_fused(a, nullptr), "adam_step");
+        a.counters = dc;
+        tfb::cuda_check(tfb::launch_adam_fused(a, c.st.stream), "adam_step");
         unsigned long long cnt[2] = {0, 0};
-        d2h(cnt, dc.p, sizeof(cnt));
+        c.st.d2h(cnt, dc, sizeof(cnt));
         // The reference rejects a non-finite gradient before mutating
         // (optimizer.hpp:123-127): the device copy is discarded, the caller's
         // arrays were never written.
         if (cnt[0] != 0) throw tfb::GradientOverflowError("adam_step: non-finite gradient");
-        d2h(p, dp, 4 * n);
-        d2h(m, dp + n, 4 * n);
-        d2h(v, dp + 2 * n, 4 * n);
+        c.st.d2h(p, dp, 4 * n);
+        c.st.d2h(m, dp + n, 4 * n);
+        c.st.d2h(v, dp + 2 * n, 4 * n);
     });
 }
 
