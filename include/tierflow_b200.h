@@ -150,7 +150,7 @@ typedef struct tfg_phase_stats {
     int32_t flush_allocation[TFG_MAX_TIERS];
     tfg_tier_observation tier_obs[TFG_MAX_TIERS];
     uint64_t n_subgroup_io;  /* entries available via tfg_engine_last_subgroup_io */
-    double device_seconds;   /* first H2D start -> last D2H end (CUDA events) */
+    double device_seconds;   /* phase start -> last D2H end (CUDA events) */
     double kernel_seconds;   /* sum of fused-kernel durations */
     double h2d_seconds;
     double d2h_seconds;
@@ -170,12 +170,13 @@ typedef struct tfg_event {
 } tfg_event;
 
 /* One subgroup's pass through the pipeline in the last phase (no reference
- * counterpart): device times from CUDA events, ms from the first H2D start;
+ * counterpart): device times from CUDA events, ms from the phase start;
  * host times ms from run_update entry. */
 typedef struct tfg_device_span {
     uint32_t id;
     float h2d_start, h2d_end, k_start, k_end, d2h_end;
     float host_resident, host_retired;
+    float d2h_start;
 } tfg_device_span;
 
 typedef struct tfg_subgroup_meta { /* Subgroup, optimizer.hpp:39-73 */

@@ -108,7 +108,7 @@ class EventC(C.Structure):
 class DeviceSpanC(C.Structure):
     _fields_ = [("id", C.c_uint32), ("h2d_start", C.c_float), ("h2d_end", C.c_float), ("k_start", C.c_float),
                 ("k_end", C.c_float), ("d2h_end", C.c_float), ("host_resident", C.c_float),
-                ("host_retired", C.c_float)]
+                ("host_retired", C.c_float), ("d2h_start", C.c_float)]
 
 
 class SubgroupMetaC(C.Structure):

@@ -26,6 +26,21 @@ constexpr std::uint64_t kSegAlign = 64;  // floats: 256-byte aligned P / m / v d
 
 std::uint64_t seg_stride(std::uint64_t pc) { return (pc + kSegAlign - 1) / kSegAlign * kSegAlign; }
 
+// Device state buffers (ring, HBM retention) keep kSegAlign floats of head
+// room in front of P: the 32 bytes just below P mirror the host block's
+// header area, so a contiguous P||m||v moves between the 4 KiB-aligned host
+// block base and P - 32 as one copy with both ends on the block's alignment.
+// (A copy starting at the payload, 32 bytes past a page boundary, loses
+// ~8 GB/s of D2H when the H2D direction is busy: profiles/r2_align_probe.json.)
+float* alloc_state_buffer(std::uint64_t stride, const char* what) {
+    float* p = nullptr;
+    cuda_check(cudaMalloc(reinterpret_cast<void**>(&p), (3 * stride + kSegAlign) * sizeof(float)), what);
+    return p + kSegAlign;
+}
+void free_state_buffer(float* p) {
+    if (p) cudaFree(p - kSegAlign);
+}
+
 }  // namespace
 
 // --- hyperparameters ---------------------------------------------------------
@@ -429,9 +444,10 @@ void OffloadWorker::setup_device() {
     cuda_check(cudaStreamCreateWithFlags(&s_h2d2_, cudaStreamNonBlocking), "cudaStreamCreate");
     ring_stride_ = seg_stride(max_params_);
     ring_.assign(static_cast<std::size_t>(dev_.device_buffers), nullptr);
+    cuda_check(cudaEventCreate(&phase_origin_), "cudaEventCreate");
     ring_ready_.assign(ring_.size(), nullptr);
     for (std::size_t b = 0; b < ring_.size(); ++b) {
-        cuda_check(cudaMalloc(reinterpret_cast<void**>(&ring_[b]), 3 * ring_stride_ * sizeof(float)), "cudaMalloc(ring)");
+        ring_[b] = alloc_state_buffer(ring_stride_, "cudaMalloc(ring)");
         cuda_check(cudaEventCreateWithFlags(&ring_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
     }
     ring_next_ = 0;
@@ -490,8 +506,7 @@ void OffloadWorker::setup_device() {
         hbm_cache_.assign(static_cast<std::size_t>(cap), nullptr);
         hbm_ready_.assign(hbm_cache_.size(), nullptr);
         for (std::size_t b = 0; b < hbm_cache_.size(); ++b) {
-            cuda_check(cudaMalloc(reinterpret_cast<void**>(&hbm_cache_[b]), 3 * ring_stride_ * sizeof(float)),
-                       "cudaMalloc(hbm retention)");
+            hbm_cache_[b] = alloc_state_buffer(ring_stride_, "cudaMalloc(hbm retention)");
             cuda_check(cudaEventCreateWithFlags(&hbm_ready_[b], cudaEventDisableTiming), "cudaEventCreate");
             hbm_free_.push_back(static_cast<int>(b));
         }
@@ -539,12 +554,14 @@ void OffloadWorker::release_device() {
                                e.h2d_half})
             if (ev) cudaEventDestroy(ev);
     events_.clear();
-    for (float* r : ring_) cudaFree(r);
+    for (float* r : ring_) free_state_buffer(r);
     ring_.clear();
+    if (phase_origin_) cudaEventDestroy(phase_origin_);
+    phase_origin_ = nullptr;
     for (cudaEvent_t ev : ring_ready_)
         if (ev) cudaEventDestroy(ev);
     ring_ready_.clear();
-    for (float* r : hbm_cache_) cudaFree(r);
+    for (float* r : hbm_cache_) free_state_buffer(r);
     for (cudaEvent_t ev : hbm_ready_)
         if (ev) cudaEventDestroy(ev);
     hbm_cache_.clear();
@@ -588,16 +605,18 @@ void OffloadWorker::release_device() {
 }
 
 // Host P||m||v (contiguous, stride pc) <-> device P / m / v segments (stride
-// seg_stride(pc), 256-byte aligned). One copy when the strides coincide.
+// seg_stride(pc), 256-byte aligned). When the strides coincide, one copy of
+// header area + payload from the block base (alloc_state_buffer); the header
+// bytes that land in the host block are rewritten by every tier write.
 void OffloadWorker::copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device,
                                cudaStream_t s) {
     const std::uint64_t ds = seg_stride(pc);
     const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
     float* host = blk.payload();
     if (ds == pc) {
-        const std::size_t bytes = 12 * pc;
-        cuda_check(to_device ? cudaMemcpyAsync(dev_base, host, bytes, kind, s)
-                             : cudaMemcpyAsync(host, dev_base, bytes, kind, s),
+        const StateSpan x = state_span(dev_base, blk, pc);
+        cuda_check(to_device ? cudaMemcpyAsync(x.dev, x.host, x.bytes, kind, s)
+                             : cudaMemcpyAsync(x.host, x.dev, x.bytes, kind, s),
                    "cudaMemcpyAsync(state)");
         return;
     }
@@ -937,6 +956,8 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         std::lock_guard<std::mutex> g(mu_);
         order_ = update_order(iteration, ids_, opt_.enable_caching);
     }
+    // timeline origin: the phase start on the H2D stream
+    cuda_check(cudaEventRecord(phase_origin_, s_h2d_), "cudaEventRecord");
     order_after_producer();
     launch_grad_check();
     cuda_check(cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), s_k_), "cudaMemsetAsync");
@@ -1047,7 +1068,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
 
     // Device timeline of the phase (CUDA events) + host retire times.
     if (!order.empty()) {
-        const cudaEvent_t origin = events_[index_of_.at(order.front())].h2d_start;
+        const cudaEvent_t origin = phase_origin_;
         auto at = [&](cudaEvent_t ev) {
             float ms = 0.0f;
             return cudaEventElapsedTime(&ms, origin, ev) == cudaSuccess ? ms : -1.0f;
@@ -1063,6 +1084,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             sp.k_end = at(e.k_end);
             sp.d2h_end = at(e.d2h_end);
             const float d2h_start = at(e.d2h_start);
+            sp.d2h_start = d2h_start;
             sp.host_resident = static_cast<float>((host_resident_ns_[k] - phase_t0_ns_) / 1e6);
             sp.host_retired = static_cast<float>((host_retired_ns_[k] - phase_t0_ns_) / 1e6);
             stats.h2d_seconds += (sp.h2d_end - sp.h2d_start) / 1e3;
@@ -1070,7 +1092,8 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             stats.d2h_seconds += (sp.d2h_end - d2h_start) / 1e3;
             stats.timeline.push_back(sp);
         }
-        stats.device_seconds = at(events_[index_of_.at(order.back())].d2h_end) / 1e3;
+        for (const DeviceSpan& sp : stats.timeline)
+            stats.device_seconds = std::max(stats.device_seconds, static_cast<double>(sp.d2h_end) / 1e3);
     }
     (void)cudaGetLastError();
 
@@ -1246,10 +1269,11 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
         if (dev_.h2d_split > 1 && ds == pc) {
             // Two concurrent halves on two copy engines: the H2D side of the
             // duplex link arbitration gets a second queue, like d2h_split.
-            const std::size_t bytes = 12 * pc;
+            const StateSpan x = state_span(d, blk, pc);
+            const std::size_t bytes = x.bytes;
             const std::size_t half = (bytes / 2) & ~static_cast<std::size_t>(4095);
-            auto* host = reinterpret_cast<const char*>(blk.payload());
-            auto* dev = reinterpret_cast<char*>(d);
+            const char* host = x.host;
+            char* dev = x.dev;
             cuda_check(cudaStreamWaitEvent(s_h2d2_, e.h2d_start, 0), "wait");
             cuda_check(cudaMemcpyAsync(dev, host, half, cudaMemcpyHostToDevice, s_h2d_), "cudaMemcpyAsync");
             cuda_check(cudaMemcpyAsync(dev + half, host + half, bytes - half, cudaMemcpyHostToDevice, s_h2d2_),
@@ -1336,10 +1360,11 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     } else if (dev_.d2h_split > 1 && ds == pc) {
         // Two concurrent D2H halves on two copy engines: the write-back gets
         // a larger share of the duplex link against the H2D stream.
-        const std::size_t bytes = 12 * pc;
+        const StateSpan x = state_span(d, blk, pc);
+        const std::size_t bytes = x.bytes;
         const std::size_t half = (bytes / 2) & ~static_cast<std::size_t>(4095);
-        auto* host = reinterpret_cast<char*>(blk.payload());
-        auto* dev = reinterpret_cast<char*>(d);
+        char* host = x.host;
+        char* dev = x.dev;
         cuda_check(cudaStreamWaitEvent(s_d2h2_, e.d2h_start, 0), "wait");
         cuda_check(cudaMemcpyAsync(host, dev, half, cudaMemcpyDeviceToHost, s_d2h_), "cudaMemcpyAsync");
         cuda_check(cudaMemcpyAsync(host + half, dev + half, bytes - half, cudaMemcpyDeviceToHost, s_d2h2_),

@@ -140,12 +140,13 @@ struct SubgroupIoTimes {
 
 // Per-subgroup timeline of one phase, milliseconds from the phase start.
 // Device times come from CUDA events on the pipeline streams (zero = the
-// first H2D start); host times from CLOCK_MONOTONIC (zero = run_update entry).
+// phase start on the H2D stream); host times from CLOCK_MONOTONIC (zero = run_update entry).
 struct DeviceSpan {
     SubgroupId id = 0;
     float h2d_start = 0, h2d_end = 0, k_start = 0, k_end = 0, d2h_end = 0;
     float host_resident = 0;  // wait_host_resident returned
     float host_retired = 0;   // completion thread retired the subgroup
+    float d2h_start = 0;      // its D2H began (= d2h_end when nothing went back)
 };
 
 struct PhaseStats {
@@ -158,7 +159,7 @@ struct PhaseStats {
     std::vector<TierObservation> tier_obs;
     std::vector<SubgroupIoTimes> subgroup_io;
     // Device side (CUDA events on the pipeline streams).
-    double device_seconds = 0.0;  // first H2D start -> last D2H end
+    double device_seconds = 0.0;  // phase start -> last D2H end
     double kernel_seconds = 0.0;  // sum of fused-kernel durations
     double h2d_seconds = 0.0;     // sum of state H2D durations
     double d2h_seconds = 0.0;     // sum of state D2H durations
@@ -364,6 +365,17 @@ private:
     std::pair<std::uint64_t, std::uint64_t> issue_device_update(SubgroupId id, int slot, const AdamConsts& c);
     void device_state_to_host(const float* dev, float* host, std::uint64_t pc);
     void writeback_hbm_copy_locked(std::size_t k, int slot);
+    // Header area + P||m||v of a contiguous state (seg_stride(pc) == pc):
+    // block base <-> 32 bytes below P in a device state buffer.
+    struct StateSpan {
+        char* host;
+        char* dev;
+        std::size_t bytes;
+    };
+    static StateSpan state_span(float* dev_p, const HostBlock& blk, std::uint64_t pc) {
+        return StateSpan{reinterpret_cast<char*>(blk.base()), reinterpret_cast<char*>(dev_p) - kHeaderBytes,
+                         kHeaderBytes + 12 * static_cast<std::size_t>(pc)};
+    }
     void copy_state(float* dev_base, const HostBlock& blk, std::uint64_t pc, bool to_device, cudaStream_t s);
     void completion_loop();
     static void CUDART_CB host_done(void* arg);
@@ -487,6 +499,7 @@ private:
     std::int64_t phase_t0_ns_ = 0;
     std::vector<std::int64_t> host_resident_ns_;  // per subgroup index
     std::vector<std::int64_t> host_retired_ns_;
+    cudaEvent_t phase_origin_ = nullptr;  // recorded on the H2D stream at run_update entry
 
     // Completion thread: retires subgroups whose D2H finished.
     std::thread completer_;
