@@ -1007,8 +1007,21 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         // per-tier fetch / flush sequences are those of the in-order loop.
         std::vector<char> issued(order.size(), 0);
         std::size_t next = 0;
+        std::deque<cudaEvent_t> h2d_queued;  // h2d_done of the state copies issued and not yet drained
+        auto h2d_backlog = [&] {
+            while (!h2d_queued.empty() && cudaEventQuery(h2d_queued.front()) == cudaSuccess) h2d_queued.pop_front();
+            (void)cudaGetLastError();  // cudaErrorNotReady
+            return static_cast<int>(h2d_queued.size());
+        };
         for (std::size_t done = 0; done < order.size(); ++done) {
             while (issued[next]) ++next;
+            // Hold the next state copy on the host while the H2D stream has
+            // kH2dAhead queued: the choice is made as late as possible.
+            while (h2d_backlog() >= kH2dAhead) {
+                std::this_thread::sleep_for(std::chrono::microseconds(500));
+                std::lock_guard<std::mutex> g(mu_);
+                if (completion_error_) std::rethrow_exception(completion_error_);
+            }
             const std::size_t j = pick_next_ready(order, issued, next);
             issued[j] = 1;
             const SubgroupId id = order[j];
@@ -1016,6 +1029,7 @@ PhaseStats OffloadWorker::run_update(int iteration) {
             const int slot = wait_host_resident(id);
             host_resident_ns_[index_of_.at(id)] = now_ns();
             const auto moved = issue_device_update(id, slot, c);
+            if (moved.first > 0) h2d_queued.push_back(events_[index_of_.at(id)].h2d_done);
             std::lock_guard<std::mutex> g(mu_);
             Subgroup& sg = subgroups_.at(id);
             sg.step_count = static_cast<std::uint64_t>(iteration) + 1;
@@ -1142,20 +1156,33 @@ PhaseStats OffloadWorker::run_update(int iteration) {
 // directory fetch holds `next`, the slots of the subgroups issued past it
 // turn over and the frontier refills them further down the plan; those must
 // stay issuable, or the H2D stream idles until the slow fetch lands.
+// Among the ready ones, a subgroup the plan flushes to a directory tier goes
+// first: its write then overlaps the PCIe traffic of the rest of the phase
+// instead of trailing it (the reference's greedy destination plan puts those
+// flushes at the end of the order, and the phase waits for every flush).
+// Fetch order (the frontier), cache hits and flush sets are unchanged.
 std::size_t OffloadWorker::pick_next_ready(const std::vector<SubgroupId>& order, const std::vector<char>& issued,
                                            std::size_t next) {
     const std::size_t window = order.size();
     std::unique_lock<std::mutex> l(mu_);
+    auto ready = [&](SubgroupId id) {
+        if (subgroups_.at(id).residency == Residency::host_cached) return true;
+        const auto f = prefetch_futures_.find(id);
+        return f != prefetch_futures_.end() && f->second.wait_for(std::chrono::seconds(0)) == std::future_status::ready;
+    };
+    auto slow_dest = [&](SubgroupId id) {
+        const TierAssignment a = dests_->assign_storage_tier(id);
+        return !a.host_retain && a.tier != kNoTier &&
+               tiers_[static_cast<std::size_t>(a.tier)]->spec().kind != TierKind::host_dram;
+    };
     for (int waited_ms = 0; waited_ms < 1000; waited_ms += 5) {
+        std::size_t first = window;
         for (std::size_t j = next; j < window; ++j) {
-            if (issued[j]) continue;
-            const SubgroupId id = order[j];
-            if (subgroups_.at(id).residency == Residency::host_cached) return j;
-            const auto f = prefetch_futures_.find(id);
-            if (f != prefetch_futures_.end() &&
-                f->second.wait_for(std::chrono::seconds(0)) == std::future_status::ready)
-                return j;
+            if (issued[j] || !ready(order[j])) continue;
+            if (slow_dest(order[j])) return j;
+            if (first == window) first = j;
         }
+        if (first != window) return first;
         if (prefetch_futures_.count(order[next]) == 0) return next;
         if (completion_error_) std::rethrow_exception(completion_error_);
         resident_cv_.wait_for(l, std::chrono::milliseconds(5));

@@ -13,8 +13,8 @@
 // streams: H2D (slot -> HBM) -> fused sm_100a Adam kernel (gradient from the
 // device-resident 16-bit gradient buffer, 16-bit working params written to
 // the device-resident parameter buffer) -> D2H (HBM -> slot). The coordinator
-// never blocks on the GPU: it issues subgroup j and moves on to j+1; a
-// completion thread retires finished subgroups (slot back to cached, lazy
+// issues subgroups as they become host-resident, keeping a few state copies
+// queued on the H2D stream (kH2dAhead); a completion thread retires finished subgroups (slot back to cached, lazy
 // flush or retention, frontier pump) exactly where the reference's
 // coordinator would after adam_step returns.
 //
@@ -108,6 +108,11 @@ struct DeviceOptions {
 
 // HBM cache mode: pinned blocks in the write-back lane.
 constexpr int kWritebackBlocks = 4;
+// State H2D copies the coordinator keeps queued on the H2D stream. Enough to
+// keep the stream busy across host issue latency; the resident subgroups
+// beyond it wait on the host, where a later-resident one the plan flushes to
+// a directory tier can still go first (pick_next_ready).
+constexpr int kH2dAhead = 3;
 // Baseline flow: pinned fp32-gradient staging blocks in rotation.
 constexpr int kGradStages = 4;
 
