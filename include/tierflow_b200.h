@@ -26,7 +26,7 @@
 extern "C" {
 #endif
 
-#define TFG_ABI_VERSION 4
+#define TFG_ABI_VERSION 5  /* 5: tfg_device_span.d2h_start */
 #define TFG_MAX_TIERS 8
 
 typedef enum tfg_status {

@@ -72,21 +72,32 @@ __device__ __forceinline__ U16x4 sum_quad16(const GradSources& gs, uint64_t q) {
 template <int GK, int GMODE, int NS>
 struct GradReg {
     U16x4 h;
+    template <bool COUNT = true>
     __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
         if constexpr (GMODE == 0)
             h = load_u16x4(reinterpret_cast<const uint16_t*>(gs.src[0]) + 4 * q);
         else
             h = sum_quad16<GK, NS>(gs, q);
-        nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
+        if constexpr (COUNT)
+            nonfinite += nonfinite16<GK>(h.x) + nonfinite16<GK>(h.y) + nonfinite16<GK>(h.z) + nonfinite16<GK>(h.w);
     }
     __device__ __forceinline__ float get(int k) const {
         return widen16<GK>(k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w);
+    }
+    // f16 straight to binary64 (one cvt.f64.f16 instead of widen + cvt.f64.f32)
+    __device__ __forceinline__ double get64(int k) const {
+        static_assert(GK == kF16, "get64: f16 gradients");
+        const uint16_t x = k == 0 ? h.x : k == 1 ? h.y : k == 2 ? h.z : h.w;
+        double d;
+        asm("cvt.f64.f16 %0, %1;" : "=d"(d) : "h"(x));
+        return d;
     }
 };
 
 template <int GK, int NS>
 struct GradReg<GK, 1, NS> {
     float4 f;
+    template <bool COUNT = true>
     __device__ __forceinline__ void load(const GradSources& gs, uint64_t q, unsigned& nonfinite) {
         f = __ldcs(reinterpret_cast<const float4*>(gs.src[0]) + q);
         nonfinite += !isfinite(f.x) + !isfinite(f.y) + !isfinite(f.z) + !isfinite(f.w);
@@ -171,7 +182,15 @@ __device__ __forceinline__ void st_state(float4* p, float4 v) {
 // PF > 0: one thread per CTA asks the TMA unit to pull the CTA's chunk PF
 // grid-stride iterations ahead into L2 (cp.async.bulk.prefetch), so more bytes
 // are in flight than the registers of 32 warps per SM can hold.
-template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0, int PF = 0>
+// OPT (vector body, one 16-bit gradient source): bit 0 skips the per-element
+// non-finite count of the gradient (the launch is behind a whole-phase check
+// that found none: a device gate or a host verdict); bit 1 widens f16
+// gradients straight to binary64.
+constexpr int kOptVerified = 1;
+constexpr int kOptF64Widen = 2;
+
+template <int GK, int GMODE, int OK, bool WD, bool VEC, int UNROLL, int DIVC, int MINB, int NS = 0, int PF = 0,
+          int OPT = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_fused_kernel(const StateIO io, const GradSources gs, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                       unsigned long long* __restrict__ counters, const unsigned long long* __restrict__ gate) {
@@ -214,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     rp[u] = ld_state<PF>(p4 + q);
                     rm[u] = ld_state<PF>(m4 + q);
                     rv[u] = ld_state<PF>(v4 + q);
-                    rg[u].load(gs, q, nonfinite);
+                    rg[u].template load<(OPT & kOptVerified) == 0>(gs, q, nonfinite);
                 }
             }
 #pragma unroll
@@ -235,6 +254,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
                             rv[u].x = rv[u].y; rv[u].y = rv[u].z; rv[u].z = rv[u].w; rv[u].w = tv;
                             gx = gy; gy = gz; gz = gw; gw = tg;
                         }
+                    } else if constexpr ((OPT & kOptF64Widen) != 0) {
+                        adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get64(0), c);
+                        adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get64(1), c);
+                        adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get64(2), c);
+                        adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get64(3), c);
                     } else {
                         adam_math<WD, DIVC>(rp[u].x, rm[u].x, rv[u].x, rg[u].get(0), c);
                         adam_math<WD, DIVC>(rp[u].y, rm[u].y, rv[u].y, rg[u].get(1), c);
@@ -285,12 +309,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
-template <int UNROLL, int DIVC, int MINB, int PF = 0>
+template <int UNROLL, int DIVC, int MINB, int PF = 0, int OPT = 0>
 struct Cfg {
     static constexpr int kUnroll = UNROLL;
     static constexpr int kDivc = DIVC;
     static constexpr int kMinBlocks = MINB;
     static constexpr int kPrefetch = PF;
+    static constexpr int kOpt = OPT;
 };
 
 GradSources sources_of(const AdamLaunch& a) {
@@ -328,7 +353,7 @@ cudaError_t launch_cfg(const AdamLaunch& a, cudaStream_t stream) {
     const GradSources gs = sources_of(a);
     if (is_vec(a)) {
         const unsigned grid = grid_for((a.n / 4 + U - 1) / U, B);
-        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS, C::kPrefetch>
+        adam_fused_kernel<GK, GMODE, OK, WD, true, U, C::kDivc, B, NS, C::kPrefetch, C::kOpt>
             <<<grid, kThreads, 0, stream>>>(state_io(a), gs, a.p16, a.n, a.c, a.counters, a.gate);
     } else {
         const unsigned grid = grid_for(a.n, B);

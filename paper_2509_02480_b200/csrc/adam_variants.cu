@@ -12,6 +12,8 @@
 //   44-46               verified fast path, second form (numerics.cuh adam_element_fast2)
 //   47                  in-range correctly rounded sqrt / division without the special-operand checks
 //   48-50               state-stream cache hints: L2::256B fetches (evict-first or not), plain cached
+//   51-53               OPT bits of the shipped form: no per-element gradient non-finite count behind a
+//                       whole-phase check (53), f16 gradients widened straight to binary64 (52), both (51)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -720,6 +722,9 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 48) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, -1>>(a, stream);
     if constexpr (V == 49) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, -2>>(a, stream);
     if constexpr (V == 50) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, -3>>(a, stream);
+    if constexpr (V == 51) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 0, kOptVerified | kOptF64Widen>>(a, stream);
+    if constexpr (V == 52) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 0, kOptF64Widen>>(a, stream);
+    if constexpr (V == 53) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 0, kOptVerified>>(a, stream);
     if constexpr (V == 47)
         return fast_rn_domain(a.c) ? launch_wd<kF16, 0, kF16, Cfg<1, 7, 4>>(a, stream)
                                    : launch_dtypes<Cfg<1, true, 4>>(a, stream);
@@ -840,10 +845,13 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 48: return launch_variant<48>(a, stream);
         case 49: return launch_variant<49>(a, stream);
         case 50: return launch_variant<50>(a, stream);
+        case 51: return launch_variant<51>(a, stream);
+        case 52: return launch_variant<52>(a, stream);
+        case 53: return launch_variant<53>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 51; }
+int adam_variant_count() { return 54; }
 
 }  // namespace tfb

@@ -47,7 +47,7 @@ def test_tuning_library_is_separate(tf):
 
 def test_abi_version_and_errors(tf):
     from paper_2509_02480_b200 import _lib
-    assert _lib.load().tfg_abi_version() == 4
+    assert _lib.load().tfg_abi_version() == 5
     with pytest.raises(tf.ConfigError):
         tf.assign_subgroups(0, [1.0])
     with pytest.raises(tf.ConfigError):
