@@ -977,10 +977,12 @@ def main(argv=None):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": ncu_traffic(params_per_launch),
                 "peak_source": pk["source"], "alg_bytes_per_param": alg_bytes,
-                "kernel": "adam_fused_kernel (float4 quads, binary64 element math, constant-divisor "
-                          "quotients, 4 CTAs x 256 threads per SM)"
-                          + (f"; {world} gradient sources summed in-kernel, {world - 1} over NVLink peer loads"
-                             if exchange == "fused" else ""),
+                "kernel": (f"adam_fused_kernel (float4 quads, binary64 element math, constant-divisor quotients, "
+                           f"4 CTAs x 256 threads per SM; {world} gradient sources summed in-kernel, {world - 1} "
+                           f"over NVLink peer loads)" if exchange == "fused" else
+                           "adam_staged_kernel (P, m, v, g tiles of 1024 params staged in shared memory by "
+                           "cp.async.bulk, 2 stages per CTA, 4 CTAs x 256 threads per SM; binary64 element math, "
+                           "constant-divisor quotients)"),
                 "traffic_source": "profiles/ncu_adam_fused.json (ncu --set full, dram bytes per 100M-param launch)",
                 "copy_sustained_gbs": dl.get("copy_sustained_gbs"),
                 "frac_of_copy_sustained": (round(achieved / dl["copy_sustained_gbs"], 4)

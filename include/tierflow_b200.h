@@ -223,7 +223,10 @@ int tfg_adam_fused(float* p, float* m, float* v, const void* grad, int grad_dtyp
  * nonzero when the kernel starts, it writes nothing. A whole-phase non-finite
  * count accumulated into the gate on the same stream (tfg_count_nonfinite16)
  * rejects the phase's updates with no host round trip: the reference's
- * check-before-mutate (harness.hpp:218-228, optimizer.hpp:123-127). */
+ * check-before-mutate (harness.hpp:218-228, optimizer.hpp:123-127). The gate
+ * is taken as that count of this launch's gradients: a gated launch does not
+ * count non-finite gradients again (counters[0] is left alone; [1] still
+ * counts overflows). */
 int tfg_adam_fused_gated(float* p, float* m, float* v, const void* grad, int grad_dtype, uint16_t* param16,
                          int param_dtype, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
                          unsigned long long* counters, const unsigned long long* gate, void* stream);

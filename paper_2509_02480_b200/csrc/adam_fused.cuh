@@ -12,11 +12,14 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "kernels.hpp"
 #include "launch_util.cuh"
 #include "numerics.cuh"
+#include "tma.cuh"
 
 namespace tfb {
 namespace {
@@ -309,6 +312,136 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
 }
 
+// One quad of the staged kernel: widen, update, narrow, store at quad index
+// qi of the tile at (p, m, v, p16).
+template <int GK, int OK, bool WD, bool CNT, int MATH>
+__device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uint2 graw, const AdamConsts& c,
+                                            unsigned& nonfinite, unsigned& overflow, float* p, float* m, float* v,
+                                            uint16_t* p16, int qi) {
+    GradReg<GK, 0, 0> rg;
+    rg.h.x = static_cast<uint16_t>(graw.x & 0xFFFFu);
+    rg.h.y = static_cast<uint16_t>(graw.x >> 16);
+    rg.h.z = static_cast<uint16_t>(graw.y & 0xFFFFu);
+    rg.h.w = static_cast<uint16_t>(graw.y >> 16);
+    if constexpr (CNT)
+        nonfinite += nonfinite16<GK>(rg.h.x) + nonfinite16<GK>(rg.h.y) + nonfinite16<GK>(rg.h.z) +
+                     nonfinite16<GK>(rg.h.w);
+    if constexpr (GK == kF16) {
+        adam_math<WD, MATH>(rp.x, rm.x, rv.x, rg.get64(0), c);
+        adam_math<WD, MATH>(rp.y, rm.y, rv.y, rg.get64(1), c);
+        adam_math<WD, MATH>(rp.z, rm.z, rv.z, rg.get64(2), c);
+        adam_math<WD, MATH>(rp.w, rm.w, rv.w, rg.get64(3), c);
+    } else {
+        adam_math<WD, MATH>(rp.x, rm.x, rv.x, rg.get(0), c);
+        adam_math<WD, MATH>(rp.y, rm.y, rv.y, rg.get(1), c);
+        adam_math<WD, MATH>(rp.z, rm.z, rv.z, rg.get(2), c);
+        adam_math<WD, MATH>(rp.w, rm.w, rv.w, rg.get(3), c);
+    }
+    U16x4 h;
+    h.x = narrow16<OK>(rp.x);
+    h.y = narrow16<OK>(rp.y);
+    h.z = narrow16<OK>(rp.z);
+    h.w = narrow16<OK>(rp.w);
+    overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
+    __stcs(reinterpret_cast<float4*>(p) + qi, rp);
+    __stcs(reinterpret_cast<float4*>(m) + qi, rm);
+    __stcs(reinterpret_cast<float4*>(v) + qi, rv);
+    store_u16x4(p16 + 4 * qi, h);
+}
+
+// ---------------------------------------------------------------------------
+// Staged form (the shipped path for one 16-bit gradient source): one elected
+// thread per CTA keeps S-1 tiles of P, m, v and g in flight into a ring of
+// shared-memory stages with 1D bulk copies (cp.async.bulk on the TMA unit,
+// completion on an mbarrier per stage); every warp computes its quads of the
+// current tile from shared memory and stores the results straight to global
+// memory. The bytes in flight per SM (MINB CTAs x (S-1) x 14 B x T) do not
+// depend on how long the binary64 chain of the current quad takes, so the
+// kernel keeps HBM busy when the power cap lowers the SM clock (the register
+// kernel's loads are only in flight between two quads' math). Tile T =
+// 1024 params (one quad per thread); one CTA barrier per tile retires a stage
+// before it is refilled. The same element math, bit for bit.
+template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
+    adam_staged_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                       const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
+                       unsigned long long* __restrict__ counters, const unsigned long long* __restrict__ gate) {
+    if (gate != nullptr && *gate != 0) return;  // the phase was rejected on this stream: no writes
+    constexpr int T = 4 * kThreads;
+    const uint64_t ntiles = n / T;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* sp = reinterpret_cast<float*>(smem);
+    float* sm = sp + S * T;
+    float* sv = sm + S * T;
+    uint16_t* sg = reinterpret_cast<uint16_t*>(sv + S * T);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](uint64_t k) {
+        const int s = static_cast<int>(k % S);
+        const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
+        mbar_arrive_expect_tx(&full[s], 14u * T);
+        bulk_load(sp + s * T, p + off, 4u * T, &full[s]);
+        bulk_load(sm + s * T, m + off, 4u * T, &full[s]);
+        bulk_load(sv + s * T, v + off, 4u * T, &full[s]);
+        bulk_load(sg + s * T, g + off, 2u * T, &full[s]);
+    };
+    if (threadIdx.x == 0)
+        for (uint64_t k = 0; k + 1 < static_cast<uint64_t>(S) && k < mine; ++k) issue(k);
+    unsigned nonfinite = 0, overflow = 0;
+    const int qi = threadIdx.x;
+    for (uint64_t k = 0; k < mine; ++k) {
+        if (threadIdx.x == 0 && k + S - 1 < mine) issue(k + S - 1);  // into the stage tile k-1 released
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
+        const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
+        float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qi];
+        float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qi];
+        float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qi];
+        const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qi];
+        staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + off, m + off, v + off,
+                                           p16 + off, qi);
+        __syncthreads();  // stage s retired: it is refilled at iteration k + 1
+    }
+    // The n % T tail (fewer than T params, whole quads then scalars) from
+    // global memory, by the last CTA.
+    if (blockIdx.x == gridDim.x - 1) {
+        const uint64_t done = ntiles * T;
+        const uint64_t nq = (n - done) / 4;
+        if (static_cast<uint64_t>(threadIdx.x) < nq) {
+            const uint64_t q = done / 4 + threadIdx.x;
+            const float4 rp = __ldcs(reinterpret_cast<const float4*>(p) + q);
+            const float4 rm = __ldcs(reinterpret_cast<const float4*>(m) + q);
+            const float4 rv = __ldcs(reinterpret_cast<const float4*>(v) + q);
+            const uint2 graw = __ldcs(reinterpret_cast<const uint2*>(g) + q);
+            staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + done, m + done,
+                                               v + done, p16 + done, threadIdx.x);
+        }
+        const uint64_t i = done + 4 * nq + threadIdx.x;
+        if (i < n) {
+            float pf = __ldcs(p + i), mf = __ldcs(m + i), vf = __ldcs(v + i);
+            const uint16_t gh = __ldcs(g + i);
+            if constexpr (CNT) nonfinite += nonfinite16<GK>(gh);
+            adam_math<WD, 1>(pf, mf, vf, widen16<GK>(gh), c);
+            const uint16_t h = narrow16<OK>(pf);
+            overflow += is_inf16<OK>(h);
+            __stcs(p + i, pf);
+            __stcs(m + i, mf);
+            __stcs(v + i, vf);
+            p16[i] = h;
+        }
+    }
+    if (counters != nullptr) {
+        if constexpr (CNT) warp_count_add(counters + 0, nonfinite);
+        warp_count_add(counters + 1, overflow);
+    }
+}
+
+
 template <int UNROLL, int DIVC, int MINB, int PF = 0, int OPT = 0>
 struct Cfg {
     static constexpr int kUnroll = UNROLL;
@@ -403,6 +536,49 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
     if (a.grad_kind == kF16 && a.out_kind == kBF16) return launch_wd<kF16, 0, kBF16, C>(a, stream);
     if (a.grad_kind == kBF16 && a.out_kind == kF16) return launch_wd<kBF16, 0, kF16, C>(a, stream);
     return launch_wd<kBF16, 0, kBF16, C>(a, stream);
+}
+
+
+// One launch of the staged kernel (its last CTA takes the n % 1024 tail).
+// Returns cudaErrorNotSupported, launching nothing, when the launch does not
+// fit the staged form (summed or fp32 gradients, separate outputs, 16-byte
+// misalignment, fewer than one tile); the caller then launches the register
+// kernel.
+template <int S, int MINB, int MATH = 1>
+cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
+    constexpr uint64_t T = 4 * kThreads;
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
+                           reinterpret_cast<uintptr_t>(a.p16);
+    if (a.n_peers > 0 || a.p_out || a.m_out || a.v_out || (a.grad_kind != kF16 && a.grad_kind != kBF16) ||
+        (a.out_kind != kF16 && a.out_kind != kBF16) || (addr & 15u) != 0 || a.n < T)
+        return cudaErrorNotSupported;
+    const uint64_t ntiles = a.n / T;
+    const bool cnt = !(a.grads_verified || a.gate != nullptr);
+    const bool wd = a.c.lr_wd != 0.0;
+    using K = void (*)(float*, float*, float*, const uint16_t*, uint16_t*, uint64_t, AdamConsts, unsigned long long*,
+                       const unsigned long long*);
+    K kern = nullptr;
+    auto pick = [&](auto gk, auto ok) {
+        constexpr int GKc = decltype(gk)::value, OKc = decltype(ok)::value;
+        if (cnt)
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH>
+                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH>;
+        else
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH>
+                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH>;
+    };
+    using F = std::integral_constant<int, kF16>;
+    using B = std::integral_constant<int, kBF16>;
+    if (a.grad_kind == kF16) a.out_kind == kF16 ? pick(F{}, F{}) : pick(F{}, B{});
+    else a.out_kind == kF16 ? pick(B{}, F{}) : pick(B{}, B{});
+    constexpr size_t smem = static_cast<size_t>(S) * T * 14 + S * sizeof(uint64_t);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
+    kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, a.n, a.c,
+                                           a.counters, a.gate);
+    return cudaGetLastError();
 }
 
 }  // namespace

@@ -14,12 +14,22 @@
 namespace tfb {
 namespace {
 
-// Shipped configuration: one quad per thread per iteration, constant-divisor
-// quotients, <= 64 registers for 4 resident CTAs (32 warps) per SM. The
-// 2026-10-17 sweep (profiles/kernel_sweep_r1.json) measured it at 474 us per
-// 100M-param launch, 5.90 TB/s algorithmic = 0.92 of the measured HBM copy
-// peak, against 1045 us for the register-heavy unroll-2 form (variant 1).
+// Shipped configuration. One 16-bit gradient source in place (the engine's
+// pipeline, the device-resident bench leg, the operator API): the staged
+// kernel, 2 shared-memory stages of 1024 params (28 KiB) per CTA, 4 CTAs of
+// 256 threads per SM, f16 gradients widened straight to binary64, no second
+// non-finite count behind a whole-phase check. Under the bench's sustained,
+// power-capped load it holds 0.875-0.886 of the HBM copy peak where the
+// register kernel holds 0.842-0.853 (interleaved rounds,
+// profiles/sustained_sweep_r2_staged.json: tuning variant 55 vs 0).
+// Everything else (summed or fp32 gradients, separate outputs, misaligned or
+// sub-tile launches, a launch's n % 1024 tail): the register kernel, one quad
+// per thread per iteration, constant-divisor quotients, <= 64 registers for 4
+// resident CTAs (32 warps) per SM (0.93-0.95 of the copy peak launched cool,
+// profiles/kernel_sweep_r1.json).
 using VariantDefault = Cfg<1, true, 4>;
+constexpr int kStages = 2;
+constexpr int kStagedCtasPerSm = 4;
 // Tuning variants (F16 gradients and params only), for the kernel sweep.
 
 // ---------------------------------------------------------------------------
@@ -54,6 +64,8 @@ __global__ void divtest_kernel(double b, double y, uint64_t n, uint64_t seed, in
 
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
+    const cudaError_t e = launch_staged<kStages, kStagedCtasPerSm>(a, stream);
+    if (e != cudaErrorNotSupported) return e;
     return launch_dtypes<VariantDefault>(a, stream);
 }
 

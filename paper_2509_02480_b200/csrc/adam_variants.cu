@@ -14,12 +14,16 @@
 //   48-50               state-stream cache hints: L2::256B fetches (evict-first or not), plain cached
 //   51-53               OPT bits of the shipped form: no per-element gradient non-finite count behind a
 //                       whole-phase check (53), f16 gradients widened straight to binary64 (52), both (51)
+//   54-57               the staged kernel (adam_fused.cuh adam_staged_kernel): S = 2 / 4 CTAs counting (54)
+//                       and verified (55), S = 3 / 4 CTAs (56), S = 3 / 3 CTAs (57); 55 with variant 47's
+//                       in-range sqrt / division (58)
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cstdint>
 
 #include "adam_fused.cuh"
+#include "tma.cuh"
 
 namespace tfb {
 namespace {
@@ -30,39 +34,6 @@ namespace {
 // counted on an mbarrier), the consumer warps compute from shared memory and
 // store straight to global. Memory parallelism comes from the stage ring
 // (S x 14 KiB per CTA in flight) instead of registers.
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(smem_addr(bar)), "r"(parity)
-            : "memory");
-    }
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_addr(dst)),
-        "l"(src), "r"(bytes), "r"(smem_addr(bar))
-        : "memory");
-}
 
 constexpr int kTmaConsumerWarps = 8;
 
@@ -725,6 +696,19 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 51) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 0, kOptVerified | kOptF64Widen>>(a, stream);
     if constexpr (V == 52) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 0, kOptF64Widen>>(a, stream);
     if constexpr (V == 53) return launch_wd<kF16, 0, kF16, Cfg<1, 1, 4, 0, kOptVerified>>(a, stream);
+    if constexpr (V >= 54 && V <= 57) {
+        AdamLaunch b = a;
+        b.grads_verified = V != 54;
+        constexpr int S = V >= 56 ? 3 : 2;
+        constexpr int M = V == 57 ? 3 : 4;
+        return launch_staged<S, M>(b, stream);
+    }
+    if constexpr (V == 58) {  // staged + in-range sqrt / division (domain-gated, as variant 47)
+        AdamLaunch b = a;
+        b.grads_verified = true;
+        return fast_rn_domain(a.c) ? launch_staged<2, 4, 7>(b, stream)
+                                   : launch_staged<2, 4>(b, stream);
+    }
     if constexpr (V == 47)
         return fast_rn_domain(a.c) ? launch_wd<kF16, 0, kF16, Cfg<1, 7, 4>>(a, stream)
                                    : launch_dtypes<Cfg<1, true, 4>>(a, stream);
@@ -848,10 +832,15 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 51: return launch_variant<51>(a, stream);
         case 52: return launch_variant<52>(a, stream);
         case 53: return launch_variant<53>(a, stream);
+        case 54: return launch_variant<54>(a, stream);
+        case 55: return launch_variant<55>(a, stream);
+        case 56: return launch_variant<56>(a, stream);
+        case 57: return launch_variant<57>(a, stream);
+        case 58: return launch_variant<58>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 54; }
+int adam_variant_count() { return 59; }
 
 }  // namespace tfb

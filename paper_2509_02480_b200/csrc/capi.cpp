@@ -266,6 +266,7 @@ int tfg_adam_step(float* p, float* m, float* v, const uint16_t* grad, int grad_d
         tfb::cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
         if (h[0] != 0) throw tfb::GradientOverflowError("adam_step: non-finite gradients");
         a.counters = dc;
+        a.grads_verified = true;  // counted above
         tfb::cuda_check(tfb::launch_adam_fused(a, s), "adam_fused");
         tfb::cuda_check(cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync");
         tfb::cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");

@@ -1219,6 +1219,9 @@ std::pair<std::uint64_t, std::uint64_t> OffloadWorker::issue_device_update(Subgr
     a.out_kind = dev_.out_kind;
     a.c = c;
     a.counters = counters_;
+    // run_update awaited the whole-phase count of exactly these gradients
+    // (await_grad_verdict) before the first issue.
+    a.grads_verified = true;
     if (dev_.zero_copy == 1) {
         // The kernel streams P||m||v straight from and back to the pinned
         // slot over PCIe: reads and writes interleave at cache-line grain,

@@ -41,6 +41,10 @@ struct AdamLaunch {
     // it on the same stream rejects every later update of the phase without
     // a host round trip between the check and the updates.
     const unsigned long long* gate = nullptr;
+    // The gradients were counted finite by a whole-phase check before this
+    // launch (a host verdict, or the gate above): the kernel does not count
+    // them again, counters[0] is left alone.
+    bool grads_verified = false;
 };
 
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream);

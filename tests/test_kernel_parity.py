@@ -135,13 +135,14 @@ def test_extreme_values(tf, cuda):
 
 def test_nonfinite_gradients_are_counted_and_step_rejected(tf, cuda):
     import torch
-    n = 1000
-    g16 = oracle.synthetic_grads(n, 1, 0, 0)
-    g16[17] = 0x7C00
-    g16[500] = 0x7E01
-    p = np.ones(n, np.float32)
-    _, _, _, _, cnt = run_fused(tf, torch, cuda, p, p * 0, p * 0, g16, 1)
-    assert cnt[0] == 2
+    for n in (5000, 1000):  # the staged kernel (whole tiles) and the register kernel
+        g16 = oracle.synthetic_grads(n, 1, 0, 0)
+        g16[17] = 0x7C00
+        g16[500] = 0x7E01
+        g16[n - 1] = 0xFC00
+        p = np.ones(n, np.float32)
+        _, _, _, _, cnt = run_fused(tf, torch, cuda, p, p * 0, p * 0, g16, 1)
+        assert cnt[0] == 3, n
     # reference semantics (optimizer.hpp:123-127): reject before mutating
     P = torch.ones(n, device=cuda)
     Mm, V = torch.zeros(n, device=cuda), torch.zeros(n, device=cuda)
@@ -154,6 +155,38 @@ def test_nonfinite_gradients_are_counted_and_step_rejected(tf, cuda):
         tf.adam_step(P, Mm, V, G, p16, 0)  # t >= 1
     with pytest.raises(tf.ConfigError):
         tf.adam_step(P, Mm, V, G, p16, 1, tf.AdamHyper(beta1=1.0))
+
+
+@pytest.mark.parametrize("gk,ok", [(0, 0), (1, 1)])
+def test_gated_launch(tf, cuda, gk, ok):
+    """A gated launch takes the gate as the whole-phase non-finite count: gate 0
+    updates bit-exactly and counts overflows but not non-finite gradients
+    (counters[0] stays 0); a nonzero gate writes nothing."""
+    import torch
+    n = 100_003
+    rng = np.random.default_rng(3)
+    p = rng.uniform(-7e4, 7e4, n).astype(np.float32)
+    m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+    v = rng.uniform(0, 0.01, n).astype(np.float32)
+    g16 = oracle.synthetic_grads(n, 42, 5, 2, kind=gk)
+    want = oracle.adam_fused(p, m, v, g16, gk, ok, 3, weight_decay=0.0)
+    assert want[4] > 0 or ok == 1  # f16 outputs overflow here, bf16 ones cannot
+    P, Mm, V, G = _dev(torch, p, cuda), _dev(torch, m, cuda), _dev(torch, v, cuda), _u16(torch, g16, cuda)
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    counters = torch.zeros(2, dtype=torch.int64, device=cuda)
+    gate = torch.ones(1, dtype=torch.int64, device=cuda)
+    tf.adam_fused(P, Mm, V, G, p16, 3, tf.AdamHyper(), gk, ok, counters=counters, gate=gate)
+    torch.cuda.synchronize()
+    assert_bits(P.cpu().numpy(), p, "P untouched")
+    assert int(counters.abs().sum()) == 0 and int(p16.abs().sum()) == 0
+    gate.zero_()
+    tf.adam_fused(P, Mm, V, G, p16, 3, tf.AdamHyper(), gk, ok, counters=counters, gate=gate)
+    torch.cuda.synchronize()
+    for got, w, what in ((P, want[0], "P"), (Mm, want[1], "m"), (V, want[2], "v")):
+        assert_bits(got.cpu().numpy(), w, what)
+    assert np.array_equal(_np16(p16), want[3])
+    c = counters.cpu().numpy()
+    assert c[0] == 0 and c[1] == want[4]
 
 
 def test_adam_step_returns_overflows(tf, cuda):
@@ -230,7 +263,7 @@ def test_constant_division_matches_div_rn(tf, cuda):
             assert mism == 0, (beta, t, first)
 
 
-@pytest.mark.parametrize("variant", range(1, 51))
+@pytest.mark.parametrize("variant", range(1, 59))
 def test_kernel_variants_bitwise(tf, cuda, variant):
     import torch
     n = 1_000_003
