@@ -39,7 +39,8 @@ import sys
 sys.path.insert(0, ".")
 import torch
 from paper_2509_02480_b200 import tierflow as tf
-n = 1_003_520  # multiple of the TMA tile so every variant takes its main path
+# a multiple of the TMA tile so every variant takes its main path (argv[2]: another size, e.g. with a tail)
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_003_520
 variants = [int(v) for v in sys.argv[1].split(",")]
 for v in variants:
     st = torch.empty(3 * n, device="cuda"); g = torch.empty(n, dtype=torch.int16, device="cuda")
@@ -53,9 +54,12 @@ tf.adam_fused_multi(st[:n], st[n:2*n], st[2*n:], srcs, p16, 2, tf.AdamHyper())
 torch.cuda.synchronize()
 print("kernels ok")
 PY
-timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,1,12,16,32,36,38 > gpurun_out/san_memcheck_kernels.log 2>&1
+timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,1,12,16,32,36,38,54,55 > gpurun_out/san_memcheck_kernels.log 2>&1
 echo "memcheck kernels rc=$?"; tail -3 gpurun_out/san_memcheck_kernels.log
-timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 12,13,16,32,33,36,38,39 > gpurun_out/san_racecheck.log 2>&1
+# the shipped staged kernel with a tail (n % 1024 = 3: one partial tile's quads and scalars in the last CTA)
+timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,55 1003523 > gpurun_out/san_memcheck_tail.log 2>&1
+echo "memcheck staged tail rc=$?"; tail -3 gpurun_out/san_memcheck_tail.log
+timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 0,12,13,16,32,33,36,38,39,55 > gpurun_out/san_racecheck.log 2>&1
 echo "racecheck rc=$?"; tail -3 gpurun_out/san_racecheck.log
-timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 12,16,32,36,38 > gpurun_out/san_synccheck.log 2>&1
+timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 0,12,16,32,36,38,55 > gpurun_out/san_synccheck.log 2>&1
 echo "synccheck rc=$?"; tail -3 gpurun_out/san_synccheck.log
