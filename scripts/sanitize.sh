@@ -43,11 +43,13 @@ from paper_2509_02480_b200 import tierflow as tf
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1_003_520
 variants = [int(v) for v in sys.argv[1].split(",")]
 for v in variants:
-    st = torch.empty(3 * n, device="cuda"); g = torch.empty(n, dtype=torch.int16, device="cuda")
-    tf.synthetic_state(st[:n], st[n:2*n], st[2*n:], 1, 0); tf.synthetic_grads(g, 1, 0, 0)
+    # P, m, v in separate (aligned) allocations: any n keeps every stream 16-byte aligned
+    P, M, V = (torch.empty(n, device="cuda") for _ in range(3)); g = torch.empty(n, dtype=torch.int16, device="cuda")
+    tf.synthetic_state(P, M, V, 1, 0); tf.synthetic_grads(g, 1, 0, 0)
     p16 = torch.empty(n, dtype=torch.int16, device="cuda")
-    tf.adam_fused_variant(v, st[:n], st[n:2*n], st[2*n:], g, p16, 1, tf.AdamHyper())
+    tf.adam_fused_variant(v, P, M, V, g, p16, 1, tf.AdamHyper())
     torch.cuda.synchronize()
+st = torch.empty(3 * n, device="cuda")
 srcs = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(3)]
 for s_ in srcs: tf.synthetic_grads(s_, 2, 0, 0)
 tf.adam_fused_multi(st[:n], st[n:2*n], st[2*n:], srcs, p16, 2, tf.AdamHyper())
