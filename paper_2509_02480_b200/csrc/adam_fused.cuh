@@ -268,16 +268,11 @@ __global__ void __launch_bounds__(kThreads, MINB)
                         adam_math<WD, DIVC>(rp[u].z, rm[u].z, rv[u].z, rg[u].get(2), c);
                         adam_math<WD, DIVC>(rp[u].w, rm[u].w, rv[u].w, rg[u].get(3), c);
                     }
-                    U16x4 h;
-                    h.x = narrow16<OK>(rp[u].x);
-                    h.y = narrow16<OK>(rp[u].y);
-                    h.z = narrow16<OK>(rp[u].z);
-                    h.w = narrow16<OK>(rp[u].w);
-                    overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
+                    const uint2 h = narrow16_quad<OK>(rp[u], overflow);
                     st_state<PF>(po4 + q, rp[u]);
                     st_state<PF>(mo4 + q, rm[u]);
                     st_state<PF>(vo4 + q, rv[u]);
-                    store_u16x4(p16 + 4 * q, h);
+                    __stcs(reinterpret_cast<uint2*>(p16) + q, h);
                 }
             }
         }
@@ -337,16 +332,11 @@ __device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uin
         adam_math<WD, MATH>(rp.z, rm.z, rv.z, rg.get(2), c);
         adam_math<WD, MATH>(rp.w, rm.w, rv.w, rg.get(3), c);
     }
-    U16x4 h;
-    h.x = narrow16<OK>(rp.x);
-    h.y = narrow16<OK>(rp.y);
-    h.z = narrow16<OK>(rp.z);
-    h.w = narrow16<OK>(rp.w);
-    overflow += is_inf16<OK>(h.x) + is_inf16<OK>(h.y) + is_inf16<OK>(h.z) + is_inf16<OK>(h.w);
+    const uint2 h = narrow16_quad<OK>(rp, overflow);
     __stcs(reinterpret_cast<float4*>(p) + qi, rp);
     __stcs(reinterpret_cast<float4*>(m) + qi, rm);
     __stcs(reinterpret_cast<float4*>(v) + qi, rv);
-    store_u16x4(p16 + 4 * qi, h);
+    __stcs(reinterpret_cast<uint2*>(p16) + qi, h);
 }
 
 // ---------------------------------------------------------------------------
@@ -361,13 +351,13 @@ __device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uin
 // kernel's loads are only in flight between two quads' math). Tile T =
 // 1024 params (one quad per thread); one CTA barrier per tile retires a stage
 // before it is refilled. The same element math, bit for bit.
-template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1>
+template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_staged_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                        const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                        unsigned long long* __restrict__ counters, const unsigned long long* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;  // the phase was rejected on this stream: no writes
-    constexpr int T = 4 * kThreads;
+    constexpr int T = 4 * kThreads * Q;  // Q quads per thread per tile
     const uint64_t ntiles = n / T;
     extern __shared__ __align__(128) unsigned char smem[];
     float* sp = reinterpret_cast<float*>(smem);
@@ -399,12 +389,16 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const int s = static_cast<int>(k % S);
         mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
         const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
-        float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qi];
-        float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qi];
-        float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qi];
-        const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qi];
-        staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + off, m + off, v + off,
-                                           p16 + off, qi);
+#pragma unroll 1
+        for (int qq = 0; qq < Q; ++qq) {
+            const int qj = qi + qq * kThreads;
+            const float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qj];
+            const float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qj];
+            const float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qj];
+            const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qj];
+            staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + off, m + off, v + off,
+                                               p16 + off, qj);
+        }
         __syncthreads();  // stage s retired: it is refilled at iteration k + 1
     }
     // The n % T tail (fewer than T params, whole quads then scalars) from
@@ -412,14 +406,14 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (blockIdx.x == gridDim.x - 1) {
         const uint64_t done = ntiles * T;
         const uint64_t nq = (n - done) / 4;
-        if (static_cast<uint64_t>(threadIdx.x) < nq) {
-            const uint64_t q = done / 4 + threadIdx.x;
+        for (uint64_t j = threadIdx.x; j < nq; j += kThreads) {
+            const uint64_t q = done / 4 + j;
             const float4 rp = __ldcs(reinterpret_cast<const float4*>(p) + q);
             const float4 rm = __ldcs(reinterpret_cast<const float4*>(m) + q);
             const float4 rv = __ldcs(reinterpret_cast<const float4*>(v) + q);
             const uint2 graw = __ldcs(reinterpret_cast<const uint2*>(g) + q);
             staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + done, m + done,
-                                               v + done, p16 + done, threadIdx.x);
+                                               v + done, p16 + done, static_cast<int>(j));
         }
         const uint64_t i = done + 4 * nq + threadIdx.x;
         if (i < n) {
@@ -544,9 +538,9 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
 // fit the staged form (summed or fp32 gradients, separate outputs, 16-byte
 // misalignment, fewer than one tile); the caller then launches the register
 // kernel.
-template <int S, int MINB, int MATH = 1>
+template <int S, int MINB, int MATH = 1, int Q = 1>
 cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
-    constexpr uint64_t T = 4 * kThreads;
+    constexpr uint64_t T = 4 * kThreads * Q;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
                            reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
                            reinterpret_cast<uintptr_t>(a.p16);
@@ -562,11 +556,11 @@ cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
     auto pick = [&](auto gk, auto ok) {
         constexpr int GKc = decltype(gk)::value, OKc = decltype(ok)::value;
         if (cnt)
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH>
-                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q>
+                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q>;
         else
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH>
-                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH, Q>
+                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH, Q>;
     };
     using F = std::integral_constant<int, kF16>;
     using B = std::integral_constant<int, kBF16>;

@@ -16,7 +16,9 @@
 //                       whole-phase check (53), f16 gradients widened straight to binary64 (52), both (51)
 //   54-57               the staged kernel (adam_fused.cuh adam_staged_kernel): S = 2 / 4 CTAs counting (54)
 //                       and verified (55), S = 3 / 4 CTAs (56), S = 3 / 3 CTAs (57); 55 with variant 47's
-//                       in-range sqrt / division (58)
+//                       in-range sqrt / division (58); 3 stages / 4 CTAs (59), 2-quad tiles: 2 stages /
+//                       3 CTAs (60), 3 stages / 2 CTAs (61), 4 stages / 2 CTAs (62); 4-quad tiles at 1 CTA
+//                       per SM: 3 stages (63), 2 stages (64)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -703,6 +705,16 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
         constexpr int M = V == 57 ? 3 : 4;
         return launch_staged<S, M>(b, stream);
     }
+    if constexpr (V >= 59 && V <= 64) {  // deeper staging / larger tiles (S stages, M CTAs per SM, Q quads per thread)
+        AdamLaunch b = a;
+        b.grads_verified = true;
+        if constexpr (V == 59) return launch_staged<3, 4>(b, stream);
+        if constexpr (V == 60) return launch_staged<2, 3, 1, 2>(b, stream);
+        if constexpr (V == 61) return launch_staged<3, 2, 1, 2>(b, stream);
+        if constexpr (V == 62) return launch_staged<4, 2, 1, 2>(b, stream);
+        if constexpr (V == 63) return launch_staged<3, 1, 1, 4>(b, stream);
+        return launch_staged<2, 1, 1, 4>(b, stream);
+    }
     if constexpr (V == 58) {  // staged + in-range sqrt / division (domain-gated, as variant 47)
         AdamLaunch b = a;
         b.grads_verified = true;
@@ -837,10 +849,16 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 56: return launch_variant<56>(a, stream);
         case 57: return launch_variant<57>(a, stream);
         case 58: return launch_variant<58>(a, stream);
+        case 59: return launch_variant<59>(a, stream);
+        case 60: return launch_variant<60>(a, stream);
+        case 61: return launch_variant<61>(a, stream);
+        case 62: return launch_variant<62>(a, stream);
+        case 63: return launch_variant<63>(a, stream);
+        case 64: return launch_variant<64>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 59; }
+int adam_variant_count() { return 65; }
 
 }  // namespace tfb
