@@ -1009,8 +1009,12 @@ PhaseStats OffloadWorker::run_update(int iteration) {
         std::size_t next = 0;
         std::deque<cudaEvent_t> h2d_queued;  // h2d_done of the state copies issued and not yet drained
         auto h2d_backlog = [&] {
-            while (!h2d_queued.empty() && cudaEventQuery(h2d_queued.front()) == cudaSuccess) h2d_queued.pop_front();
-            (void)cudaGetLastError();  // cudaErrorNotReady
+            while (!h2d_queued.empty()) {
+                const cudaError_t q = cudaEventQuery(h2d_queued.front());
+                if (q == cudaErrorNotReady) break;
+                cuda_check(q, "cudaEventQuery(h2d)");
+                h2d_queued.pop_front();
+            }
             return static_cast<int>(h2d_queued.size());
         };
         for (std::size_t done = 0; done < order.size(); ++done) {
