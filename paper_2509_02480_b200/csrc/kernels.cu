@@ -103,7 +103,24 @@ __global__ void __launch_bounds__(kThreads)
     const uint4* s8 = reinterpret_cast<const uint4*>(src);
     const bool vec = (reinterpret_cast<uintptr_t>(src) & 15u) == 0;
     if (vec) {
-        for (uint64_t q = tid; q < nq; q += nthreads) {
+        // 4 independent 16-byte loads in flight per thread before any is
+        // counted: a read-only stream needs the bytes in flight, not the ALU.
+        constexpr int U = 4;
+        uint64_t q = tid;
+        for (; q + (U - 1) * nthreads < nq; q += U * nthreads) {
+            uint4 r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = __ldcs(s8 + q + u * nthreads);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t w[4] = {r[u].x, r[u].y, r[u].z, r[u].w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    bad += nonfinite16<K>(static_cast<uint16_t>(w[k] & 0xFFFFu)) +
+                           nonfinite16<K>(static_cast<uint16_t>(w[k] >> 16));
+            }
+        }
+        for (; q < nq; q += nthreads) {
             const uint4 r = __ldcs(s8 + q);
             const uint32_t w[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
