@@ -351,7 +351,7 @@ __device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uin
 // kernel's loads are only in flight between two quads' math). Tile T =
 // 1024 params (one quad per thread); one CTA barrier per tile retires a stage
 // before it is refilled. The same element math, bit for bit.
-template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1>
+template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     adam_staged_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                        const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
@@ -386,6 +386,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
     const int qi = threadIdx.x;
     for (uint64_t k = 0; k < mine; ++k) {
         if (threadIdx.x == 0 && k + S - 1 < mine) issue(k + S - 1);  // into the stage tile k-1 released
+        if constexpr (PFL2 > 0) {  // tuning: tile k + S - 1 + PFL2 pulled into L2 ahead of its bulk load
+            if (threadIdx.x == 0 && k + S - 1 + PFL2 < mine) {
+                const uint64_t po = (blockIdx.x + (k + S - 1 + PFL2) * gridDim.x) * static_cast<uint64_t>(T);
+                prefetch_l2(p + po, 4u * T);
+                prefetch_l2(m + po, 4u * T);
+                prefetch_l2(v + po, 4u * T);
+                prefetch_l2(g + po, 2u * T);
+            }
+        }
         const int s = static_cast<int>(k % S);
         mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
         const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
@@ -538,7 +547,7 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
 // fit the staged form (summed or fp32 gradients, separate outputs, 16-byte
 // misalignment, fewer than one tile); the caller then launches the register
 // kernel.
-template <int S, int MINB, int MATH = 1, int Q = 1>
+template <int S, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0>
 cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
     constexpr uint64_t T = 4 * kThreads * Q;
     const uintptr_t addr = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
@@ -556,11 +565,11 @@ cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
     auto pick = [&](auto gk, auto ok) {
         constexpr int GKc = decltype(gk)::value, OKc = decltype(ok)::value;
         if (cnt)
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q>
-                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2>
+                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2>;
         else
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH, Q>
-                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH, Q>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH, Q, PFL2>
+                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH, Q, PFL2>;
     };
     using F = std::integral_constant<int, kF16>;
     using B = std::integral_constant<int, kBF16>;

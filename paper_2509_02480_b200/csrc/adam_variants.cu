@@ -18,7 +18,8 @@
 //                       and verified (55), S = 3 / 4 CTAs (56), S = 3 / 3 CTAs (57); 55 with variant 47's
 //                       in-range sqrt / division (58); 3 stages / 4 CTAs (59), 2-quad tiles: 2 stages /
 //                       3 CTAs (60), 3 stages / 2 CTAs (61), 4 stages / 2 CTAs (62); 4-quad tiles at 1 CTA
-//                       per SM: 3 stages (63), 2 stages (64)
+//                       per SM: 3 stages (63), 2 stages (64); the shipped shape with an L2 bulk prefetch 1 (65)
+//                       or 2 (66) tiles beyond its look-ahead
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -715,6 +716,11 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
         if constexpr (V == 63) return launch_staged<3, 1, 1, 4>(b, stream);
         return launch_staged<2, 1, 1, 4>(b, stream);
     }
+    if constexpr (V == 65 || V == 66) {  // shipped shape + L2 prefetch 1 / 2 tiles beyond the staged look-ahead
+        AdamLaunch b = a;
+        b.grads_verified = true;
+        return launch_staged<2, 4, 1, 1, V == 65 ? 1 : 2>(b, stream);
+    }
     if constexpr (V == 58) {  // staged + in-range sqrt / division (domain-gated, as variant 47)
         AdamLaunch b = a;
         b.grads_verified = true;
@@ -855,10 +861,12 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 62: return launch_variant<62>(a, stream);
         case 63: return launch_variant<63>(a, stream);
         case 64: return launch_variant<64>(a, stream);
+        case 65: return launch_variant<65>(a, stream);
+        case 66: return launch_variant<66>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 65; }
+int adam_variant_count() { return 67; }
 
 }  // namespace tfb
