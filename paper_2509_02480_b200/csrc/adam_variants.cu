@@ -20,6 +20,8 @@
 //                       3 CTAs (60), 3 stages / 2 CTAs (61), 4 stages / 2 CTAs (62); 4-quad tiles at 1 CTA
 //                       per SM: 3 stages (63), 2 stages (64); the shipped shape with an L2 bulk prefetch 1 (65)
 //                       or 2 (66) tiles beyond its look-ahead
+//   67                  tile-interleaved state layout ([P | m | v] per 1024-param tile; timing only, its bits
+//                       land in the interleaved positions — scripts/layout_probe.py, not the bitwise test)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -645,6 +647,70 @@ __global__ void fast_rn_selftest_kernel(uint64_t n, uint64_t seed, unsigned long
 }
 
 
+// ---------------------------------------------------------------------------
+// Layout experiment (variant 67): the state tile-interleaved in HBM — for each
+// tile of T = 1024 params, P, m and v contiguous ([P | m | v], 12 KiB) — so a
+// tile is one 12 KiB bulk load and three contiguous stores, and the DRAM
+// sees two read and two write streams per tile instead of four and four.
+// `p` is the interleaved buffer's base (m, v unused); g and p16 as usual.
+// Same element math; the bits land in the interleaved positions.
+template <bool WD>
+__global__ void __launch_bounds__(kThreads, 4)
+    adam_staged_interleaved_kernel(float* __restrict__ st, const uint16_t* __restrict__ g, uint16_t* __restrict__ p16,
+                                   uint64_t ntiles, AdamConsts c, unsigned long long* __restrict__ counters) {
+    constexpr int S = 2;
+    constexpr int T = 4 * kThreads;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* sst = reinterpret_cast<float*>(smem);                    // S x [P | m | v]
+    uint16_t* sg = reinterpret_cast<uint16_t*>(sst + S * 3 * T);     // S x g
+    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const uint64_t mine = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    auto issue = [&](uint64_t k) {
+        const int s = static_cast<int>(k % S);
+        const uint64_t t = blockIdx.x + k * gridDim.x;
+        mbar_arrive_expect_tx(&full[s], 14u * T);
+        bulk_load(sst + s * 3 * T, st + t * 3 * T, 12u * T, &full[s]);
+        bulk_load(sg + s * T, g + t * T, 2u * T, &full[s]);
+    };
+    if (threadIdx.x == 0 && mine > 0) issue(0);
+    unsigned nonfinite = 0, overflow = 0;
+    const int qi = threadIdx.x;
+    for (uint64_t k = 0; k < mine; ++k) {
+        if (threadIdx.x == 0 && k + 1 < mine) issue(k + 1);
+        const int s = static_cast<int>(k % S);
+        mbar_wait(&full[s], static_cast<uint32_t>(k / S) & 1u);
+        const uint64_t t = blockIdx.x + k * gridDim.x;
+        const float* ss = sst + s * 3 * T;
+        const float4 rp = reinterpret_cast<const float4*>(ss)[qi];
+        const float4 rm = reinterpret_cast<const float4*>(ss + T)[qi];
+        const float4 rv = reinterpret_cast<const float4*>(ss + 2 * T)[qi];
+        const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qi];
+        float* dst = st + t * 3 * T;
+        staged_quad<kF16, kF16, WD, false, 1>(rp, rm, rv, graw, c, nonfinite, overflow, dst, dst + T, dst + 2 * T,
+                                              p16 + t * T, qi);
+        __syncthreads();
+    }
+    if (counters != nullptr) warp_count_add(counters + 1, overflow);
+}
+
+cudaError_t launch_staged_interleaved(const AdamLaunch& a, cudaStream_t stream) {
+    constexpr uint64_t T = 4 * kThreads;
+    const uint64_t ntiles = a.n / T;  // timing experiment: whole tiles only
+    if (ntiles == 0) return cudaErrorInvalidValue;
+    constexpr size_t smem = 2 * T * 14 + 2 * sizeof(uint64_t);
+    auto kern = a.c.lr_wd != 0.0 ? adam_staged_interleaved_kernel<true> : adam_staged_interleaved_kernel<false>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * 4));
+    kern<<<grid, kThreads, smem, stream>>>(a.p, static_cast<const uint16_t*>(a.g), a.p16, ntiles, a.c, a.counters);
+    return cudaGetLastError();
+}
+
 template <int V>
 cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
     if constexpr (V == 1) return launch_wd<kF16, 0, kF16, Cfg<2, false, 1>>(a, stream);
@@ -716,6 +782,7 @@ cudaError_t launch_variant(const AdamLaunch& a, cudaStream_t stream) {
         if constexpr (V == 63) return launch_staged<3, 1, 1, 4>(b, stream);
         return launch_staged<2, 1, 1, 4>(b, stream);
     }
+    if constexpr (V == 67) return launch_staged_interleaved(a, stream);
     if constexpr (V == 65 || V == 66) {  // shipped shape + L2 prefetch 1 / 2 tiles beyond the staged look-ahead
         AdamLaunch b = a;
         b.grads_verified = true;
@@ -863,10 +930,11 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
         case 64: return launch_variant<64>(a, stream);
         case 65: return launch_variant<65>(a, stream);
         case 66: return launch_variant<66>(a, stream);
+        case 67: return launch_variant<67>(a, stream);
         default: return cudaErrorInvalidValue;
     }
 }
 
-int adam_variant_count() { return 67; }
+int adam_variant_count() { return 68; }
 
 }  // namespace tfb
