@@ -16,6 +16,8 @@ import bench  # noqa: E402
 from paper_2509_02480_b200 import tierflow as tf  # noqa: E402
 
 variants = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,26").split(",")]
+if 67 in variants:  # it reads the state as tile-interleaved: it would corrupt the shared P || m || v buffers
+    sys.exit("variant 67 changes the state layout: use scripts/layout_probe.py")
 rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 steps = int(sys.argv[3]) if len(sys.argv) > 3 else 6
 sizes = bench.subgroup_sizes(6_738_415_616, 100_000_000)
