@@ -26,6 +26,13 @@ int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint
                            uint64_t n, const tfg_adam_hyper* hyper, uint64_t t, unsigned long long* counters,
                            void* stream);
 
+/* The fused reduce + update (tfg_adam_fused_multi) in form `variant`:
+ * 0 = the staged n-source kernel (2, 4 or 8 sources), 1 = the register
+ * n-source kernel. F16/F16. */
+int tfg_adam_fused_multi_variant(int variant, float* p, float* m, float* v, const void* const* grads, int n_sources,
+                                 uint16_t* param16, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                                 unsigned long long* counters, void* stream);
+
 /* Self-test of the second verified fast path (variants 44-46): the largest
  * relative error of its approximate step against the exact chain over n
  * random (m, v, t), and the elements whose P/m/v bits differ from the

@@ -235,6 +235,8 @@ _SIGS = {
 _TUNING_SIGS = {
     "tfg_adam_variant_count": (_i, [C.POINTER(_i)]),
     "tfg_adam_fused_variant": (_i, [_i, _vp, _vp, _vp, _vp, _vp, _u64, C.POINTER(AdamHyperC), _u64, _vp, _vp]),
+    "tfg_adam_fused_multi_variant": (_i, [_i, _vp, _vp, _vp, C.POINTER(_vp), _i, _vp, _u64, C.POINTER(AdamHyperC),
+                                          _u64, _vp, _vp]),
     "tfg_selftest_fast_step": (_i, [_u64, _u64, C.POINTER(_d), C.POINTER(_u64)]),
     "tfg_selftest_fast_rn": (_i, [_u64, _u64, C.POINTER(_u64)]),
 }

@@ -39,6 +39,31 @@ struct GradSources {
     int n;
 };
 
+__device__ __forceinline__ uint2 pack_u16x4(const U16x4& h) {
+    return make_uint2(static_cast<uint32_t>(h.x) | (static_cast<uint32_t>(h.y) << 16),
+                      static_cast<uint32_t>(h.z) | (static_cast<uint32_t>(h.w) << 16));
+}
+
+// In-order fp32 sum of NS quads already loaded, rounded once to GK (the same
+// rule as sum_quad16).
+template <int GK, int NS>
+__device__ __forceinline__ U16x4 sum16x4(const U16x4 (&x)[NS]) {
+    float4 acc = make_float4(-0.f, -0.f, -0.f, -0.f);
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        acc.x = __fadd_rn(acc.x, widen16<GK>(x[s].x));
+        acc.y = __fadd_rn(acc.y, widen16<GK>(x[s].y));
+        acc.z = __fadd_rn(acc.z, widen16<GK>(x[s].z));
+        acc.w = __fadd_rn(acc.w, widen16<GK>(x[s].w));
+    }
+    U16x4 h;
+    h.x = narrow16<GK>(acc.x);
+    h.y = narrow16<GK>(acc.y);
+    h.z = narrow16<GK>(acc.z);
+    h.w = narrow16<GK>(acc.w);
+    return h;
+}
+
 // In-order fp32 sum of one quad over the sources, rounded once to GK.
 template <int GK, int NS>
 __device__ __forceinline__ U16x4 sum_quad16(const GradSources& gs, uint64_t q) {
@@ -351,20 +376,25 @@ __device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uin
 // kernel's loads are only in flight between two quads' math). Tile T =
 // 1024 params (one quad per thread); one CTA barrier per tile retires a stage
 // before it is refilled. The same element math, bit for bit.
-template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0>
+// NS > 0: the gradient is the in-order fp32 sum of NS 16-bit sources (the
+// peers' contributions, NVLink-mapped), each staged by its own bulk copy per
+// tile and summed from shared memory, rounded once to GK (sum_quad16's rule).
+template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0, int NS = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
-    adam_staged_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                       const uint16_t* __restrict__ g, uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
+    adam_staged_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const GradSources gs,
+                       uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                        unsigned long long* __restrict__ counters, const unsigned long long* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;  // the phase was rejected on this stream: no writes
     constexpr int T = 4 * kThreads * Q;  // Q quads per thread per tile
+    constexpr int G = NS > 0 ? NS : 1;   // gradient tiles per stage
+    const uint16_t* __restrict__ g = static_cast<const uint16_t*>(gs.src[0]);
     const uint64_t ntiles = n / T;
     extern __shared__ __align__(128) unsigned char smem[];
     float* sp = reinterpret_cast<float*>(smem);
     float* sm = sp + S * T;
     float* sv = sm + S * T;
     uint16_t* sg = reinterpret_cast<uint16_t*>(sv + S * T);
-    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * T);
+    uint64_t* full = reinterpret_cast<uint64_t*>(sg + S * G * T);
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -374,11 +404,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
     auto issue = [&](uint64_t k) {
         const int s = static_cast<int>(k % S);
         const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
-        mbar_arrive_expect_tx(&full[s], 14u * T);
+        mbar_arrive_expect_tx(&full[s], (12u + 2u * G) * T);
         bulk_load(sp + s * T, p + off, 4u * T, &full[s]);
         bulk_load(sm + s * T, m + off, 4u * T, &full[s]);
         bulk_load(sv + s * T, v + off, 4u * T, &full[s]);
-        bulk_load(sg + s * T, g + off, 2u * T, &full[s]);
+#pragma unroll
+        for (int j = 0; j < G; ++j)
+            bulk_load(sg + (s * G + j) * T, static_cast<const uint16_t*>(gs.src[j]) + off, 2u * T, &full[s]);
     };
     if (threadIdx.x == 0)
         for (uint64_t k = 0; k + 1 < static_cast<uint64_t>(S) && k < mine; ++k) issue(k);
@@ -404,7 +436,19 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qj];
             const float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qj];
             const float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qj];
-            const uint2 graw = reinterpret_cast<const uint2*>(sg + s * T)[qj];
+            uint2 graw;
+            if constexpr (NS == 0) {
+                graw = reinterpret_cast<const uint2*>(sg + s * T)[qj];
+            } else {
+                U16x4 x[NS];
+#pragma unroll
+                for (int j = 0; j < NS; ++j) {
+                    const uint2 r = reinterpret_cast<const uint2*>(sg + (s * G + j) * T)[qj];
+                    x[j] = U16x4{static_cast<uint16_t>(r.x & 0xFFFFu), static_cast<uint16_t>(r.x >> 16),
+                                 static_cast<uint16_t>(r.y & 0xFFFFu), static_cast<uint16_t>(r.y >> 16)};
+                }
+                graw = pack_u16x4(sum16x4<GK, NS>(x));
+            }
             staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + off, m + off, v + off,
                                                p16 + off, qj);
         }
@@ -420,14 +464,25 @@ __global__ void __launch_bounds__(kThreads, MINB)
             const float4 rp = __ldcs(reinterpret_cast<const float4*>(p) + q);
             const float4 rm = __ldcs(reinterpret_cast<const float4*>(m) + q);
             const float4 rv = __ldcs(reinterpret_cast<const float4*>(v) + q);
-            const uint2 graw = __ldcs(reinterpret_cast<const uint2*>(g) + q);
+            uint2 graw;
+            if constexpr (NS == 0) graw = __ldcs(reinterpret_cast<const uint2*>(g) + q);
+            else graw = pack_u16x4(sum_quad16<GK, NS>(gs, q));
             staged_quad<GK, OK, WD, CNT, MATH>(rp, rm, rv, graw, c, nonfinite, overflow, p + done, m + done,
                                                v + done, p16 + done, static_cast<int>(j));
         }
         const uint64_t i = done + 4 * nq + threadIdx.x;
         if (i < n) {
             float pf = __ldcs(p + i), mf = __ldcs(m + i), vf = __ldcs(v + i);
-            const uint16_t gh = __ldcs(g + i);
+            uint16_t gh;
+            if constexpr (NS == 0) {
+                gh = __ldcs(g + i);
+            } else {
+                float acc = -0.f;  // -0 + x == x: the sum starts at source 0
+#pragma unroll
+                for (int j = 0; j < NS; ++j)
+                    acc = __fadd_rn(acc, widen16<GK>(__ldcs(static_cast<const uint16_t*>(gs.src[j]) + i)));
+                gh = narrow16<GK>(acc);
+            }
             if constexpr (CNT) nonfinite += nonfinite16<GK>(gh);
             adam_math<WD, 1>(pf, mf, vf, widen16<GK>(gh), c);
             const uint16_t h = narrow16<OK>(pf);
@@ -543,44 +598,51 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
 
 
 // One launch of the staged kernel (its last CTA takes the n % 1024 tail).
-// Returns cudaErrorNotSupported, launching nothing, when the launch does not
-// fit the staged form (summed or fp32 gradients, separate outputs, 16-byte
-// misalignment, fewer than one tile); the caller then launches the register
-// kernel.
-template <int S, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0>
+// NS > 0: the fused multi-source form, a.n_peers == NS. Returns
+// cudaErrorNotSupported, launching nothing, when the launch does not fit the
+// staged form (fp32 gradients, a source count other than NS, separate
+// outputs, 16-byte misalignment, fewer than one tile); the caller then
+// launches the register kernel.
+template <int S, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0, int NS = 0>
 cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
     constexpr uint64_t T = 4 * kThreads * Q;
-    const uintptr_t addr = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
-                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g) |
-                           reinterpret_cast<uintptr_t>(a.p16);
-    if (a.n_peers > 0 || a.p_out || a.m_out || a.v_out || (a.grad_kind != kF16 && a.grad_kind != kBF16) ||
+    constexpr int G = NS > 0 ? NS : 1;
+    const GradSources gs = sources_of(a);
+    uintptr_t addr = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                     reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.p16);
+    for (int j = 0; j < gs.n; ++j) addr |= reinterpret_cast<uintptr_t>(gs.src[j]);
+    if (a.n_peers != NS || a.p_out || a.m_out || a.v_out || (a.grad_kind != kF16 && a.grad_kind != kBF16) ||
         (a.out_kind != kF16 && a.out_kind != kBF16) || (addr & 15u) != 0 || a.n < T)
         return cudaErrorNotSupported;
     const uint64_t ntiles = a.n / T;
-    const bool cnt = !(a.grads_verified || a.gate != nullptr);
+    // a summed gradient is only known after the sum: counted in-kernel
+    const bool cnt = NS > 0 || !(a.grads_verified || a.gate != nullptr);
     const bool wd = a.c.lr_wd != 0.0;
-    using K = void (*)(float*, float*, float*, const uint16_t*, uint16_t*, uint64_t, AdamConsts, unsigned long long*,
-                       const unsigned long long*);
+    using K = void (*)(float*, float*, float*, const GradSources, uint16_t*, uint64_t, AdamConsts,
+                       unsigned long long*, const unsigned long long*);
     K kern = nullptr;
     auto pick = [&](auto gk, auto ok) {
         constexpr int GKc = decltype(gk)::value, OKc = decltype(ok)::value;
-        if (cnt)
+        if constexpr (NS > 0) {
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2, NS>
+                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2, NS>;
+        } else if (cnt) {
             kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2>
                       : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2>;
-        else
+        } else {
             kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH, Q, PFL2>
                       : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH, Q, PFL2>;
+        }
     };
     using F = std::integral_constant<int, kF16>;
     using B = std::integral_constant<int, kBF16>;
     if (a.grad_kind == kF16) a.out_kind == kF16 ? pick(F{}, F{}) : pick(F{}, B{});
     else a.out_kind == kF16 ? pick(B{}, F{}) : pick(B{}, B{});
-    constexpr size_t smem = static_cast<size_t>(S) * T * 14 + S * sizeof(uint64_t);
+    constexpr size_t smem = static_cast<size_t>(S) * T * (12 + 2 * G) + S * sizeof(uint64_t);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
-    kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, static_cast<const uint16_t*>(a.g), a.p16, a.n, a.c,
-                                           a.counters, a.gate);
+    kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters, a.gate);
     return cudaGetLastError();
 }
 

@@ -64,7 +64,17 @@ __global__ void divtest_kernel(double b, double y, uint64_t n, uint64_t seed, in
 
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
-    const cudaError_t e = launch_staged<kStages, kStagedCtasPerSm>(a, stream);
+    cudaError_t e = cudaErrorNotSupported;
+    // The fused exchange sums n ranks' contributions in the update. With the
+    // sources in local HBM under sustained load (profiles/multi_sustained_r2.json)
+    // the staged form wins at 8 sources (0.920 vs 0.876 of the copy peak) and
+    // the register form at 2 and 4 (0.938 / 0.956 vs 0.892), whose extra
+    // loads per thread already keep enough bytes in flight.
+    switch (a.n_peers) {
+        case 0: e = launch_staged<kStages, kStagedCtasPerSm>(a, stream); break;
+        case 8: e = launch_staged<kStages, 3, 1, 1, 0, 8>(a, stream); break;  // 56 KiB per CTA: 3 fit an SM
+        default: break;
+    }
     if (e != cudaErrorNotSupported) return e;
     return launch_dtypes<VariantDefault>(a, stream);
 }

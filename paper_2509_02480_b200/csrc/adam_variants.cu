@@ -859,6 +859,17 @@ cudaError_t launch_fast_step_selftest(uint64_t n, uint64_t seed, unsigned long l
     return cudaGetLastError();
 }
 
+cudaError_t launch_adam_fused_multi_variant(const AdamLaunch& a, int variant, cudaStream_t stream) {
+    if (a.n == 0) return cudaSuccess;
+    if (variant == 1) return launch_dtypes<Cfg<1, true, 4>>(a, stream);
+    // 0: the staged n-source kernel (2, 4, 8 sources; anything else the register form)
+    cudaError_t e = cudaErrorNotSupported;
+    if (a.n_peers == 2) e = launch_staged<2, 4, 1, 1, 0, 2>(a, stream);
+    if (a.n_peers == 4) e = launch_staged<2, 4, 1, 1, 0, 4>(a, stream);
+    if (a.n_peers == 8) e = launch_staged<2, 3, 1, 1, 0, 8>(a, stream);
+    return e == cudaErrorNotSupported ? launch_dtypes<Cfg<1, true, 4>>(a, stream) : e;
+}
+
 cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
     if (variant == 0) return launch_adam_fused(a, stream);

@@ -50,6 +50,8 @@ struct AdamLaunch {
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream);
 // Tuning variants of the fused kernel (0 = default; F16/F16 only otherwise).
 cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStream_t stream);
+// The n-source launch in form `variant` (0 = shipped dispatch, 1 = register kernel).
+cudaError_t launch_adam_fused_multi_variant(const AdamLaunch& a, int variant, cudaStream_t stream);
 int adam_variant_count();
 // Self-test of the second verified fast path: out[0] = largest |D'/D - 1| (double bits), out[1] += bit mismatches.
 cudaError_t launch_fast_step_selftest(uint64_t n, uint64_t seed, unsigned long long* out, cudaStream_t stream);

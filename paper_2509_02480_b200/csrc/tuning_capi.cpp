@@ -71,6 +71,37 @@ int tfg_adam_fused_variant(int variant, float* p, float* m, float* v, const uint
     });
 }
 
+int tfg_adam_fused_multi_variant(int variant, float* p, float* m, float* v, const void* const* grads, int n_sources,
+                                 uint16_t* param16, uint64_t n, const tfg_adam_hyper* hyper, uint64_t t,
+                                 unsigned long long* counters, void* stream) {
+    return guard([&] {
+        if (variant < 0 || variant > 1) throw tfb::ConfigError("unknown multi-source kernel form");
+        if (hyper == nullptr) throw tfb::ConfigError("hyper must not be NULL");
+        if (n_sources < 1 || n_sources > tfb::kMaxGradSources) throw tfb::ConfigError("1..8 gradient sources");
+        if (n > 0 && (!p || !m || !v || !grads || !param16)) throw tfb::ConfigError("null buffer");
+        tfb::AdamHyper h;
+        h.lr = hyper->lr;
+        h.beta1 = hyper->beta1;
+        h.beta2 = hyper->beta2;
+        h.eps = hyper->eps;
+        h.weight_decay = hyper->weight_decay;
+        tfb::AdamLaunch a;
+        a.p = p;
+        a.m = m;
+        a.v = v;
+        for (int s = 0; s < n_sources; ++s) a.peers[s] = grads[s];
+        a.n_peers = n_sources;
+        a.p16 = param16;
+        a.n = n;
+        a.grad_kind = TFG_F16;
+        a.out_kind = TFG_F16;
+        a.c = h.consts(t);
+        a.counters = counters;
+        tfb::cuda_check(tfb::launch_adam_fused_multi_variant(a, variant, static_cast<cudaStream_t>(stream)),
+                        "adam_fused_multi_variant");
+    });
+}
+
 int tfg_selftest_fast_step(uint64_t n, uint64_t seed, double* worst_rel_err, uint64_t* mismatches) {
     return guard([&] {
         unsigned long long* d = nullptr;

@@ -815,6 +815,17 @@ def adam_fused_variant(variant: int, p, m, v, grad16, param16, t: int, hyper: Ad
               C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
 
 
+def adam_fused_multi_variant(variant: int, p, m, v, grads: Sequence, param16, t: int, hyper: AdamHyper = AdamHyper(),
+                             counters=None, stream=None) -> None:
+    """Tuning hook: the n-source reduce + update in form `variant` (0 = staged kernel for 2/4/8 sources,
+    1 = register kernel; F16/F16). grads: tensors or raw device pointers."""
+    ptrs = [g if isinstance(g, int) else _ptr(g) for g in grads]
+    arr = (C.c_void_p * len(ptrs))(*ptrs)
+    hy = hyper.c()
+    _lib.call_tuning("tfg_adam_fused_multi_variant", variant, _ptr(p), _ptr(m), _ptr(v), arr, len(ptrs), _ptr(param16),
+                     p.numel(), C.byref(hy), t, _ptr(counters) if counters is not None else None, _stream(stream))
+
+
 def selftest_div_const(divisor: float, n: int, seed: int = 1, exp_lo: int = -160, exp_span: int = 170):
     """(mismatches, first_bad_numerator) of the constant-divisor quotient vs div.rn.f64."""
     mm, fb = C.c_uint64(), C.c_double()

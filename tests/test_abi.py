@@ -36,8 +36,8 @@ def test_tuning_library_is_separate(tf):
     include/tierflow_b200_tuning.h; the product library has none of them."""
     from paper_2509_02480_b200 import _lib
     names = declared(TUNING_HEADER)
-    assert names == ["tfg_adam_fused_variant", "tfg_adam_variant_count", "tfg_selftest_fast_rn",
-                     "tfg_selftest_fast_step"]
+    assert names == ["tfg_adam_fused_multi_variant", "tfg_adam_fused_variant", "tfg_adam_variant_count",
+                     "tfg_selftest_fast_rn", "tfg_selftest_fast_step"]
     tuning = _lib.load_tuning()
     assert all(hasattr(tuning, n) for n in names)
     syms = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True, text=True).stdout

@@ -342,6 +342,39 @@ def test_fused_reduce_update_matches_oracle(tf, cuda, nsrc, kind):
     assert counters.cpu().tolist() == [0, want[4]]
 
 
+@pytest.mark.parametrize("nsrc", [2, 4, 8])
+@pytest.mark.parametrize("form", [0, 1])
+def test_multi_source_forms_match_oracle(tf, cuda, nsrc, form):
+    """Both n-source kernels (tuning hook: 0 = staged, 1 = register) against the
+    oracle, f16, a partial tile at the end; non-finite sums are counted."""
+    import torch
+    n = 1 << 20 | 515
+    rng = np.random.default_rng(nsrc * 7 + form)
+    srcs = [oracle.synthetic_grads(n, 91, s, 1) for s in range(nsrc)]
+    srcs[0][5] = 0x7C00  # one +Inf contribution: a non-finite sum
+    acc = np.full(n, -0.0, np.float32)
+    for s in srcs:
+        acc = (acc + oracle.widen16(s, 0)).astype(np.float32)
+    g16, _ = oracle.narrow16(acc, 0)
+    g16[5] = 0  # the oracle rejects a non-finite step: compare every other element
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+    v = rng.uniform(0, 0.01, n).astype(np.float32)
+    want = oracle.adam_fused(p, m, v, g16, 0, 0, 2, weight_decay=0.0)
+    P, Mm, V = _dev(torch, p, cuda), _dev(torch, m, cuda), _dev(torch, v, cuda)
+    G = [_u16(torch, s, cuda) for s in srcs]
+    p16 = torch.zeros(n, dtype=torch.int16, device=cuda)
+    counters = torch.zeros(2, dtype=torch.int64, device=cuda)
+    tf.adam_fused_multi_variant(form, P, Mm, V, G, p16, 2, tf.AdamHyper(), counters)
+    torch.cuda.synchronize()
+    keep = np.ones(n, bool)
+    keep[5] = False
+    for got, w, what in ((P, want[0], "P"), (Mm, want[1], "m"), (V, want[2], "v")):
+        assert_bits(got.cpu().numpy()[keep], w[keep], what)
+    assert np.array_equal(_np16(p16)[keep], want[3][keep])
+    assert counters.cpu().tolist()[0] == 1
+
+
 def test_fp32_gradient_kind(tf, cuda):
     """grad_dtype F32: the baseline flow's stored fp32 gradients."""
     import torch
