@@ -11,7 +11,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:adam
   -o gpurun_out/prof_adam -f python scripts/profile_kernel.py > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"; tail -3 gpurun_out/ncu_full.log
 for k in ${MULTI:-2 8}; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:adam_fused -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k "regex:adam_(staged|fused)" -s 2 -c 1 \
     -o gpurun_out/prof_multi$k -f python scripts/profile_kernel.py 100000000 4 0 $k > gpurun_out/ncu_multi$k.log 2>&1
   echo "multi$k rc=$?"
 done

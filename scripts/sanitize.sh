@@ -50,9 +50,11 @@ for v in variants:
     tf.adam_fused_variant(v, P, M, V, g, p16, 1, tf.AdamHyper())
     torch.cuda.synchronize()
 st = torch.empty(3 * n, device="cuda")
-srcs = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(3)]
+srcs = [torch.empty(n, dtype=torch.int16, device="cuda") for _ in range(8)]
 for s_ in srcs: tf.synthetic_grads(s_, 2, 0, 0)
-tf.adam_fused_multi(st[:n], st[n:2*n], st[2*n:], srcs, p16, 2, tf.AdamHyper())
+tf.adam_fused_multi(st[:n], st[n:2*n], st[2*n:], srcs[:3], p16, 2, tf.AdamHyper())  # register n-source form
+P, M, V = (torch.empty(n, device="cuda") for _ in range(3)); tf.synthetic_state(P, M, V, 1, 0)
+tf.adam_fused_multi(P, M, V, srcs, p16, 3, tf.AdamHyper())  # 8 sources: the staged n-source kernel
 torch.cuda.synchronize()
 print("kernels ok")
 PY
