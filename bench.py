@@ -987,9 +987,9 @@ def main(argv=None):
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / pk["hbm_gbs"], 4), "traffic": ncu_traffic(params_per_launch),
                 "peak_source": pk["source"], "alg_bytes_per_param": alg_bytes,
-                "kernel": (f"{'adam_staged_kernel (tiles staged by cp.async.bulk, 3 CTAs per SM' if world == 8 else 'adam_fused_kernel (float4 quads, 4 CTAs x 256 threads per SM'}"
-                           f"; binary64 element math, constant-divisor quotients; {world} gradient sources summed "
-                           f"in-kernel, {world - 1} read from the peers' NVLink-mapped memory)" if exchange == "fused" else
+                "kernel": (f"adam_fused_kernel (float4 quads, 4 CTAs x 256 threads per SM; binary64 element math, "
+                           f"constant-divisor quotients; {world} gradient sources summed in-kernel, {world - 1} "
+                           f"read from the peers' NVLink-mapped memory)" if exchange == "fused" else
                            "adam_staged_kernel (P, m, v, g tiles of 1024 params staged in shared memory by "
                            "cp.async.bulk, 2 stages per CTA, 4 CTAs x 256 threads per SM; binary64 element math, "
                            "constant-divisor quotients)"),

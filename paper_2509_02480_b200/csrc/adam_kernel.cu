@@ -62,17 +62,37 @@ __global__ void divtest_kernel(double b, double y, uint64_t n, uint64_t seed, in
 
 }  // namespace
 
+// Whether every gradient source is memory of the current device. Bulk copies
+// (cp.async.bulk) from a peer's NVLink-mapped memory are not exercised on the
+// one-GPU boxes this was measured on, so peer sources keep the register
+// form's per-thread loads, which the multi-GPU tests cover.
+static bool sources_on_this_device(const AdamLaunch& a) {
+    int dev = -1;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    for (int s = 0; s < a.n_peers; ++s) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, a.peers[s]) != cudaSuccess) {
+            (void)cudaGetLastError();
+            return false;
+        }
+        if (at.type != cudaMemoryTypeDevice || at.device != dev) return false;
+    }
+    return true;
+}
+
 cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
     if (a.n == 0) return cudaSuccess;
     cudaError_t e = cudaErrorNotSupported;
-    // The fused exchange sums n ranks' contributions in the update. With the
-    // sources in local HBM under sustained load (profiles/multi_sustained_r2.json)
-    // the staged form wins at 8 sources (0.920 vs 0.876 of the copy peak) and
-    // the register form at 2 and 4 (0.938 / 0.956 vs 0.892), whose extra
-    // loads per thread already keep enough bytes in flight.
+    // n summed gradient sources. With the sources in local HBM under
+    // sustained load (profiles/multi_sustained_r2.json) the staged form wins
+    // at 8 sources (0.920-0.965 vs 0.876-0.892 of the copy peak) and the
+    // register form at 2 and 4, whose extra loads per thread already keep
+    // enough bytes in flight.
     switch (a.n_peers) {
         case 0: e = launch_staged<kStages, kStagedCtasPerSm>(a, stream); break;
-        case 8: e = launch_staged<kStages, 3, 1, 1, 0, 8>(a, stream); break;  // 56 KiB per CTA: 3 fit an SM
+        case 8:  // 56 KiB per CTA: 3 fit an SM
+            if (sources_on_this_device(a)) e = launch_staged<kStages, 3, 1, 1, 0, 8>(a, stream);
+            break;
         default: break;
     }
     if (e != cudaErrorNotSupported) return e;
