@@ -731,7 +731,8 @@ def e2e_line(r, world, extra):
 # capped to a third of the rest).
 
 
-def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=4, steps=4, pool=8, ring=4, M=12):
+def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=4, steps=4, pool=8, ring=4, M=12,
+              lock_width=1):
     """SURVEY C4 sample. warmup 4: the first phases write subgroup files to
     tiers they have not been on yet (a fresh file is allocated on first
     write: 4.1 vs 5.5 GB/s for an in-place overwrite); the
@@ -762,9 +763,9 @@ def spill_leg(tf, sizes, base_id, rank, world, tier_root, seed, warmup=4, steps=
     same_device = os.stat(root / "nvme").st_dev == os.stat(root / "remote").st_dev
     lock_dev = 1 if same_device else 0
     dirs = [tf.Tier(tf.TierSpec(1, tf.TierKind.local_dir, str(root / "nvme"), 0.0, 0.0, io_parallelism=4,
-                                lock_device=lock_dev)),
+                                lock_width=lock_width, lock_device=lock_dev)),
             tf.Tier(tf.TierSpec(2, tf.TierKind.remote_dir, str(root / "remote"), 0.0, 0.0, io_parallelism=4,
-                                lock_device=lock_dev))]
+                                lock_width=lock_width, lock_device=lock_dev))]
     probes = [t.probe_bandwidth(1 << 30, 3) for t in dirs]
     dram = tf.Tier(tf.TierSpec(0, tf.TierKind.host_dram, "dram", 50e9, 50e9, capacity_bytes=dram_cap * block))
     tiers = [dram] + dirs
@@ -921,6 +922,8 @@ def main(argv=None):
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-spill", action="store_true", help="skip the directory-tier spill sample (SURVEY C4)")
+    ap.add_argument("--spill-lock-width", type=int, default=1,
+                    help="concurrent transfers the spill sample's device semaphore admits")
     ap.add_argument("--skip-nccl", action="store_true")
     ap.add_argument("--c0-steps", type=int, default=5, help="timed phases of the C=0 streaming e2e (0: skip)")
     ap.add_argument("--host-grads", action="store_true",
@@ -1004,7 +1007,8 @@ def main(argv=None):
     spill = None
     if exchange == "none" and not a.skip_e2e and not a.skip_spill:
         try:
-            r = spill_leg(tf, sizes, rank * len(sizes), rank, world, a.tier_root, a.seed)
+            r = spill_leg(tf, sizes, rank * len(sizes), rank, world, a.tier_root, a.seed,
+                          lock_width=a.spill_lock_width)
             s_ms = allmax(world, r["ms"])
             spill = {"value": allsum(world, r["params"]) / (s_ms / 1e3), "unit": "params/s",
                      "ms_per_step": round(s_ms, 1), "phase_ms": r["phase_ms"],
