@@ -1005,7 +1005,7 @@ def main(argv=None):
     # not measured behind the e2e leg's directory-tier writes still draining
     # on the box's (virtualised) disk.
     spill = None
-    if exchange == "none" and not a.skip_e2e and not a.skip_spill:
+    if exchange == "none" and not a.skip_spill:
         try:
             r = spill_leg(tf, sizes, rank * len(sizes), rank, world, a.tier_root, a.seed,
                           lock_width=a.spill_lock_width)

@@ -35,7 +35,7 @@ if launches.exists():
         agg[name][1] += float(r[vi].replace(",", "")) * UNIT.get(r[ui], 1.0)
     total = sum(v[1] for v in agg.values())
     lines = [f"# ncu launch list ({tag}): `ncu --metrics gpu__time_duration.sum --clock-control none "
-             f"python bench.py --steps 2 --warmup 1 --skip-e2e --skip-cpu`",
+             f"python bench.py --steps 2 --warmup 1 --skip-e2e --skip-cpu --skip-spill`",
              "", "Cold-cache, serialised per-launch times: compare shares, not absolutes.", "",
              "| kernel | launches | total us | mean us | share |", "|---|---|---|---|---|"]
     for name, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
