@@ -34,7 +34,7 @@ CXX_SOURCES = ["tier.cpp", "engine.cpp", "capi.cpp", "capi_host.cpp"]
 # The tuning library (include/tierflow_b200_tuning.h): the measured kernel
 # variants, for sweeps and the all-variants parity test; linked against the
 # product library, never loaded by it.
-TUNING_CU = ["adam_variants.cu"]
+TUNING_CU = ["adam_variants.cu", "adam_variants_hi.cu"]
 TUNING_CXX = ["tuning_capi.cpp"]
 
 
