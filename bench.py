@@ -993,8 +993,8 @@ def main(argv=None):
                 "kernel": (f"adam_fused_kernel (float4 quads, 4 CTAs x 256 threads per SM; binary64 element math, "
                            f"constant-divisor quotients; {world} gradient sources summed in-kernel, {world - 1} "
                            f"read from the peers' NVLink-mapped memory)" if exchange == "fused" else
-                           "adam_staged_kernel (P, m, v, g tiles of 1024 params staged in shared memory by "
-                           "cp.async.bulk, 2 stages per CTA, 4 CTAs x 256 threads per SM; binary64 element math, "
+                           "adam_staged_kernel (P, m, v, g tiles of 2048 params staged in shared memory by "
+                           "cp.async.bulk, 2 stages per CTA, 2 CTAs x 512 threads per SM; binary64 element math, "
                            "constant-divisor quotients)"),
                 "traffic_source": "profiles/ncu_adam_fused.json (ncu --set full, dram bytes per 100M-param launch)",
                 "copy_sustained_gbs": dl.get("copy_sustained_gbs"),

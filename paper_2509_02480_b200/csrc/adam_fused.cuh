@@ -379,13 +379,14 @@ __device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uin
 // NS > 0: the gradient is the in-order fp32 sum of NS 16-bit sources (the
 // peers' contributions, NVLink-mapped), each staged by its own bulk copy per
 // tile and summed from shared memory, rounded once to GK (sum_quad16's rule).
-template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0, int NS = 0>
-__global__ void __launch_bounds__(kThreads, MINB)
+template <int GK, int OK, bool WD, int S, bool CNT, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0, int NS = 0,
+          int NT = kThreads>
+__global__ void __launch_bounds__(NT, MINB)
     adam_staged_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v, const GradSources gs,
                        uint16_t* __restrict__ p16, uint64_t n, AdamConsts c,
                        unsigned long long* __restrict__ counters, const unsigned long long* __restrict__ gate) {
     if (gate != nullptr && *gate != 0) return;  // the phase was rejected on this stream: no writes
-    constexpr int T = 4 * kThreads * Q;  // Q quads per thread per tile
+    constexpr int T = 4 * NT * Q;  // Q quads per thread per tile
     constexpr int G = NS > 0 ? NS : 1;   // gradient tiles per stage
     const uint16_t* __restrict__ g = static_cast<const uint16_t*>(gs.src[0]);
     const uint64_t ntiles = n / T;
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
         const uint64_t off = (blockIdx.x + k * gridDim.x) * static_cast<uint64_t>(T);
 #pragma unroll 1
         for (int qq = 0; qq < Q; ++qq) {
-            const int qj = qi + qq * kThreads;
+            const int qj = qi + qq * NT;
             const float4 rp = reinterpret_cast<const float4*>(sp + s * T)[qj];
             const float4 rm = reinterpret_cast<const float4*>(sm + s * T)[qj];
             const float4 rv = reinterpret_cast<const float4*>(sv + s * T)[qj];
@@ -459,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (blockIdx.x == gridDim.x - 1) {
         const uint64_t done = ntiles * T;
         const uint64_t nq = (n - done) / 4;
-        for (uint64_t j = threadIdx.x; j < nq; j += kThreads) {
+        for (uint64_t j = threadIdx.x; j < nq; j += NT) {
             const uint64_t q = done / 4 + j;
             const float4 rp = __ldcs(reinterpret_cast<const float4*>(p) + q);
             const float4 rm = __ldcs(reinterpret_cast<const float4*>(m) + q);
@@ -603,9 +604,9 @@ cudaError_t launch_dtypes(const AdamLaunch& a, cudaStream_t stream) {
 // staged form (fp32 gradients, a source count other than NS, separate
 // outputs, 16-byte misalignment, fewer than one tile); the caller then
 // launches the register kernel.
-template <int S, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0, int NS = 0>
+template <int S, int MINB, int MATH = 1, int Q = 1, int PFL2 = 0, int NS = 0, int NT = kThreads>
 cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
-    constexpr uint64_t T = 4 * kThreads * Q;
+    constexpr uint64_t T = 4 * NT * Q;
     constexpr int G = NS > 0 ? NS : 1;
     const GradSources gs = sources_of(a);
     uintptr_t addr = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
@@ -624,14 +625,14 @@ cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
     auto pick = [&](auto gk, auto ok) {
         constexpr int GKc = decltype(gk)::value, OKc = decltype(ok)::value;
         if constexpr (NS > 0) {
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2, NS>
-                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2, NS>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2, NS, NT>
+                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2, NS, NT>;
         } else if (cnt) {
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2>
-                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, true, MINB, MATH, Q, PFL2, 0, NT>
+                      : adam_staged_kernel<GKc, OKc, false, S, true, MINB, MATH, Q, PFL2, 0, NT>;
         } else {
-            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH, Q, PFL2>
-                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH, Q, PFL2>;
+            kern = wd ? adam_staged_kernel<GKc, OKc, true, S, false, MINB, MATH, Q, PFL2, 0, NT>
+                      : adam_staged_kernel<GKc, OKc, false, S, false, MINB, MATH, Q, PFL2, 0, NT>;
         }
     };
     using F = std::integral_constant<int, kF16>;
@@ -642,7 +643,7 @@ cudaError_t launch_staged(const AdamLaunch& a, cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(ntiles, static_cast<uint64_t>(num_sms()) * MINB));
-    kern<<<grid, kThreads, smem, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters, a.gate);
+    kern<<<grid, NT, smem, stream>>>(a.p, a.m, a.v, gs, a.p16, a.n, a.c, a.counters, a.gate);
     return cudaGetLastError();
 }
 

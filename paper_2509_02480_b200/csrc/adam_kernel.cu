@@ -16,12 +16,14 @@ namespace {
 
 // Shipped configuration. One 16-bit gradient source in place (the engine's
 // pipeline, the device-resident bench leg, the operator API): the staged
-// kernel, 2 shared-memory stages of 1024 params (28 KiB) per CTA, 4 CTAs of
-// 256 threads per SM, f16 gradients widened straight to binary64, no second
-// non-finite count behind a whole-phase check. Under the bench's sustained,
-// power-capped load it holds 0.875-0.886 of the HBM copy peak where the
-// register kernel holds 0.842-0.853 (interleaved rounds,
-// profiles/sustained_sweep_r2_staged.json: tuning variant 55 vs 0).
+// kernel, 2 shared-memory stages of 2048 params (56 KiB) per CTA, 2 CTAs of
+// 512 threads per SM (32 warps, 64 registers), f16 gradients widened straight
+// to binary64, no second non-finite count behind a whole-phase check. Under
+// the bench's sustained, power-capped load it holds 0.909-0.929 of the HBM
+// copy peak on three boxes against 0.893-0.894 for the 256-thread / 4-CTA
+// shape (tuning variants 70 vs 55, profiles/sustained_sweep_r2_nt_box*.json)
+// and 0.84-0.85 for the register kernel; launched cool, 456 us per 100M
+// params = 0.937, the best of every measured form (profiles/kernel_sweep_r2.json).
 // Everything else (summed or fp32 gradients, separate outputs, misaligned or
 // sub-tile launches, a launch's n % 1024 tail): the register kernel, one quad
 // per thread per iteration, constant-divisor quotients, <= 64 registers for 4
@@ -29,7 +31,8 @@ namespace {
 // profiles/kernel_sweep_r1.json).
 using VariantDefault = Cfg<1, true, 4>;
 constexpr int kStages = 2;
-constexpr int kStagedCtasPerSm = 4;
+constexpr int kStagedCtasPerSm = 2;
+constexpr int kStagedThreads = 512;
 // Tuning variants (F16 gradients and params only), for the kernel sweep.
 
 // ---------------------------------------------------------------------------
@@ -89,7 +92,7 @@ cudaError_t launch_adam_fused(const AdamLaunch& a, cudaStream_t stream) {
     // register form at 2 and 4, whose extra loads per thread already keep
     // enough bytes in flight.
     switch (a.n_peers) {
-        case 0: e = launch_staged<kStages, kStagedCtasPerSm>(a, stream); break;
+        case 0: e = launch_staged<kStages, kStagedCtasPerSm, 1, 1, 0, 0, kStagedThreads>(a, stream); break;
         case 8:  // 56 KiB per CTA: 3 fit an SM
             if (sources_on_this_device(a)) e = launch_staged<kStages, 3, 1, 1, 0, 8>(a, stream);
             break;

@@ -104,6 +104,6 @@ cudaError_t launch_adam_fused_variant(const AdamLaunch& a, int variant, cudaStre
     }
 }
 
-int adam_variant_count() { return 68; }
+int adam_variant_count() { return 72; }
 
 }  // namespace tfb

@@ -20,6 +20,8 @@
 //                       3 CTAs (60), 3 stages / 2 CTAs (61), 4 stages / 2 CTAs (62); 4-quad tiles at 1 CTA
 //                       per SM: 3 stages (63), 2 stages (64); the shipped shape with an L2 bulk prefetch 1 (65)
 //                       or 2 (66) tiles beyond its look-ahead
+//   68-71               the staged kernel with larger CTAs: 320 threads x 3 (68), 384 x 2 (69), 512 x 2 with
+//                       2 (70) or 3 (71) stages — tiles of 4 x threads params
 //   67                  tile-interleaved state layout ([P | m | v] per 1024-param tile; timing only, its bits
 //                       land in the interleaved positions — scripts/layout_probe.py, not the bitwise test)
 #pragma once

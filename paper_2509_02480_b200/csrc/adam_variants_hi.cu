@@ -5,8 +5,21 @@
 
 namespace tfb {
 
+// Variants 68-71: the staged kernel with larger CTAs (NT threads): bigger
+// tiles (4 x NT params, i.e. larger bulk copies) at full occupancy.
+template <int S, int M, int NT>
+cudaError_t launch_staged_nt(const AdamLaunch& a, cudaStream_t stream) {
+    AdamLaunch b = a;
+    b.grads_verified = true;
+    return launch_staged<S, M, 1, 1, 0, 0, NT>(b, stream);
+}
+
 cudaError_t launch_adam_fused_variant_hi(const AdamLaunch& a, int variant, cudaStream_t stream) {
     switch (variant) {
+        case 68: return launch_staged_nt<2, 3, 320>(a, stream);
+        case 69: return launch_staged_nt<2, 2, 384>(a, stream);
+        case 70: return launch_staged_nt<2, 2, 512>(a, stream);
+        case 71: return launch_staged_nt<3, 2, 512>(a, stream);
         case 34: return launch_variant<34>(a, stream);
         case 35: return launch_variant<35>(a, stream);
         case 36: return launch_variant<36>(a, stream);

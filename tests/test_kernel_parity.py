@@ -263,7 +263,7 @@ def test_constant_division_matches_div_rn(tf, cuda):
             assert mism == 0, (beta, t, first)
 
 
-@pytest.mark.parametrize("variant", range(1, 67))
+@pytest.mark.parametrize("variant", [v for v in range(1, 72) if v != 67])  # 67: tile-interleaved layout
 def test_kernel_variants_bitwise(tf, cuda, variant):
     import torch
     n = 1_000_003
