@@ -63,7 +63,10 @@ echo "memcheck kernels rc=$?"; tail -3 gpurun_out/san_memcheck_kernels.log
 # the shipped staged kernel with a tail (n % 1024 = 3: one partial tile's quads and scalars in the last CTA)
 timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,55 1003523 > gpurun_out/san_memcheck_tail.log 2>&1
 echo "memcheck staged tail rc=$?"; tail -3 gpurun_out/san_memcheck_tail.log
-timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 0,12,13,16,32,33,36,38,39,55 > gpurun_out/san_racecheck.log 2>&1
+# a partial 2048-param tile of 577 params (n % 4 = 1) for the shipped 2 x 512 shape
+timeout 900 $CS --tool memcheck --error-exitcode 9 python /tmp/san_kernels.py 0,70 1000001 > gpurun_out/san_memcheck_tail2.log 2>&1
+echo "memcheck staged tail2 rc=$?"; tail -3 gpurun_out/san_memcheck_tail2.log
+timeout 900 $CS --tool racecheck --error-exitcode 9 python /tmp/san_kernels.py 0,12,13,16,32,33,36,38,39,55,70 > gpurun_out/san_racecheck.log 2>&1
 echo "racecheck rc=$?"; tail -3 gpurun_out/san_racecheck.log
-timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 0,12,16,32,36,38,55 > gpurun_out/san_synccheck.log 2>&1
+timeout 900 $CS --tool synccheck --error-exitcode 9 python /tmp/san_kernels.py 0,12,16,32,36,38,55,70 > gpurun_out/san_synccheck.log 2>&1
 echo "synccheck rc=$?"; tail -3 gpurun_out/san_synccheck.log

@@ -484,3 +484,43 @@ def test_one_billion_param_subgroup_is_chunk_invariant(tf, cuda):
     assert np.array_equal(st[n + ti].cpu().numpy().view(np.uint32), want[1].view(np.uint32))
     assert np.array_equal(st[2 * n + ti].cpu().numpy().view(np.uint32), want[2].view(np.uint32))
     assert np.array_equal(p16a[ti].cpu().numpy().view(np.uint16), want[3])
+
+
+# Tile edges of the shipped staged shape (2048-param tiles, 2 CTAs x 512 threads per SM on 148 SMs):
+# one tile, one tile +-1, a partial quad, one full wave of CTAs plus a 577-param tail.
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [2048, 2049, 4095, 4097, 2048 * 296 + 577, 2048 * 296 * 3 + 2, 1_000_001])
+def test_staged_tile_edges_and_canaries(tf, cuda, n):
+    """Bits equal the oracle at the tile edges, and nothing outside [0, n) is written: every stream sits
+    between 16-byte-aligned canary regions (the kernel's own bounds, checked without a sanitizer)."""
+    import torch
+    pad = 4096
+    rng = np.random.default_rng(n)
+    p = rng.uniform(-2, 2, n).astype(np.float32)
+    m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+    v = rng.uniform(0, 0.01, n).astype(np.float32)
+    g16 = oracle.synthetic_grads(n, 7, n % 31, 2, kind=0)
+    want = oracle.adam_fused(p, m, v, g16, 0, 0, 3, weight_decay=0.01)
+
+    def framed(a, dtype, fill):
+        buf = torch.full((pad + a.size + pad,), fill, dtype=dtype, device=cuda)
+        buf[pad:pad + a.size] = torch.from_numpy(a.view(np.int16) if dtype == torch.int16 else a).to(cuda)
+        return buf
+
+    P, M, V = (framed(a, torch.float32, 1234.5) for a in (p, m, v))
+    G = framed(g16, torch.int16, 0x3C00)
+    P16 = torch.full((pad + n + pad,), 0x7E00, dtype=torch.int16, device=cuda)
+    counters = torch.zeros(2, dtype=torch.int64, device=cuda)
+    sl = slice(pad, pad + n)
+    tf.adam_fused(P[sl], M[sl], V[sl], G[sl], P16[sl], 3, tf.AdamHyper(weight_decay=0.01), 0, 0, counters=counters)
+    torch.cuda.synchronize()
+    for name, buf, fill in (("P", P, 1234.5), ("m", M, 1234.5), ("v", V, 1234.5)):
+        h = buf.cpu().numpy()
+        assert np.all(h[:pad] == fill) and np.all(h[pad + n:] == fill), f"{name}: write outside [0, n)"
+    h16 = P16.cpu().numpy()
+    assert np.all(h16[:pad] == 0x7E00) and np.all(h16[pad + n:] == 0x7E00), "params16: write outside [0, n)"
+    assert_bits(P[sl].cpu().numpy(), want[0], "P")
+    assert_bits(M[sl].cpu().numpy(), want[1], "m")
+    assert_bits(V[sl].cpu().numpy(), want[2], "v")
+    assert np.array_equal(_np16(P16[sl]), want[3])
+    assert counters.cpu().numpy()[1] == want[4]
