@@ -374,7 +374,8 @@ __device__ __forceinline__ void staged_quad(float4 rp, float4 rm, float4 rv, uin
 // depend on how long the binary64 chain of the current quad takes, so the
 // kernel keeps HBM busy when the power cap lowers the SM clock (the register
 // kernel's loads are only in flight between two quads' math). Tile T =
-// 1024 params (one quad per thread); one CTA barrier per tile retires a stage
+// 4 x NT params (one quad per thread: 2048 at the shipped NT = 512); one CTA
+// barrier per tile retires a stage
 // before it is refilled. The same element math, bit for bit.
 // NS > 0: the gradient is the in-order fp32 sum of NS 16-bit sources (the
 // peers' contributions, NVLink-mapped), each staged by its own bulk copy per

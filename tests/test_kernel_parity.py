@@ -524,3 +524,48 @@ def test_staged_tile_edges_and_canaries(tf, cuda, n):
     assert_bits(V[sl].cpu().numpy(), want[2], "v")
     assert np.array_equal(_np16(P16[sl]), want[3])
     assert counters.cpu().numpy()[1] == want[4]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("nsrc", [2, 8])
+@pytest.mark.parametrize("n", [4097, 2048 * 296 + 577])
+def test_multi_source_canaries(tf, cuda, nsrc, n):
+    """The n-source reduce + update (8 sources: the staged form) writes nothing outside [0, n) and reads
+    its sources only inside [0, n): a source's out-of-range neighbours are NaN, so a stray read of one
+    would reach the non-finite counter or the bits."""
+    import torch
+    pad = 4096
+    rng = np.random.default_rng(nsrc * 1000 + n)
+    srcs = [oracle.synthetic_grads(n, 5, s, 2, kind=0) for s in range(nsrc)]
+    acc = np.full(n, -0.0, np.float32)
+    for s in srcs:
+        acc = (acc + oracle.widen16(s, 0)).astype(np.float32)
+    g16, _ = oracle.narrow16(acc, 0)
+    p = rng.uniform(-1, 1, n).astype(np.float32)
+    m = (rng.uniform(-0.5, 0.5, n) * 0.1).astype(np.float32)
+    v = rng.uniform(0, 0.01, n).astype(np.float32)
+    want = oracle.adam_fused(p, m, v, g16, 0, 0, 2, weight_decay=0.01)
+
+    def framed(a, dtype, fill):
+        buf = torch.full((pad + a.size + pad,), fill, dtype=dtype, device=cuda)
+        buf[pad:pad + a.size] = torch.from_numpy(a.view(np.int16) if dtype == torch.int16 else a).to(cuda)
+        return buf
+
+    sl = slice(pad, pad + n)
+    P, M, V = (framed(a, torch.float32, -77.25) for a in (p, m, v))
+    G = [framed(s, torch.int16, 0x7E00) for s in srcs]  # f16 NaN around every source
+    P16 = torch.full((pad + n + pad,), 0x1234, dtype=torch.int16, device=cuda)
+    counters = torch.zeros(2, dtype=torch.int64, device=cuda)
+    tf.adam_fused_multi(P[sl], M[sl], V[sl], [g[sl] for g in G], P16[sl], 2, tf.AdamHyper(weight_decay=0.01), 0, 0,
+                        counters)
+    torch.cuda.synchronize()
+    for name, buf in (("P", P), ("m", M), ("v", V)):
+        h = buf.cpu().numpy()
+        assert np.all(h[:pad] == -77.25) and np.all(h[pad + n:] == -77.25), f"{name}: write outside [0, n)"
+    h16 = P16.cpu().numpy()
+    assert np.all(h16[:pad] == 0x1234) and np.all(h16[pad + n:] == 0x1234), "params16: write outside [0, n)"
+    assert_bits(P[sl].cpu().numpy(), want[0], "P")
+    assert_bits(M[sl].cpu().numpy(), want[1], "m")
+    assert_bits(V[sl].cpu().numpy(), want[2], "v")
+    assert np.array_equal(_np16(P16[sl]), want[3])
+    assert counters.cpu().tolist() == [0, want[4]]
